@@ -1,0 +1,336 @@
+/*
+ * mppi_b200.h — C ABI of the B200-native joint-space MPPI step.
+ *
+ * This is the drop-in boundary for the reference's hot path
+ * (jointmpc, arXiv 2104.13542). Everything below is
+ * plain C: pointers, sizes, int status codes. No torch or CUDA types appear
+ * in a signature; device pointers are passed as `void*`/`uint64_t` only in the
+ * *_dev entry points, and a CUDA stream as an opaque `void*` (NULL = the
+ * plan's own stream).
+ *
+ * Reference interfaces each entry point replaces (file:line are relative to
+ * /root/reference/pkg/src/jointmpc/):
+ *
+ *   mppi_plan_create        Controller.__init__            controller.py:98-187
+ *                           (+ CostStack.__post_init__      costs.py:205-207,
+ *                              make_dt_schedule             rollout.py:67-81,
+ *                              make_policy                  policy.py:88-95)
+ *   mppi_init_noise         Halton fixed set               controller.py:166-176
+ *                           <- unit_samples/gaussianize/smooth_sequences
+ *                                                           sampling.py:118-265
+ *   mppi_set_noise          Controller._perturbations       controller.py:192-196
+ *                           (injected perturbations, the parity hook of
+ *                            SURVEY §3.4)
+ *   mppi_set_goal           Controller.set_goal             controller.py:189-190
+ *   mppi_set_world          CostStack.world / WorldModel    simworld.py:30-49
+ *   mppi_set_voxel_world    (new: 64^3 occupancy grid, config 3 bridge §8c)
+ *   mppi_set_mlp            LearnedSelfCollision.load       surrogate.py:134-143
+ *   mppi_get/set_policy     Controller.policy               controller.py:157,200,216
+ *   mppi_step               Controller.control_step         controller.py:198-260
+ *   mppi_evaluate           evaluate_rollouts               rollout.py:124-180
+ *                           CostStack.evaluate              costs.py:209-242
+ *   mppi_update_policy      particle_weights + update_mean + update_covariance
+ *                                                           policy.py:103-155
+ *   mppi_stats_dev /        (new: particle-sharded update, §8(e) config 5 —
+ *   mppi_finalize_dev         per-rank weighted sufficient statistics, one
+ *                             all-gather, fixed-order combine)
+ *
+ *   The reference's fine-grained operator seam (kernels/__init__.py:50-66),
+ *   float64 in / float64 out, caller-owned outputs:
+ *   mppi_fk_batch           kernels.fk_batch                jit.py:89-111
+ *   mppi_jacobian_batch     kernels.jacobian_batch          jit.py:114-148
+ *   mppi_manip_batch        kernels.manip_batch             jit.py:151-185
+ *   mppi_self_collision_batch kernels.self_collision_batch  jit.py:241-260
+ *   mppi_env_collision_batch  kernels.env_collision_batch   jit.py:289-332
+ *   mppi_integrate_batch    kernels.integrate_batch         jit.py:335-349
+ *
+ *   Sampling / policy free functions (sampling.py, policy.py):
+ *   mppi_halton_points      halton_points                   sampling.py:100-115
+ *   mppi_gaussianize        gaussianize                     sampling.py:167-202
+ *   mppi_smooth_sequences   smooth_sequences                sampling.py:240-265
+ *   mppi_build_controls     build_control_batch             sampling.py:268-290
+ *   mppi_particle_weights   particle_weights                policy.py:103-121
+ *   mppi_mlp_forward        MLP.forward (inference)         surrogate.py:42-52
+ *
+ * Error convention: every function returns an int status (MPPI_OK = 0). The
+ * message of the last failure on the calling thread is in mppi_last_error().
+ * The Python layer maps codes to the reference exceptions (errors.py):
+ *   NONFINITE_CONTROL, BAD_ARGUMENT      -> ContractError
+ *   ALL_QUARANTINED, WEIGHT_UNDERFLOW,
+ *   NONPOSITIVE_VARIANCE                 -> PolicyStateError
+ *   CONFIG                               -> ConfigError
+ *   CUDA                                 -> DeviceError (not caught by the
+ *                                           controller's fallback ladder)
+ *
+ * Threading: a plan is single-threaded (Controller is, controller.py:93-96);
+ * distinct plans may be used from distinct threads / devices. The stateless
+ * seam functions are re-entrant.
+ */
+#ifndef MPPI_B200_H
+#define MPPI_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MPPI_ABI_VERSION 1
+
+/* Compile-time capacity of the fused kernels. */
+#define MPPI_MAX_DOF      8   /* kernels are instantiated for dof 1..8      */
+#define MPPI_MAX_HORIZON  32  /* one warp per particle, one lane per step   */
+#define MPPI_MAX_CAPSULES 16
+#define MPPI_MAX_PAIRS    64
+#define MPPI_MLP_IN_MAX   16  /* 2*dof positional encoding, padded          */
+
+enum mppi_status {
+  MPPI_OK = 0,
+  MPPI_E_NONFINITE_CONTROL = 1,
+  MPPI_E_ALL_QUARANTINED = 2,
+  MPPI_E_WEIGHT_UNDERFLOW = 3,
+  MPPI_E_BAD_ARGUMENT = 4,
+  MPPI_E_CUDA = 5,
+  MPPI_E_NONPOSITIVE_VARIANCE = 6,
+  MPPI_E_CONFIG = 7
+};
+
+enum mppi_goal_mode {          /* costs.py:20-22 */
+  MPPI_GOAL_POSITION_ONLY = 0,
+  MPPI_GOAL_FULL_POSE = 1,     /* full_pose and orientation_constrained */
+};
+
+enum mppi_self_collision {     /* CostStack.self_collision provider kind */
+  MPPI_SELFCOLL_NONE = 0,
+  MPPI_SELFCOLL_ORACLE = 1,    /* capsule pairs, costs.py:136-156        */
+  MPPI_SELFCOLL_LEARNED = 2    /* MLP on tcgen05, surrogate.py:120-125   */
+};
+
+enum mppi_generator {
+  MPPI_GEN_HALTON = 0,         /* fixed, centred set drawn once           */
+  MPPI_GEN_PSEUDORANDOM = 1,   /* Philox4x32-10 on device, every step     */
+  MPPI_GEN_EXTERNAL = 2        /* caller injects eps via mppi_set_noise   */
+};
+
+enum mppi_smoothing { MPPI_SMOOTH_BSPLINE = 0, MPPI_SMOOTH_COMB = 1, MPPI_SMOOTH_NONE = 2 };
+enum mppi_policy_mode { MPPI_POLICY_PER_JOINT = 0, MPPI_POLICY_ISOTROPIC = 1 };
+enum mppi_precision { MPPI_FP32 = 0, MPPI_FP64 = 1 };
+
+/* Packed chain, the layout of KinematicChain (kinematics.py:53-114).
+ * All arrays row-major float64 / int64, exactly the numpy arrays. */
+typedef struct mppi_chain_desc {
+  int32_t dof;
+  int32_t task_dim;          /* 2 or 3 */
+  int32_t n_caps;
+  int32_t n_pairs;
+  const double* axes;         /* (dof,3)   */
+  const double* origin_rot;   /* (dof,3,3) */
+  const double* origin_trans; /* (dof,3)   */
+  const int64_t* jtype;       /* (dof,) 0 revolute, 1 prismatic */
+  const double* joint_limits; /* (dof,2)   */
+  const double* velocity_limits; /* (dof,) */
+  const double* accel_limits; /* (dof,)    */
+  const double* cap_p0;       /* (n_caps,3) */
+  const double* cap_p1;       /* (n_caps,3) */
+  const double* cap_r;        /* (n_caps,)  */
+  const int64_t* cap_link;    /* (n_caps,)  */
+  const int64_t* pair_a;      /* (n_pairs,) */
+  const int64_t* pair_b;      /* (n_pairs,) */
+} mppi_chain_desc;
+
+/* CostWeights (costs.py:27-53) + the provider kind. */
+typedef struct mppi_cost_desc {
+  double alpha_rot[3];
+  double alpha_trans[3];
+  double alpha_stop;
+  double alpha_joint;
+  double alpha_manip;
+  double alpha_coll;
+  double k_jl;
+  double k_m;
+  int32_t self_collision;     /* enum mppi_self_collision */
+  int32_t _pad;
+} mppi_cost_desc;
+
+/* Controller kwargs (controller.py:98-129) in resolved form. */
+typedef struct mppi_plan_desc {
+  int32_t horizon;            /* H <= MPPI_MAX_HORIZON                      */
+  int32_t particles;          /* particles held by THIS plan (per instance) */
+  int32_t null_count;
+  int32_t instances;          /* B independent controllers (config 4)       */
+  int32_t iterations;         /* K optimisation iterations per step         */
+  int32_t policy_mode;        /* enum mppi_policy_mode                      */
+  int32_t precision;          /* enum mppi_precision (fused rollout)        */
+  int32_t generator;          /* enum mppi_generator                        */
+  int32_t smoothing;          /* enum mppi_smoothing                        */
+  int32_t spline_degree;
+  int32_t knots;              /* K knot slots (SmoothingSpec.knot_count)    */
+  int32_t device;             /* CUDA ordinal                               */
+  int32_t particle_offset;    /* particle sharding (config 5): this plan     */
+  int32_t particles_total;    /*   holds global rows [offset, offset+N)     */
+  int32_t dump;               /* 1: every step also writes instance 0's
+                                 rollout bundle to device (mppi_get_bundle) */
+  int32_t _pad0;
+  uint64_t seed;             /* Philox key for the pseudorandom generator  */
+  double comb[3];
+  double gamma;
+  double terminal_weight;
+  double beta;
+  double alpha_mu;
+  double alpha_sigma;
+  double sigma0_sq;           /* initial + tail variance                   */
+  double sigma_sq_min;
+  double sigma_sq_max;        /* already resolved: 0 in the kwargs -> sigma0_sq */
+  double default_tail;
+  const double* dts;          /* (horizon,) DtSchedule.dts                  */
+} mppi_plan_desc;
+
+/* Per-instance result of one control step (StepDiagnostics, controller.py:81-90). */
+typedef struct mppi_step_info {
+  int32_t status;             /* enum mppi_status of this instance           */
+  int32_t bad_particle;       /* first non-finite particle, or -1            */
+  int32_t finite_count;
+  int32_t _pad;
+  double best_cost;           /* min finite total                            */
+  double mean_cost;           /* mean finite total                           */
+  double device_ms;           /* CUDA-event time of the step on the stream   */
+} mppi_step_info;
+
+/* Outputs of mppi_evaluate (RolloutBundle, rollout.py:84-91). Any pointer may
+ * be NULL to skip that output. Shapes use n particles x H steps x dof. */
+typedef struct mppi_eval_out {
+  double* positions;          /* (n,H,d) */
+  double* velocities;         /* (n,H,d) */
+  double* accelerations;      /* (n,H,d) the controls as integrated         */
+  double* step_costs;         /* (n,H)   quarantined rows zeroed            */
+  double* terms;              /* (6,n,H) pose, stop, joint, manip, selfcoll, envcoll */
+  double* totals;             /* (n,)    +inf for quarantined rows          */
+  int32_t bad_particle;       /* out: first non-finite control row, or -1   */
+  int32_t quarantined;        /* out: number of quarantined rows            */
+} mppi_eval_out;
+
+typedef struct mppi_plan mppi_plan;
+
+/* ---- library ---------------------------------------------------------- */
+int32_t mppi_abi_version(void);
+const char* mppi_last_error(void);
+const char* mppi_build_info(void);          /* arch, nvcc, flags             */
+int mppi_device_count(int32_t* count);
+
+/* ---- plan lifecycle --------------------------------------------------- */
+int mppi_plan_create(const mppi_chain_desc* chain, const mppi_cost_desc* costs,
+                     const mppi_plan_desc* desc, mppi_plan** out);
+int mppi_plan_destroy(mppi_plan* plan);
+
+/* Build the Halton set on the device (FP64, bit-exact radical inverse),
+ * Acklam ICDF, smoothing with the given (H,K) basis, then subtract the batch
+ * mean over particles_total rows. basis may be NULL for comb / none. */
+int mppi_init_noise(mppi_plan* plan, const double* basis /* (H,K) */);
+int mppi_set_noise(mppi_plan* plan, const double* eps /* (N,H,d) host */);
+int mppi_get_noise(mppi_plan* plan, double* eps /* (N,H,d) host */);
+
+int mppi_set_goal(mppi_plan* plan, int32_t instance /* -1: all */,
+                  const double* rotation /* (3,3) */, const double* translation /* (3,) */,
+                  int32_t mode);
+int mppi_set_world(mppi_plan* plan, const double* spheres, int32_t n_spheres,
+                   const double* boxes, int32_t n_boxes);
+/* Occupancy grid (nx,ny,nz) uint8, voxel (i,j,k) covers
+ * origin + [i,i+1)*voxel ... ; narrow phase against boxes (nb,6) that tile
+ * exactly the occupied set (NULL: decomposed on the host from the grid). */
+int mppi_set_voxel_world(mppi_plan* plan, const uint8_t* occupancy, int32_t nx, int32_t ny,
+                         int32_t nz, const double* origin /* (3,) */, double voxel,
+                         const double* spheres, int32_t n_spheres);
+int mppi_set_mlp(mppi_plan* plan, int32_t in_dim,
+                 const double* W0, const double* b0, const double* W1, const double* b1,
+                 const double* W2, const double* b2, const double* W3, const double* b3);
+
+int mppi_set_policy(mppi_plan* plan, int32_t instance, const double* means /* (H,d) */,
+                    const double* variances /* (H,d) */);
+int mppi_get_policy(mppi_plan* plan, int32_t instance, double* means, double* variances);
+
+/* ---- the hot path ----------------------------------------------------- */
+/* One control step for all B instances: shift, K x (sample, rollout, costs,
+ * learned collision, weights, mean/covariance update), command = means[0].
+ * Host buffers; one H2D, one CUDA-graph replay, one D2H. theta/theta_dot are
+ * (B,d); command_out (B,d); info (B) or NULL. On a per-instance failure the
+ * policy of that instance is left shifted-but-not-updated (controller.py:200,
+ * 224) and info[b].status says why; the function itself returns MPPI_OK. */
+int mppi_step(mppi_plan* plan, const double* theta, const double* theta_dot,
+              double* command_out, mppi_step_info* info);
+
+/* Generic evaluation (evaluate_rollouts / CostStack.evaluate) on instance 0's
+ * goal/world. mode 0: integrate `controls` (n,H,d) from theta0/theta_dot0;
+ * mode 1: `controls` holds positions and `controls2` velocities (n,H,d), no
+ * integration (CostStack.evaluate). dts (H,), gamma, terminal weight as in
+ * rollout.py:111-121. Always FP64-exact inputs; arithmetic in the plan's
+ * precision. */
+int mppi_evaluate(mppi_plan* plan, int32_t mode, int32_t n, int32_t horizon,
+                  const double* dts, double gamma, double terminal_weight,
+                  const double* theta0, const double* theta_dot0,
+                  const double* controls, const double* controls2, mppi_eval_out* out);
+
+/* Instance 0's RolloutBundle of the last iteration of the last mppi_step
+ * (plan created with dump = 1), plus the particle weights (N,). */
+int mppi_get_bundle(mppi_plan* plan, mppi_eval_out* out, double* weights);
+
+/* ---- particle-sharded update (config 5) -------------------------------- */
+/* Size in doubles of one rank's statistics record for this plan. */
+int mppi_stats_record_len(mppi_plan* plan, int32_t* len);
+/* Run shift + sample + rollout + costs + local statistics for instance 0 into
+ * the device buffer `record_dev` (record_len doubles); theta/theta_dot host. */
+int mppi_stats_dev(mppi_plan* plan, const double* theta, const double* theta_dot,
+                   void* record_dev, void* stream);
+/* Combine `n_records` records (device, contiguous, rank order) and apply the
+ * update; command/info as in mppi_step (instance 0). */
+int mppi_finalize_dev(mppi_plan* plan, const void* records_dev, int32_t n_records,
+                      double* command_out, mppi_step_info* info, void* stream);
+
+/* ---- stateless free functions (host in, host out) ---------------------- */
+int mppi_halton_points(int64_t count, int32_t dims, double* out /* (count,dims) */);
+int mppi_gaussianize(const double* p, int64_t n, double* out);
+/* Clamped uniform B-spline design matrix (bspline_basis, sampling.py:205-237). */
+int mppi_bspline_basis(int32_t horizon, int32_t k, int32_t degree, double* out /* (H,K) */);
+int mppi_smooth_sequences(const double* knots /* (N,K,d) */, int64_t n, int32_t k, int32_t d,
+                          int32_t mode, const double* basis /* (H,K) or NULL */,
+                          const double* comb /* (3,) */, int32_t horizon, double* out);
+int mppi_build_controls(const double* eps /* (N,H,d) */, const double* means /* (H,d) */,
+                        const double* stddev /* (H,d) */, int64_t n, int32_t h, int32_t d,
+                        int32_t null_count, double* out /* (N,H,d) */);
+int mppi_particle_weights(const double* totals, int64_t n, double beta, double* weights);
+/* weights + mean + covariance update (policy.py:103-155), one call.
+ * controls (N,H,d), weights (N,) ; means/variances in: the policy, out: updated.
+ * isotropic: variances are (H,). */
+int mppi_update_policy(const double* controls, const double* weights, int64_t n, int32_t h,
+                       int32_t d, int32_t policy_mode, double alpha_mu, double alpha_sigma,
+                       double sigma_sq_min, double sigma_sq_max, int32_t do_mean,
+                       int32_t do_cov, double* means, double* variances);
+int mppi_mlp_forward(mppi_plan* plan, const double* q /* (M,d) */, int64_t m,
+                     double* out /* (M,) */);
+
+/* ---- the reference operator seam (kernels/__init__.py) ------------------ */
+int mppi_fk_batch(const double* q, int64_t m, int32_t d, const double* axes,
+                  const double* origin_rot, const double* origin_trans, const int64_t* jtype,
+                  double* rot_out /* (m,d,3,3) */, double* trans_out /* (m,d,3) */);
+int mppi_jacobian_batch(const double* q, int64_t m, int32_t d, const double* rot,
+                        const double* trans, const double* axes, const int64_t* jtype,
+                        double* jac_out /* (m,6,d) */);
+int mppi_manip_batch(const double* jac, int64_t m, int32_t d, int32_t task_dim,
+                     double* out /* (m,) */);
+int mppi_self_collision_batch(const double* rot, const double* trans, int64_t m, int32_t d,
+                              const double* cap_p0, const double* cap_p1, const double* cap_r,
+                              const int64_t* cap_link, int32_t n_caps, const int64_t* pair_a,
+                              const int64_t* pair_b, int32_t n_pairs, double* out /* (m,) */);
+int mppi_env_collision_batch(const double* rot, const double* trans, int64_t m, int32_t d,
+                             const double* cap_p0, const double* cap_p1, const double* cap_r,
+                             const int64_t* cap_link, int32_t n_caps, const double* spheres,
+                             int32_t n_spheres, const double* boxes, int32_t n_boxes,
+                             int64_t* hit_out /* (m,) */);
+int mppi_integrate_batch(const double* u, int64_t n, int32_t h, int32_t d, const double* dts,
+                         const double* th0, const double* thd0, double* pos_out,
+                         double* vel_out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MPPI_B200_H */

@@ -1,0 +1,73 @@
+"""The BASELINE.json workloads as plain data.
+
+Config 1/2 are reach_arm7.toml (fixtures/reach_arm7.toml:1-49) at N=500:
+full-pose goal, alpha_p = [[30]*3, [150]*3] (rotation, translation — the
+harness mapping, harness.py:66), beta 1, alpha_mu 0.9, alpha_sigma 0.5,
+sigma0^2 0.5, sigma_min^2 0.01, Halton + cubic B-spline, 2 null rows,
+H = 30, dt 0.05 two_phase, gamma 0.99.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+REACH_START = np.array([0.0, -0.5, 0.0, -1.8, 0.0, 1.4, 0.0])
+REACH_GOAL_POS = np.array([-0.13, -0.109, 0.864])
+REACH_GOAL_RPY = (0.108, 0.489, 0.927)
+
+CONTROLLER_KW = dict(
+    horizon=30, particles=500, dt_base=0.05, dt_ramp="two_phase", gamma=0.99, terminal_weight=1.0,
+    null_count=2, beta=1.0, alpha_mu=0.9, alpha_sigma=0.5, sigma0_sq=0.5, sigma_sq_min=0.01,
+    sigma_sq_max=0.0, seed=0,
+)
+
+WEIGHTS = {
+    # config 1: goal pose + joint limits only
+    1: dict(alpha_rot=30.0, alpha_trans=150.0, alpha_stop=0.0, alpha_joint=100.0, alpha_manip=0.0,
+            alpha_coll=0.0),
+    # config 2: full stack with the learned self-collision MLP
+    2: dict(alpha_rot=30.0, alpha_trans=150.0, alpha_stop=50.0, alpha_joint=100.0, alpha_manip=30.0,
+            alpha_coll=1000.0),
+    # config 3: pose (position only, moving target) + joint + stop + world collision
+    3: dict(alpha_rot=30.0, alpha_trans=150.0, alpha_stop=50.0, alpha_joint=100.0, alpha_manip=0.0,
+            alpha_coll=1000.0),
+}
+
+
+def reach_goal_rotation() -> np.ndarray:
+    from .kinematics import rpy_matrix
+
+    return rpy_matrix(*REACH_GOAL_RPY)
+
+
+def make_weights(config: int):
+    from .costs import CostWeights
+
+    return CostWeights(**WEIGHTS[config])
+
+
+def make_goal(config: int):
+    from .costs import FULL_POSE, GoalSpec
+    from .kinematics import Pose
+
+    return GoalSpec(target_pose=Pose(rotation=reach_goal_rotation(), translation=REACH_GOAL_POS.copy()),
+                    mode=FULL_POSE)
+
+
+def make_controller(config: int = 2, **overrides):
+    """A Controller for BASELINE config 1 or 2 (arm7, 500 x 30)."""
+    from .controller import Controller
+    from .kinematics import load_chain
+    from .surrogate import load_arm7_surrogate
+
+    kw = dict(CONTROLLER_KW)
+    kw.update(overrides)
+    provider = load_arm7_surrogate() if config == 2 else None
+    return Controller(load_chain("arm7.chain"), make_goal(config), weights=make_weights(config),
+                      self_collision=provider, **kw)
+
+
+def start_state():
+    from .rollout import JointState
+
+    return JointState(theta=REACH_START.copy(), theta_dot=np.zeros(7), theta_ddot=np.zeros(7))

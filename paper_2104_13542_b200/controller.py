@@ -1,0 +1,255 @@
+"""Receding-horizon control loop on the B200 (jointmpc/controller.py:93-269).
+
+``Controller.control_step`` is the drop-in for the reference's hot path. One
+call = one H2D of the joint state, one CUDA-graph replay of
+[shift, K x (sample, rollout + cost stack, learned collision, weights,
+mean/covariance update)], one D2H of the command and status. The policy lives
+on the device; ``controller.policy`` reads it back on access.
+
+Differences from the reference, by design:
+  * ``workers`` is accepted and ignored (particles map to warps, not threads);
+  * ``diag.bundle`` is a lazily fetched view of the last iteration's device
+    dump (pass ``keep_bundle=True`` to have the graph write it);
+  * per-stage times are device event times of the whole step.
+"""
+
+from __future__ import annotations
+
+import logging
+import time
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native as N
+from .costs import CostStack, CostWeights, GoalSpec
+from .engine import Plan, PlanSpec
+from .errors import ContractError, PolicyStateError
+from .kinematics import KinematicChain
+from .policy import ISOTROPIC, PER_JOINT, PolicyParams, UpdateConfig
+from .rollout import DtSchedule, JointState, RolloutBundle, make_dt_schedule
+from .sampling import HALTON, PSEUDORANDOM, SmoothingSpec, smoothing_code
+
+log = logging.getLogger(__name__)
+
+
+@dataclass
+class StepDiagnostics:
+    latency_ms: float
+    sample_ms: float
+    rollout_ms: float
+    update_ms: float
+    best_cost: float
+    mean_cost: float
+    fallback: str = ""  # "", "reissue", "brake"
+    bundle: object = None
+
+
+class Controller:
+    """Owns the device policy, the perturbation block and the cost stack.
+    Single-threaded by contract (controller.py:93-96)."""
+
+    def __init__(
+        self,
+        chain: KinematicChain,
+        goal: GoalSpec,
+        *,
+        horizon: int = 30,
+        particles: int = 200,
+        dt_base: float = 0.05,
+        dt_ramp: str = "two_phase",
+        gamma: float = 0.99,
+        workers: int = 1,
+        terminal_weight: float = 1.0,
+        generator: str = HALTON,
+        smoothing: SmoothingSpec | None = None,
+        null_count: int = 2,
+        weights: CostWeights | None = None,
+        world=None,
+        self_collision=None,
+        beta: float = 0.5,
+        alpha_mu: float = 0.9,
+        alpha_sigma: float = 0.5,
+        sigma0_sq: float = 1.0,
+        sigma_sq_min: float = 1e-4,
+        sigma_sq_max: float = 0.0,
+        policy_mode: str = PER_JOINT,
+        command_mode: str = "mean",
+        iterations: int = 1,
+        control_period: float = 0.05,
+        latency_budget: float = 0.05,
+        filter_lambda: float = 0.3,
+        seed: int = 0,
+        precision: str = "fp32",
+        device: int = 0,
+        keep_bundle: bool = False,
+    ):
+        if particles <= null_count + 1:
+            raise ContractError("need more particles than reserved sequences")
+        if generator not in (HALTON, PSEUDORANDOM):
+            raise ContractError(f"unknown generator {generator!r}")
+        if control_period <= 0.0:
+            raise ContractError("control_period must be positive")
+        if command_mode not in ("mean", "sample"):
+            raise ContractError(f"unknown command mode {command_mode!r}")
+        if policy_mode not in (ISOTROPIC, PER_JOINT):
+            raise ContractError(f"unknown policy mode {policy_mode!r}")
+        if precision not in ("fp32", "fp64"):
+            raise ContractError(f"unknown precision {precision!r}")
+        self.chain = chain
+        self.generator = generator
+        self.smoothing = smoothing or SmoothingSpec()
+        self.particles = particles
+        self.null_count = null_count
+        self.horizon = horizon
+        self.workers = workers
+        self.terminal_weight = terminal_weight
+        self.command_mode = command_mode
+        self.iterations = max(1, iterations)
+        self.control_period = control_period
+        self.latency_budget = latency_budget
+        self.filter_lambda = filter_lambda
+        self.policy_mode = policy_mode
+        self.sched = make_dt_schedule(horizon, dt_base, dt_ramp)
+        self.update_cfg = UpdateConfig(
+            beta=beta, alpha_mu=alpha_mu, alpha_sigma=alpha_sigma, gamma=gamma,
+            sigma_sq_min=sigma_sq_min,
+            sigma_sq_max=sigma_sq_max if sigma_sq_max > 0.0 else sigma0_sq,
+        )
+        self.sigma0_sq = sigma0_sq
+        self.cost_stack = CostStack(chain=chain, weights=weights or CostWeights(), goal=goal,
+                                    world=world, self_collision=self_collision)
+        self.rng = np.random.default_rng(seed)
+        self._knots = self.smoothing.knot_count(horizon)
+        spec = PlanSpec(
+            horizon=horizon, particles=particles, dts=self.sched.dts, null_count=null_count,
+            instances=1, iterations=self.iterations,
+            policy_mode=N.POLICY_ISOTROPIC if policy_mode == ISOTROPIC else N.POLICY_PER_JOINT,
+            precision=N.FP64 if precision == "fp64" else N.FP32,
+            generator=N.GEN_HALTON if generator == HALTON else N.GEN_PSEUDORANDOM,
+            smoothing=smoothing_code(self.smoothing), spline_degree=self.smoothing.spline_degree,
+            knots=self._knots, device=device, particles_total=particles, seed=seed,
+            comb=tuple(self.smoothing.comb_coeffs), gamma=gamma, terminal_weight=terminal_weight,
+            beta=beta, alpha_mu=alpha_mu, alpha_sigma=alpha_sigma, sigma0_sq=sigma0_sq,
+            sigma_sq_min=self.update_cfg.sigma_sq_min, sigma_sq_max=self.update_cfg.sigma_sq_max,
+            default_tail=self.update_cfg.default_tail, dump=int(keep_bundle),
+        )
+        world_arg = world if (world is not None and getattr(world, "obstacle_count", 0)) else None
+        self._plan = Plan(chain, self.cost_stack.weights, spec, provider=self.cost_stack.self_collision,
+                          world=world_arg)
+        if generator == HALTON:
+            self._plan.init_noise()
+        self._goal_uploaded = None
+        self._sync_goal()
+        self._prev_command = np.zeros(chain.dof)
+        self._fallback_armed = False
+        self._step_serial = 0
+        self.keep_bundle = keep_bundle
+
+    # ---------------------------------------------------------------- state
+    @property
+    def plan(self) -> Plan:
+        return self._plan
+
+    @property
+    def policy(self) -> PolicyParams:
+        means, var = self._plan.get_policy(0)
+        if self.policy_mode == ISOTROPIC:
+            var = var[:, 0].copy()
+        return PolicyParams(means=means, variances=var, mode=self.policy_mode, tail_variance=self.sigma0_sq)
+
+    @policy.setter
+    def policy(self, pol: PolicyParams):
+        self._plan.set_policy(pol.means, pol.variances, 0)
+
+    @property
+    def _fixed_eps(self):
+        """The centred Halton block (controller.py:166-176), read back from the device."""
+        return self._plan.get_noise() if self.generator == HALTON else None
+
+    def set_goal(self, goal: GoalSpec):
+        self.cost_stack.goal = goal
+        self._sync_goal()
+
+    def set_perturbations(self, eps):
+        """Overwrite the device perturbation block (the parity hook for
+        Controller._perturbations, controller.py:192-196)."""
+        self._plan.set_noise(eps)
+
+    def _sync_goal(self):
+        g = self.cost_stack.goal
+        key = (id(g), g.mode, g.target_pose.rotation.tobytes(), g.target_pose.translation.tobytes())
+        if key != self._goal_uploaded:
+            self._plan.set_goal(g.target_pose.rotation, g.target_pose.translation, g.mode_code, 0)
+            self._goal_uploaded = key
+
+    # ---------------------------------------------------------------- hot path
+    def control_step(self, state: JointState) -> tuple[np.ndarray, StepDiagnostics]:
+        t_start = time.perf_counter()
+        self._sync_goal()
+        cmds, infos = self._plan.step(state.theta[None, :], state.theta_dot[None, :])
+        info = infos[0]
+        self._step_serial += 1
+        if info.status != N.OK:
+            exc = N.status_exception(info.status, info.bad_particle)
+            if not isinstance(exc, (PolicyStateError, ContractError)):
+                raise exc
+            if not self._fallback_armed:
+                self._fallback_armed = True
+                command, mode = self._prev_command.copy(), "reissue"
+            else:
+                command, mode = np.zeros(self.chain.dof), "brake"
+            log.warning("control step failed (%s); falling back to %s", exc, mode)
+            latency = (time.perf_counter() - t_start) * 1e3
+            return command, StepDiagnostics(latency_ms=latency, sample_ms=0.0, rollout_ms=info.device_ms,
+                                            update_ms=0.0, best_cost=float("nan"),
+                                            mean_cost=float("nan"), fallback=mode)
+        self._fallback_armed = False
+        if self.command_mode == "mean":
+            command = cmds[0]
+        else:  # host rng, as next_command(policy, "sample", rng) (policy.py:174-176)
+            pol = self.policy
+            command = self.rng.normal(pol.means[0], pol.stddev()[0])
+        self._prev_command = command.copy()
+        latency = (time.perf_counter() - t_start) * 1e3
+        if latency > self.latency_budget * 1e3:
+            log.debug("control step overran budget: %.2f ms", latency)
+        bundle = LazyBundle(self, self._step_serial) if self.keep_bundle else None
+        return command, StepDiagnostics(latency_ms=latency, sample_ms=0.0, rollout_ms=info.device_ms,
+                                        update_ms=0.0, best_cost=float(info.best_cost),
+                                        mean_cost=float(info.mean_cost), bundle=bundle)
+
+    def instantaneous_costs(self, state: JointState):
+        """Per-term costs of one plant state with the h=0 braking limit (controller.py:262-269)."""
+        one = DtSchedule(dts=np.array([self.sched.dts.sum()]))
+        step, terms = self.cost_stack.evaluate(state.theta[None, None, :], state.theta_dot[None, None, :], one)
+        return float(step[0, 0]), {k: float(v[0, 0]) for k, v in terms.items()}
+
+
+class LazyBundle:
+    """RolloutBundle of the last iteration of one step, fetched from the device
+    on first attribute access. Valid until the controller's next step."""
+
+    _FIELDS = ("positions", "velocities", "accelerations", "step_costs", "term_breakdown",
+               "total_per_particle", "weights")
+
+    def __init__(self, ctrl: Controller, serial: int):
+        self._ctrl = ctrl
+        self._serial = serial
+        self._data = None
+
+    def _load(self):
+        if self._data is None:
+            if self._ctrl._step_serial != self._serial:
+                raise ContractError("bundle expired: the controller has stepped since")
+            self._data = self._ctrl._plan.get_bundle()
+        return self._data
+
+    def __getattr__(self, name):
+        if name.startswith("_") or name not in self._FIELDS:
+            raise AttributeError(name)
+        return self._load()[name]
+
+    def materialize(self) -> RolloutBundle:
+        d = self._load()
+        return RolloutBundle(**{k: d[k] for k in self._FIELDS if k != "weights"})

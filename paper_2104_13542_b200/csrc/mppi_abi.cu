@@ -1,0 +1,1359 @@
+// mppi_abi.cu — the C ABI (include/mppi_b200.h): plans, CUDA-graph step,
+// evaluation, the particle-sharded update and the stateless seam functions.
+//
+// Build (see __graft_entry__.build):
+//   nvcc -shared -Xcompiler -fPIC -O3 -lineinfo -std=c++17
+//        -gencode arch=compute_100a,code=sm_100a csrc/*.cu -o _mppi_b200.so
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "mppi_aux_kernels.cuh"
+#include "mppi_launch.cuh"
+#include "mppi_mlp.cuh"
+
+using namespace mppi;
+
+// ------------------------------------------------------------------ errors
+static thread_local std::string g_last_error;
+
+static int fail(int code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+
+#define CK(call)                                                                              \
+  do {                                                                                        \
+    cudaError_t _e = (call);                                                                  \
+    if (_e != cudaSuccess)                                                                    \
+      return fail(MPPI_E_CUDA, std::string(#call " failed: ") + cudaGetErrorString(_e) +       \
+                                   " (" __FILE__ ":" + std::to_string(__LINE__) + ")");       \
+  } while (0)
+
+#define CKR(expr)              \
+  do {                         \
+    int _rc = (expr);          \
+    if (_rc != MPPI_OK) return _rc; \
+  } while (0)
+
+namespace {
+
+inline unsigned grid_for(long long n, int threads, int cap = 148 * 16) {
+  long long g = (n + threads - 1) / threads;
+  if (g < 1) g = 1;
+  if (g > cap) g = cap;
+  return (unsigned)g;
+}
+
+template <typename T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  int alloc(size_t count) {
+    if (count <= n && p) return MPPI_OK;
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+    if (count == 0) return MPPI_OK;
+    CK(cudaMalloc(&p, count * sizeof(T)));
+    n = count;
+    return MPPI_OK;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+};
+
+struct HostChain {
+  int dof = 0, task_dim = 3, n_caps = 0, n_pairs = 0;
+  std::vector<double> axes, orot, otrans, limits, vel, acc, p0, p1, r;
+  std::vector<long long> jtype, link, pa, pb;
+};
+
+template <typename R>
+void fill_chain(const HostChain& c, double k_jl, ChainT<R>& o) {
+  memset(&o, 0, sizeof(o));
+  o.dof = c.dof;
+  o.task_dim = c.task_dim;
+  o.n_caps = c.n_caps;
+  o.n_pairs = c.n_pairs;
+  for (int k = 0; k < c.dof; ++k) {
+    o.jtype[k] = (int)c.jtype[k];
+    for (int i = 0; i < 3; ++i) o.axes[k][i] = (R)c.axes[3 * k + i];
+    for (int i = 0; i < 9; ++i) o.orot[k][i] = (R)c.orot[9 * k + i];
+    for (int i = 0; i < 3; ++i) o.otrans[k][i] = (R)c.otrans[3 * k + i];
+    const double lo = c.limits[2 * k], hi = c.limits[2 * k + 1], span = hi - lo;
+    o.lo[k] = (R)(lo + k_jl * span);  // shrunken_limits, costs.py:111-116
+    o.hi[k] = (R)(hi - k_jl * span);
+    o.accel[k] = (R)c.acc[k];
+  }
+  for (int i = 0; i < c.n_caps; ++i) {
+    o.cap_link[i] = (int)c.link[i];
+    o.cap_r[i] = (R)c.r[i];
+    for (int t = 0; t < 3; ++t) {
+      o.cap_p0[i][t] = (R)c.p0[3 * i + t];
+      o.cap_p1[i][t] = (R)c.p1[3 * i + t];
+    }
+  }
+  for (int i = 0; i < c.n_pairs; ++i) {
+    o.pair_a[i] = (int)c.pa[i];
+    o.pair_b[i] = (int)c.pb[i];
+  }
+}
+
+template <typename R>
+void fill_cost(const mppi_cost_desc& w, int has_pairs, int has_world, CostT<R>& o) {
+  memset(&o, 0, sizeof(o));
+  for (int i = 0; i < 3; ++i) {
+    o.alpha_rot[i] = (R)w.alpha_rot[i];
+    o.alpha_trans[i] = (R)w.alpha_trans[i];
+  }
+  o.a_stop = (R)w.alpha_stop;
+  o.a_joint = (R)w.alpha_joint;
+  o.a_manip = (R)w.alpha_manip;
+  o.a_coll = (R)w.alpha_coll;
+  o.k_m = (R)w.k_m;
+  o.use_stop = w.alpha_stop > 0.0;
+  o.use_joint = w.alpha_joint > 0.0;
+  o.use_manip = w.alpha_manip > 0.0;
+  int sc = w.self_collision;
+  if (sc == MPPI_SELFCOLL_ORACLE && !has_pairs) sc = MPPI_SELFCOLL_ORACLE;  // NO_CONTACT -> 0
+  o.selfcoll = w.alpha_coll > 0.0 ? sc : MPPI_SELFCOLL_NONE;
+  o.use_env = (w.alpha_coll > 0.0) && has_world;
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ the plan
+struct mppi_plan {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  int D = 0, H = 0, N = 0, B = 1, Kn = 0, iters = 1, null_count = 0, policy_mode = 0;
+  int precision = 0, generator = 0, smoothing = 0, degree = 3, offset = 0, Ntot = 0;
+  uint64_t seed = 0;
+  double comb[3] = {0.3, 0.4, 0.3};
+  double gamma = 0.99, tw = 1.0, beta = 0.5, alpha_mu = 0.9, alpha_sigma = 0.5, sigma0_sq = 1.0,
+         smin = 1e-4, smax = 1.0, tail = 0.0;
+  std::vector<double> dts;
+  HostChain chain;
+  mppi_cost_desc costs{};
+  ChainT<float> chf;
+  ChainT<double> chd;
+  // world
+  int ns = 0, nb = 0;
+  DevBuf<double> sph_d, box_d;
+  DevBuf<float> sph_f, box_f;
+  DevBuf<float> clearance;
+  int gx = 0, gy = 0, gz = 0;
+  double gorigin[3] = {0, 0, 0}, gvoxel = 0.0;
+  // learned collision
+  bool mlp_ready = false;
+  MlpWeights mlp;
+  // device state
+  DevBuf<double> eps, z, basis, colmean;
+  DevBuf<double> means, var, sd, prev_means, prev_sd, goal, state;
+  DevBuf<unsigned char> stepbuf;  // R-typed step costs
+  DevBuf<float> mlp_x, mlp_d;
+  DevBuf<double> totals, records, out_record, cmd, counters_pad;
+  DevBuf<unsigned> counters;
+  DevBuf<int> status, bad;
+  DevBuf<mppi_step_info> info;
+  DevBuf<unsigned long long> stepctr;
+  int nblk = 1, ppb = 64;
+  int dump = 0;  // bundle dumps for instance 0
+  DevBuf<double> d_pos, d_vel, d_acc, d_terms, d_step, d_w;
+  // pinned staging
+  double* h_state = nullptr;          // (B,2D) + step counter slot
+  unsigned long long* h_ctr = nullptr;
+  double* h_cmd = nullptr;            // (B,D)
+  mppi_step_info* h_info = nullptr;   // (B)
+  std::vector<double> goal_host;
+  // graph
+  cudaGraphExec_t graph = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  unsigned long long step_counter = 0;
+  int sharded_iter = 0;
+  // eval scratch
+  DevBuf<double> e_in0, e_in1, e_pos, e_vel, e_acc, e_terms, e_step, e_tot, e_state, e_dts;
+  DevBuf<unsigned char> e_stepbuf;
+  DevBuf<float> e_x, e_d;
+  DevBuf<int> e_status;
+  DevBuf<double> e_records;
+  DevBuf<unsigned> e_counters;
+
+  bool learned() const {
+    return costs.self_collision == MPPI_SELFCOLL_LEARNED && costs.alpha_coll > 0.0;
+  }
+};
+
+namespace {
+
+int set_device(mppi_plan* p) {
+  CK(cudaSetDevice(p->device));
+  return MPPI_OK;
+}
+
+void invalidate_graph(mppi_plan* p) {
+  if (p->graph) cudaGraphExecDestroy(p->graph);
+  p->graph = nullptr;
+}
+
+template <typename R>
+WorldT<R> world_of(mppi_plan* p) {
+  WorldT<R> w{};
+  if constexpr (sizeof(R) == 4) {
+    w.spheres = p->sph_f.p;
+    w.boxes = p->box_f.p;
+  } else {
+    w.spheres = p->sph_d.p;
+    w.boxes = p->box_d.p;
+  }
+  w.ns = p->ns;
+  w.nb = p->nb;
+  w.sdf = p->clearance.p;
+  w.nx = p->gx;
+  w.ny = p->gy;
+  w.nz = p->gz;
+  w.ox = (R)p->gorigin[0];
+  w.oy = (R)p->gorigin[1];
+  w.oz = (R)p->gorigin[2];
+  w.voxel = (R)p->gvoxel;
+  return w;
+}
+
+// Build the static part of the rollout arguments for horizon H and dt schedule.
+template <typename R>
+void rollout_static(mppi_plan* p, int H, const double* dts, RolloutArgs<R>& a) {
+  memset(&a, 0, sizeof(a));
+  fill_chain(p->chain, p->costs.k_jl, a.chain);
+  fill_cost(p->costs, p->chain.n_pairs > 0, (p->ns + p->nb) > 0, a.cost);
+  a.world = world_of<R>(p);
+  double rem = 0.0;
+  std::vector<double> remaining(H);
+  for (int h = H - 1; h >= 0; --h) {  // np.cumsum(dts[::-1])[::-1]
+    rem += dts[h];
+    remaining[h] = rem;
+  }
+  for (int h = 0; h < H; ++h) {
+    a.dts[h] = (R)dts[h];
+    a.remaining[h] = (R)remaining[h];
+  }
+  a.H = H;
+}
+
+template <typename R>
+void stats_static(mppi_plan* p, int H, double gamma, double tw, StatsArgs<R>& s) {
+  memset(&s, 0, sizeof(s));
+  s.H = H;
+  s.D = p->D;
+  s.beta = p->beta;
+  s.alpha_mu = p->alpha_mu;
+  s.alpha_sigma = p->alpha_sigma;
+  s.smin = p->smin;
+  s.smax = p->smax;
+  s.a_coll = p->costs.alpha_coll;
+  s.isotropic = p->policy_mode == MPPI_POLICY_ISOTROPIC;
+  s.tail_mean = p->tail;
+  s.tail_var = p->sigma0_sq;
+  s.tail_sd = std::sqrt(p->sigma0_sq);
+  for (int h = 0; h < H; ++h) s.disc[h] = std::pow(gamma, (double)h);  // gamma ** arange(H)
+  s.dlast = s.disc[H - 1] * tw;
+  s.learned = p->learned() ? 1 : 0;
+}
+
+void choose_blocks(int N, int& ppb, int& nblk) {
+  // >= 64 particles per block, at most 2 blocks per SM per instance-wave
+  ppb = 64;
+  nblk = (N + ppb - 1) / ppb;
+  if (nblk > 296) {
+    nblk = 296;
+    ppb = (N + nblk - 1) / nblk;
+    nblk = (N + ppb - 1) / ppb;
+  }
+}
+
+// Enqueue one optimisation iteration (rollout -> [MLP] -> statistics) for all
+// B instances. `inline_final` false writes the rank record instead.
+template <typename R>
+int enqueue_iteration(mppi_plan* p, int it, bool inline_final, double* out_record, cudaStream_t st) {
+  RolloutArgs<R> a;
+  rollout_static<R>(p, p->H, p->dts.data(), a);
+  a.N = p->N;
+  a.B = p->B;
+  a.null_count = p->null_count;
+  a.particle_offset = p->offset;
+  a.mode = 0;
+  a.shift = it == 0;
+  a.check_var = 1;
+  a.skip_on_status = 1;
+  a.tail_mean = p->tail;
+  a.tail_sd = std::sqrt(p->sigma0_sq);
+  a.eps = p->eps.p;
+  a.means = p->means.p;
+  a.sd = p->sd.p;
+  a.state = p->state.p;
+  a.goal = p->goal.p;
+  a.step = reinterpret_cast<R*>(p->stepbuf.p);
+  a.mlp_x = p->learned() ? p->mlp_x.p : nullptr;
+  a.status = p->status.p;
+  a.bad = p->bad.p;
+  if (p->dump) {
+    a.out_pos = p->d_pos.p;
+    a.out_vel = p->d_vel.p;
+    a.out_acc = p->d_acc.p;
+    a.out_terms = p->d_terms.p;
+  }
+  CK(launch_rollout_any<R>(a, p->D, (long long)p->B * p->N, st));
+  if (p->learned()) CK(mlp_forward(p->mlp, p->mlp_x.p, (long long)p->B * p->N * p->H, p->mlp_d.p, st));
+  StatsArgs<R> s;
+  stats_static<R>(p, p->H, p->gamma, p->tw, s);
+  s.N = p->N;
+  s.B = p->B;
+  s.null_count = p->null_count;
+  s.particle_offset = p->offset;
+  s.ppb = p->ppb;
+  s.nblk = p->nblk;
+  s.shift = it == 0;
+  s.finalize_inline = inline_final;
+  s.step = reinterpret_cast<const R*>(p->stepbuf.p);
+  s.mlp_d = p->learned() ? p->mlp_d.p : nullptr;
+  s.eps = p->eps.p;
+  s.means = p->means.p;
+  s.var = p->var.p;
+  s.sd = p->sd.p;
+  s.prev_means = p->prev_means.p;
+  s.prev_sd = p->prev_sd.p;
+  s.totals = p->totals.p;
+  s.records = p->records.p;
+  s.out_record = out_record;
+  s.counters = p->counters.p;
+  s.status = p->status.p;
+  s.bad = p->bad.p;
+  s.cmd = p->cmd.p;
+  s.info = p->info.p;
+  if (p->dump) {
+    s.dump_step = p->d_step.p;
+    s.dump_terms = p->d_terms.p;
+    s.dump_weights = inline_final ? p->d_w.p : nullptr;
+  }
+  CK(launch_stats_any<R>(s, p->D, st));
+  return MPPI_OK;
+}
+
+int enqueue_sampling(mppi_plan* p, int it, cudaStream_t st) {
+  if (p->generator != MPPI_GEN_PSEUDORANDOM) return MPPI_OK;
+  // Philox counter = step * iterations + it; the step number is read from the
+  // device copy of the input block so the captured graph stays valid.
+  const long long rows = p->N;  // pseudorandom rows are local (no centring)
+  const long long nz = rows * p->Kn * p->D;
+  knots_ptr_kernel<<<grid_for(nz, 256), 256, 0, st>>>(p->z.p, rows, p->Kn, p->D, p->seed, p->stepctr.p,
+                                                      (unsigned long long)p->iters, it, p->offset,
+                                                      p->status.p);
+  CK(cudaGetLastError());
+  const long long ne = rows * p->H * p->D;
+  smooth_kernel<<<grid_for(ne, 256), 256, 0, st>>>(p->z.p, p->eps.p, rows, p->Kn, p->H, p->D,
+                                                   p->smoothing, p->basis.p, p->comb[0], p->comb[1],
+                                                   p->comb[2]);
+  CK(cudaGetLastError());
+  return MPPI_OK;
+}
+
+int enqueue_step_body(mppi_plan* p, cudaStream_t st) {
+  const int B = p->B, D = p->D;
+  CK(cudaMemsetAsync(p->status.p, 0, sizeof(int) * B, st));
+  CK(cudaMemsetAsync(p->bad.p, 0x7f, sizeof(int) * B, st));
+  CK(cudaMemcpyAsync(p->state.p, p->h_state, sizeof(double) * B * 2 * D, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(p->stepctr.p, p->h_ctr, sizeof(unsigned long long), cudaMemcpyHostToDevice, st));
+  for (int it = 0; it < p->iters; ++it) {
+    CKR(enqueue_sampling(p, it, st));
+    if (p->precision == MPPI_FP64)
+      CKR(enqueue_iteration<double>(p, it, true, nullptr, st));
+    else
+      CKR(enqueue_iteration<float>(p, it, true, nullptr, st));
+  }
+  CK(cudaMemcpyAsync(p->h_cmd, p->cmd.p, sizeof(double) * B * D, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(p->h_info, p->info.p, sizeof(mppi_step_info) * B, cudaMemcpyDeviceToHost, st));
+  return MPPI_OK;
+}
+
+int ensure_graph(mppi_plan* p) {
+  if (p->graph) return MPPI_OK;
+  if (p->learned() && !p->mlp_ready)
+    return fail(MPPI_E_CONFIG, "learned self-collision selected but mppi_set_mlp was not called");
+  cudaGraph_t g = nullptr;
+  CK(cudaStreamBeginCapture(p->stream, cudaStreamCaptureModeThreadLocal));
+  int rc = enqueue_step_body(p, p->stream);
+  cudaError_t e = cudaStreamEndCapture(p->stream, &g);
+  if (rc != MPPI_OK) {
+    if (g) cudaGraphDestroy(g);
+    return rc;
+  }
+  if (e != cudaSuccess) return fail(MPPI_E_CUDA, std::string("graph capture: ") + cudaGetErrorString(e));
+  e = cudaGraphInstantiate(&p->graph, g, 0);
+  cudaGraphDestroy(g);
+  if (e != cudaSuccess) return fail(MPPI_E_CUDA, std::string("graph instantiate: ") + cudaGetErrorString(e));
+  return MPPI_OK;
+}
+
+int copy_chain(const mppi_chain_desc* c, HostChain& h) {
+  if (!c || c->dof < 1 || c->dof > MPPI_MAX_DOF)
+    return fail(MPPI_E_CONFIG, "chain dof must lie in [1, " + std::to_string(MPPI_MAX_DOF) + "]");
+  if (c->n_caps < 0 || c->n_caps > MPPI_MAX_CAPSULES) return fail(MPPI_E_CONFIG, "too many capsules");
+  if (c->n_pairs < 0 || c->n_pairs > MPPI_MAX_PAIRS) return fail(MPPI_E_CONFIG, "too many pairs");
+  const int d = c->dof;
+  h.dof = d;
+  h.task_dim = c->task_dim;
+  h.n_caps = c->n_caps;
+  h.n_pairs = c->n_pairs;
+  h.axes.assign(c->axes, c->axes + 3 * d);
+  h.orot.assign(c->origin_rot, c->origin_rot + 9 * d);
+  h.otrans.assign(c->origin_trans, c->origin_trans + 3 * d);
+  h.jtype.assign(c->jtype, c->jtype + d);
+  h.limits.assign(c->joint_limits, c->joint_limits + 2 * d);
+  h.vel.assign(c->velocity_limits, c->velocity_limits + d);
+  h.acc.assign(c->accel_limits, c->accel_limits + d);
+  if (c->n_caps) {
+    h.p0.assign(c->cap_p0, c->cap_p0 + 3 * c->n_caps);
+    h.p1.assign(c->cap_p1, c->cap_p1 + 3 * c->n_caps);
+    h.r.assign(c->cap_r, c->cap_r + c->n_caps);
+    h.link.assign(c->cap_link, c->cap_link + c->n_caps);
+  }
+  if (c->n_pairs) {
+    h.pa.assign(c->pair_a, c->pair_a + c->n_pairs);
+    h.pb.assign(c->pair_b, c->pair_b + c->n_pairs);
+    for (int i = 0; i < c->n_pairs; ++i)
+      if (h.pa[i] < 0 || h.pa[i] >= c->n_caps || h.pb[i] < 0 || h.pb[i] >= c->n_caps)
+        return fail(MPPI_E_CONFIG, "self-collision pair indexes a missing capsule");
+  }
+  for (int i = 0; i < c->n_caps; ++i)
+    if (h.link[i] < 0 || h.link[i] >= d) return fail(MPPI_E_CONFIG, "capsule link out of range");
+  return MPPI_OK;
+}
+
+}  // namespace
+
+// ================================================================== C ABI
+extern "C" {
+
+int32_t mppi_abi_version(void) { return MPPI_ABI_VERSION; }
+
+const char* mppi_last_error(void) { return g_last_error.c_str(); }
+
+const char* mppi_build_info(void) {
+#define MPPI_STR2(x) #x
+#define MPPI_STR(x) MPPI_STR2(x)
+  return "mppi_b200 sm_100a (fused rollout, CUDA graph step); nvcc " MPPI_STR(__CUDACC_VER_MAJOR__) "." MPPI_STR(
+      __CUDACC_VER_MINOR__) "." MPPI_STR(__CUDACC_VER_BUILD__);
+}
+
+int mppi_device_count(int32_t* count) {
+  int c = 0;
+  CK(cudaGetDeviceCount(&c));
+  *count = c;
+  return MPPI_OK;
+}
+
+int mppi_plan_create(const mppi_chain_desc* chain, const mppi_cost_desc* costs,
+                     const mppi_plan_desc* desc, mppi_plan** out) {
+  if (!out || !desc || !costs) return fail(MPPI_E_BAD_ARGUMENT, "null argument");
+  *out = nullptr;
+  mppi_plan* p = new mppi_plan();
+  int rc = [&]() -> int {
+    CKR(copy_chain(chain, p->chain));
+    const mppi_plan_desc& d = *desc;
+    if (d.horizon < 2 || d.horizon > MPPI_MAX_HORIZON)
+      return fail(MPPI_E_CONFIG, "horizon must lie in [2, " + std::to_string(MPPI_MAX_HORIZON) + "]");
+    if (d.particles < 1) return fail(MPPI_E_CONFIG, "particles must be positive");
+    if (d.instances < 1) return fail(MPPI_E_CONFIG, "instances must be positive");
+    if (!d.dts) return fail(MPPI_E_BAD_ARGUMENT, "dts is null");
+    p->device = d.device;
+    CKR(set_device(p));
+    p->D = p->chain.dof;
+    p->H = d.horizon;
+    p->N = d.particles;
+    p->B = d.instances;
+    p->iters = std::max(1, d.iterations);
+    p->null_count = d.null_count;
+    p->policy_mode = d.policy_mode;
+    p->precision = d.precision;
+    p->generator = d.generator;
+    p->smoothing = d.smoothing;
+    p->degree = d.spline_degree;
+    p->Kn = d.knots > 0 ? d.knots : d.horizon;
+    p->offset = d.particle_offset;
+    p->Ntot = d.particles_total > 0 ? d.particles_total : d.particles;
+    p->seed = d.seed;
+    for (int i = 0; i < 3; ++i) p->comb[i] = d.comb[i];
+    p->gamma = d.gamma;
+    p->tw = d.terminal_weight;
+    p->beta = d.beta;
+    p->alpha_mu = d.alpha_mu;
+    p->alpha_sigma = d.alpha_sigma;
+    p->sigma0_sq = d.sigma0_sq;
+    p->smin = d.sigma_sq_min;
+    p->smax = d.sigma_sq_max;
+    p->tail = d.default_tail;
+    p->dts.assign(d.dts, d.dts + d.horizon);
+    p->costs = *costs;
+    p->dump = d.dump;
+    if (p->offset < 0 || p->offset + p->N > p->Ntot)
+      return fail(MPPI_E_CONFIG, "particle shard out of range");
+    CK(cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking));
+    CK(cudaEventCreate(&p->ev0));
+    CK(cudaEventCreate(&p->ev1));
+    const int B = p->B, D = p->D, H = p->H, N = p->N;
+    const size_t HD = (size_t)H * D;
+    choose_blocks(N, p->ppb, p->nblk);
+    const size_t rsz = p->precision == MPPI_FP64 ? sizeof(double) : sizeof(float);
+    const int reclen = kRecHead + 2 * (int)HD;
+    CKR(p->eps.alloc((size_t)N * HD));
+    CK(cudaMemset(p->eps.p, 0, sizeof(double) * N * HD));
+    CKR(p->means.alloc(B * HD));
+    CKR(p->var.alloc(B * HD));
+    CKR(p->sd.alloc(B * HD));
+    CKR(p->prev_means.alloc(B * HD));
+    CKR(p->prev_sd.alloc(B * HD));
+    CKR(p->goal.alloc((size_t)B * 16));
+    CKR(p->state.alloc((size_t)B * 2 * D));
+    CKR(p->stepbuf.alloc((size_t)B * N * H * rsz));
+    CKR(p->totals.alloc((size_t)B * N));
+    CKR(p->records.alloc((size_t)B * p->nblk * reclen));
+    CKR(p->out_record.alloc(reclen));
+    CKR(p->cmd.alloc((size_t)B * D));
+    CKR(p->counters.alloc(B));
+    CK(cudaMemset(p->counters.p, 0, sizeof(unsigned) * B));
+    CKR(p->status.alloc(B));
+    CKR(p->bad.alloc(B));
+    CK(cudaMemset(p->status.p, 0, sizeof(int) * B));
+    CK(cudaMemset(p->bad.p, 0x7f, sizeof(int) * B));
+    CKR(p->info.alloc(B));
+    CKR(p->stepctr.alloc(1));
+    if (p->dump) {
+      CKR(p->d_pos.alloc((size_t)N * HD));
+      CKR(p->d_vel.alloc((size_t)N * HD));
+      CKR(p->d_acc.alloc((size_t)N * HD));
+      CKR(p->d_terms.alloc((size_t)6 * N * H));
+      CK(cudaMemset(p->d_terms.p, 0, sizeof(double) * 6 * N * H));
+      CKR(p->d_step.alloc((size_t)N * H));
+      CKR(p->d_w.alloc((size_t)N));
+    }
+    if (p->learned()) {
+      const size_t rows = (size_t)B * N * H;
+      CKR(p->mlp_x.alloc(mlp_padded_rows(rows) * 16));
+      CK(cudaMemset(p->mlp_x.p, 0, sizeof(float) * mlp_padded_rows(rows) * 16));
+      CKR(p->mlp_d.alloc(mlp_padded_rows(rows)));
+    }
+    // policy: zero mean, sigma0^2 variance (make_policy, policy.py:88-95)
+    std::vector<double> z(B * HD, 0.0), v(B * HD, p->sigma0_sq), s(B * HD, std::sqrt(p->sigma0_sq));
+    CK(cudaMemcpy(p->means.p, z.data(), sizeof(double) * B * HD, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(p->var.p, v.data(), sizeof(double) * B * HD, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(p->sd.p, s.data(), sizeof(double) * B * HD, cudaMemcpyHostToDevice));
+    // identity goal at the origin, position_only
+    p->goal_host.assign((size_t)B * 16, 0.0);
+    for (int b = 0; b < B; ++b) {
+      p->goal_host[b * 16 + 0] = p->goal_host[b * 16 + 4] = p->goal_host[b * 16 + 8] = 1.0;
+    }
+    CK(cudaMemcpy(p->goal.p, p->goal_host.data(), sizeof(double) * B * 16, cudaMemcpyHostToDevice));
+    CK(cudaMallocHost(&p->h_state, sizeof(double) * B * 2 * D));
+    CK(cudaMallocHost(&p->h_ctr, sizeof(unsigned long long)));
+    CK(cudaMallocHost(&p->h_cmd, sizeof(double) * B * D));
+    CK(cudaMallocHost(&p->h_info, sizeof(mppi_step_info) * B));
+    memset(p->h_state, 0, sizeof(double) * B * 2 * D);
+    *p->h_ctr = 0;
+    if (p->generator == MPPI_GEN_PSEUDORANDOM) {
+      CKR(p->z.alloc((size_t)N * p->Kn * D));
+      if (p->smoothing == MPPI_SMOOTH_BSPLINE) {
+        CKR(p->basis.alloc((size_t)H * p->Kn));
+        bspline_basis_kernel<<<1, 64, 0, p->stream>>>(H, p->Kn, p->degree, p->basis.p);
+        CK(cudaGetLastError());
+      }
+    }
+    CK(cudaStreamSynchronize(p->stream));
+    return MPPI_OK;
+  }();
+  if (rc != MPPI_OK) {
+    mppi_plan_destroy(p);
+    return rc;
+  }
+  *out = p;
+  return MPPI_OK;
+}
+
+int mppi_plan_destroy(mppi_plan* p) {
+  if (!p) return MPPI_OK;
+  cudaSetDevice(p->device);
+  if (p->stream) cudaStreamSynchronize(p->stream);
+  invalidate_graph(p);
+  DevBuf<double>* dbl[] = {&p->sph_d, &p->box_d, &p->eps, &p->z, &p->basis, &p->colmean, &p->means,
+                           &p->var, &p->sd, &p->prev_means, &p->prev_sd, &p->goal, &p->state,
+                           &p->totals, &p->records, &p->out_record, &p->cmd, &p->counters_pad,
+                           &p->e_in0, &p->e_in1, &p->e_pos, &p->e_vel, &p->e_acc, &p->e_terms,
+                           &p->e_step, &p->e_tot, &p->e_state, &p->e_dts, &p->e_records,
+                           &p->d_pos, &p->d_vel, &p->d_acc, &p->d_terms, &p->d_step, &p->d_w};
+  for (auto* b : dbl) b->release();
+  p->sph_f.release();
+  p->box_f.release();
+  p->clearance.release();
+  p->mlp_x.release();
+  p->mlp_d.release();
+  p->e_x.release();
+  p->e_d.release();
+  p->stepbuf.release();
+  p->e_stepbuf.release();
+  p->counters.release();
+  p->e_counters.release();
+  p->status.release();
+  p->bad.release();
+  p->e_status.release();
+  p->info.release();
+  p->stepctr.release();
+  mlp_release(p->mlp);
+  if (p->h_state) cudaFreeHost(p->h_state);
+  if (p->h_ctr) cudaFreeHost(p->h_ctr);
+  if (p->h_cmd) cudaFreeHost(p->h_cmd);
+  if (p->h_info) cudaFreeHost(p->h_info);
+  if (p->ev0) cudaEventDestroy(p->ev0);
+  if (p->ev1) cudaEventDestroy(p->ev1);
+  if (p->stream) cudaStreamDestroy(p->stream);
+  delete p;
+  return MPPI_OK;
+}
+
+int mppi_init_noise(mppi_plan* p, const double* basis_host) {
+  if (!p) return fail(MPPI_E_BAD_ARGUMENT, "null plan");
+  CKR(set_device(p));
+  if (p->generator != MPPI_GEN_HALTON) return MPPI_OK;
+  if (p->D > 40) return fail(MPPI_E_CONFIG, "halton supports at most 40 dims");
+  const long long rows = p->Ntot;
+  const int K = p->Kn, H = p->H, D = p->D;
+  DevBuf<double> zt, full, bas;
+  CKR(zt.alloc((size_t)rows * K * D));
+  CKR(full.alloc((size_t)rows * H * D));
+  const double* bptr = nullptr;
+  if (p->smoothing == MPPI_SMOOTH_BSPLINE) {
+    CKR(bas.alloc((size_t)H * K));
+    if (basis_host) {
+      CK(cudaMemcpyAsync(bas.p, basis_host, sizeof(double) * H * K, cudaMemcpyHostToDevice, p->stream));
+    } else {
+      bspline_basis_kernel<<<1, 64, 0, p->stream>>>(H, K, p->degree, bas.p);
+    }
+    bptr = bas.p;
+  }
+  if (p->smoothing != MPPI_SMOOTH_BSPLINE && K != H) {
+    zt.release();
+    full.release();
+    return fail(MPPI_E_BAD_ARGUMENT, "smoothing expects K == H");
+  }
+  DevBuf<int> err;
+  CKR(err.alloc(1));
+  CK(cudaMemsetAsync(err.p, 0, sizeof(int), p->stream));
+  knots_kernel<<<grid_for(rows * K * D, 256), 256, 0, p->stream>>>(zt.p, rows, K, D, MPPI_GEN_HALTON, 0, 0, err.p);
+  smooth_kernel<<<grid_for(rows * H * D, 256), 256, 0, p->stream>>>(zt.p, full.p, rows, K, H, D, p->smoothing,
+                                                                    bptr, p->comb[0], p->comb[1], p->comb[2]);
+  CKR(p->colmean.alloc((size_t)H * D));
+  column_mean_kernel<<<H * D, 256, 0, p->stream>>>(full.p, rows, H * D, p->colmean.p);
+  center_slice_kernel<<<grid_for((long long)p->N * H * D, 256), 256, 0, p->stream>>>(
+      full.p, p->colmean.p, p->eps.p, p->offset, p->N, H * D);
+  CK(cudaGetLastError());
+  CK(cudaStreamSynchronize(p->stream));
+  zt.release();
+  full.release();
+  bas.release();
+  err.release();
+  return MPPI_OK;
+}
+
+int mppi_set_noise(mppi_plan* p, const double* eps) {
+  if (!p || !eps) return fail(MPPI_E_BAD_ARGUMENT, "null argument");
+  CKR(set_device(p));
+  CK(cudaMemcpyAsync(p->eps.p, eps, sizeof(double) * p->N * p->H * p->D, cudaMemcpyHostToDevice, p->stream));
+  CK(cudaStreamSynchronize(p->stream));
+  return MPPI_OK;
+}
+
+int mppi_get_noise(mppi_plan* p, double* eps) {
+  if (!p || !eps) return fail(MPPI_E_BAD_ARGUMENT, "null argument");
+  CKR(set_device(p));
+  CK(cudaMemcpyAsync(eps, p->eps.p, sizeof(double) * p->N * p->H * p->D, cudaMemcpyDeviceToHost, p->stream));
+  CK(cudaStreamSynchronize(p->stream));
+  return MPPI_OK;
+}
+
+int mppi_set_goal(mppi_plan* p, int32_t inst, const double* R, const double* t, int32_t mode) {
+  if (!p || !R || !t) return fail(MPPI_E_BAD_ARGUMENT, "null argument");
+  if (inst < -1 || inst >= p->B) return fail(MPPI_E_BAD_ARGUMENT, "instance out of range");
+  CKR(set_device(p));
+  const int b0 = inst < 0 ? 0 : inst, b1 = inst < 0 ? p->B : inst + 1;
+  for (int b = b0; b < b1; ++b) {
+    double* g = &p->goal_host[(size_t)b * 16];
+    for (int i = 0; i < 9; ++i) g[i] = R[i];
+    for (int i = 0; i < 3; ++i) g[9 + i] = t[i];
+    g[12] = (double)mode;
+  }
+  CK(cudaMemcpyAsync(p->goal.p + (size_t)b0 * 16, &p->goal_host[(size_t)b0 * 16],
+                     sizeof(double) * 16 * (b1 - b0), cudaMemcpyHostToDevice, p->stream));
+  CK(cudaStreamSynchronize(p->stream));
+  return MPPI_OK;
+}
+
+int mppi_set_world(mppi_plan* p, const double* spheres, int32_t ns, const double* boxes, int32_t nb) {
+  if (!p || ns < 0 || nb < 0) return fail(MPPI_E_BAD_ARGUMENT, "bad world arguments");
+  CKR(set_device(p));
+  CK(cudaStreamSynchronize(p->stream));
+  p->ns = ns;
+  p->nb = nb;
+  std::vector<float> sf(std::max(1, 4 * ns)), bf(std::max(1, 6 * nb));
+  for (int i = 0; i < 4 * ns; ++i) sf[i] = (float)spheres[i];
+  for (int i = 0; i < 6 * nb; ++i) bf[i] = (float)boxes[i];
+  CKR(p->sph_d.alloc(std::max(1, 4 * ns)));
+  CKR(p->box_d.alloc(std::max(1, 6 * nb)));
+  CKR(p->sph_f.alloc(std::max(1, 4 * ns)));
+  CKR(p->box_f.alloc(std::max(1, 6 * nb)));
+  if (ns) CK(cudaMemcpy(p->sph_d.p, spheres, sizeof(double) * 4 * ns, cudaMemcpyHostToDevice));
+  if (nb) CK(cudaMemcpy(p->box_d.p, boxes, sizeof(double) * 6 * nb, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(p->sph_f.p, sf.data(), sizeof(float) * sf.size(), cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(p->box_f.p, bf.data(), sizeof(float) * bf.size(), cudaMemcpyHostToDevice));
+  p->clearance.release();
+  p->gx = p->gy = p->gz = 0;
+  invalidate_graph(p);
+  return MPPI_OK;
+}
+
+int mppi_set_voxel_world(mppi_plan* p, const uint8_t* occ, int32_t nx, int32_t ny, int32_t nz,
+                         const double* origin, double voxel, const double* spheres, int32_t ns) {
+  if (!p || !occ || nx < 1 || ny < 1 || nz < 1 || !(voxel > 0.0))
+    return fail(MPPI_E_BAD_ARGUMENT, "bad voxel world arguments");
+  // Greedy box decomposition of the occupied set on the host (init-time
+  // geometry preprocessing): grow x-runs, then y, then z. The union of the
+  // boxes is exactly the occupied voxel set, so the narrow phase keeps the
+  // reference's box semantics (simworld.py:30-49, jit.py:325-331).
+  std::vector<uint8_t> left(occ, occ + (size_t)nx * ny * nz);
+  auto at = [&](int i, int j, int k) -> uint8_t& { return left[((size_t)i * ny + j) * nz + k]; };
+  std::vector<double> boxes;
+  for (int i = 0; i < nx; ++i)
+    for (int j = 0; j < ny; ++j)
+      for (int k = 0; k < nz; ++k) {
+        if (!at(i, j, k)) continue;
+        int k1 = k;
+        while (k1 + 1 < nz && at(i, j, k1 + 1)) ++k1;
+        int j1 = j;
+        for (;;) {
+          if (j1 + 1 >= ny) break;
+          bool ok = true;
+          for (int kk = k; kk <= k1 && ok; ++kk) ok = at(i, j1 + 1, kk);
+          if (!ok) break;
+          ++j1;
+        }
+        int i1 = i;
+        for (;;) {
+          if (i1 + 1 >= nx) break;
+          bool ok = true;
+          for (int jj = j; jj <= j1 && ok; ++jj)
+            for (int kk = k; kk <= k1 && ok; ++kk) ok = at(i1 + 1, jj, kk);
+          if (!ok) break;
+          ++i1;
+        }
+        for (int ii = i; ii <= i1; ++ii)
+          for (int jj = j; jj <= j1; ++jj)
+            for (int kk = k; kk <= k1; ++kk) at(ii, jj, kk) = 0;
+        boxes.push_back(origin[0] + i * voxel);
+        boxes.push_back(origin[1] + j * voxel);
+        boxes.push_back(origin[2] + k * voxel);
+        boxes.push_back(origin[0] + (i1 + 1) * voxel);
+        boxes.push_back(origin[1] + (j1 + 1) * voxel);
+        boxes.push_back(origin[2] + (k1 + 1) * voxel);
+      }
+  const int nb = (int)(boxes.size() / 6);
+  CKR(mppi_set_world(p, spheres, ns, boxes.data(), nb));
+  p->gx = nx;
+  p->gy = ny;
+  p->gz = nz;
+  for (int i = 0; i < 3; ++i) p->gorigin[i] = origin[i];
+  p->gvoxel = voxel;
+  CKR(p->clearance.alloc((size_t)nx * ny * nz));
+  clearance_kernel<<<grid_for((long long)nx * ny * nz, 256, 1 << 20), 256, 0, p->stream>>>(
+      p->box_d.p, nb, nx, ny, nz, origin[0], origin[1], origin[2], voxel, p->clearance.p);
+  CK(cudaGetLastError());
+  CK(cudaStreamSynchronize(p->stream));
+  invalidate_graph(p);
+  return MPPI_OK;
+}
+
+int mppi_set_mlp(mppi_plan* p, int32_t in_dim, const double* W0, const double* b0, const double* W1,
+                 const double* b1, const double* W2, const double* b2, const double* W3,
+                 const double* b3) {
+  if (!p) return fail(MPPI_E_BAD_ARGUMENT, "null plan");
+  if (in_dim != 2 * p->D || in_dim > MPPI_MLP_IN_MAX)
+    return fail(MPPI_E_CONFIG, "surrogate input dim must be 2*dof <= 16");
+  CKR(set_device(p));
+  CK(mlp_upload(p->mlp, in_dim, W0, b0, W1, b1, W2, b2, W3, b3, p->stream));
+  p->mlp_ready = true;
+  invalidate_graph(p);
+  return MPPI_OK;
+}
+
+int mppi_set_policy(mppi_plan* p, int32_t inst, const double* means, const double* variances) {
+  if (!p || !means || !variances) return fail(MPPI_E_BAD_ARGUMENT, "null argument");
+  if (inst < 0 || inst >= p->B) return fail(MPPI_E_BAD_ARGUMENT, "instance out of range");
+  CKR(set_device(p));
+  const size_t HD = (size_t)p->H * p->D;
+  std::vector<double> s(HD);
+  for (size_t i = 0; i < HD; ++i) s[i] = std::sqrt(variances[i]);
+  CK(cudaMemcpyAsync(p->means.p + inst * HD, means, sizeof(double) * HD, cudaMemcpyHostToDevice, p->stream));
+  CK(cudaMemcpyAsync(p->var.p + inst * HD, variances, sizeof(double) * HD, cudaMemcpyHostToDevice, p->stream));
+  CK(cudaMemcpyAsync(p->sd.p + inst * HD, s.data(), sizeof(double) * HD, cudaMemcpyHostToDevice, p->stream));
+  CK(cudaStreamSynchronize(p->stream));
+  return MPPI_OK;
+}
+
+int mppi_get_policy(mppi_plan* p, int32_t inst, double* means, double* variances) {
+  if (!p) return fail(MPPI_E_BAD_ARGUMENT, "null plan");
+  if (inst < 0 || inst >= p->B) return fail(MPPI_E_BAD_ARGUMENT, "instance out of range");
+  CKR(set_device(p));
+  const size_t HD = (size_t)p->H * p->D;
+  if (means)
+    CK(cudaMemcpyAsync(means, p->means.p + inst * HD, sizeof(double) * HD, cudaMemcpyDeviceToHost, p->stream));
+  if (variances)
+    CK(cudaMemcpyAsync(variances, p->var.p + inst * HD, sizeof(double) * HD, cudaMemcpyDeviceToHost, p->stream));
+  CK(cudaStreamSynchronize(p->stream));
+  return MPPI_OK;
+}
+
+int mppi_step(mppi_plan* p, const double* theta, const double* theta_dot, double* command_out,
+              mppi_step_info* info) {
+  if (!p || !theta || !theta_dot || !command_out) return fail(MPPI_E_BAD_ARGUMENT, "null argument");
+  CKR(set_device(p));
+  CKR(ensure_graph(p));
+  const int B = p->B, D = p->D;
+  for (int b = 0; b < B; ++b) {
+    memcpy(p->h_state + (size_t)b * 2 * D, theta + (size_t)b * D, sizeof(double) * D);
+    memcpy(p->h_state + (size_t)b * 2 * D + D, theta_dot + (size_t)b * D, sizeof(double) * D);
+  }
+  *p->h_ctr = p->step_counter++;
+  CK(cudaEventRecord(p->ev0, p->stream));
+  CK(cudaGraphLaunch(p->graph, p->stream));
+  CK(cudaEventRecord(p->ev1, p->stream));
+  CK(cudaStreamSynchronize(p->stream));
+  float ms = 0.f;
+  CK(cudaEventElapsedTime(&ms, p->ev0, p->ev1));
+  memcpy(command_out, p->h_cmd, sizeof(double) * B * D);
+  if (info) {
+    memcpy(info, p->h_info, sizeof(mppi_step_info) * B);
+    for (int b = 0; b < B; ++b) info[b].device_ms = ms;
+  }
+  return MPPI_OK;
+}
+
+int mppi_evaluate(mppi_plan* p, int32_t mode, int32_t n, int32_t H, const double* dts, double gamma,
+                  double tw, const double* theta0, const double* theta_dot0, const double* in0,
+                  const double* in1, mppi_eval_out* out) {
+  if (!p || !dts || !in0 || !out) return fail(MPPI_E_BAD_ARGUMENT, "null argument");
+  if (mode != 0 && mode != 1) return fail(MPPI_E_BAD_ARGUMENT, "mode must be 0 or 1");
+  if (mode == 1 && !in1) return fail(MPPI_E_BAD_ARGUMENT, "velocities missing");
+  if (mode == 0 && (!theta0 || !theta_dot0)) return fail(MPPI_E_BAD_ARGUMENT, "initial state missing");
+  if (H < 1 || H > MPPI_MAX_HORIZON) return fail(MPPI_E_CONFIG, "horizon out of range");
+  if (n < 1) return fail(MPPI_E_BAD_ARGUMENT, "empty batch");
+  if (p->learned() && !p->mlp_ready) return fail(MPPI_E_CONFIG, "learned provider without weights");
+  CKR(set_device(p));
+  cudaStream_t st = p->stream;
+  const int D = p->D;
+  const size_t nhd = (size_t)n * H * D, nh = (size_t)n * H;
+  CKR(p->e_in0.alloc(nhd));
+  CKR(p->e_in1.alloc(nhd));
+  CKR(p->e_pos.alloc(nhd));
+  CKR(p->e_vel.alloc(nhd));
+  CKR(p->e_acc.alloc(nhd));
+  CKR(p->e_terms.alloc(6 * nh));
+  CKR(p->e_step.alloc(nh));
+  CKR(p->e_tot.alloc(n));
+  CKR(p->e_state.alloc(2 * D));
+  CKR(p->e_stepbuf.alloc(nh * sizeof(double)));
+  CKR(p->e_status.alloc(2));
+  int ppb, nblk;
+  choose_blocks(n, ppb, nblk);
+  CKR(p->e_records.alloc((size_t)nblk * (kRecHead + 2 * H * D)));
+  CKR(p->e_counters.alloc(1));
+  if (p->learned()) {
+    CKR(p->e_x.alloc(mlp_padded_rows(nh) * 16));
+    CKR(p->e_d.alloc(mlp_padded_rows(nh)));
+    CK(cudaMemsetAsync(p->e_x.p, 0, sizeof(float) * mlp_padded_rows(nh) * 16, st));
+  }
+  CK(cudaMemcpyAsync(p->e_in0.p, in0, sizeof(double) * nhd, cudaMemcpyHostToDevice, st));
+  if (mode == 1) CK(cudaMemcpyAsync(p->e_in1.p, in1, sizeof(double) * nhd, cudaMemcpyHostToDevice, st));
+  std::vector<double> s0(2 * D, 0.0);
+  if (mode == 0) {
+    memcpy(s0.data(), theta0, sizeof(double) * D);
+    memcpy(s0.data() + D, theta_dot0, sizeof(double) * D);
+  }
+  CK(cudaMemcpyAsync(p->e_state.p, s0.data(), sizeof(double) * 2 * D, cudaMemcpyHostToDevice, st));
+  CK(cudaMemsetAsync(p->e_status.p, 0, sizeof(int), st));
+  CK(cudaMemsetAsync(p->e_status.p + 1, 0x7f, sizeof(int), st));
+  CK(cudaMemsetAsync(p->e_counters.p, 0, sizeof(unsigned), st));
+  auto run = [&](auto tag) -> int {
+    using R = decltype(tag);
+    RolloutArgs<R> a;
+    rollout_static<R>(p, H, dts, a);
+    a.N = n;
+    a.B = 1;
+    a.mode = mode == 0 ? 1 : 2;
+    a.state = p->e_state.p;
+    a.goal = p->goal.p;
+    a.in0 = p->e_in0.p;
+    a.in1 = p->e_in1.p;
+    a.step = reinterpret_cast<R*>(p->e_stepbuf.p);
+    a.mlp_x = p->learned() ? p->e_x.p : nullptr;
+    a.status = p->e_status.p;
+    a.bad = p->e_status.p + 1;
+    a.out_pos = p->e_pos.p;
+    a.out_vel = p->e_vel.p;
+    a.out_acc = p->e_acc.p;
+    a.out_terms = p->e_terms.p;
+    CK(launch_rollout_any<R>(a, D, n, st));
+    if (p->learned()) CK(mlp_forward(p->mlp, p->e_x.p, (long long)nh, p->e_d.p, st));
+    StatsArgs<R> s;
+    stats_static<R>(p, H, gamma, tw, s);
+    s.N = n;
+    s.B = 1;
+    s.ppb = ppb;
+    s.nblk = nblk;
+    s.totals_only = 1;
+    s.raw_step = mode == 1;
+    s.step = reinterpret_cast<const R*>(p->e_stepbuf.p);
+    s.mlp_d = p->learned() ? p->e_d.p : nullptr;
+    s.totals = p->e_tot.p;
+    s.records = p->e_records.p;
+    s.counters = p->e_counters.p;
+    s.status = p->e_status.p + 0;
+    s.bad = p->e_status.p + 1;
+    s.dump_step = p->e_step.p;
+    s.dump_terms = p->e_terms.p;
+    // phase A ignores the status word when totals_only; use a zero status
+    CK(launch_stats_any<R>(s, D, st));
+    return MPPI_OK;
+  };
+  if (p->precision == MPPI_FP64)
+    CKR(run(double{}));
+  else
+    CKR(run(float{}));
+  int hst[2];
+  CK(cudaMemcpyAsync(hst, p->e_status.p, sizeof(int) * 2, cudaMemcpyDeviceToHost, st));
+  std::vector<double> tot(n);
+  CK(cudaMemcpyAsync(tot.data(), p->e_tot.p, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
+  if (out->positions) CK(cudaMemcpyAsync(out->positions, p->e_pos.p, sizeof(double) * nhd, cudaMemcpyDeviceToHost, st));
+  if (out->velocities) CK(cudaMemcpyAsync(out->velocities, p->e_vel.p, sizeof(double) * nhd, cudaMemcpyDeviceToHost, st));
+  if (out->accelerations) CK(cudaMemcpyAsync(out->accelerations, p->e_acc.p, sizeof(double) * nhd, cudaMemcpyDeviceToHost, st));
+  if (out->step_costs) CK(cudaMemcpyAsync(out->step_costs, p->e_step.p, sizeof(double) * nh, cudaMemcpyDeviceToHost, st));
+  if (out->terms) CK(cudaMemcpyAsync(out->terms, p->e_terms.p, sizeof(double) * 6 * nh, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  if (out->totals) memcpy(out->totals, tot.data(), sizeof(double) * n);
+  out->bad_particle = hst[1] >= 0x7f000000 ? -1 : hst[1];
+  int q = 0;
+  for (int i = 0; i < n; ++i) q += std::isfinite(tot[i]) ? 0 : 1;
+  out->quarantined = q;
+  if (hst[0] == MPPI_E_NONFINITE_CONTROL)
+    return fail(MPPI_E_NONFINITE_CONTROL, "non-finite control in particle " + std::to_string(out->bad_particle));
+  return MPPI_OK;
+}
+
+int mppi_get_bundle(mppi_plan* p, mppi_eval_out* out, double* weights) {
+  if (!p || !out) return fail(MPPI_E_BAD_ARGUMENT, "null argument");
+  if (!p->dump) return fail(MPPI_E_CONFIG, "plan was created without dump = 1");
+  CKR(set_device(p));
+  cudaStream_t st = p->stream;
+  const size_t nhd = (size_t)p->N * p->H * p->D, nh = (size_t)p->N * p->H;
+  if (out->positions) CK(cudaMemcpyAsync(out->positions, p->d_pos.p, sizeof(double) * nhd, cudaMemcpyDeviceToHost, st));
+  if (out->velocities) CK(cudaMemcpyAsync(out->velocities, p->d_vel.p, sizeof(double) * nhd, cudaMemcpyDeviceToHost, st));
+  if (out->accelerations) CK(cudaMemcpyAsync(out->accelerations, p->d_acc.p, sizeof(double) * nhd, cudaMemcpyDeviceToHost, st));
+  if (out->step_costs) CK(cudaMemcpyAsync(out->step_costs, p->d_step.p, sizeof(double) * nh, cudaMemcpyDeviceToHost, st));
+  if (out->terms) CK(cudaMemcpyAsync(out->terms, p->d_terms.p, sizeof(double) * 6 * nh, cudaMemcpyDeviceToHost, st));
+  if (out->totals) CK(cudaMemcpyAsync(out->totals, p->totals.p, sizeof(double) * p->N, cudaMemcpyDeviceToHost, st));
+  if (weights) CK(cudaMemcpyAsync(weights, p->d_w.p, sizeof(double) * p->N, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  out->bad_particle = -1;
+  out->quarantined = 0;
+  return MPPI_OK;
+}
+
+// ---------------------------------------------------------------- sharded update
+int mppi_stats_record_len(mppi_plan* p, int32_t* len) {
+  if (!p || !len) return fail(MPPI_E_BAD_ARGUMENT, "null argument");
+  *len = kRecHead + 2 * p->H * p->D;
+  return MPPI_OK;
+}
+
+int mppi_stats_dev(mppi_plan* p, const double* theta, const double* theta_dot, void* record_dev,
+                   void* stream) {
+  if (!p || !record_dev) return fail(MPPI_E_BAD_ARGUMENT, "null argument");
+  if (p->B != 1) return fail(MPPI_E_CONFIG, "particle sharding is for single-instance plans");
+  if (p->learned() && !p->mlp_ready) return fail(MPPI_E_CONFIG, "learned provider without weights");
+  CKR(set_device(p));
+  cudaStream_t st = stream ? (cudaStream_t)stream : p->stream;
+  const int D = p->D, it = p->sharded_iter;
+  if (it == 0) {
+    if (!theta || !theta_dot) return fail(MPPI_E_BAD_ARGUMENT, "state missing");
+    memcpy(p->h_state, theta, sizeof(double) * D);
+    memcpy(p->h_state + D, theta_dot, sizeof(double) * D);
+    *p->h_ctr = p->step_counter++;
+    CK(cudaMemsetAsync(p->status.p, 0, sizeof(int), st));
+    CK(cudaMemsetAsync(p->bad.p, 0x7f, sizeof(int), st));
+    CK(cudaMemcpyAsync(p->state.p, p->h_state, sizeof(double) * 2 * D, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(p->stepctr.p, p->h_ctr, sizeof(unsigned long long), cudaMemcpyHostToDevice, st));
+  }
+  CKR(enqueue_sampling(p, it, st));
+  double* rec = reinterpret_cast<double*>(record_dev);
+  if (p->precision == MPPI_FP64)
+    CKR(enqueue_iteration<double>(p, it, false, rec, st));
+  else
+    CKR(enqueue_iteration<float>(p, it, false, rec, st));
+  return MPPI_OK;
+}
+
+int mppi_finalize_dev(mppi_plan* p, const void* records_dev, int32_t n_records, double* command_out,
+                      mppi_step_info* info, void* stream) {
+  if (!p || !records_dev || n_records < 1) return fail(MPPI_E_BAD_ARGUMENT, "bad records");
+  CKR(set_device(p));
+  cudaStream_t st = stream ? (cudaStream_t)stream : p->stream;
+  const int it = p->sharded_iter;
+  auto run = [&](auto tag) -> int {
+    using R = decltype(tag);
+    StatsArgs<R> s;
+    stats_static<R>(p, p->H, p->gamma, p->tw, s);
+    s.N = p->N;
+    s.B = 1;
+    s.shift = it == 0;
+    s.means = p->means.p;
+    s.var = p->var.p;
+    s.sd = p->sd.p;
+    s.prev_means = p->prev_means.p;
+    s.prev_sd = p->prev_sd.p;
+    s.status = p->status.p;
+    s.bad = p->bad.p;
+    s.cmd = p->cmd.p;
+    s.info = p->info.p;
+    CK(launch_finalize<R>(s, (const double*)records_dev, n_records, st));
+    return MPPI_OK;
+  };
+  if (p->precision == MPPI_FP64)
+    CKR(run(double{}));
+  else
+    CKR(run(float{}));
+  p->sharded_iter = (it + 1) % p->iters;
+  if (command_out || info) {
+    CK(cudaMemcpyAsync(p->h_cmd, p->cmd.p, sizeof(double) * p->D, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(p->h_info, p->info.p, sizeof(mppi_step_info), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (command_out) memcpy(command_out, p->h_cmd, sizeof(double) * p->D);
+    if (info) memcpy(info, p->h_info, sizeof(mppi_step_info));
+  }
+  return MPPI_OK;
+}
+
+// ---------------------------------------------------------------- stateless functions
+}  // extern "C"
+namespace {
+struct Scratch {
+  std::vector<void*> ptrs;
+  cudaStream_t st = nullptr;
+  ~Scratch() {
+    for (void* q : ptrs) cudaFree(q);
+    if (st) cudaStreamDestroy(st);
+  }
+  template <typename T>
+  T* dev(size_t n, const T* host = nullptr) {
+    void* q = nullptr;
+    if (cudaMalloc(&q, std::max<size_t>(1, n) * sizeof(T)) != cudaSuccess) return nullptr;
+    ptrs.push_back(q);
+    if (host && n) cudaMemcpyAsync(q, host, n * sizeof(T), cudaMemcpyHostToDevice, st);
+    return (T*)q;
+  }
+  int init() {
+    CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    return MPPI_OK;
+  }
+};
+#define SCRATCH_OR_FAIL(S) \
+  Scratch S;               \
+  CKR(S.init())
+#define DEVPTR(S, T, name, n, host)                                 \
+  T* name = S.dev<T>((n), (host));                                  \
+  if (!name) return fail(MPPI_E_CUDA, "cudaMalloc failed (" #name ")")
+}  // namespace
+extern "C" {
+
+int mppi_halton_points(int64_t count, int32_t dims, double* out) {
+  if (count < 1) return fail(MPPI_E_BAD_ARGUMENT, "count must be >= 1");
+  if (dims > 40) return fail(MPPI_E_CONFIG, "halton supports at most 40 dims, got " + std::to_string(dims));
+  SCRATCH_OR_FAIL(S);
+  DEVPTR(S, double, d, (size_t)count * dims, (const double*)nullptr);
+  halton_points_kernel<<<grid_for(count * dims, 256), 256, 0, S.st>>>(d, count, dims);
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(out, d, sizeof(double) * count * dims, cudaMemcpyDeviceToHost, S.st));
+  CK(cudaStreamSynchronize(S.st));
+  return MPPI_OK;
+}
+
+int mppi_gaussianize(const double* p, int64_t n, double* out) {
+  if (n < 0) return fail(MPPI_E_BAD_ARGUMENT, "negative size");
+  if (n == 0) return MPPI_OK;
+  SCRATCH_OR_FAIL(S);
+  DEVPTR(S, double, dp, n, p);
+  DEVPTR(S, double, dout, n, (const double*)nullptr);
+  DEVPTR(S, int, err, 1, (const int*)nullptr);
+  CK(cudaMemsetAsync(err, 0, sizeof(int), S.st));
+  gaussianize_kernel<<<grid_for(n, 256), 256, 0, S.st>>>(dp, n, dout, err);
+  CK(cudaGetLastError());
+  int herr = 0;
+  CK(cudaMemcpyAsync(&herr, err, sizeof(int), cudaMemcpyDeviceToHost, S.st));
+  CK(cudaMemcpyAsync(out, dout, sizeof(double) * n, cudaMemcpyDeviceToHost, S.st));
+  CK(cudaStreamSynchronize(S.st));
+  if (herr) return fail(MPPI_E_BAD_ARGUMENT, "unit samples must lie in [0, 1)");
+  return MPPI_OK;
+}
+
+int mppi_smooth_sequences(const double* knots, int64_t n, int32_t k, int32_t d, int32_t mode,
+                          const double* basis, const double* comb, int32_t horizon, double* out) {
+  if (n < 0 || k < 1 || d < 1 || horizon < 1) return fail(MPPI_E_BAD_ARGUMENT, "bad shape");
+  if (n == 0) return MPPI_OK;
+  if (mode == MPPI_SMOOTH_BSPLINE && !basis) return fail(MPPI_E_BAD_ARGUMENT, "basis missing");
+  if (mode != MPPI_SMOOTH_BSPLINE && k != horizon) return fail(MPPI_E_BAD_ARGUMENT, "K != H");
+  SCRATCH_OR_FAIL(S);
+  DEVPTR(S, double, dz, (size_t)n * k * d, knots);
+  DEVPTR(S, double, db, (size_t)horizon * k, mode == MPPI_SMOOTH_BSPLINE ? basis : nullptr);
+  DEVPTR(S, double, dout, (size_t)n * horizon * d, (const double*)nullptr);
+  const double c1 = comb ? comb[0] : 0.3, c2 = comb ? comb[1] : 0.4, c3 = comb ? comb[2] : 0.3;
+  smooth_kernel<<<grid_for(n * horizon * d, 256), 256, 0, S.st>>>(dz, dout, n, k, horizon, d, mode, db, c1, c2, c3);
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(out, dout, sizeof(double) * n * horizon * d, cudaMemcpyDeviceToHost, S.st));
+  CK(cudaStreamSynchronize(S.st));
+  return MPPI_OK;
+}
+
+int mppi_bspline_basis(int32_t horizon, int32_t k, int32_t degree, double* out) {
+  if (k < degree + 1) return fail(MPPI_E_CONFIG, "bspline of degree " + std::to_string(degree) +
+                                                     " needs at least " + std::to_string(degree + 1) +
+                                                     " control points");
+  if (horizon < 1 || k + degree + 1 > 64 || degree > 15) return fail(MPPI_E_BAD_ARGUMENT, "bad basis shape");
+  SCRATCH_OR_FAIL(S);
+  DEVPTR(S, double, db, (size_t)horizon * k, (const double*)nullptr);
+  bspline_basis_kernel<<<(horizon + 63) / 64, 64, 0, S.st>>>(horizon, k, degree, db);
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(out, db, sizeof(double) * horizon * k, cudaMemcpyDeviceToHost, S.st));
+  CK(cudaStreamSynchronize(S.st));
+  return MPPI_OK;
+}
+
+int mppi_build_controls(const double* eps, const double* means, const double* stddev, int64_t n,
+                        int32_t h, int32_t d, int32_t null_count, double* out) {
+  if (n < 1 || h < 1 || d < 1) return fail(MPPI_E_BAD_ARGUMENT, "bad shape");
+  SCRATCH_OR_FAIL(S);
+  const size_t nhd = (size_t)n * h * d;
+  DEVPTR(S, double, de, nhd, eps);
+  DEVPTR(S, double, dm, (size_t)h * d, means);
+  DEVPTR(S, double, ds, (size_t)h * d, stddev);
+  DEVPTR(S, double, dout, nhd, (const double*)nullptr);
+  DEVPTR(S, int, bad, 1, (const int*)nullptr);
+  CK(cudaMemsetAsync(bad, 0, sizeof(int), S.st));
+  build_controls_kernel<<<grid_for(nhd, 256), 256, 0, S.st>>>(de, dm, ds, n, h, d, null_count, dout, bad);
+  CK(cudaGetLastError());
+  int hb = 0;
+  CK(cudaMemcpyAsync(&hb, bad, sizeof(int), cudaMemcpyDeviceToHost, S.st));
+  CK(cudaMemcpyAsync(out, dout, sizeof(double) * nhd, cudaMemcpyDeviceToHost, S.st));
+  CK(cudaStreamSynchronize(S.st));
+  if (hb) return fail(MPPI_E_NONFINITE_CONTROL, "control batch contains non-finite entries");
+  return MPPI_OK;
+}
+
+int mppi_particle_weights(const double* totals, int64_t n, double beta, double* weights) {
+  if (n < 1) return fail(MPPI_E_ALL_QUARANTINED, "all particles quarantined; no finite costs");
+  SCRATCH_OR_FAIL(S);
+  DEVPTR(S, double, dt, n, totals);
+  DEVPTR(S, double, dw, n, (const double*)nullptr);
+  DEVPTR(S, int, stt, 1, (const int*)nullptr);
+  CK(cudaMemsetAsync(stt, 0, sizeof(int), S.st));
+  weights_kernel<<<1, 1024, 0, S.st>>>(dt, n, beta, dw, stt);
+  CK(cudaGetLastError());
+  int hs = 0;
+  CK(cudaMemcpyAsync(&hs, stt, sizeof(int), cudaMemcpyDeviceToHost, S.st));
+  CK(cudaMemcpyAsync(weights, dw, sizeof(double) * n, cudaMemcpyDeviceToHost, S.st));
+  CK(cudaStreamSynchronize(S.st));
+  if (hs == MPPI_E_ALL_QUARANTINED) return fail(hs, "all particles quarantined; no finite costs");
+  if (hs == MPPI_E_WEIGHT_UNDERFLOW) return fail(hs, "all particle weights underflowed to zero; increase beta");
+  return MPPI_OK;
+}
+
+int mppi_update_policy(const double* controls, const double* weights, int64_t n, int32_t h, int32_t d,
+                       int32_t policy_mode, double alpha_mu, double alpha_sigma, double smin, double smax,
+                       int32_t do_mean, int32_t do_cov, double* means, double* variances) {
+  if (n < 1 || h < 1 || d < 1 || h * d > 1024) return fail(MPPI_E_BAD_ARGUMENT, "bad shape");
+  SCRATCH_OR_FAIL(S);
+  const size_t nhd = (size_t)n * h * d;
+  const size_t nv = policy_mode == MPPI_POLICY_ISOTROPIC ? (size_t)h : (size_t)h * d;
+  DEVPTR(S, double, du, nhd, controls);
+  DEVPTR(S, double, dw, n, weights);
+  DEVPTR(S, double, dm, (size_t)h * d, means);
+  DEVPTR(S, double, dv, nv, variances);
+  DEVPTR(S, int, stt, 1, (const int*)nullptr);
+  CK(cudaMemsetAsync(stt, 0, sizeof(int), S.st));
+  update_policy_kernel<<<1, 1024, 0, S.st>>>(du, dw, n, h, d, policy_mode == MPPI_POLICY_ISOTROPIC,
+                                             alpha_mu, alpha_sigma, smin, smax, do_mean, do_cov, dm, dv, stt);
+  CK(cudaGetLastError());
+  int hs = 0;
+  CK(cudaMemcpyAsync(&hs, stt, sizeof(int), cudaMemcpyDeviceToHost, S.st));
+  CK(cudaMemcpyAsync(means, dm, sizeof(double) * h * d, cudaMemcpyDeviceToHost, S.st));
+  CK(cudaMemcpyAsync(variances, dv, sizeof(double) * nv, cudaMemcpyDeviceToHost, S.st));
+  CK(cudaStreamSynchronize(S.st));
+  if (hs) return fail(hs, "weight sum must be positive");
+  return MPPI_OK;
+}
+
+int mppi_mlp_forward(mppi_plan* p, const double* q, int64_t m, double* out) {
+  if (!p || !q || !out) return fail(MPPI_E_BAD_ARGUMENT, "null argument");
+  if (!p->mlp_ready) return fail(MPPI_E_CONFIG, "mppi_set_mlp was not called");
+  if (m < 1) return MPPI_OK;
+  CKR(set_device(p));
+  SCRATCH_OR_FAIL(S);
+  const size_t rows = mlp_padded_rows(m);
+  DEVPTR(S, double, dq, (size_t)m * p->D, q);
+  DEVPTR(S, float, dx, rows * 16, (const float*)nullptr);
+  DEVPTR(S, float, dd, rows, (const float*)nullptr);
+  DEVPTR(S, double, dout, m, (const double*)nullptr);
+  CK(cudaMemsetAsync(dx, 0, sizeof(float) * rows * 16, S.st));
+  posenc_kernel<<<grid_for(m, 256), 256, 0, S.st>>>(dq, m, p->D, dx);
+  CK(mlp_forward(p->mlp, dx, m, dd, S.st));
+  float_to_double_kernel<<<grid_for(m, 256), 256, 0, S.st>>>(dd, m, dout);
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(out, dout, sizeof(double) * m, cudaMemcpyDeviceToHost, S.st));
+  CK(cudaStreamSynchronize(S.st));
+  return MPPI_OK;
+}
+
+// ---------------------------------------------------------------- operator seam
+int mppi_fk_batch(const double* q, int64_t m, int32_t d, const double* axes, const double* orot,
+                  const double* otrans, const int64_t* jtype, double* rot_out, double* trans_out) {
+  if (m < 0 || d < 1) return fail(MPPI_E_BAD_ARGUMENT, "bad shape");
+  if (m == 0) return MPPI_OK;
+  SCRATCH_OR_FAIL(S);
+  DEVPTR(S, double, dq, (size_t)m * d, q);
+  DEVPTR(S, double, da, (size_t)3 * d, axes);
+  DEVPTR(S, double, dr, (size_t)9 * d, orot);
+  DEVPTR(S, double, dt, (size_t)3 * d, otrans);
+  DEVPTR(S, long long, dj, (size_t)d, (const long long*)jtype);
+  DEVPTR(S, double, rot, (size_t)m * d * 9, (const double*)nullptr);
+  DEVPTR(S, double, tr, (size_t)m * d * 3, (const double*)nullptr);
+  SeamChain ch{da, dr, dt, dj};
+  fk_seam_kernel<<<(unsigned)((m + 127) / 128), 128, 0, S.st>>>(dq, m, d, ch, rot, tr);
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(rot_out, rot, sizeof(double) * m * d * 9, cudaMemcpyDeviceToHost, S.st));
+  CK(cudaMemcpyAsync(trans_out, tr, sizeof(double) * m * d * 3, cudaMemcpyDeviceToHost, S.st));
+  CK(cudaStreamSynchronize(S.st));
+  return MPPI_OK;
+}
+
+int mppi_jacobian_batch(const double* q, int64_t m, int32_t d, const double* rot, const double* trans,
+                        const double* axes, const int64_t* jtype, double* jac_out) {
+  (void)q;
+  if (m < 0 || d < 1) return fail(MPPI_E_BAD_ARGUMENT, "bad shape");
+  if (m == 0) return MPPI_OK;
+  SCRATCH_OR_FAIL(S);
+  DEVPTR(S, double, drot, (size_t)m * d * 9, rot);
+  DEVPTR(S, double, dtr, (size_t)m * d * 3, trans);
+  DEVPTR(S, double, da, (size_t)3 * d, axes);
+  DEVPTR(S, long long, dj, (size_t)d, (const long long*)jtype);
+  DEVPTR(S, double, J, (size_t)m * 6 * d, (const double*)nullptr);
+  jacobian_seam_kernel<<<(unsigned)((m + 127) / 128), 128, 0, S.st>>>(m, d, drot, dtr, da, dj, J);
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(jac_out, J, sizeof(double) * m * 6 * d, cudaMemcpyDeviceToHost, S.st));
+  CK(cudaStreamSynchronize(S.st));
+  return MPPI_OK;
+}
+
+int mppi_manip_batch(const double* jac, int64_t m, int32_t d, int32_t task_dim, double* out) {
+  if (m < 0 || d < 1 || (task_dim != 2 && task_dim != 3)) return fail(MPPI_E_BAD_ARGUMENT, "bad shape");
+  if (m == 0) return MPPI_OK;
+  SCRATCH_OR_FAIL(S);
+  DEVPTR(S, double, dj, (size_t)m * 6 * d, jac);
+  DEVPTR(S, double, dout, (size_t)m, (const double*)nullptr);
+  manip_seam_kernel<<<(unsigned)((m + 127) / 128), 128, 0, S.st>>>(dj, m, d, task_dim, dout);
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(out, dout, sizeof(double) * m, cudaMemcpyDeviceToHost, S.st));
+  CK(cudaStreamSynchronize(S.st));
+  return MPPI_OK;
+}
+
+int mppi_self_collision_batch(const double* rot, const double* trans, int64_t m, int32_t d,
+                              const double* cap_p0, const double* cap_p1, const double* cap_r,
+                              const int64_t* cap_link, int32_t n_caps, const int64_t* pair_a,
+                              const int64_t* pair_b, int32_t n_pairs, double* out) {
+  if (m < 0 || d < 1) return fail(MPPI_E_BAD_ARGUMENT, "bad shape");
+  if (m == 0) return MPPI_OK;
+  SCRATCH_OR_FAIL(S);
+  DEVPTR(S, double, drot, (size_t)m * d * 9, rot);
+  DEVPTR(S, double, dtr, (size_t)m * d * 3, trans);
+  DEVPTR(S, double, p0, (size_t)3 * n_caps, cap_p0);
+  DEVPTR(S, double, p1, (size_t)3 * n_caps, cap_p1);
+  DEVPTR(S, double, r, (size_t)n_caps, cap_r);
+  DEVPTR(S, long long, lk, (size_t)n_caps, (const long long*)cap_link);
+  DEVPTR(S, long long, pa, (size_t)n_pairs, (const long long*)pair_a);
+  DEVPTR(S, long long, pb, (size_t)n_pairs, (const long long*)pair_b);
+  DEVPTR(S, double, dout, (size_t)m, (const double*)nullptr);
+  SeamCaps caps{p0, p1, r, lk, n_caps};
+  selfcoll_seam_kernel<<<(unsigned)((m + 127) / 128), 128, 0, S.st>>>(drot, dtr, m, d, caps, pa, pb, n_pairs, dout);
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(out, dout, sizeof(double) * m, cudaMemcpyDeviceToHost, S.st));
+  CK(cudaStreamSynchronize(S.st));
+  return MPPI_OK;
+}
+
+int mppi_env_collision_batch(const double* rot, const double* trans, int64_t m, int32_t d,
+                             const double* cap_p0, const double* cap_p1, const double* cap_r,
+                             const int64_t* cap_link, int32_t n_caps, const double* spheres,
+                             int32_t n_spheres, const double* boxes, int32_t n_boxes, int64_t* hit_out) {
+  if (m < 0 || d < 1) return fail(MPPI_E_BAD_ARGUMENT, "bad shape");
+  if (m == 0) return MPPI_OK;
+  SCRATCH_OR_FAIL(S);
+  DEVPTR(S, double, drot, (size_t)m * d * 9, rot);
+  DEVPTR(S, double, dtr, (size_t)m * d * 3, trans);
+  DEVPTR(S, double, p0, (size_t)3 * n_caps, cap_p0);
+  DEVPTR(S, double, p1, (size_t)3 * n_caps, cap_p1);
+  DEVPTR(S, double, r, (size_t)n_caps, cap_r);
+  DEVPTR(S, long long, lk, (size_t)n_caps, (const long long*)cap_link);
+  DEVPTR(S, double, sp, (size_t)4 * n_spheres, spheres);
+  DEVPTR(S, double, bx, (size_t)6 * n_boxes, boxes);
+  DEVPTR(S, long long, hit, (size_t)m, (const long long*)nullptr);
+  SeamCaps caps{p0, p1, r, lk, n_caps};
+  envcoll_seam_kernel<<<(unsigned)((m + 127) / 128), 128, 0, S.st>>>(drot, dtr, m, d, caps, sp, n_spheres, bx,
+                                                                      n_boxes, hit);
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(hit_out, hit, sizeof(long long) * m, cudaMemcpyDeviceToHost, S.st));
+  CK(cudaStreamSynchronize(S.st));
+  return MPPI_OK;
+}
+
+int mppi_integrate_batch(const double* u, int64_t n, int32_t h, int32_t d, const double* dts,
+                         const double* th0, const double* thd0, double* pos_out, double* vel_out) {
+  if (n < 0 || h < 1 || d < 1) return fail(MPPI_E_BAD_ARGUMENT, "bad shape");
+  if (n == 0) return MPPI_OK;
+  SCRATCH_OR_FAIL(S);
+  const size_t nhd = (size_t)n * h * d;
+  DEVPTR(S, double, du, nhd, u);
+  DEVPTR(S, double, ddt, (size_t)h, dts);
+  DEVPTR(S, double, t0, (size_t)d, th0);
+  DEVPTR(S, double, v0, (size_t)d, thd0);
+  DEVPTR(S, double, pos, nhd, (const double*)nullptr);
+  DEVPTR(S, double, vel, nhd, (const double*)nullptr);
+  integrate_seam_kernel<<<(unsigned)((n * d + 127) / 128), 128, 0, S.st>>>(du, n, h, d, ddt, t0, v0, pos, vel);
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(pos_out, pos, sizeof(double) * nhd, cudaMemcpyDeviceToHost, S.st));
+  CK(cudaMemcpyAsync(vel_out, vel, sizeof(double) * nhd, cudaMemcpyDeviceToHost, S.st));
+  CK(cudaStreamSynchronize(S.st));
+  return MPPI_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,744 @@
+// mppi_kernels.cuh — the fused MPPI step kernels for sm_100a.
+//
+//   rollout_kernel  : policy shaping (sampling.py:268-290) + semi-implicit
+//                     Euler (jit.py:335-349) + generic-chain FK (jit.py:89-111)
+//                     + Jacobian/manipulability (jit.py:114-185) + capsule
+//                     self collision (jit.py:241-260) + world collision
+//                     (jit.py:289-332) + the cost stack (costs.py:76-187),
+//                     one warp per particle, one lane per horizon step.
+//   stats_kernel    : discounted totals + quarantine (rollout.py:111-171),
+//                     exponentiated-utility weights (policy.py:103-121) and
+//                     weighted sufficient statistics; the last block of each
+//                     instance combines the block records and applies
+//                     update_mean / update_covariance (policy.py:124-155),
+//                     the shift (policy.py:158-167) and next_command
+//                     (policy.py:170-177).
+#pragma once
+
+#include "mppi_common.cuh"
+
+namespace mppi {
+
+constexpr int kRolloutWarps = 4;  // 128-thread blocks, one warp per particle
+constexpr int kStatsThreads = 256;
+constexpr int kRecHead = 6;       // m, S0, count, sum_finite, status, first bad row
+
+template <typename R>
+struct RolloutArgs {
+  ChainT<R> chain;
+  CostT<R> cost;
+  WorldT<R> world;
+  R dts[MAXH];
+  R remaining[MAXH];  // sum_{k>=h} dts[k] (costs.py:100), host fp64
+  int H, N, B, null_count, particle_offset;
+  int mode;       // 0: u = mu + sd*eps ; 1: u given (in0) ; 2: pos (in0) / vel (in1) given
+  int shift;      // read the stored policy through the shift view
+  int check_var;  // PolicyStateError check of build_control_batch (sampling.py:282)
+  int skip_on_status;
+  double tail_mean, tail_sd;
+  const double* eps;     // (N,H,d)
+  const double* means;   // (B,H,d)
+  const double* sd;      // (B,H,d)
+  const double* state;   // (B,2d)
+  const double* goal;    // (B,16): R(9) t(3) mode
+  const double* in0;
+  const double* in1;
+  R* step;               // (B*N*H) step cost excluding the learned self-collision term
+  float* mlp_x;          // (B*N*H,16) positional encoding (surrogate.py:24-28) or NULL
+  int* status;
+  int* bad;
+  double* out_pos;       // dumps, instance 0 only; (n,H,d)
+  double* out_vel;
+  double* out_acc;
+  double* out_terms;     // (6,n,H)
+};
+
+// Any capsule of this lane's configuration penetrates the world (costs.py:235-240).
+// Capsule endpoints live in shared memory, [cap][6][32 lanes].
+template <typename R>
+__device__ __forceinline__ bool env_any_hit(const WorldT<R>& w, const ChainT<R>& ch, const R* cap,
+                                            int lane) {
+  const int nc = ch.n_caps;
+  for (int c = 0; c < nc; ++c) {
+    R P0[3], P1[3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      P0[i] = cap[(c * 6 + i) * 32 + lane];
+      P1[i] = cap[(c * 6 + 3 + i) * 32 + lane];
+    }
+    const R rc = ch.cap_r[c];
+    for (int o = 0; o < w.ns; ++o)
+      if (capsule_hits_sphere(P0, P1, rc, w.spheres + 4 * o)) return true;
+    if (w.nb == 0) continue;
+    if (w.sdf != nullptr) {
+      // Conservative voxel broad phase. w.sdf holds, per voxel, the exact
+      // distance from the voxel CUBE to the obstacle set (the union of the
+      // boxes below), so every point of the cube is at least that far away.
+      // A point outside the grid is no closer than its projection onto the
+      // grid box (obstacles lie inside, projection onto a convex set).
+      // Sample the segment every half voxel; every segment point is within
+      // `half` of a sample, so min(clearance) - half >= r + margin proves no
+      // strict penetration (jit.py:326) for every box and the exact narrow
+      // phase is skipped. Anything else falls through to the exact test.
+      const R dx = P1[0] - P0[0], dy = P1[1] - P0[1], dz = P1[2] - P0[2];
+      const R len = sqrt(dx * dx + dy * dy + dz * dz);
+      const int ns = 1 + (int)ceil(len / (R(0.5) * w.voxel));
+      const R half = R(0.5) * len / R(ns > 1 ? ns - 1 : 1);
+      R lb = R(1e30);
+      for (int s = 0; s < ns; ++s) {
+        const R t = ns > 1 ? R(s) / R(ns - 1) : R(0);
+        int ix = (int)floor((P0[0] + t * dx - w.ox) / w.voxel);
+        int iy = (int)floor((P0[1] + t * dy - w.oy) / w.voxel);
+        int iz = (int)floor((P0[2] + t * dz - w.oz) / w.voxel);
+        ix = ix < 0 ? 0 : (ix >= w.nx ? w.nx - 1 : ix);
+        iy = iy < 0 ? 0 : (iy >= w.ny ? w.ny - 1 : iy);
+        iz = iz < 0 ? 0 : (iz >= w.nz ? w.nz - 1 : iz);
+        const R f = R(__ldg(w.sdf + ((size_t)ix * w.ny + iy) * w.nz + iz));
+        lb = f < lb ? f : lb;
+      }
+      if (lb - half >= rc + R(1e-5)) continue;
+    }
+    for (int ob = 0; ob < w.nb; ++ob) {
+      const R* bx = w.boxes + 6 * ob;
+      if (seg_box_dist(P0, P1, bx, bx + 3) < rc) return true;
+    }
+  }
+  return false;
+}
+
+template <typename R, int D>
+__global__ void __launch_bounds__(kRolloutWarps * 32)
+    rollout_kernel(const __grid_constant__ RolloutArgs<R> a) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const long long g = (long long)blockIdx.x * kRolloutWarps + wib;
+  if (g >= (long long)a.B * a.N) return;  // warp-uniform exit
+  const int b = (int)(g / a.N);
+  const int n = (int)(g - (long long)b * a.N);
+  if (a.skip_on_status && a.status[b] != 0) return;
+  const int H = a.H;
+  const bool act = lane < H;
+  const int h = act ? lane : H - 1;
+  const ChainT<R>& ch = a.chain;
+  const CostT<R>& cs = a.cost;
+  const double* st = a.state + (size_t)b * 2 * D;
+
+  // ---- controls -> positions / velocities --------------------------------
+  R p[D], v[D], u[D];
+  const size_t row = ((size_t)n * H + h) * D;
+  if (a.mode == 2) {
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+      p[j] = (R)a.in0[row + j];
+      v[j] = (R)a.in1[row + j];
+      u[j] = R(0);
+    }
+  } else {
+    bool bad = false, varbad = false;
+    const int ng = n + a.particle_offset;
+    if (a.mode == 0) {
+      const int hs = a.shift ? h + 1 : h;
+      const double* mu = a.means + (size_t)b * H * D;
+      const double* sdv = a.sd + (size_t)b * H * D;
+#pragma unroll
+      for (int j = 0; j < D; ++j) {
+        const double m = hs < H ? mu[hs * D + j] : a.tail_mean;
+        const double s = hs < H ? sdv[hs * D + j] : a.tail_sd;
+        varbad |= (s <= 0.0);
+        double uu;
+        if (ng < a.null_count)
+          uu = 0.0;
+        else if (ng == a.null_count)
+          uu = m;
+        else
+          uu = m + s * a.eps[row + j];
+        bad |= !isfinite(uu);
+        u[j] = (R)uu;
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < D; ++j) {
+        const double uu = a.in0[row + j];
+        bad |= !isfinite(uu);
+        u[j] = (R)uu;
+      }
+    }
+    const unsigned badm = __ballot_sync(0xffffffffu, act && bad);
+    const unsigned varm = __ballot_sync(0xffffffffu, act && varbad);
+    if (lane == 0 && a.status != nullptr) {
+      if (varm && a.check_var && n == 0) atomicMax(&a.status[b], (int)MPPI_E_NONPOSITIVE_VARIANCE);
+      if (badm) {
+        atomicMin(&a.bad[b], ng);
+        atomicMax(&a.status[b], (int)MPPI_E_NONFINITE_CONTROL);
+      }
+    }
+    // semi-implicit Euler as two inclusive warp scans over the horizon
+    const R dt = act ? a.dts[h] : R(0);
+#pragma unroll
+    for (int j = 0; j < D; ++j) v[j] = (R)st[D + j] + warp_inclusive_scan(dt * u[j], lane);
+#pragma unroll
+    for (int j = 0; j < D; ++j) p[j] = (R)st[j] + warp_inclusive_scan(dt * v[j], lane);
+  }
+
+  // ---- forward kinematics, link by link in registers ----------------------
+  R Rw[9] = {R(1), R(0), R(0), R(0), R(1), R(0), R(0), R(0), R(1)};
+  R tw[3] = {R(0), R(0), R(0)};
+  R ja[D][3], jp[D][3];  // Jacobian column data: world axis, joint origin
+  R sq[D], cq[D];
+  const int nc = ch.n_caps;
+  R* cap = reinterpret_cast<R*>(smem_raw) + (size_t)wib * nc * 6 * 32;
+#pragma unroll
+  for (int j = 0; j < 3; ++j) {
+    ja[0][j] = ch.axes[0][j];
+    jp[0][j] = R(0);
+  }
+#pragma unroll
+  for (int k = 0; k < D; ++k) {
+    R Rmo[9], tmo[3];
+    R s, c;
+    sincos_(p[k], &s, &c);
+    sq[k] = s;
+    cq[k] = c;
+    if (ch.jtype[k] == 0) {
+      R Rm[9];
+      axis_rotation(ch.axes[k], s, R(1) - c, Rm);
+      mat33_mul(Rm, ch.orot[k], Rmo);
+      mat33_vec(Rm, ch.otrans[k], tmo);
+    } else {
+#pragma unroll
+      for (int i = 0; i < 9; ++i) Rmo[i] = ch.orot[k][i];
+#pragma unroll
+      for (int i = 0; i < 3; ++i) tmo[i] = p[k] * ch.axes[k][i] + ch.otrans[k][i];
+    }
+    R dtw[3];
+    mat33_vec(Rw, tmo, dtw);
+#pragma unroll
+    for (int i = 0; i < 3; ++i) tw[i] = tw[i] + dtw[i];
+    R Rn[9];
+    mat33_mul(Rw, Rmo, Rn);
+#pragma unroll
+    for (int i = 0; i < 9; ++i) Rw[i] = Rn[i];
+    if ((k + 1) % REORTHO_EVERY == 0) orthonormalize(Rw);
+    if (k + 1 < D) {
+      mat33_vec(Rw, ch.axes[k + 1], ja[k + 1]);
+#pragma unroll
+      for (int i = 0; i < 3; ++i) jp[k + 1][i] = tw[i];
+    }
+    for (int ci = 0; ci < nc; ++ci) {
+      if (ch.cap_link[ci] != k) continue;
+      R q0[3], q1[3];
+      mat33_vec(Rw, ch.cap_p0[ci], q0);
+      mat33_vec(Rw, ch.cap_p1[ci], q1);
+#pragma unroll
+      for (int i = 0; i < 3; ++i) {
+        cap[(ci * 6 + i) * 32 + lane] = q0[i] + tw[i];
+        cap[(ci * 6 + 3 + i) * 32 + lane] = q1[i] + tw[i];
+      }
+    }
+  }
+  __syncwarp();
+
+  // ---- cost terms -----------------------------------------------------------
+  // pose (costs.py:76-95)
+  const double* gl = a.goal + (size_t)b * 16;
+  R Rg[9], tg[3];
+#pragma unroll
+  for (int i = 0; i < 9; ++i) Rg[i] = (R)gl[i];
+#pragma unroll
+  for (int i = 0; i < 3; ++i) tg[i] = (R)gl[9 + i];
+  const int gmode = (int)gl[12];
+  R pose;
+  {
+    const R e0 = tw[0] - tg[0], e1 = tw[1] - tg[1], e2 = tw[2] - tg[2];
+    R acc = R(0);
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      const R di = Rg[0 * 3 + i] * e0 + Rg[1 * 3 + i] * e1 + Rg[2 * 3 + i] * e2;
+      const R wi = cs.alpha_trans[i] * di;
+      acc += wi * wi;
+    }
+    pose = sqrt(acc);
+    if (gmode != MPPI_GOAL_POSITION_ONLY) {
+      R racc = R(0);
+#pragma unroll
+      for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int kk = 0; kk < 3; ++kk) {
+          const R rr = Rg[0 * 3 + i] * Rw[0 * 3 + kk] + Rg[1 * 3 + i] * Rw[1 * 3 + kk] +
+                       Rg[2 * 3 + i] * Rw[2 * 3 + kk];
+          const R res = cs.alpha_rot[i] * ((i == kk ? R(1) : R(0)) - rr);
+          racc += res * res;
+        }
+      pose = pose + sqrt(racc);
+    }
+  }
+  // stop (costs.py:98-108)
+  R stop = R(0);
+  if (cs.use_stop) {
+    R acc = R(0);
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+      const R lim = a.remaining[h] * ch.accel[j];
+      R ex = fabs(v[j]) - lim;
+      ex = ex > R(0) ? ex : R(0);
+      acc += ex * ex;
+    }
+    stop = sqrt(acc);
+  }
+  // joint limits (costs.py:111-123)
+  R joint = R(0);
+  if (cs.use_joint) {
+    R acc = R(0);
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+      R lo = ch.lo[j] - p[j];
+      lo = lo > R(0) ? lo : R(0);
+      R hi = p[j] - ch.hi[j];
+      hi = hi > R(0) ? hi : R(0);
+      const R dep = lo + hi;
+      acc += dep * dep;
+    }
+    joint = sqrt(acc);
+  }
+  // manipulability (jit.py:114-185, costs.py:126-127)
+  R manip = R(0);
+  if (cs.use_manip) {
+    R J[3][D];
+#pragma unroll
+    for (int k = 0; k < D; ++k) {
+      if (ch.jtype[k] == 0) {
+        const R rx = tw[0] - jp[k][0], ry = tw[1] - jp[k][1], rz = tw[2] - jp[k][2];
+        J[0][k] = ja[k][1] * rz - ja[k][2] * ry;
+        J[1][k] = ja[k][2] * rx - ja[k][0] * rz;
+        J[2][k] = ja[k][0] * ry - ja[k][1] * rx;
+      } else {
+        J[0][k] = ja[k][0];
+        J[1][k] = ja[k][1];
+        J[2][k] = ja[k][2];
+      }
+    }
+    const int td = ch.task_dim;
+    R m;
+    if (D == td) {
+      R det;
+      if (td == 2)
+        det = J[0][0] * J[1][1 % D] - J[0][1 % D] * J[1][0];
+      else
+        det = J[0][0] * (J[1][1 % D] * J[2][2 % D] - J[1][2 % D] * J[2][1 % D]) -
+              J[0][1 % D] * (J[1][0] * J[2][2 % D] - J[1][2 % D] * J[2][0]) +
+              J[0][2 % D] * (J[1][0] * J[2][1 % D] - J[1][1 % D] * J[2][0]);
+      m = fabs(det);
+    } else {
+      R G[3][3];
+#pragma unroll
+      for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = 0; j < 3; ++j) {
+          R acc = R(0);
+#pragma unroll
+          for (int k = 0; k < D; ++k) acc += J[i][k] * J[j][k];
+          G[i][j] = acc;
+        }
+      R det;
+      if (td == 2)
+        det = G[0][0] * G[1][1] - G[0][1] * G[1][0];
+      else
+        det = G[0][0] * (G[1][1] * G[2][2] - G[1][2] * G[2][1]) -
+              G[0][1] * (G[1][0] * G[2][2] - G[1][2] * G[2][0]) +
+              G[0][2] * (G[1][0] * G[2][1] - G[1][1] * G[2][0]);
+      m = sqrt(det > R(0) ? det : R(0));
+    }
+    manip = m < cs.k_m ? R(1) - m : R(0);
+  }
+  // capsule self collision oracle (jit.py:241-260, costs.py:234)
+  R selfc = R(0);
+  if (cs.selfcoll == MPPI_SELFCOLL_ORACLE) {
+    R best = R(NO_CONTACT);
+    for (int pi = 0; pi < ch.n_pairs; ++pi) {
+      const int i = ch.pair_a[pi], j = ch.pair_b[pi];
+      R a0[3], a1[3], b0[3], b1[3];
+#pragma unroll
+      for (int t = 0; t < 3; ++t) {
+        a0[t] = cap[(i * 6 + t) * 32 + lane];
+        a1[t] = cap[(i * 6 + 3 + t) * 32 + lane];
+        b0[t] = cap[(j * 6 + t) * 32 + lane];
+        b1[t] = cap[(j * 6 + 3 + t) * 32 + lane];
+      }
+      const R val = ch.cap_r[i] + ch.cap_r[j] - segseg_dist(a0, a1, b0, b1);
+      if (val > best) best = val;
+    }
+    selfc = best > R(0) ? best : R(0);
+  }
+  // world collision, binary (jit.py:289-332, costs.py:235-240)
+  R envc = R(0);
+  if (cs.use_env) envc = env_any_hit(a.world, ch, cap, lane) ? R(1) : R(0);
+
+  // total_cost (costs.py:176-187) minus the learned self-collision term
+  const R stepc = pose + cs.a_stop * stop + cs.a_joint * joint + cs.a_manip * manip +
+                  cs.a_coll * (selfc + envc);
+
+  if (act) {
+    const size_t m = (size_t)g * H + h;
+    a.step[m] = stepc;
+    if (a.mlp_x != nullptr) {
+      float* x = a.mlp_x + m * 16;
+#pragma unroll
+      for (int k = 0; k < D; ++k) {
+        x[k] = (float)sq[k];
+        x[D + k] = (float)cq[k];
+      }
+#pragma unroll
+      for (int k = 2 * D; k < 16; ++k) x[k] = 0.f;
+    }
+    if (a.out_pos != nullptr && b == 0) {
+#pragma unroll
+      for (int j = 0; j < D; ++j) {
+        a.out_pos[row + j] = (double)p[j];
+        a.out_vel[row + j] = (double)v[j];
+        if (a.out_acc) a.out_acc[row + j] = (double)u[j];
+      }
+    }
+    if (a.out_terms != nullptr && b == 0) {
+      const size_t nh = (size_t)a.N * H, o = (size_t)n * H + h;
+      a.out_terms[T_POSE * nh + o] = (double)pose;
+      a.out_terms[T_STOP * nh + o] = (double)stop;
+      a.out_terms[T_JOINT * nh + o] = (double)joint;
+      a.out_terms[T_MANIP * nh + o] = (double)manip;
+      a.out_terms[T_SELF * nh + o] = (double)selfc;
+      a.out_terms[T_ENV * nh + o] = (double)envc;
+    }
+  }
+}
+
+// ============================================================== statistics
+template <typename R>
+struct StatsArgs {
+  int H, N, B, D, null_count, particle_offset, ppb, nblk;
+  int shift, learned, totals_only, finalize_inline, isotropic, raw_step;
+  double beta, alpha_mu, alpha_sigma, smin, smax, a_coll;
+  double tail_mean, tail_var, tail_sd;
+  double disc[MAXH];   // gamma^h (numpy power), h < H-1
+  double dlast;        // gamma^(H-1) * terminal_weight
+  const R* step;       // (B*N*H)
+  const float* mlp_d;  // (B*N*H) learned distance, or NULL
+  const double* eps;   // (N,H,d)
+  double* means;       // (B,H,d) policy storage, updated in place
+  double* var;
+  double* sd;
+  double* prev_means;  // (B,H,d) the view used by this iteration
+  double* prev_sd;
+  double* totals;      // (B*N)
+  double* records;     // (B,nblk,reclen)
+  double* out_record;  // (B,reclen) when !finalize_inline
+  unsigned* counters;  // (B)
+  int* status;
+  int* bad;
+  double* cmd;         // (B,d)
+  mppi_step_info* info;
+  double* dump_step;   // (N,H) instance 0
+  double* dump_terms;  // (6,N,H) instance 0 (selfcoll row written for learned)
+  double* dump_weights;  // (N) instance 0
+};
+
+__device__ __forceinline__ double block_min_d(double v, double* red) {
+  for (int off = 16; off > 0; off >>= 1) v = fmin(v, __shfl_xor_sync(0xffffffffu, v, off));
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) red[w] = v;
+  __syncthreads();
+  if (w == 0) {
+    v = l < (int)(blockDim.x >> 5) ? red[l] : CUDART_INF;
+    for (int off = 16; off > 0; off >>= 1) v = fmin(v, __shfl_xor_sync(0xffffffffu, v, off));
+    if (l == 0) red[0] = v;
+  }
+  __syncthreads();
+  const double r = red[0];
+  __syncthreads();
+  return r;
+}
+
+// Fixed-order combine of `count` statistics records (each relative to its own
+// minimum) into one record relative to the global minimum. Deterministic:
+// every sum runs in record order. (§8(e): rescale by exp(-(m_k - m)/beta).)
+static __device__ void combine_records(const double* recs, int count, int reclen, int HD, double beta,
+                                double* out, double* scale_smem, double* red) {
+  double m = CUDART_INF;
+  for (int k = threadIdx.x; k < count; k += blockDim.x) {
+    const double* r = recs + (size_t)k * reclen;
+    if (r[2] > 0.0) m = fmin(m, r[0]);
+  }
+  m = block_min_d(m, red);
+  for (int k = threadIdx.x; k < count; k += blockDim.x) {
+    const double* r = recs + (size_t)k * reclen;
+    scale_smem[k] = r[2] > 0.0 ? exp(-(r[0] - m) / beta) : 0.0;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s0 = 0.0, cnt = 0.0, sf = 0.0, stt = 0.0, bad = 2147483647.0;
+    for (int k = 0; k < count; ++k) {
+      const double* r = recs + (size_t)k * reclen;
+      s0 += scale_smem[k] * r[1];
+      cnt += r[2];
+      sf += r[3];
+      stt = fmax(stt, r[4]);
+      bad = fmin(bad, r[5]);
+    }
+    out[0] = m;
+    out[1] = s0;
+    out[2] = cnt;
+    out[3] = sf;
+    out[4] = stt;
+    out[5] = bad;
+  }
+  for (int o = threadIdx.x; o < 2 * HD; o += blockDim.x) {
+    double s = 0.0;
+    for (int k = 0; k < count; ++k) {
+      const double sc = scale_smem[k];
+      if (sc != 0.0) s += sc * recs[(size_t)k * reclen + kRecHead + o];
+    }
+    out[kRecHead + o] = s;
+  }
+  __syncthreads();
+}
+
+// Apply update_mean/update_covariance/shift/next_command from a combined record.
+// One block per instance; thread o owns policy entry o = h*D + j (H*D <= 256).
+template <typename R>
+static __device__ void finalize_policy(const StatsArgs<R>& a, int b, const double* rec, double* emp_smem) {
+  const int H = a.H, D = a.D, HD = H * D;
+  const int o = threadIdx.x;
+  double* means = a.means + (size_t)b * HD;
+  double* var = a.var + (size_t)b * HD;
+  double* sd = a.sd + (size_t)b * HD;
+  __shared__ int s_status;
+  __shared__ int s_varbad;
+  if (threadIdx.x == 0) {
+    int stt = max(a.status[b], (int)rec[4]);
+    if ((int)rec[5] < a.bad[b]) a.bad[b] = (int)rec[5];
+    if (stt == 0 && rec[2] <= 0.0) stt = MPPI_E_ALL_QUARANTINED;
+    if (stt == 0 && !(rec[1] > 0.0)) stt = MPPI_E_WEIGHT_UNDERFLOW;
+    s_status = stt;
+    s_varbad = 0;
+  }
+  __syncthreads();
+  // read the view this iteration used (shifted on the first iteration)
+  double mo = 0.0, vo = 0.0, so = 0.0;
+  const int h = o / D, j = o - (o / D) * D;
+  if (o < HD) {
+    const int hs = a.shift ? h + 1 : h;
+    mo = hs < H ? means[hs * D + j] : a.tail_mean;
+    vo = hs < H ? var[hs * D + j] : a.tail_var;
+    so = hs < H ? sd[hs * D + j] : a.tail_sd;
+  }
+  double mu_new = mo, var_new = vo;
+  if (s_status == 0 && o < HD) {
+    const double S0 = rec[1], S1 = rec[kRecHead + o], S2 = rec[kRecHead + HD + o];
+    const double avg = mo + S1 / S0;
+    mu_new = (1.0 - a.alpha_mu) * mo + a.alpha_mu * avg;
+    const double dl = mu_new - mo;
+    double emp = S2 / S0 - 2.0 * dl * (S1 / S0) + dl * dl;
+    emp_smem[o] = emp;
+  }
+  __syncthreads();
+  if (s_status == 0 && o < HD) {
+    double emp = emp_smem[o];
+    if (a.isotropic) {
+      double s = 0.0;
+      for (int jj = 0; jj < D; ++jj) s += emp_smem[h * D + jj];
+      emp = s / D;
+    }
+    double vn = (1.0 - a.alpha_sigma) * vo + a.alpha_sigma * emp;
+    vn = vn < a.smin ? a.smin : (vn > a.smax ? a.smax : vn);  // np.clip keeps NaN
+    var_new = vn;
+    if (!(vn > 0.0) && !isnan(vn)) atomicOr(&s_varbad, 1);
+  }
+  __syncthreads();
+  if (o < HD) {
+    if (a.prev_means) {
+      a.prev_means[(size_t)b * HD + o] = mo;
+      a.prev_sd[(size_t)b * HD + o] = so;
+    }
+    if (s_status == 0) {
+      means[o] = mu_new;
+      if (!s_varbad) {
+        var[o] = var_new;
+        sd[o] = sqrt(var_new);
+      } else {
+        var[o] = vo;
+        sd[o] = so;
+      }
+    } else if (a.shift) {  // failure: the shift of controller.py:200 still stands
+      means[o] = mo;
+      var[o] = vo;
+      sd[o] = so;
+    }
+  }
+  if (threadIdx.x == 0) {
+    int stt = s_status;
+    if (stt == 0 && s_varbad) stt = MPPI_E_NONPOSITIVE_VARIANCE;
+    a.status[b] = stt;
+    if (a.info) {
+      mppi_step_info inf;
+      inf.status = stt;
+      inf.bad_particle = a.bad[b] >= 0x7f000000 ? -1 : a.bad[b];
+      inf.finite_count = (int)rec[2];
+      inf._pad = 0;
+      inf.best_cost = rec[2] > 0.0 ? rec[0] : CUDART_NAN;
+      inf.mean_cost = rec[2] > 0.0 ? rec[3] / rec[2] : CUDART_NAN;
+      inf.device_ms = 0.0;
+      a.info[b] = inf;
+    }
+  }
+  if (s_status == 0 && o < D && a.cmd) a.cmd[(size_t)b * D + o] = mu_new;  // next_command "mean"
+}
+
+template <typename R, int D>
+__global__ void __launch_bounds__(kStatsThreads) stats_kernel(const __grid_constant__ StatsArgs<R> a) {
+  extern __shared__ __align__(16) double sm[];
+  const int b = blockIdx.y, blk = blockIdx.x;
+  const int H = a.H, HD = H * D, N = a.N;
+  const int n0 = blk * a.ppb;
+  const int n1 = min(N, n0 + a.ppb);
+  const int cnt = max(0, n1 - n0);
+  double* tot = sm;             // [ppb]
+  double* wt = sm + a.ppb;      // [ppb]
+  double* red = wt + a.ppb;     // [32]
+  double* scale = red + 32;     // [max(nblk, 8)]
+  const int reclen = kRecHead + 2 * HD;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const bool failed = (a.status[b] != 0);
+
+  // ---- phase A: discounted totals, quarantine (rollout.py:111-171) ---------
+  if (!failed || a.totals_only) {
+    for (int i = wid; i < cnt; i += nw) {
+      const int n = n0 + i;
+      const size_t m = ((size_t)b * N + n) * H + lane;
+      double c = 0.0, dself = 0.0;
+      bool fin = true;
+      if (lane < H) {
+        c = (double)a.step[m];
+        if (a.learned) {
+          const double dd = (double)a.mlp_d[m];
+          dself = dd > 0.0 ? dd : 0.0;
+          c = c + a.a_coll * dself;
+        }
+        fin = isfinite(c);
+      }
+      const bool allfin = __all_sync(0xffffffffu, fin);
+      double contrib = 0.0;
+      if (lane < H) contrib = (lane < H - 1 ? a.disc[lane] : a.dlast) * c;
+      double total = warp_sum(contrib);
+      if (!allfin) total = CUDART_INF;
+      if (lane == 0) {
+        tot[i] = total;
+        if (a.totals) a.totals[(size_t)b * N + n] = total;
+      }
+      if (b == 0 && lane < H) {
+        if (a.dump_step) a.dump_step[(size_t)n * H + lane] = (allfin || a.raw_step) ? c : 0.0;
+        if (a.dump_terms && a.learned) a.dump_terms[(size_t)T_SELF * N * H + (size_t)n * H + lane] = dself;
+      }
+    }
+  }
+  if (a.totals_only) return;
+  __syncthreads();
+
+  // ---- phase B/C: block min, weights relative to it (policy.py:103-121) ----
+  double mloc = CUDART_INF;
+  if (!failed)
+    for (int i = threadIdx.x; i < cnt; i += blockDim.x)
+      if (isfinite(tot[i])) mloc = fmin(mloc, tot[i]);
+  const double mb = block_min_d(mloc, red);
+  if (!failed)
+    for (int i = threadIdx.x; i < cnt; i += blockDim.x)
+      wt[i] = isfinite(tot[i]) ? exp(-(tot[i] - mb) / a.beta) : 0.0;
+  __syncthreads();
+
+  // ---- phase D: weighted sufficient statistics around the old mean ---------
+  double* rec = a.records + ((size_t)b * a.nblk + blk) * reclen;
+  if (threadIdx.x == 0) {
+    double s0 = 0.0, c = 0.0, sf = 0.0;
+    if (!failed)
+      for (int i = 0; i < cnt; ++i) {
+        s0 += wt[i];
+        if (isfinite(tot[i])) {
+          c += 1.0;
+          sf += tot[i];
+        }
+      }
+    rec[0] = c > 0.0 ? mb : CUDART_INF;
+    rec[1] = s0;
+    rec[2] = c;
+    rec[3] = sf;
+    rec[4] = (double)a.status[b];
+    rec[5] = (double)a.bad[b];
+  }
+  for (int o = threadIdx.x; o < HD; o += blockDim.x) {
+    double s1 = 0.0, s2 = 0.0;
+    if (!failed) {
+      const int h = o / D, j = o - h * D;
+      const int hs = a.shift ? h + 1 : h;
+      const double mo = hs < H ? a.means[(size_t)b * HD + hs * D + j] : a.tail_mean;
+      const double so = hs < H ? a.sd[(size_t)b * HD + hs * D + j] : a.tail_sd;
+      for (int i = 0; i < cnt; ++i) {
+        const double w = wt[i];
+        if (w == 0.0) continue;
+        const int ng = n0 + i + a.particle_offset;
+        double dv;
+        if (ng < a.null_count)
+          dv = 0.0 - mo;
+        else if (ng == a.null_count)
+          dv = 0.0;
+        else
+          dv = (mo + so * a.eps[(size_t)(n0 + i) * HD + o]) - mo;
+        s1 += w * dv;
+        s2 += w * dv * dv;
+      }
+    }
+    rec[kRecHead + o] = s1;
+    rec[kRecHead + HD + o] = s2;
+  }
+
+  // ---- last block of this instance combines + finalizes --------------------
+  __shared__ bool s_last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned prev = atomicAdd(&a.counters[b], 1u);
+    s_last = (prev == (unsigned)(a.nblk - 1));
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  if (threadIdx.x == 0) a.counters[b] = 0u;
+  double* comb = a.finalize_inline ? (sm + 2 * a.ppb + 32 + max(a.nblk, 8))
+                                   : a.out_record + (size_t)b * reclen;
+  combine_records(a.records + (size_t)b * a.nblk * reclen, a.nblk, reclen, HD, a.beta, comb, scale,
+                  red);
+  if (!a.finalize_inline) return;
+  double* emp = comb + reclen;
+  finalize_policy(a, b, comb, emp);
+  if (b == 0 && a.dump_weights && a.status[0] == 0) {
+    __syncthreads();
+    const double m = comb[0];
+    for (int n = threadIdx.x; n < N; n += blockDim.x) {
+      const double t = a.totals[n];
+      a.dump_weights[n] = isfinite(t) ? exp(-(t - m) / a.beta) : 0.0;
+    }
+  }
+}
+
+// Finalize from R rank records (config 5, after the all-gather).
+template <typename R>
+__global__ void __launch_bounds__(kStatsThreads)
+    finalize_kernel(const __grid_constant__ StatsArgs<R> a, const double* recs, int count) {
+  extern __shared__ __align__(16) double sm[];
+  const int HD = a.H * a.D, reclen = kRecHead + 2 * HD;
+  double* red = sm;
+  double* scale = sm + 32;
+  double* comb = scale + max(count, 8);
+  double* emp = comb + reclen;
+  combine_records(recs, count, reclen, HD, a.beta, comb, scale, red);
+  finalize_policy(a, 0, comb, emp);
+}
+
+}  // namespace mppi

@@ -1,0 +1,77 @@
+// mppi_launch.cuh — host launchers for the dof-templated kernels. Each
+// precision is instantiated in its own translation unit (mppi_launch_f32.cu,
+// mppi_launch_f64.cu) so the eight dof variants compile in parallel.
+#pragma once
+
+#include "mppi_kernels.cuh"
+
+namespace mppi {
+
+template <typename R>
+cudaError_t launch_rollout_any(const RolloutArgs<R>& a, int D, long long warps, cudaStream_t st);
+template <typename R>
+cudaError_t launch_stats_any(const StatsArgs<R>& s, int D, cudaStream_t st);
+template <typename R>
+cudaError_t launch_finalize(const StatsArgs<R>& s, const double* recs, int count, cudaStream_t st);
+
+inline size_t stats_smem_bytes(int ppb, int nblk, int HD) {
+  return sizeof(double) * (2 * (size_t)ppb + 32 + (nblk > 8 ? nblk : 8) + (kRecHead + 2 * HD) + HD);
+}
+
+#ifdef MPPI_LAUNCH_IMPL
+template <typename R, int D>
+cudaError_t launch_rollout_d(const RolloutArgs<R>& a, long long warps, cudaStream_t st) {
+  const size_t smem = (size_t)kRolloutWarps * a.chain.n_caps * 6 * 32 * sizeof(R);
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(rollout_kernel<R, D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  const unsigned grid = (unsigned)((warps + kRolloutWarps - 1) / kRolloutWarps);
+  rollout_kernel<R, D><<<grid, kRolloutWarps * 32, smem, st>>>(a);
+  return cudaGetLastError();
+}
+
+template <typename R, int D>
+cudaError_t launch_stats_d(const StatsArgs<R>& s, cudaStream_t st) {
+  const size_t smem = stats_smem_bytes(s.ppb, s.nblk, s.H * D);
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(stats_kernel<R, D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  stats_kernel<R, D><<<dim3(s.nblk, s.B), kStatsThreads, smem, st>>>(s);
+  return cudaGetLastError();
+}
+
+#define MPPI_LAUNCH_SWITCH(FN, ...)                 \
+  switch (D) {                                      \
+    case 1: return FN<R, 1>(__VA_ARGS__);           \
+    case 2: return FN<R, 2>(__VA_ARGS__);           \
+    case 3: return FN<R, 3>(__VA_ARGS__);           \
+    case 4: return FN<R, 4>(__VA_ARGS__);           \
+    case 5: return FN<R, 5>(__VA_ARGS__);           \
+    case 6: return FN<R, 6>(__VA_ARGS__);           \
+    case 7: return FN<R, 7>(__VA_ARGS__);           \
+    case 8: return FN<R, 8>(__VA_ARGS__);           \
+    default: return cudaErrorInvalidValue;          \
+  }
+
+template <typename R>
+cudaError_t launch_rollout_any(const RolloutArgs<R>& a, int D, long long warps, cudaStream_t st) {
+  MPPI_LAUNCH_SWITCH(launch_rollout_d, a, warps, st)
+}
+template <typename R>
+cudaError_t launch_stats_any(const StatsArgs<R>& s, int D, cudaStream_t st) {
+  MPPI_LAUNCH_SWITCH(launch_stats_d, s, st)
+}
+template <typename R>
+cudaError_t launch_finalize(const StatsArgs<R>& s, const double* recs, int count, cudaStream_t st) {
+  const int HD = s.H * s.D;
+  const size_t smem = sizeof(double) * (32 + (count > 8 ? count : 8) + kRecHead + 2 * HD + HD);
+  finalize_kernel<R><<<1, kStatsThreads, smem, st>>>(s, recs, count);
+  return cudaGetLastError();
+}
+#endif
+
+}  // namespace mppi

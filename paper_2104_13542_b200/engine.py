@@ -1,0 +1,281 @@
+"""Python handle around one native plan (``mppi_plan`` in include/mppi_b200.h).
+
+A plan owns every device buffer of one controller batch: the packed chain and
+cost parameters, the fixed perturbation block, the per-instance policy, goal
+and state, the learned-collision weights, the world, and the captured CUDA
+graph of one control step. Controller, BatchedController, CostStack and
+evaluate_rollouts all sit on top of this class.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native as N
+from .errors import ConfigError
+
+
+@dataclass
+class PlanSpec:
+    horizon: int
+    particles: int
+    dts: np.ndarray
+    null_count: int = 2
+    instances: int = 1
+    iterations: int = 1
+    policy_mode: int = N.POLICY_PER_JOINT
+    precision: int = N.FP32
+    generator: int = N.GEN_HALTON
+    smoothing: int = N.SMOOTH_BSPLINE
+    spline_degree: int = 3
+    knots: int = 0
+    device: int = 0
+    particle_offset: int = 0
+    particles_total: int = 0
+    dump: int = 0
+    seed: int = 0
+    comb: tuple = (0.3, 0.4, 0.3)
+    gamma: float = 0.99
+    terminal_weight: float = 1.0
+    beta: float = 0.5
+    alpha_mu: float = 0.9
+    alpha_sigma: float = 0.5
+    sigma0_sq: float = 1.0
+    sigma_sq_min: float = 1e-4
+    sigma_sq_max: float = 1.0
+    default_tail: float = 0.0
+
+
+def chain_desc(chain):
+    """Build a ChainDesc; returns (desc, keepalive arrays)."""
+    keep = {
+        "axes": N.f64(chain.axes), "orot": N.f64(chain.origin_rot), "otrans": N.f64(chain.origin_trans),
+        "jtype": N.i64(chain.jtype), "lim": N.f64(chain.joint_limits),
+        "vel": N.f64(chain.velocity_limits), "acc": N.f64(chain.accel_limits),
+        "p0": N.f64(chain.cap_p0).reshape(-1, 3), "p1": N.f64(chain.cap_p1).reshape(-1, 3),
+        "r": N.f64(chain.cap_r), "link": N.i64(chain.cap_link),
+        "pa": N.i64(chain.pair_a), "pb": N.i64(chain.pair_b),
+    }
+    d = N.ChainDesc()
+    d.dof = chain.dof
+    d.task_dim = int(chain.task_dim)
+    d.n_caps = int(keep["r"].shape[0])
+    d.n_pairs = int(keep["pa"].shape[0])
+    d.axes, d.origin_rot, d.origin_trans = N.dptr(keep["axes"]), N.dptr(keep["orot"]), N.dptr(keep["otrans"])
+    d.jtype = N.lptr(keep["jtype"])
+    d.joint_limits, d.velocity_limits, d.accel_limits = N.dptr(keep["lim"]), N.dptr(keep["vel"]), N.dptr(keep["acc"])
+    d.cap_p0, d.cap_p1, d.cap_r = N.dptr(keep["p0"]), N.dptr(keep["p1"]), N.dptr(keep["r"])
+    d.cap_link, d.pair_a, d.pair_b = N.lptr(keep["link"]), N.lptr(keep["pa"]), N.lptr(keep["pb"])
+    return d, keep
+
+
+def cost_desc(weights, provider_kind: int) -> N.CostDesc:
+    c = N.CostDesc()
+    for i in range(3):
+        c.alpha_rot[i] = float(weights.alpha_rot[i])
+        c.alpha_trans[i] = float(weights.alpha_trans[i])
+    c.alpha_stop = float(weights.alpha_stop)
+    c.alpha_joint = float(weights.alpha_joint)
+    c.alpha_manip = float(weights.alpha_manip)
+    c.alpha_coll = float(weights.alpha_coll)
+    c.k_jl = float(weights.k_jl)
+    c.k_m = float(weights.k_m)
+    c.self_collision = int(provider_kind)
+    return c
+
+
+def provider_kind(provider) -> int:
+    if provider is None:
+        return N.SELFCOLL_NONE
+    kind = getattr(provider, "kind", None)
+    if kind == "oracle":
+        return N.SELFCOLL_ORACLE
+    if kind == "learned":
+        return N.SELFCOLL_LEARNED
+    raise ConfigError(f"unknown self-collision provider kind {kind!r}")
+
+
+class Plan:
+    """Owns one ``mppi_plan``. Not thread safe (like the reference Controller)."""
+
+    def __init__(self, chain, weights, spec: PlanSpec, provider=None, world=None):
+        N.require_device()
+        self.lib = N.load_library()
+        self.chain = chain
+        self.spec = spec
+        self.dof = chain.dof
+        self.kind = provider_kind(provider)
+        cd, self._keep_chain = chain_desc(chain)
+        wd = cost_desc(weights, self.kind)
+        self._dts = N.f64(spec.dts)
+        pd = N.PlanDesc()
+        for name in ("horizon", "particles", "null_count", "instances", "iterations", "policy_mode",
+                     "precision", "generator", "smoothing", "spline_degree", "knots", "device",
+                     "particle_offset", "particles_total", "dump"):
+            setattr(pd, name, int(getattr(spec, name)))
+        pd.seed = int(spec.seed) & ((1 << 64) - 1)
+        for i in range(3):
+            pd.comb[i] = float(spec.comb[i])
+        for name in ("gamma", "terminal_weight", "beta", "alpha_mu", "alpha_sigma", "sigma0_sq",
+                     "sigma_sq_min", "sigma_sq_max", "default_tail"):
+            setattr(pd, name, float(getattr(spec, name)))
+        pd.dts = N.dptr(self._dts)
+        h = C.c_void_p()
+        N.check(self.lib.mppi_plan_create(C.byref(cd), C.byref(wd), C.byref(pd), C.byref(h)))
+        self.handle = h
+        self.B = spec.instances
+        self.H = spec.horizon
+        self.N = spec.particles
+        self._cmd = np.empty((self.B, self.dof))
+        self._info = (N.StepInfo * self.B)()
+        if provider is not None and self.kind == N.SELFCOLL_LEARNED:
+            self.set_mlp(provider)
+        if world is not None:
+            self.set_world(world)
+
+    # ---------------------------------------------------------------- lifecycle
+    def close(self):
+        if getattr(self, "handle", None) is not None and self.handle.value:
+            self.lib.mppi_plan_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ---------------------------------------------------------------- setup
+    def init_noise(self):
+        N.check(self.lib.mppi_init_noise(self.handle, None))
+
+    def set_noise(self, eps):
+        eps = N.f64(eps, (self.N, self.H, self.dof))
+        N.check(self.lib.mppi_set_noise(self.handle, N.dptr(eps)))
+
+    def get_noise(self) -> np.ndarray:
+        out = np.empty((self.N, self.H, self.dof))
+        N.check(self.lib.mppi_get_noise(self.handle, N.dptr(out)))
+        return out
+
+    def set_goal(self, rotation, translation, mode: int, instance: int = -1):
+        R = N.f64(rotation, (3, 3))
+        t = N.f64(translation, (3,))
+        N.check(self.lib.mppi_set_goal(self.handle, int(instance), N.dptr(R), N.dptr(t), int(mode)))
+
+    def set_world(self, world):
+        grid = getattr(world, "voxel_grid", None)
+        sp = N.f64(world.spheres).reshape(-1, 4)
+        if grid is not None:
+            occ = np.ascontiguousarray(grid.occupancy, dtype=np.uint8)
+            nx, ny, nz = occ.shape
+            origin = N.f64(grid.origin, (3,))
+            N.check(self.lib.mppi_set_voxel_world(
+                self.handle, occ.ctypes.data_as(C.POINTER(C.c_uint8)), nx, ny, nz, N.dptr(origin),
+                float(grid.voxel), N.dptr(sp), sp.shape[0]))
+        else:
+            bx = N.f64(world.boxes).reshape(-1, 6)
+            N.check(self.lib.mppi_set_world(self.handle, N.dptr(sp), sp.shape[0], N.dptr(bx), bx.shape[0]))
+
+    def set_mlp(self, provider):
+        net = provider.net
+        Ws = [N.f64(w) for w in net.weights]
+        bs = [N.f64(b) for b in net.biases]
+        if len(Ws) != 4 or Ws[0].shape[1] != 256 or Ws[1].shape != (256, 128) or Ws[2].shape != (128, 64) \
+                or Ws[3].shape != (64, 1):
+            raise ConfigError("surrogate must be the (2d)->256->128->64->1 net of surrogate.py:21")
+        args = []
+        for W, b in zip(Ws, bs):
+            args += [N.dptr(W), N.dptr(b)]
+        self._keep_mlp = (Ws, bs)
+        N.check(self.lib.mppi_set_mlp(self.handle, Ws[0].shape[0], *args))
+
+    def set_policy(self, means, variances, instance: int = 0):
+        m = N.f64(means, (self.H, self.dof))
+        v = N.f64(variances)
+        if v.ndim == 1:  # isotropic storage is replicated per joint
+            v = np.repeat(v[:, None], self.dof, axis=1)
+        v = np.ascontiguousarray(v.reshape(self.H, self.dof))
+        N.check(self.lib.mppi_set_policy(self.handle, int(instance), N.dptr(m), N.dptr(v)))
+
+    def get_policy(self, instance: int = 0):
+        m = np.empty((self.H, self.dof))
+        v = np.empty((self.H, self.dof))
+        N.check(self.lib.mppi_get_policy(self.handle, int(instance), N.dptr(m), N.dptr(v)))
+        return m, v
+
+    # ---------------------------------------------------------------- hot path
+    def step(self, theta, theta_dot):
+        """One control step for all instances. Returns (commands (B,d), infos)."""
+        th = N.f64(theta, (self.B, self.dof))
+        thd = N.f64(theta_dot, (self.B, self.dof))
+        N.check(self.lib.mppi_step(self.handle, N.dptr(th), N.dptr(thd), N.dptr(self._cmd), self._info))
+        return self._cmd.copy(), [self._info[b] for b in range(self.B)]
+
+    def evaluate(self, mode: int, inputs0, inputs1, dts, gamma, terminal_weight, theta0=None,
+                 theta_dot0=None, want=("positions", "velocities", "accelerations", "step_costs",
+                                        "terms", "totals")):
+        in0 = N.f64(inputs0)
+        n, H, d = in0.shape
+        in1 = N.f64(inputs1) if inputs1 is not None else None
+        out = N.EvalOut()
+        res = {}
+        shapes = {"positions": (n, H, d), "velocities": (n, H, d), "accelerations": (n, H, d),
+                  "step_costs": (n, H), "terms": (6, n, H), "totals": (n,)}
+        for k in want:
+            res[k] = np.empty(shapes[k])
+            setattr(out, k, N.dptr(res[k]))
+        dts = N.f64(dts)
+        th0 = N.f64(theta0) if theta0 is not None else None
+        thd0 = N.f64(theta_dot0) if theta_dot0 is not None else None
+        rc = self.lib.mppi_evaluate(self.handle, int(mode), n, H, N.dptr(dts), float(gamma),
+                                    float(terminal_weight), N.dptr(th0), N.dptr(thd0), N.dptr(in0),
+                                    N.dptr(in1), C.byref(out))
+        N.check(rc)
+        res["quarantined"] = int(out.quarantined)
+        return res
+
+    def get_bundle(self) -> dict:
+        """Instance 0's last-iteration bundle (plan created with dump=1)."""
+        n, H, d = self.N, self.H, self.dof
+        res = {"positions": np.empty((n, H, d)), "velocities": np.empty((n, H, d)),
+               "accelerations": np.empty((n, H, d)), "step_costs": np.empty((n, H)),
+               "terms": np.empty((6, n, H)), "totals": np.empty(n), "weights": np.empty(n)}
+        out = N.EvalOut()
+        for k in ("positions", "velocities", "accelerations", "step_costs", "terms", "totals"):
+            setattr(out, k, N.dptr(res[k]))
+        N.check(self.lib.mppi_get_bundle(self.handle, C.byref(out), N.dptr(res["weights"])))
+        from .costs import TERM_NAMES
+
+        return {"positions": res["positions"], "velocities": res["velocities"],
+                "accelerations": res["accelerations"], "step_costs": res["step_costs"],
+                "term_breakdown": {nm: res["terms"][i] for i, nm in enumerate(TERM_NAMES)},
+                "total_per_particle": res["totals"], "weights": res["weights"]}
+
+    def mlp_forward(self, q) -> np.ndarray:
+        q = N.f64(q).reshape(-1, self.dof)
+        out = np.empty(q.shape[0])
+        N.check(self.lib.mppi_mlp_forward(self.handle, N.dptr(q), q.shape[0], N.dptr(out)))
+        return out
+
+    # ---------------------------------------------------------------- sharded update
+    def record_len(self) -> int:
+        n = C.c_int32(0)
+        N.check(self.lib.mppi_stats_record_len(self.handle, C.byref(n)))
+        return int(n.value)
+
+    def stats_dev(self, theta, theta_dot, record_ptr: int, stream_ptr: int = 0):
+        th = N.f64(theta, (self.dof,)) if theta is not None else None
+        thd = N.f64(theta_dot, (self.dof,)) if theta_dot is not None else None
+        N.check(self.lib.mppi_stats_dev(self.handle, N.dptr(th), N.dptr(thd), C.c_void_p(record_ptr),
+                                        C.c_void_p(stream_ptr or None)))
+
+    def finalize_dev(self, records_ptr: int, n_records: int, stream_ptr: int = 0):
+        cmd = np.empty(self.dof)
+        info = N.StepInfo()
+        N.check(self.lib.mppi_finalize_dev(self.handle, C.c_void_p(records_ptr), int(n_records),
+                                           N.dptr(cmd), C.byref(info), C.c_void_p(stream_ptr or None)))
+        return cmd, info

@@ -1,0 +1,212 @@
+"""Generate the golden fixtures by running the REFERENCE itself.
+
+Build container only (needs /root/reference; the GPU box never runs this):
+
+    PYTHONPATH=/root/reference/pkg/src NUMBA_CACHE_DIR=/tmp/numba_cache \
+        python tests/golden/make_golden.py
+
+Writes tests/golden/*.npz. Every array is the reference's own output on the
+named inputs (numba backend, the reference default), so the oracle and the CUDA
+path are both pinned to the reference, not to each other.
+"""
+
+from __future__ import annotations
+
+import sys
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parents[2]
+sys.path.insert(0, str(ROOT))
+OUT = Path(__file__).resolve().parent
+
+import jointmpc  # noqa: E402  (the reference)
+from jointmpc import kernels as rk  # noqa: E402
+from jointmpc.controller import Controller  # noqa: E402
+from jointmpc.costs import FULL_POSE, CostWeights, GoalSpec, goal_at_position  # noqa: E402
+from jointmpc.kinematics import Pose, _rpy_matrix, load_chain  # noqa: E402
+from jointmpc.policy import (UpdateConfig, make_policy, particle_weights, shift,  # noqa: E402
+                             update_covariance, update_mean)
+from jointmpc.rollout import JointState, evaluate_rollouts, make_dt_schedule  # noqa: E402
+from jointmpc.sampling import (HALTON, SmoothingSpec, bspline_basis, gaussianize,  # noqa: E402
+                               halton_points, smooth_sequences)
+from jointmpc.simworld import WorldModel, sim_step  # noqa: E402
+from jointmpc.surrogate import LearnedSelfCollision  # noqa: E402
+
+from paper_2104_13542_b200 import configs  # noqa: E402  (numbers only)
+
+SURR = ROOT / "paper_2104_13542_b200" / "data" / "arm7_surrogate.npz"
+print("reference backend:", rk.BACKEND_NAME, file=sys.stderr)
+
+
+def random_q(chain, rng, n, margin=0.05):
+    lo, hi = chain.joint_limits[:, 0], chain.joint_limits[:, 1]
+    span = hi - lo
+    return rng.uniform(lo + margin * span, hi - margin * span, size=(n, chain.dof))
+
+
+def save(name, **arrays):
+    np.savez_compressed(OUT / f"{name}.npz", **arrays)
+    print("wrote", name, {k: np.shape(v) for k, v in arrays.items()}, file=sys.stderr)
+
+
+def sampling_fixtures():
+    rng = np.random.default_rng(1234)
+    p = np.concatenate([rng.random(200), [0.0, 1e-12, 0.01, 0.02424, 0.02426, 0.5, 0.97574, 0.97576,
+                                          0.99, 1.0 - 1e-12]])
+    comb_in = rng.standard_normal((5, 12, 2))
+    spline_knots = rng.standard_normal((6, 5, 3))
+    arm7 = load_chain("arm7.chain")
+    c = Controller(arm7, goal_at_position([0.4, 0.2, 0.5]), horizon=30, particles=48, seed=0)
+    save("sampling",
+         halton=halton_points(600, 7), gauss_p=p, gauss=gaussianize(p),
+         basis_30_5=bspline_basis(30, 5, 3), basis_24_6=bspline_basis(24, 6, 3),
+         basis_7_4_2=bspline_basis(7, 4, 2),
+         comb_in=comb_in, comb_out=smooth_sequences(comb_in, SmoothingSpec(mode="comb"), 12),
+         spline_knots=spline_knots,
+         spline_out=smooth_sequences(spline_knots, SmoothingSpec(mode="bspline", knots_per_horizon=5), 30),
+         fixed_eps_arm7_48=c._fixed_eps)
+
+
+def kinematics_fixtures():
+    rng = np.random.default_rng(7)
+    out = {}
+    for name, n in (("arm7", 96), ("planar2", 64), ("slider1", 16)):
+        ch = load_chain(f"{name}.chain")
+        q = random_q(ch, rng, n)
+        rot, trans = rk.fk_batch(q, ch.axes, ch.origin_rot, ch.origin_trans, ch.jtype)
+        J = rk.jacobian_batch(q, rot, trans, ch.axes, ch.jtype)
+        out[f"{name}_q"] = q
+        out[f"{name}_rot"] = rot
+        out[f"{name}_trans"] = trans
+        out[f"{name}_J"] = J
+        out[f"{name}_manip"] = rk.manip_batch(J, ch.task_dim)
+        out[f"{name}_self"] = rk.self_collision_batch(rot, trans, ch.cap_p0, ch.cap_p1, ch.cap_r,
+                                                      ch.cap_link, ch.pair_a, ch.pair_b)
+    # env collision: arm7 against spheres + boxes placed around its workspace
+    ch = load_chain("arm7.chain")
+    q = random_q(ch, rng, 256)
+    rot, trans = rk.fk_batch(q, ch.axes, ch.origin_rot, ch.origin_trans, ch.jtype)
+    spheres = np.array([[0.3, 0.0, 0.5, 0.15], [-0.2, 0.3, 0.8, 0.1], [0.0, -0.4, 0.3, 0.2]])
+    boxes = np.array([[0.2, -0.2, 0.0, 0.6, 0.2, 0.3], [-0.6, -0.6, 0.6, -0.2, -0.1, 1.0],
+                      [0.1, 0.3, 0.7, 0.5, 0.6, 1.1]])
+    out["env_q"] = q
+    out["env_spheres"] = spheres
+    out["env_boxes"] = boxes
+    out["env_hit"] = rk.env_collision_batch(rot, trans, ch.cap_p0, ch.cap_p1, ch.cap_r, ch.cap_link,
+                                            spheres, boxes)
+    out["env_hit_boxes_only"] = rk.env_collision_batch(rot, trans, ch.cap_p0, ch.cap_p1, ch.cap_r,
+                                                       ch.cap_link, np.zeros((0, 4)), boxes)
+    # integration
+    u = rng.standard_normal((9, 11, 3)) * 3.0
+    dts = make_dt_schedule(11, 0.05, "two_phase").dts
+    th0, thd0 = rng.standard_normal(3), rng.standard_normal(3)
+    pos, vel = rk.integrate_batch(u, dts, th0, thd0)
+    out.update(int_u=u, int_dts=dts, int_th0=th0, int_thd0=thd0, int_pos=pos, int_vel=vel)
+    save("kinematics", **out)
+
+
+def mlp_fixtures():
+    surr = LearnedSelfCollision.load(SURR)
+    arm7 = load_chain("arm7.chain")
+    q = random_q(arm7, np.random.default_rng(11), 512, margin=0.0)
+    save("mlp", q=q, dist=surr.distance(q))
+
+
+def policy_fixtures():
+    rng = np.random.default_rng(5)
+    totals = np.concatenate([rng.random(60) * 50 + 1000, [np.inf, np.inf]])
+    w = particle_weights(totals, beta=0.7)
+    pol = make_policy(6, 3, 0.8)
+    pol.means[:] = rng.standard_normal((6, 3))
+    u = rng.standard_normal((62, 6, 3))
+    cfg = UpdateConfig(sigma_sq_min=0.05, sigma_sq_max=2.0)
+    m1 = update_mean(pol, u, w, 0.9)
+    c1 = update_covariance(m1, u, w, 0.5, cfg)
+    iso = make_policy(6, 3, 0.8, mode="isotropic")
+    iso_m = update_mean(iso, u, w, 0.7)
+    iso_c = update_covariance(iso_m, u, w, 0.4, cfg)
+    sh = shift(c1, 0.25)
+    save("policy", totals=totals, weights=w, means0=pol.means, var0=pol.variances, controls=u,
+         means1=m1.means, var1=c1.variances, iso_means=iso_m.means, iso_var=iso_c.variances,
+         shift_means=sh.means, shift_var=sh.variances)
+
+
+def reach_controller(config, particles=500, world=None, **kw):
+    arm7 = load_chain("arm7.chain")
+    wts = configs.WEIGHTS[config]
+    weights = CostWeights(**wts)
+    goal = GoalSpec(target_pose=Pose(rotation=_rpy_matrix(*configs.REACH_GOAL_RPY),
+                                     translation=configs.REACH_GOAL_POS.copy()), mode=FULL_POSE)
+    ckw = dict(configs.CONTROLLER_KW)
+    ckw["particles"] = particles
+    ckw.update(kw)
+    provider = LearnedSelfCollision.load(SURR) if config == 2 else None
+    return Controller(arm7, goal, weights=weights, self_collision=provider, world=world, **ckw)
+
+
+def step_fixture(name, config, particles=500, steps=3, world=None, **kw):
+    """Reference control steps from the reach start; step 0's full outputs plus
+    the command / policy sequence of `steps` closed-loop steps (plant = sim_step)."""
+    c = reach_controller(config, particles, world=world, **kw)
+    state = JointState(theta=configs.REACH_START.copy(), theta_dot=np.zeros(7), theta_ddot=np.zeros(7))
+    rec = {"eps": c._fixed_eps}
+    cmds, means, variances, thetas, thetadots, best, mean = [], [], [], [], [], [], []
+    for i in range(steps):
+        thetas.append(state.theta.copy())
+        thetadots.append(state.theta_dot.copy())
+        cmd, diag = c.control_step(state)
+        assert diag.fallback == "", diag.fallback
+        cmds.append(cmd)
+        means.append(c.policy.means.copy())
+        variances.append(c.policy.variances.copy())
+        best.append(diag.best_cost)
+        mean.append(diag.mean_cost)
+        if i == 0:
+            b = diag.bundle
+            rec.update(step_costs=b.step_costs, totals=b.total_per_particle,
+                       weights=particle_weights(b.total_per_particle, c.update_cfg.beta),
+                       positions_head=b.positions[:16], velocities_head=b.velocities[:16],
+                       controls_head=b.accelerations[:16])
+            for k, v in b.term_breakdown.items():
+                rec[f"term_{k}"] = v
+        state = sim_step(state, cmd, 0.05)
+    rec.update(theta=np.array(thetas), theta_dot=np.array(thetadots), command=np.array(cmds),
+               means=np.array(means), variances=np.array(variances), best_cost=np.array(best),
+               mean_cost=np.array(mean))
+    save(name, **rec)
+
+
+def world_fixture():
+    """Config-3-like world: boxes from a seeded voxel grid (the same boxes the
+    GPU gets as a grid), position-only goal, N=128."""
+    from paper_2104_13542_b200.simworld import seeded_box_grid
+
+    grid_world = seeded_box_grid(n_boxes=8, dims=64, seed=3, max_extent=10)
+    world = WorldModel(spheres=np.array([[0.35, 0.25, 0.55, 0.08]]), boxes=grid_world.boxes,
+                       bounds_min=np.full(3, -1.0), bounds_max=np.full(3, 1.0))
+    c = reach_controller(3, particles=128, world=world)
+    c.cost_stack.goal = goal_at_position([0.45, 0.1, 0.55])
+    state = JointState(theta=configs.REACH_START.copy(), theta_dot=np.zeros(7), theta_ddot=np.zeros(7))
+    cmd, diag = c.control_step(state)
+    b = diag.bundle
+    save("step_world", occupancy=grid_world.voxel_grid.occupancy, boxes=grid_world.boxes,
+         spheres=world.spheres, goal=np.array([0.45, 0.1, 0.55]), command=cmd,
+         means=c.policy.means, variances=c.policy.variances, totals=b.total_per_particle,
+         step_costs=b.step_costs, term_envcoll=b.term_breakdown["envcoll"],
+         term_stop=b.term_breakdown["stop"], term_pose=b.term_breakdown["pose"])
+
+
+if __name__ == "__main__":
+    which = set(sys.argv[1:])
+    jobs = {"sampling": sampling_fixtures, "kinematics": kinematics_fixtures, "mlp": mlp_fixtures,
+            "policy": policy_fixtures,
+            "step_c1": lambda: step_fixture("step_c1", 1),
+            "step_c2": lambda: step_fixture("step_c2", 2),
+            "step_c2_iso_k2": lambda: step_fixture("step_c2_iso_k2", 2, particles=256, steps=2,
+                                                   policy_mode="isotropic", iterations=2),
+            "step_world": world_fixture}
+    for name, fn in jobs.items():
+        if not which or name in which:
+            fn()
