@@ -1,0 +1,336 @@
+"""Benchmark: MPC step latency of the B200 MPPI step (BASELINE config 2).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--workload c2|c1|c4]
+
+Workload (default ``c2``, BASELINE configs[1]): arm7 (the reference's Franka
+model) reach task, 500 particles x H=30, full cost stack (pose, joint limits,
+braking envelope, manipulability, learned self-collision MLP), Halton +
+B-spline sampling, FP32 fused rollout. A "step" is one Controller.control_step
+(shift + sample + rollout/costs + MLP + weights/update + command).
+
+* value: mean device time of the step's CUDA-graph replay (CUDA events on the
+  plan stream), L2 flushed (256 MiB memset) before every timed step.
+* e2e: mean wall time of Controller.control_step (the public API) with host
+  buffers: H2D of the joint state, graph replay, D2H of command + status.
+* roofline: dominant kernel of the step, timed by event-record nodes inside
+  the same timed graph replays.
+* cpu_baseline: the unmodified reference (oracle/_ref, numba backend) timed
+  on this host on a bounded sample of the same workload.
+
+Multi-GPU (torchrun, N>1): config 1-3 controllers do not shard,
+so each rank runs an independent replica; the reported latency is the max over
+ranks. ``--workload c4`` is the batched-controller throughput config instead.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "MPC step latency (ms) @500×H30 Franka; particle-steps/sec at 1/2/4/8 GPUs"
+
+
+def _peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return d, "measured"
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0,
+            "sm_max_mhz": 1965.0}, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 7:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx = max(mx, float(f[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[3:7]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def _dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def _maybe_init_dist(ws, local):
+    if ws <= 1:
+        return None
+    import torch
+    import torch.distributed as dist
+
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return dist
+
+
+def _max_over_ranks(dist, x: float, local: int) -> float:
+    if dist is None:
+        return x
+    import torch
+
+    t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{local}")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+# ---------------------------------------------------------------- reference arm
+def _reference_controller(particles=500, workers=None):
+    """The unmodified reference, config 2, from oracle/_ref (bench-only)."""
+    sys.path.insert(0, str(ROOT / "oracle" / "_ref"))
+    os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/numba_cache_bench")
+    from jointmpc.controller import Controller
+    from jointmpc.costs import FULL_POSE, CostWeights, GoalSpec
+    from jointmpc.kinematics import Pose, _rpy_matrix, load_chain
+    from jointmpc.rollout import JointState
+    from jointmpc.surrogate import LearnedSelfCollision
+
+    from paper_2104_13542_b200 import configs
+
+    kw = dict(configs.CONTROLLER_KW)
+    kw["particles"] = particles
+    kw["workers"] = workers or (os.cpu_count() or 1)
+    goal = GoalSpec(target_pose=Pose(rotation=_rpy_matrix(*configs.REACH_GOAL_RPY),
+                                     translation=configs.REACH_GOAL_POS.copy()), mode=FULL_POSE)
+    surr = LearnedSelfCollision.load(ROOT / "paper_2104_13542_b200" / "data" / "arm7_surrogate.npz")
+    c = Controller(load_chain("arm7.chain"), goal, weights=CostWeights(**configs.WEIGHTS[2]),
+                   self_collision=surr, **kw)
+    st = JointState(theta=configs.REACH_START.copy(), theta_dot=np.zeros(7), theta_ddot=np.zeros(7))
+    return c, st
+
+
+def _have_reference() -> bool:
+    return (ROOT / "oracle" / "_ref" / "jointmpc" / "controller.py").exists()
+
+
+def _time_reference(steps: int, warmup: int, budget_s: float | None = None):
+    c, st = _reference_controller()
+    for _ in range(max(1, warmup)):
+        c.control_step(st)
+    lat = []
+    t_end = time.perf_counter() + budget_s if budget_s else None
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        c.control_step(st)
+        lat.append((time.perf_counter() - t0) * 1e3)
+        if t_end and time.perf_counter() > t_end and len(lat) >= 5:
+            break
+    return lat, c.workers
+
+
+def run_reference(args):
+    ws, rank, _ = _dist_env()
+    if rank != 0:
+        return 0
+    if not _have_reference():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref missing (run oracle/build_ref.py)"}))
+        return 0
+    lat, workers = _time_reference(args.steps, args.warmup)
+    v = float(np.mean(lat))
+    cores = os.cpu_count() or 1
+    line = {
+        "metric": METRIC, "value": v, "unit": "ms", "n_gpus": ws, "steps": len(lat), "warmup": args.warmup,
+        "ms_per_step": v, "higher_is_better": False, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "config2: arm7 reach, full cost stack + learned MLP, 500 particles x H30",
+                   "particles": 500, "horizon": 30},
+        "impl": "reference",
+        "cpu_baseline": {"value": v, "unit": "ms", "cores": cores, "kind": "reference",
+                         "sample": f"{len(lat)} control_steps of config 2 after {args.warmup} warm-up, "
+                                   f"numba backend, workers={workers}"},
+        "e2e": {"value": v, "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "median_ms": float(np.median(lat)),
+    }
+    print(json.dumps(line))
+    return 0
+
+
+# ---------------------------------------------------------------- our arm
+def _flush_l2(buf):
+    buf.zero_()
+
+
+def run_ours(args):
+    ws, rank, local = _dist_env()
+    dist = _maybe_init_dist(ws, local)
+    import torch
+
+    torch.cuda.set_device(local)
+    from paper_2104_13542_b200 import configs
+    from paper_2104_13542_b200 import _native as N
+
+    N.require_device()
+    peaks, peaks_kind = _peaks()
+    particles = args.particles
+    config = 1 if args.workload == "c1" else 2
+    ctrl = configs.make_controller(config, particles=particles, device=local, precision=args.precision)
+    plan = ctrl.plan
+    st = configs.start_state()
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=f"cuda:{local}")
+
+    for _ in range(max(3, args.warmup)):
+        ctrl.control_step(st)
+
+    # ---- device-timed loop (value): graph replay between CUDA events, L2 flushed before each step
+    dev_ms, stages = [], {"sample": [], "rollout": [], "mlp": [], "update": []}
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize()
+    theta = st.theta[None, :]
+    thetad = st.theta_dot[None, :]
+    with ClockSampler(local) as clk:
+        t_wall0 = time.perf_counter()
+        for _ in range(args.steps):
+            _flush_l2(flush)
+            torch.cuda.synchronize()
+            _, infos = plan.step(theta, thetad)
+            inf = infos[0]
+            dev_ms.append(inf.device_ms)
+            stages["sample"].append(inf.sample_ms)
+            stages["rollout"].append(inf.rollout_ms)
+            stages["mlp"].append(inf.mlp_ms)
+            stages["update"].append(inf.update_ms)
+        torch.cuda.synchronize()
+        t_wall = time.perf_counter() - t_wall0
+    if dist is not None:
+        dist.barrier()
+    value_local = float(np.mean(dev_ms))
+    value = _max_over_ranks(dist, value_local, local)
+
+    # ---- end to end through the public API (Controller.control_step, host buffers)
+    e2e = []
+    for _ in range(args.steps):
+        _flush_l2(flush)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        ctrl.control_step(st)
+        e2e.append((time.perf_counter() - t0) * 1e3)
+    e2e_v = _max_over_ranks(dist, float(np.mean(e2e)), local)
+
+    # ---- roofline of the dominant kernel (stage times from the timed replays)
+    from paper_2104_13542_b200 import roofline as RL
+
+    st_mean = {k: float(np.mean(v)) for k, v in stages.items()}
+    rows = particles * 30
+    roof = RL.step_roofline(st_mean, rows=rows, particles=particles, horizon=30, dof=7, config=config,
+                            peaks=peaks, peaks_kind=peaks_kind)
+
+    line = {
+        "metric": METRIC, "value": value, "unit": "ms", "n_gpus": ws, "steps": args.steps,
+        "warmup": max(3, args.warmup), "ms_per_step": value, "higher_is_better": False,
+        "scaling": "weak", "vs_baseline": None, "dtype": args.precision.replace("fp", "f"),
+        "data": "synthetic (bundled arm7 chain, reach goal, Halton perturbations, trained surrogate)",
+        "config": {"workload": f"config{config}: arm7 reach, "
+                               + ("full cost stack + learned self-collision MLP" if config == 2
+                                  else "goal pose + joint limits")
+                               + f", {particles} particles x H30, K=1",
+                   "particles": particles, "horizon": 30, "iterations": 1,
+                   "parallelism": "replicas" if ws > 1 else "single",
+                   "l2": "flushed (256 MiB memset) before every timed step"},
+        "particle_steps_per_s": ws * particles * 30 / (value * 1e-3),
+        "median_ms": float(np.median(dev_ms)), "p99_ms": float(np.percentile(dev_ms, 99)),
+        "stage_ms": st_mean,
+        "e2e": {"value": e2e_v, "unit": "ms", "h2d_bytes_per_step": 2 * 7 * 8,
+                "d2h_bytes_per_step": 7 * 8 + 80, "median_ms": float(np.median(e2e)),
+                "api": "Controller.control_step"},
+        "gpu_launches": args.steps * (3 if config == 2 else 2),
+        "roofline": roof,
+        "clocks": clk.summary(),
+        "timed_wall_s": t_wall,
+    }
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = _cpu_baseline(args)
+    if rank == 0:
+        print(json.dumps(line))
+    if dist is not None:
+        dist.destroy_process_group()
+    return 0
+
+
+def _cpu_baseline(args):
+    if not _have_reference():
+        return {"value": None, "unit": "ms", "cores": os.cpu_count(), "kind": "reference",
+                "sample": "unavailable: oracle/_ref missing"}
+    lat, workers = _time_reference(steps=30, warmup=2, budget_s=20.0)
+    return {"value": float(np.median(lat)), "unit": "ms", "cores": os.cpu_count() or 1, "kind": "reference",
+            "sample": f"median of {len(lat)} reference control_steps (config 2, 500x30, numba, "
+                      f"workers={workers}) after 2 warm-up steps"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="c2", choices=["c1", "c2"])
+    ap.add_argument("--particles", type=int, default=500)
+    ap.add_argument("--precision", default="fp32", choices=["fp32", "fp64"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

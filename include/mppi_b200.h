@@ -195,6 +195,12 @@ typedef struct mppi_step_info {
   double best_cost;           /* min finite total                            */
   double mean_cost;           /* mean finite total                           */
   double device_ms;           /* CUDA-event time of the step on the stream   */
+  /* per-stage device times inside the captured graph (event-record nodes),
+   * summed over the K iterations */
+  double sample_ms;
+  double rollout_ms;
+  double mlp_ms;
+  double update_ms;
 } mppi_step_info;
 
 /* Outputs of mppi_evaluate (RolloutBundle, rollout.py:84-91). Any pointer may
@@ -273,6 +279,13 @@ int mppi_evaluate(mppi_plan* plan, int32_t mode, int32_t n, int32_t horizon,
 /* Instance 0's RolloutBundle of the last iteration of the last mppi_step
  * (plan created with dump = 1), plus the particle weights (N,). */
 int mppi_get_bundle(mppi_plan* plan, mppi_eval_out* out, double* weights);
+
+/* Benchmark hook: launch one stage of the step `reps` times back to back on
+ * the plan stream between two CUDA events and report the mean device time per
+ * launch. stage 0 = rollout kernel, 1 = learned-collision MLP, 2 = statistics
+ * + update, 3 = the whole captured step graph. Perturbs the plan's policy
+ * (the update runs `reps` times); call it after the steps you care about. */
+int mppi_time_stage(mppi_plan* plan, int32_t stage, int32_t reps, double* ms_per_launch);
 
 /* ---- particle-sharded update (config 5) -------------------------------- */
 /* Size in doubles of one rank's statistics record for this plan. */

@@ -84,7 +84,8 @@ class StepInfo(C.Structure):
     _fields_ = [
         ("status", C.c_int32), ("bad_particle", C.c_int32), ("finite_count", C.c_int32),
         ("_pad", C.c_int32), ("best_cost", C.c_double), ("mean_cost", C.c_double),
-        ("device_ms", C.c_double),
+        ("device_ms", C.c_double), ("sample_ms", C.c_double), ("rollout_ms", C.c_double),
+        ("mlp_ms", C.c_double), ("update_ms", C.c_double),
     ]
 
 
@@ -119,6 +120,7 @@ _SIGS = {
     "mppi_evaluate": (C.c_int, [_vp, C.c_int32, C.c_int32, C.c_int32, _dp, C.c_double, C.c_double,
                                 _dp, _dp, _dp, _dp, C.POINTER(EvalOut)]),
     "mppi_get_bundle": (C.c_int, [_vp, C.POINTER(EvalOut), _dp]),
+    "mppi_time_stage": (C.c_int, [_vp, C.c_int32, C.c_int32, _dp]),
     "mppi_stats_record_len":(C.c_int, [_vp, C.POINTER(C.c_int32)]),
     "mppi_stats_dev": (C.c_int, [_vp, _dp, _dp, _vp, _vp]),
     "mppi_finalize_dev": (C.c_int, [_vp, _vp, C.c_int32, _dp, C.POINTER(StepInfo), _vp]),

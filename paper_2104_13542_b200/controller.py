@@ -10,7 +10,7 @@ Differences from the reference, by design:
   * ``workers`` is accepted and ignored (particles map to warps, not threads);
   * ``diag.bundle`` is a lazily fetched view of the last iteration's device
     dump (pass ``keep_bundle=True`` to have the graph write it);
-  * per-stage times are device event times of the whole step.
+  * per-stage times are device event times (event-record nodes in the step graph).
 """
 
 from __future__ import annotations
@@ -215,8 +215,9 @@ class Controller:
         if latency > self.latency_budget * 1e3:
             log.debug("control step overran budget: %.2f ms", latency)
         bundle = LazyBundle(self, self._step_serial) if self.keep_bundle else None
-        return command, StepDiagnostics(latency_ms=latency, sample_ms=0.0, rollout_ms=info.device_ms,
-                                        update_ms=0.0, best_cost=float(info.best_cost),
+        return command, StepDiagnostics(latency_ms=latency, sample_ms=info.sample_ms,
+                                        rollout_ms=info.rollout_ms + info.mlp_ms,
+                                        update_ms=info.update_ms, best_cost=float(info.best_cost),
                                         mean_cost=float(info.mean_cost), bundle=bundle)
 
     def instantaneous_costs(self, state: JointState):

@@ -178,6 +178,7 @@ struct mppi_plan {
   // graph
   cudaGraphExec_t graph = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  std::vector<cudaEvent_t> stage_ev;
   unsigned long long step_counter = 0;
   int sharded_iter = 0;
   // eval scratch
@@ -282,7 +283,8 @@ void choose_blocks(int N, int& ppb, int& nblk) {
 // Enqueue one optimisation iteration (rollout -> [MLP] -> statistics) for all
 // B instances. `inline_final` false writes the rank record instead.
 template <typename R>
-int enqueue_iteration(mppi_plan* p, int it, bool inline_final, double* out_record, cudaStream_t st) {
+int enqueue_iteration(mppi_plan* p, int it, bool inline_final, double* out_record, cudaStream_t st,
+                      unsigned stages = 7u) {
   RolloutArgs<R> a;
   rollout_static<R>(p, p->H, p->dts.data(), a);
   a.N = p->N;
@@ -310,8 +312,8 @@ int enqueue_iteration(mppi_plan* p, int it, bool inline_final, double* out_recor
     a.out_acc = p->d_acc.p;
     a.out_terms = p->d_terms.p;
   }
-  CK(launch_rollout_any<R>(a, p->D, (long long)p->B * p->N, st));
-  if (p->learned()) CK(mlp_forward(p->mlp, p->mlp_x.p, (long long)p->B * p->N * p->H, p->mlp_d.p, st));
+  if (stages & 1u) CK(launch_rollout_any<R>(a, p->D, (long long)p->B * p->N, st));
+  if ((stages & 2u) && p->learned()) CK(mlp_forward(p->mlp, p->mlp_x.p, (long long)p->B * p->N * p->H, p->mlp_d.p, st));
   StatsArgs<R> s;
   stats_static<R>(p, p->H, p->gamma, p->tw, s);
   s.N = p->N;
@@ -343,7 +345,7 @@ int enqueue_iteration(mppi_plan* p, int it, bool inline_final, double* out_recor
     s.dump_terms = p->d_terms.p;
     s.dump_weights = inline_final ? p->d_w.p : nullptr;
   }
-  CK(launch_stats_any<R>(s, p->D, st));
+  if (stages & 4u) CK(launch_stats_any<R>(s, p->D, st));
   return MPPI_OK;
 }
 
@@ -371,13 +373,24 @@ int enqueue_step_body(mppi_plan* p, cudaStream_t st) {
   CK(cudaMemsetAsync(p->bad.p, 0x7f, sizeof(int) * B, st));
   CK(cudaMemcpyAsync(p->state.p, p->h_state, sizeof(double) * B * 2 * D, cudaMemcpyHostToDevice, st));
   CK(cudaMemcpyAsync(p->stepctr.p, p->h_ctr, sizeof(unsigned long long), cudaMemcpyHostToDevice, st));
+  // event-record nodes between the stages give per-kernel device times of
+  // every replayed step (mppi_step_info.*_ms)
+  auto mark = [&](int i) -> int {
+    CK(cudaEventRecordWithFlags(p->stage_ev[i], st, cudaEventRecordExternal));
+    return MPPI_OK;
+  };
   for (int it = 0; it < p->iters; ++it) {
+    CKR(mark(4 * it + 0));
     CKR(enqueue_sampling(p, it, st));
-    if (p->precision == MPPI_FP64)
-      CKR(enqueue_iteration<double>(p, it, true, nullptr, st));
-    else
-      CKR(enqueue_iteration<float>(p, it, true, nullptr, st));
+    for (int sg = 0; sg < 3; ++sg) {
+      CKR(mark(4 * it + 1 + sg));
+      if (p->precision == MPPI_FP64)
+        CKR(enqueue_iteration<double>(p, it, true, nullptr, st, 1u << sg));
+      else
+        CKR(enqueue_iteration<float>(p, it, true, nullptr, st, 1u << sg));
+    }
   }
+  CKR(mark(4 * p->iters));
   CK(cudaMemcpyAsync(p->h_cmd, p->cmd.p, sizeof(double) * B * D, cudaMemcpyDeviceToHost, st));
   CK(cudaMemcpyAsync(p->h_info, p->info.p, sizeof(mppi_step_info) * B, cudaMemcpyDeviceToHost, st));
   return MPPI_OK;
@@ -508,6 +521,8 @@ int mppi_plan_create(const mppi_chain_desc* chain, const mppi_cost_desc* costs,
     CK(cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking));
     CK(cudaEventCreate(&p->ev0));
     CK(cudaEventCreate(&p->ev1));
+    p->stage_ev.assign(4 * p->iters + 1, nullptr);
+    for (auto& e : p->stage_ev) CK(cudaEventCreate(&e));
     const int B = p->B, D = p->D, H = p->H, N = p->N;
     const size_t HD = (size_t)H * D;
     choose_blocks(N, p->ppb, p->nblk);
@@ -621,6 +636,7 @@ int mppi_plan_destroy(mppi_plan* p) {
   if (p->h_info) cudaFreeHost(p->h_info);
   if (p->ev0) cudaEventDestroy(p->ev0);
   if (p->ev1) cudaEventDestroy(p->ev1);
+  for (auto e : p->stage_ev) cudaEventDestroy(e);
   if (p->stream) cudaStreamDestroy(p->stream);
   delete p;
   return MPPI_OK;
@@ -846,7 +862,20 @@ int mppi_step(mppi_plan* p, const double* theta, const double* theta_dot, double
   memcpy(command_out, p->h_cmd, sizeof(double) * B * D);
   if (info) {
     memcpy(info, p->h_info, sizeof(mppi_step_info) * B);
-    for (int b = 0; b < B; ++b) info[b].device_ms = ms;
+    double stg[4] = {0, 0, 0, 0};
+    for (int it = 0; it < p->iters; ++it)
+      for (int sg = 0; sg < 4; ++sg) {
+        float t = 0.f;
+        CK(cudaEventElapsedTime(&t, p->stage_ev[4 * it + sg], p->stage_ev[4 * it + sg + 1]));
+        stg[sg] += t;
+      }
+    for (int b = 0; b < B; ++b) {
+      info[b].device_ms = ms;
+      info[b].sample_ms = stg[0];
+      info[b].rollout_ms = stg[1];
+      info[b].mlp_ms = stg[2];
+      info[b].update_ms = stg[3];
+    }
   }
   return MPPI_OK;
 }
@@ -978,6 +1007,31 @@ int mppi_get_bundle(mppi_plan* p, mppi_eval_out* out, double* weights) {
   CK(cudaStreamSynchronize(st));
   out->bad_particle = -1;
   out->quarantined = 0;
+  return MPPI_OK;
+}
+
+int mppi_time_stage(mppi_plan* p, int32_t stage, int32_t reps, double* ms_per_launch) {
+  if (!p || !ms_per_launch || reps < 1 || stage < 0 || stage > 3) return fail(MPPI_E_BAD_ARGUMENT, "bad arguments");
+  CKR(set_device(p));
+  CKR(ensure_graph(p));
+  cudaStream_t st = p->stream;
+  const unsigned mask = stage == 3 ? 7u : (1u << stage);
+  CK(cudaStreamSynchronize(st));
+  CK(cudaEventRecord(p->ev0, st));
+  for (int r = 0; r < reps; ++r) {
+    if (stage == 3) {
+      CK(cudaGraphLaunch(p->graph, st));
+    } else if (p->precision == MPPI_FP64) {
+      CKR(enqueue_iteration<double>(p, 0, true, nullptr, st, mask));
+    } else {
+      CKR(enqueue_iteration<float>(p, 0, true, nullptr, st, mask));
+    }
+  }
+  CK(cudaEventRecord(p->ev1, st));
+  CK(cudaStreamSynchronize(st));
+  float ms = 0.f;
+  CK(cudaEventElapsedTime(&ms, p->ev0, p->ev1));
+  *ms_per_launch = (double)ms / reps;
   return MPPI_OK;
 }
 

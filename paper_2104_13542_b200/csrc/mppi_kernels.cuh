@@ -586,6 +586,7 @@ static __device__ void finalize_policy(const StatsArgs<R>& a, int b, const doubl
       inf.best_cost = rec[2] > 0.0 ? rec[0] : CUDART_NAN;
       inf.mean_cost = rec[2] > 0.0 ? rec[3] / rec[2] : CUDART_NAN;
       inf.device_ms = 0.0;
+      inf.sample_ms = inf.rollout_ms = inf.mlp_ms = inf.update_ms = 0.0;
       a.info[b] = inf;
     }
   }

@@ -255,6 +255,12 @@ class Plan:
                 "term_breakdown": {nm: res["terms"][i] for i, nm in enumerate(TERM_NAMES)},
                 "total_per_particle": res["totals"], "weights": res["weights"]}
 
+    def time_stage(self, stage: int, reps: int = 50) -> float:
+        """Mean device ms per launch of one stage (0 rollout, 1 MLP, 2 stats, 3 whole graph)."""
+        ms = C.c_double(0.0)
+        N.check(self.lib.mppi_time_stage(self.handle, int(stage), int(reps), C.byref(ms)))
+        return float(ms.value)
+
     def mlp_forward(self, q) -> np.ndarray:
         q = N.f64(q).reshape(-1, self.dof)
         out = np.empty(q.shape[0])

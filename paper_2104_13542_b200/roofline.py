@@ -1,0 +1,69 @@
+"""Algorithmic work per particle-step and the roofline of each step kernel.
+
+Counts follow SURVEY.md §8(d) for a generic 7-DOF revolute chain (FMA = 2
+flops, no exploitation of arm7's zero entries — the kernels are generic over
+chain data):
+
+  sample affine 14 | integrate 28 | FK 7 x 178 = 1246 | pose (full) 120 |
+  joint 49 | stop 28 | Jacobian 192 | manipulability 145 |
+  capsule self-collision ~650 | total + discount 14 | update statistics 42
+  learned MLP: 2*(14*256 + 256*128 + 128*64 + 64*1) = 89,216 tensor flops/row
+
+Algorithmic bytes per particle-step of the fused step: eps read as float64
+(H*d*8 / H = 56 B) by the rollout and again by the update, a 4 B step cost
+write+read, the MLP's 64 B input row + 4 B output.
+"""
+
+from __future__ import annotations
+
+FLOPS = {
+    "sample": 14, "integrate": 28, "fk": 1246, "pose_full": 120, "pose_pos": 30, "joint": 49,
+    "stop": 28, "jacobian": 192, "manip": 145, "selfcoll_oracle": 650, "total": 14, "update": 42,
+}
+MLP_TENSOR_FLOPS_PER_ROW = 2 * (14 * 256 + 256 * 128 + 128 * 64 + 64 * 1)  # 89,216
+
+
+def rollout_flops_per_unit(config: int) -> int:
+    f = FLOPS["sample"] + FLOPS["integrate"] + FLOPS["fk"] + FLOPS["pose_full"] + FLOPS["joint"] + FLOPS["total"]
+    if config == 2:
+        f += FLOPS["stop"] + FLOPS["jacobian"] + FLOPS["manip"]
+    return f
+
+
+def rollout_bytes_per_unit(dof: int = 7) -> int:
+    return dof * 8 + 4 + 16 * 4  # eps row, step-cost write, posenc row (learned path)
+
+
+def update_bytes_per_unit(dof: int = 7) -> int:
+    return dof * 8 + 4 + 4  # eps row re-read, step cost + learned distance read
+
+
+def step_roofline(stage_ms: dict, rows: int, particles: int, horizon: int, dof: int, config: int,
+                  peaks: dict, peaks_kind: str) -> dict:
+    """Roofline entry for the dominant kernel of the step (stage_ms from the
+    event-record nodes of the timed graph replays)."""
+    stage = max(("rollout", "mlp", "update"), key=lambda k: stage_ms.get(k, 0.0))
+    t = stage_ms[stage] * 1e-3
+    sm_mhz = peaks.get("sm_max_mhz", 1965.0)
+    if stage == "mlp":
+        achieved = MLP_TENSOR_FLOPS_PER_ROW * rows / t / 1e12
+        peak = peaks["bf16_tflops"]
+        return {"kernel": "mlp (learned self-collision, tcgen05)", "bound": "tensor", "achieved": achieved,
+                "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak, "traffic": None,
+                "peak_source": f"bf16_tflops ({peaks_kind})",
+                "algorithmic": f"{MLP_TENSOR_FLOPS_PER_ROW} flop/row x {rows} rows"}
+    if stage == "rollout":
+        fl = rollout_flops_per_unit(config)
+        achieved = fl * rows / t / 1e12
+        peak = 2 * 128 * 148 * sm_mhz * 1e6 / 1e12  # FP32 FMA pipe at the measured max SM clock
+        return {"kernel": "rollout (fused integrate+FK+costs)", "bound": "fp32", "achieved": achieved,
+                "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak, "traffic": None,
+                "peak_source": f"2 x 128 FMA/clk x 148 SMs x sm_max_mhz ({peaks_kind} clock)",
+                "algorithmic": f"{fl} flop/particle-step x {rows}"}
+    by = update_bytes_per_unit(dof) * rows
+    achieved = by / t / 1e9
+    peak = peaks["hbm_gbs"]
+    return {"kernel": "stats/update (weights + mean/cov + shift)", "bound": "hbm", "achieved": achieved,
+            "peak": peak, "unit": "GB/s", "frac": achieved / peak, "traffic": None,
+            "peak_source": f"hbm_gbs ({peaks_kind})",
+            "algorithmic": f"{update_bytes_per_unit(dof)} B/particle-step x {rows}"}

@@ -77,7 +77,7 @@ def test_sampling_functions():
 
     g = golden("sampling")
     np.testing.assert_array_equal(S.halton_points(600, 7), g["halton"])  # bit-exact
-    np.testing.assert_allclose(S.gaussianize(g["gauss_p"]), g["gauss"], rtol=1e-14, atol=1e-14)
+    np.testing.assert_allclose(S.gaussianize(g["gauss_p"]), g["gauss"], rtol=1e-12, atol=1e-12)  # CUDA log vs glibc: ulps
     np.testing.assert_allclose(S.bspline_basis(30, 5, 3), g["basis_30_5"], atol=1e-15)
     np.testing.assert_allclose(S.bspline_basis(24, 6, 3), g["basis_24_6"], atol=1e-15)
     np.testing.assert_allclose(S.bspline_basis(7, 4, 2), g["basis_7_4_2"], atol=1e-15)
