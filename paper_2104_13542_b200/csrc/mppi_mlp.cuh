@@ -1,103 +1,473 @@
-// mppi_mlp.cuh — learned self-collision distance (surrogate.py:42-52):
-// x = [sin q, cos q] (14) -> 256 -> 128 -> 64 -> 1, ReLU between layers.
+// mppi_mlp.cuh — learned self-collision MLP on the 5th-gen tensor cores.
 //
-// This first version is a CUDA-core FP32 kernel (one thread per row, weights
-// broadcast from L1/L2). It is the correctness baseline the tcgen05 kernel is
-// developed against.
+// Reference: surrogate.py:42-52 (+ posenc :24-28): x = [sin q, cos q] (2d=14,
+// padded to 16) -> 256 -> 128 -> 64 -> 1, ReLU between layers, float64 on
+// the CPU. Here: one 128-row tile per CTA iteration, all three hidden layers
+// on tcgen05.mma (kind::f16, FP32 accumulation in TMEM), the 64 -> 1 output
+// layer fused into the last epilogue on the CUDA cores.
+//
+// Precision: every operand is split into an FP16 pair
+// hi + lo (lo = fp16(x - hi)), and each product is computed as
+// A_hi B_hi + A_hi B_lo + A_lo B_hi (three MMAs into the same accumulator):
+// ~22 significant bits, within ~1e-6 m of the float64 reference distance,
+// where a single bf16/tf32 pass is not parity safe. Weights are pre-scaled by
+// a per-layer power of two so their lo parts stay clear of FP16 subnormals;
+// the epilogue undoes the scale exactly.
+//
+// Data movement: the whole weight image (W0..W2 hi/lo in the UMMA canonical
+// K-major no-swizzle layout, 176 KiB, + fp32 biases) is copied global -> smem
+// once per CTA with cp.async.bulk (TMA bulk engine, three mbarriers so layer 1
+// starts while W1/W2 are still in flight). The CTA is persistent over tiles.
+//
+// Pipeline per tile (one elected thread issues all MMAs; 128 threads = 128
+// TMEM lanes run the epilogues, thread t owns row t of the tile):
+//   L1 chunk c (64 of 256 outputs) -> TMEM acc1[c%2] ; epilogue (bias, ReLU,
+//   split) -> smem A ; L2 K-chunk c accumulates into acc2 ; L1 chunk c+2 is
+//   issued right behind it. Then layer 2's output goes back through smem in
+//   two 64-wide K-chunks into L3 (acc3), and the final epilogue does the
+//   64 -> 1 dot product.
 #pragma once
 
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
+#include <cmath>
+#include <cstring>
 #include <vector>
 
 namespace mppi {
 
 constexpr int kMlpH0 = 256, kMlpH1 = 128, kMlpH2 = 64, kMlpIn = 16;
 
-struct MlpWeights {
-  int in_dim = 0;
-  float* w = nullptr;  // packed fp32: W0 (16x256, rows >= in_dim zero) | b0 | W1 | b1 | W2 | b2 | W3 | b3
-};
-
 inline size_t mlp_padded_rows(size_t rows) { return (rows + 127) / 128 * 128; }
 
-constexpr size_t kOffW0 = 0;
-constexpr size_t kOffB0 = kOffW0 + kMlpIn * kMlpH0;
-constexpr size_t kOffW1 = kOffB0 + kMlpH0;
-constexpr size_t kOffB1 = kOffW1 + kMlpH0 * kMlpH1;
-constexpr size_t kOffW2 = kOffB1 + kMlpH1;
-constexpr size_t kOffB2 = kOffW2 + kMlpH1 * kMlpH2;
-constexpr size_t kOffW3 = kOffB2 + kMlpH2;
-constexpr size_t kOffB3 = kOffW3 + kMlpH2;
-constexpr size_t kMlpParams = kOffB3 + 1;
+// ---- shared-memory image (byte offsets); identical in global memory so one
+// bulk copy per segment lands every operand in place.
+constexpr uint32_t kW0Bytes = kMlpH0 * kMlpIn * 2;   // 8 KiB per hi/lo
+constexpr uint32_t kW1Bytes = kMlpH1 * kMlpH0 * 2;   // 64 KiB
+constexpr uint32_t kW2Bytes = kMlpH2 * kMlpH1 * 2;   // 16 KiB
+constexpr uint32_t OFF_W0H = 0;
+constexpr uint32_t OFF_W0L = OFF_W0H + kW0Bytes;
+constexpr uint32_t OFF_PAR = OFF_W0L + kW0Bytes;                  // fp32 params
+constexpr uint32_t kParFloats = kMlpH0 + kMlpH1 + kMlpH2 + kMlpH2 + 4;  // b0 b1 b2 w3 | b3 s0 s1 s2
+constexpr uint32_t kParBytes = kParFloats * 4;                    // 2064
+constexpr uint32_t OFF_W1H = OFF_PAR + ((kParBytes + 127) / 128) * 128;
+constexpr uint32_t OFF_W1L = OFF_W1H + kW1Bytes;
+constexpr uint32_t OFF_W2H = OFF_W1L + kW1Bytes;
+constexpr uint32_t OFF_W2L = OFF_W2H + kW2Bytes;
+constexpr uint32_t kImgBytes = OFF_W2L + kW2Bytes;
+constexpr uint32_t kSeg0 = OFF_W1H;                 // W0 + params
+constexpr uint32_t kSeg1 = OFF_W2H - OFF_W1H;       // W1
+constexpr uint32_t kSeg2 = kImgBytes - OFF_W2H;     // W2
+constexpr uint32_t OFF_XH = kImgBytes;              // X tile 128 x 16 fp16
+constexpr uint32_t OFF_XL = OFF_XH + 128 * 16 * 2;
+constexpr uint32_t OFF_AH = OFF_XL + 128 * 16 * 2;  // activation K-chunk 128 x 64 fp16
+constexpr uint32_t OFF_AL = OFF_AH + 128 * 64 * 2;
+constexpr uint32_t OFF_BAR = OFF_AL + 128 * 64 * 2;  // 8 mbarriers
+constexpr uint32_t OFF_TMEMPTR = OFF_BAR + 8 * 8;
+constexpr uint32_t kMlpSmem = OFF_TMEMPTR + 16;
 
-__global__ void __launch_bounds__(128) mlp_simt_kernel(const float* __restrict__ x, long long rows,
-                                                       const float* __restrict__ w,
-                                                       float* __restrict__ out) {
-  const long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (r >= rows) return;
-  float in[kMlpIn];
+static_assert(kMlpSmem <= 232448, "MLP tile does not fit the 227 KiB of shared memory");
+static_assert(kSeg0 % 16 == 0 && kSeg1 % 16 == 0 && kSeg2 % 16 == 0, "bulk copy sizes");
+
+// byte offset of element (row, k) of a K-major, no-swizzle UMMA operand with
+// K columns: 8x8 core matrices (8 rows x 16 B), K-chunks adjacent (LBO = 128 B),
+// 8-row groups K*16 B apart (SBO).
+__host__ __device__ constexpr uint32_t umma_off(uint32_t row, uint32_t k, uint32_t K) {
+  return (row >> 3) * (K * 16) + (k >> 3) * 128 + (row & 7) * 16 + (k & 7) * 2;
+}
+
+struct MlpWeights {
+  int in_dim = 0;
+  unsigned char* img = nullptr;  // kImgBytes, device
+};
+
+// ------------------------------------------------------------------ PTX helpers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t phase) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra WAIT_%=;\n}" ::"r"(bar),
+      "r"(phase)
+      : "memory");
+}
+
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+      "l"(src), "r"(bytes), "r"(bar)
+      : "memory");
+}
+
+__device__ __forceinline__ void fence_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+
+__device__ __forceinline__ uint64_t umma_desc(uint32_t addr, uint32_t lbo, uint32_t sbo) {
+  return (uint64_t)((addr >> 4) & 0x3FFFu) | ((uint64_t)((lbo >> 4) & 0x3FFFu) << 16) |
+         ((uint64_t)((sbo >> 4) & 0x3FFFu) << 32) | (1ull << 46);  // version 1, SWIZZLE_NONE
+}
+
+// kind::f16 instruction descriptor: F16 x F16 -> F32, both K-major, M=128.
+__host__ __device__ constexpr uint32_t umma_idesc(uint32_t N) {
+  return (1u << 4) | ((N >> 3) << 17) | ((128u >> 4) << 24);
+}
+
+__device__ __forceinline__ void umma_f16(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc,
+                                         uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
+__device__ __forceinline__ void umma_commit(uint32_t bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
+               : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),
+        "=r"(r[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
-  for (int k = 0; k < kMlpIn; ++k) in[k] = x[r * kMlpIn + k];
-  float h2[kMlpH1];
+  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+__device__ __forceinline__ uint32_t pack_h2(__half a, __half b) {
+  return (uint32_t)__half_as_ushort(a) | ((uint32_t)__half_as_ushort(b) << 16);
+}
+
+// Split 16 fp32 activations of one row into fp16 hi/lo and store them as two
+// 16-byte core-matrix rows each (k0 multiple of 16) of a K-wide operand.
+__device__ __forceinline__ void store_split16(unsigned char* sm, uint32_t off_h, uint32_t off_l,
+                                              uint32_t row, uint32_t k0, uint32_t K, const float* y) {
+  uint32_t h[8], l[8];
 #pragma unroll
-  for (int j = 0; j < kMlpH1; ++j) h2[j] = w[kOffB1 + j];
-  for (int i = 0; i < kMlpH0; ++i) {
-    float a = w[kOffB0 + i];
-#pragma unroll
-    for (int k = 0; k < kMlpIn; ++k) a += in[k] * w[kOffW0 + k * kMlpH0 + i];
-    a = a > 0.f ? a : 0.f;
-#pragma unroll
-    for (int j = 0; j < kMlpH1; ++j) h2[j] += a * w[kOffW1 + i * kMlpH1 + j];
+  for (int i = 0; i < 8; ++i) {
+    const __half h0 = __float2half_rn(y[2 * i]), h1 = __float2half_rn(y[2 * i + 1]);
+    const __half l0 = __float2half_rn(y[2 * i] - __half2float(h0));
+    const __half l1 = __float2half_rn(y[2 * i + 1] - __half2float(h1));
+    h[i] = pack_h2(h0, h1);
+    l[i] = pack_h2(l0, l1);
   }
-  float h3[kMlpH2];
 #pragma unroll
-  for (int j = 0; j < kMlpH2; ++j) h3[j] = w[kOffB2 + j];
-#pragma unroll
-  for (int i = 0; i < kMlpH1; ++i) {
-    const float a = h2[i] > 0.f ? h2[i] : 0.f;
-#pragma unroll
-    for (int j = 0; j < kMlpH2; ++j) h3[j] += a * w[kOffW2 + i * kMlpH2 + j];
+  for (int c = 0; c < 2; ++c) {
+    const uint32_t o = umma_off(row, k0 + 8 * c, K);
+    *reinterpret_cast<uint4*>(sm + off_h + o) = make_uint4(h[4 * c], h[4 * c + 1], h[4 * c + 2], h[4 * c + 3]);
+    *reinterpret_cast<uint4*>(sm + off_l + o) = make_uint4(l[4 * c], l[4 * c + 1], l[4 * c + 2], l[4 * c + 3]);
   }
-  float o = w[kOffB3];
+}
+
+// ------------------------------------------------------------------ the kernel
+// x: (M_pad,16) fp32 positional encodings; out: (M) fp32 distances.
+__global__ void __launch_bounds__(128, 1)
+    mlp_tcgen05_kernel(const float* __restrict__ x, long long M, const unsigned char* __restrict__ img,
+                       float* __restrict__ out) {
+  extern __shared__ __align__(1024) unsigned char mlp_smem[];
+  unsigned char* sm = mlp_smem;
+  const int tid = threadIdx.x, warp = tid >> 5;
+  const uint32_t sb = smem_u32(sm);
+  const uint32_t barW0 = sb + OFF_BAR, barW1 = barW0 + 8, barW2 = barW0 + 16;
+  const uint32_t barL1a = barW0 + 24, barL1b = barW0 + 32, barL2 = barW0 + 40, barL3 = barW0 + 48;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sm + OFF_TMEMPTR);
+
+  if (tid == 0) {
+    for (int i = 0; i < 7; ++i) mbar_init(barW0 + 8 * i, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    fence_async_smem();
+  }
+  if (warp == 0) {  // 512 TMEM columns: acc1 x2 (64+64) | acc2 (128) | acc3 (64)
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t acc1[2] = {tmem, tmem + 64}, acc2 = tmem + 128, acc3 = tmem + 256;
+  const uint32_t lane_base = (uint32_t)(warp * 32) << 16;
+
+  if (tid == 0) {  // weights: three bulk-copy segments, each on its own barrier
+    mbar_expect_tx(barW0, kSeg0);
+    bulk_g2s(sb + 0, img, kSeg0, barW0);
+    mbar_expect_tx(barW1, kSeg1);
+    for (uint32_t o = 0; o < kSeg1; o += 32768)
+      bulk_g2s(sb + OFF_W1H + o, img + OFF_W1H + o, min(32768u, kSeg1 - o), barW1);
+    mbar_expect_tx(barW2, kSeg2);
+    bulk_g2s(sb + OFF_W2H, img + OFF_W2H, kSeg2, barW2);
+  }
+  const float* par = reinterpret_cast<const float*>(sm + OFF_PAR);
+  const float* b0 = par;
+  const float* b1 = par + kMlpH0;
+  const float* b2 = b1 + kMlpH1;
+  const float* w3 = b2 + kMlpH2;
+
+  const uint32_t id64 = umma_idesc(64), id128 = umma_idesc(128);
+  uint32_t phL1[2] = {0, 0}, phL2 = 0, phL3 = 0;
+  bool weights_ready = false;
+  const long long ntiles = (M + 127) / 128;
+
+  for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const long long row = tile * 128 + tid;
+    {  // X tile: fp32 -> fp16 hi/lo, K-major core-matrix layout
+      float xv[16];
+      if (row < M) {
+        const float4* src = reinterpret_cast<const float4*>(x + row * 16);
 #pragma unroll
-  for (int i = 0; i < kMlpH2; ++i) o += (h3[i] > 0.f ? h3[i] : 0.f) * w[kOffW3 + i];
-  out[r] = o;
+        for (int i = 0; i < 4; ++i) {
+          const float4 f = __ldg(src + i);
+          xv[4 * i] = f.x;
+          xv[4 * i + 1] = f.y;
+          xv[4 * i + 2] = f.z;
+          xv[4 * i + 3] = f.w;
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < 16; ++i) xv[i] = 0.f;
+      }
+      store_split16(sm, OFF_XH, OFF_XL, tid, 0, 16, xv);
+    }
+    fence_async_smem();
+    if (!weights_ready) mbar_wait(barW0, 0);  // W0 + biases; W1/W2 still streaming
+    __syncthreads();
+    tc_fence_after();
+
+    auto issue_l1 = [&](int c) {  // acc1[c%2] = X . W0t[64c:64c+64]^T   (N = 64)
+      const uint64_t xh = umma_desc(sb + OFF_XH, 128, 256), xl = umma_desc(sb + OFF_XL, 128, 256);
+      const uint64_t wh = umma_desc(sb + OFF_W0H + umma_off(64 * c, 0, 16), 128, 256);
+      const uint64_t wl = umma_desc(sb + OFF_W0L + umma_off(64 * c, 0, 16), 128, 256);
+      umma_f16(acc1[c & 1], xh, wh, id64, 0);
+      umma_f16(acc1[c & 1], xh, wl, id64, 1);
+      umma_f16(acc1[c & 1], xl, wh, id64, 1);
+      umma_commit((c & 1) ? barL1b : barL1a);
+    };
+    auto issue_l2 = [&](int c) {  // acc2 += A_c . W1t[:, 64c:64c+64]^T   (N = 128)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const uint64_t ah = umma_desc(sb + OFF_AH + j * 256, 128, 1024);
+        const uint64_t al = umma_desc(sb + OFF_AL + j * 256, 128, 1024);
+        const uint64_t wh = umma_desc(sb + OFF_W1H + (8 * c + 2 * j) * 128, 128, 4096);
+        const uint64_t wl = umma_desc(sb + OFF_W1L + (8 * c + 2 * j) * 128, 128, 4096);
+        umma_f16(acc2, ah, wh, id128, (c | j) ? 1u : 0u);
+        umma_f16(acc2, ah, wl, id128, 1);
+        umma_f16(acc2, al, wh, id128, 1);
+      }
+      umma_commit(barL2);
+    };
+    auto issue_l3 = [&](int hh) {  // acc3 += A_h . W2t[:, 64h:64h+64]^T   (N = 64)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const uint64_t ah = umma_desc(sb + OFF_AH + j * 256, 128, 1024);
+        const uint64_t al = umma_desc(sb + OFF_AL + j * 256, 128, 1024);
+        const uint64_t wh = umma_desc(sb + OFF_W2H + (8 * hh + 2 * j) * 128, 128, 2048);
+        const uint64_t wl = umma_desc(sb + OFF_W2L + (8 * hh + 2 * j) * 128, 128, 2048);
+        umma_f16(acc3, ah, wh, id64, (hh | j) ? 1u : 0u);
+        umma_f16(acc3, ah, wl, id64, 1);
+        umma_f16(acc3, al, wh, id64, 1);
+      }
+      umma_commit(barL3);
+    };
+
+    if (tid == 0) {
+      issue_l1(0);
+      issue_l1(1);
+    }
+    const float s0 = par[kMlpH0 + kMlpH1 + 2 * kMlpH2 + 1];
+    const float s1 = par[kMlpH0 + kMlpH1 + 2 * kMlpH2 + 2];
+    const float s2 = par[kMlpH0 + kMlpH1 + 2 * kMlpH2 + 3];
+
+    // ---- layer 1 (4 chunks of 64) feeding layer 2
+    for (int c = 0; c < 4; ++c) {
+      mbar_wait((c & 1) ? barL1b : barL1a, phL1[c & 1]);
+      phL1[c & 1] ^= 1;
+      tc_fence_after();
+      float y[64];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) tmem_ld16(acc1[c & 1] + lane_base + 16 * q, y + 16 * q);
+#pragma unroll
+      for (int i = 0; i < 64; ++i) {
+        const float t = fmaf(y[i], s0, b0[64 * c + i]);
+        y[i] = t > 0.f ? t : 0.f;
+      }
+      if (c > 0) {  // layer-2 MMAs of the previous chunk must be done reading A
+        mbar_wait(barL2, phL2);
+        phL2 ^= 1;
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) store_split16(sm, OFF_AH, OFF_AL, tid, 16 * q, 64, y + 16 * q);
+      fence_async_smem();
+      tc_fence_before();
+      __syncthreads();
+      tc_fence_after();
+      if (tid == 0) {
+        if (!weights_ready && c == 0) mbar_wait(barW1, 0);
+        issue_l2(c);
+        if (c + 2 < 4) issue_l1(c + 2);
+      }
+    }
+    mbar_wait(barL2, phL2);
+    phL2 ^= 1;
+    tc_fence_after();
+
+    // ---- layer 2 output (2 K-chunks of 64) feeding layer 3
+    for (int hh = 0; hh < 2; ++hh) {
+      float y[64];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) tmem_ld16(acc2 + lane_base + 64 * hh + 16 * q, y + 16 * q);
+#pragma unroll
+      for (int i = 0; i < 64; ++i) {
+        const float t = fmaf(y[i], s1, b1[64 * hh + i]);
+        y[i] = t > 0.f ? t : 0.f;
+      }
+      if (hh > 0) {
+        mbar_wait(barL3, phL3);
+        phL3 ^= 1;
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) store_split16(sm, OFF_AH, OFF_AL, tid, 16 * q, 64, y + 16 * q);
+      fence_async_smem();
+      tc_fence_before();
+      __syncthreads();
+      tc_fence_after();
+      if (tid == 0) {
+        if (!weights_ready && hh == 0) mbar_wait(barW2, 0);
+        issue_l3(hh);
+      }
+    }
+    weights_ready = true;
+    mbar_wait(barL3, phL3);
+    phL3 ^= 1;
+    tc_fence_after();
+
+    // ---- layer 3 epilogue + the 64 -> 1 output layer on the CUDA cores
+    float o = par[kMlpH0 + kMlpH1 + 2 * kMlpH2];  // b3
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      float y[16];
+      tmem_ld16(acc3 + lane_base + 16 * q, y);
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        float t = fmaf(y[i], s2, b2[16 * q + i]);
+        t = t > 0.f ? t : 0.f;
+        o = fmaf(t, w3[16 * q + i], o);
+      }
+    }
+    if (row < M) out[row] = o;
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+  }
+  if (!weights_ready && tid == 0) {  // CTA got no tile: drain the weight copies before exit
+    mbar_wait(barW0, 0);
+    mbar_wait(barW1, 0);
+    mbar_wait(barW2, 0);
+  }
+  __syncthreads();
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+}
+
+// ------------------------------------------------------------------ host side
+inline int pow2_scale(const double* w, size_t n) {
+  double m = 0.0;
+  for (size_t i = 0; i < n; ++i) m = std::fmax(m, std::fabs(w[i]));
+  if (!(m > 0.0)) return 0;
+  return 13 - (int)std::ceil(std::log2(m));  // max |w| * 2^s in (2^12, 2^13]
+}
+
+// Pack one layer W (in, out) row-major (the reference layout, surrogate.py:39)
+// as Wt (out x K) hi/lo into the image.
+inline void pack_layer(std::vector<unsigned char>& img, uint32_t off_h, uint32_t off_l, const double* W,
+                       int in, int out, int K, int s) {
+  const double sc = std::ldexp(1.0, s);
+  for (int n = 0; n < out; ++n)
+    for (int k = 0; k < K; ++k) {
+      const double v = k < in ? W[(size_t)k * out + n] * sc : 0.0;
+      const __half h = __float2half_rn((float)v);
+      const __half l = __float2half_rn((float)(v - (double)__half2float(h)));
+      const uint32_t o = umma_off(n, k, K);
+      memcpy(&img[off_h + o], &h, 2);
+      memcpy(&img[off_l + o], &l, 2);
+    }
 }
 
 inline cudaError_t mlp_upload(MlpWeights& m, int in_dim, const double* W0, const double* b0,
-                              const double* W1, const double* b1, const double* W2,
-                              const double* b2, const double* W3, const double* b3,
-                              cudaStream_t st) {
-  std::vector<float> h(kMlpParams, 0.f);
-  for (int k = 0; k < in_dim; ++k)
-    for (int i = 0; i < kMlpH0; ++i) h[kOffW0 + k * kMlpH0 + i] = (float)W0[k * kMlpH0 + i];
-  for (int i = 0; i < kMlpH0; ++i) h[kOffB0 + i] = (float)b0[i];
-  for (int i = 0; i < kMlpH0 * kMlpH1; ++i) h[kOffW1 + i] = (float)W1[i];
-  for (int i = 0; i < kMlpH1; ++i) h[kOffB1 + i] = (float)b1[i];
-  for (int i = 0; i < kMlpH1 * kMlpH2; ++i) h[kOffW2 + i] = (float)W2[i];
-  for (int i = 0; i < kMlpH2; ++i) h[kOffB2 + i] = (float)b2[i];
-  for (int i = 0; i < kMlpH2; ++i) h[kOffW3 + i] = (float)W3[i];
-  h[kOffB3] = (float)b3[0];
+                              const double* W1, const double* b1, const double* W2, const double* b2,
+                              const double* W3, const double* b3, cudaStream_t st) {
+  std::vector<unsigned char> img(kImgBytes, 0);
+  const int s0 = pow2_scale(W0, (size_t)in_dim * kMlpH0), s1 = pow2_scale(W1, (size_t)kMlpH0 * kMlpH1),
+            s2 = pow2_scale(W2, (size_t)kMlpH1 * kMlpH2);
+  pack_layer(img, OFF_W0H, OFF_W0L, W0, in_dim, kMlpH0, kMlpIn, s0);
+  pack_layer(img, OFF_W1H, OFF_W1L, W1, kMlpH0, kMlpH1, kMlpH0, s1);
+  pack_layer(img, OFF_W2H, OFF_W2L, W2, kMlpH1, kMlpH2, kMlpH1, s2);
+  float* par = reinterpret_cast<float*>(&img[OFF_PAR]);
+  for (int i = 0; i < kMlpH0; ++i) par[i] = (float)b0[i];
+  for (int i = 0; i < kMlpH1; ++i) par[kMlpH0 + i] = (float)b1[i];
+  for (int i = 0; i < kMlpH2; ++i) par[kMlpH0 + kMlpH1 + i] = (float)b2[i];
+  for (int i = 0; i < kMlpH2; ++i) par[kMlpH0 + kMlpH1 + kMlpH2 + i] = (float)W3[i];
+  float* tail = par + kMlpH0 + kMlpH1 + 2 * kMlpH2;
+  tail[0] = (float)b3[0];
+  tail[1] = (float)std::ldexp(1.0, -s0);
+  tail[2] = (float)std::ldexp(1.0, -s1);
+  tail[3] = (float)std::ldexp(1.0, -s2);
   cudaError_t e = cudaSuccess;
-  if (!m.w) e = cudaMalloc(&m.w, kMlpParams * sizeof(float));
+  if (!m.img) e = cudaMalloc(&m.img, kImgBytes);
   if (e != cudaSuccess) return e;
   m.in_dim = in_dim;
-  e = cudaMemcpyAsync(m.w, h.data(), kMlpParams * sizeof(float), cudaMemcpyHostToDevice, st);
+  e = cudaMemcpyAsync(m.img, img.data(), kImgBytes, cudaMemcpyHostToDevice, st);
   if (e != cudaSuccess) return e;
   return cudaStreamSynchronize(st);
 }
 
 inline cudaError_t mlp_forward(const MlpWeights& m, const float* x, long long rows, float* out,
                                cudaStream_t st) {
-  const long long blocks = (rows + 127) / 128;
-  mlp_simt_kernel<<<(unsigned)blocks, 128, 0, st>>>(x, rows, m.w, out);
+  static bool attr_set[64] = {};
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64 || !attr_set[dev]) {
+    cudaError_t e = cudaFuncSetAttribute(mlp_tcgen05_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)kMlpSmem);
+    if (e != cudaSuccess) return e;
+    if (dev >= 0 && dev < 64) attr_set[dev] = true;
+  }
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const long long tiles = (rows + 127) / 128;
+  const unsigned grid = (unsigned)(tiles < sms ? tiles : sms);
+  mlp_tcgen05_kernel<<<grid, 128, kMlpSmem, st>>>(x, rows, m.img, out);
   return cudaGetLastError();
 }
 
 inline void mlp_release(MlpWeights& m) {
-  if (m.w) cudaFree(m.w);
-  m.w = nullptr;
+  if (m.img) cudaFree(m.img);
+  m.img = nullptr;
 }
 
 }  // namespace mppi
