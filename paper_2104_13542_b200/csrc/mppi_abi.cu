@@ -170,10 +170,16 @@ struct mppi_plan {
   int dump = 0;  // bundle dumps for instance 0
   DevBuf<double> d_pos, d_vel, d_acc, d_terms, d_step, d_w;
   // pinned staging
-  double* h_state = nullptr;          // (B,2D) + step counter slot
+  // pinned, mapped host staging: the step graph's prologue kernel reads the
+  // state straight from h_state, the finalize writes h_cmd / h_info directly
+  double* h_state = nullptr;          // (B,2D)
   unsigned long long* h_ctr = nullptr;
   double* h_cmd = nullptr;            // (B,D)
   mppi_step_info* h_info = nullptr;   // (B)
+  double* m_state = nullptr;          // device aliases of the above
+  unsigned long long* m_ctr = nullptr;
+  double* m_cmd = nullptr;
+  mppi_step_info* m_info = nullptr;
   std::vector<double> goal_host;
   // graph
   cudaGraphExec_t graph = nullptr;
@@ -270,8 +276,9 @@ void stats_static(mppi_plan* p, int H, double gamma, double tw, StatsArgs<R>& s)
 }
 
 void choose_blocks(int N, int& ppb, int& nblk) {
-  // >= 64 particles per block, at most 2 blocks per SM per instance-wave
-  ppb = 64;
+  // 32 particles per block (latency: more blocks pull eps/step costs in
+  // parallel), at most 296 blocks per instance (the combine is linear in it)
+  ppb = 32;
   nblk = (N + ppb - 1) / ppb;
   if (nblk > 296) {
     nblk = 296;
@@ -338,8 +345,8 @@ int enqueue_iteration(mppi_plan* p, int it, bool inline_final, double* out_recor
   s.counters = p->counters.p;
   s.status = p->status.p;
   s.bad = p->bad.p;
-  s.cmd = p->cmd.p;
-  s.info = p->info.p;
+  s.cmd = p->m_cmd;   // mapped host memory: no D2H copy node
+  s.info = p->m_info;
   if (p->dump) {
     s.dump_step = p->d_step.p;
     s.dump_terms = p->d_terms.p;
@@ -369,10 +376,9 @@ int enqueue_sampling(mppi_plan* p, int it, cudaStream_t st) {
 
 int enqueue_step_body(mppi_plan* p, cudaStream_t st) {
   const int B = p->B, D = p->D;
-  CK(cudaMemsetAsync(p->status.p, 0, sizeof(int) * B, st));
-  CK(cudaMemsetAsync(p->bad.p, 0x7f, sizeof(int) * B, st));
-  CK(cudaMemcpyAsync(p->state.p, p->h_state, sizeof(double) * B * 2 * D, cudaMemcpyHostToDevice, st));
-  CK(cudaMemcpyAsync(p->stepctr.p, p->h_ctr, sizeof(unsigned long long), cudaMemcpyHostToDevice, st));
+  step_prologue_kernel<<<grid_for((long long)B * 2 * D, 256, 148), 256, 0, st>>>(
+      p->m_state, p->m_ctr, p->state.p, p->stepctr.p, p->status.p, p->bad.p, B, 2 * D);
+  CK(cudaGetLastError());
   // event-record nodes between the stages give per-kernel device times of
   // every replayed step (mppi_step_info.*_ms)
   auto mark = [&](int i) -> int {
@@ -381,7 +387,7 @@ int enqueue_step_body(mppi_plan* p, cudaStream_t st) {
   };
   for (int it = 0; it < p->iters; ++it) {
     CKR(mark(4 * it + 0));
-    CKR(enqueue_sampling(p, it, st));
+    CKR(enqueue_sampling(p, it, st));  // no-op (and a zero-length stage) unless pseudorandom
     for (int sg = 0; sg < 3; ++sg) {
       CKR(mark(4 * it + 1 + sg));
       if (p->precision == MPPI_FP64)
@@ -391,8 +397,6 @@ int enqueue_step_body(mppi_plan* p, cudaStream_t st) {
     }
   }
   CKR(mark(4 * p->iters));
-  CK(cudaMemcpyAsync(p->h_cmd, p->cmd.p, sizeof(double) * B * D, cudaMemcpyDeviceToHost, st));
-  CK(cudaMemcpyAsync(p->h_info, p->info.p, sizeof(mppi_step_info) * B, cudaMemcpyDeviceToHost, st));
   return MPPI_OK;
 }
 
@@ -576,10 +580,14 @@ int mppi_plan_create(const mppi_chain_desc* chain, const mppi_cost_desc* costs,
       p->goal_host[b * 16 + 0] = p->goal_host[b * 16 + 4] = p->goal_host[b * 16 + 8] = 1.0;
     }
     CK(cudaMemcpy(p->goal.p, p->goal_host.data(), sizeof(double) * B * 16, cudaMemcpyHostToDevice));
-    CK(cudaMallocHost(&p->h_state, sizeof(double) * B * 2 * D));
-    CK(cudaMallocHost(&p->h_ctr, sizeof(unsigned long long)));
-    CK(cudaMallocHost(&p->h_cmd, sizeof(double) * B * D));
-    CK(cudaMallocHost(&p->h_info, sizeof(mppi_step_info) * B));
+    CK(cudaHostAlloc(&p->h_state, sizeof(double) * B * 2 * D, cudaHostAllocMapped));
+    CK(cudaHostAlloc(&p->h_ctr, sizeof(unsigned long long), cudaHostAllocMapped));
+    CK(cudaHostAlloc(&p->h_cmd, sizeof(double) * B * D, cudaHostAllocMapped));
+    CK(cudaHostAlloc(&p->h_info, sizeof(mppi_step_info) * B, cudaHostAllocMapped));
+    CK(cudaHostGetDevicePointer((void**)&p->m_state, p->h_state, 0));
+    CK(cudaHostGetDevicePointer((void**)&p->m_ctr, p->h_ctr, 0));
+    CK(cudaHostGetDevicePointer((void**)&p->m_cmd, p->h_cmd, 0));
+    CK(cudaHostGetDevicePointer((void**)&p->m_info, p->h_info, 0));
     memset(p->h_state, 0, sizeof(double) * B * 2 * D);
     *p->h_ctr = 0;
     if (p->generator == MPPI_GEN_PSEUDORANDOM) {
@@ -1055,10 +1063,9 @@ int mppi_stats_dev(mppi_plan* p, const double* theta, const double* theta_dot, v
     memcpy(p->h_state, theta, sizeof(double) * D);
     memcpy(p->h_state + D, theta_dot, sizeof(double) * D);
     *p->h_ctr = p->step_counter++;
-    CK(cudaMemsetAsync(p->status.p, 0, sizeof(int), st));
-    CK(cudaMemsetAsync(p->bad.p, 0x7f, sizeof(int), st));
-    CK(cudaMemcpyAsync(p->state.p, p->h_state, sizeof(double) * 2 * D, cudaMemcpyHostToDevice, st));
-    CK(cudaMemcpyAsync(p->stepctr.p, p->h_ctr, sizeof(unsigned long long), cudaMemcpyHostToDevice, st));
+    step_prologue_kernel<<<1, 256, 0, st>>>(p->m_state, p->m_ctr, p->state.p, p->stepctr.p, p->status.p,
+                                            p->bad.p, 1, 2 * D);
+    CK(cudaGetLastError());
   }
   CKR(enqueue_sampling(p, it, st));
   double* rec = reinterpret_cast<double*>(record_dev);
@@ -1089,8 +1096,8 @@ int mppi_finalize_dev(mppi_plan* p, const void* records_dev, int32_t n_records, 
     s.prev_sd = p->prev_sd.p;
     s.status = p->status.p;
     s.bad = p->bad.p;
-    s.cmd = p->cmd.p;
-    s.info = p->info.p;
+    s.cmd = p->m_cmd;
+    s.info = p->m_info;
     CK(launch_finalize<R>(s, (const double*)records_dev, n_records, st));
     return MPPI_OK;
   };
@@ -1100,8 +1107,6 @@ int mppi_finalize_dev(mppi_plan* p, const void* records_dev, int32_t n_records, 
     CKR(run(float{}));
   p->sharded_iter = (it + 1) % p->iters;
   if (command_out || info) {
-    CK(cudaMemcpyAsync(p->h_cmd, p->cmd.p, sizeof(double) * p->D, cudaMemcpyDeviceToHost, st));
-    CK(cudaMemcpyAsync(p->h_info, p->info.p, sizeof(mppi_step_info), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     if (command_out) memcpy(command_out, p->h_cmd, sizeof(double) * p->D);
     if (info) memcpy(info, p->h_info, sizeof(mppi_step_info));

@@ -610,33 +610,50 @@ __global__ void __launch_bounds__(kStatsThreads) stats_kernel(const __grid_const
   const bool failed = (a.status[b] != 0);
 
   // ---- phase A: discounted totals, quarantine (rollout.py:111-171) ---------
+  // Each warp takes PA particles at a time and issues all their loads before
+  // the first reduction, so the HBM/L2 latency is paid once per batch.
   if (!failed || a.totals_only) {
-    for (int i = wid; i < cnt; i += nw) {
-      const int n = n0 + i;
-      const size_t m = ((size_t)b * N + n) * H + lane;
-      double c = 0.0, dself = 0.0;
-      bool fin = true;
-      if (lane < H) {
-        c = (double)a.step[m];
-        if (a.learned) {
-          const double dd = (double)a.mlp_d[m];
-          dself = dd > 0.0 ? dd : 0.0;
-          c = c + a.a_coll * dself;
+    constexpr int PA = 4;
+    for (int i0 = wid * PA; i0 < cnt; i0 += nw * PA) {
+      double cv[PA], dv[PA];
+#pragma unroll
+      for (int u = 0; u < PA; ++u) {
+        cv[u] = 0.0;
+        dv[u] = 0.0;
+        if (i0 + u < cnt && lane < H) {
+          const size_t m = ((size_t)b * N + n0 + i0 + u) * H + lane;
+          cv[u] = (double)a.step[m];
+          if (a.learned) dv[u] = (double)a.mlp_d[m];
         }
-        fin = isfinite(c);
       }
-      const bool allfin = __all_sync(0xffffffffu, fin);
-      double contrib = 0.0;
-      if (lane < H) contrib = (lane < H - 1 ? a.disc[lane] : a.dlast) * c;
-      double total = warp_sum(contrib);
-      if (!allfin) total = CUDART_INF;
-      if (lane == 0) {
-        tot[i] = total;
-        if (a.totals) a.totals[(size_t)b * N + n] = total;
-      }
-      if (b == 0 && lane < H) {
-        if (a.dump_step) a.dump_step[(size_t)n * H + lane] = (allfin || a.raw_step) ? c : 0.0;
-        if (a.dump_terms && a.learned) a.dump_terms[(size_t)T_SELF * N * H + (size_t)n * H + lane] = dself;
+#pragma unroll
+      for (int u = 0; u < PA; ++u) {
+        const int i = i0 + u;
+        if (i >= cnt) break;  // warp-uniform
+        const int n = n0 + i;
+        double c = 0.0, dself = 0.0;
+        bool fin = true;
+        if (lane < H) {
+          c = cv[u];
+          if (a.learned) {
+            dself = dv[u] > 0.0 ? dv[u] : 0.0;
+            c = c + a.a_coll * dself;
+          }
+          fin = isfinite(c);
+        }
+        const bool allfin = __all_sync(0xffffffffu, fin);
+        double contrib = 0.0;
+        if (lane < H) contrib = (lane < H - 1 ? a.disc[lane] : a.dlast) * c;
+        double total = warp_sum(contrib);
+        if (!allfin) total = CUDART_INF;
+        if (lane == 0) {
+          tot[i] = total;
+          if (a.totals) a.totals[(size_t)b * N + n] = total;
+        }
+        if (b == 0 && lane < H) {
+          if (a.dump_step) a.dump_step[(size_t)n * H + lane] = (allfin || a.raw_step) ? c : 0.0;
+          if (a.dump_terms && a.learned) a.dump_terms[(size_t)T_SELF * N * H + (size_t)n * H + lane] = dself;
+        }
       }
     }
   }
@@ -655,24 +672,47 @@ __global__ void __launch_bounds__(kStatsThreads) stats_kernel(const __grid_const
   __syncthreads();
 
   // ---- phase D: weighted sufficient statistics around the old mean ---------
+  // Particles whose weight underflowed to exactly 0 contribute nothing; warp 0
+  // compacts the others (ascending, so the summation order is fixed) and every
+  // output then runs a branch-free loop with PD independent eps loads in flight.
   double* rec = a.records + ((size_t)b * a.nblk + blk) * reclen;
-  if (threadIdx.x == 0) {
+  int* nz = reinterpret_cast<int*>(sm + 2 * a.ppb + 32 + max(a.nblk, 8) + reclen + HD);
+  __shared__ int s_nnz;
+  if (wid == 0) {
+    int base = 0;
+    if (!failed)
+      for (int c0 = 0; c0 < cnt; c0 += 32) {
+        const int i = c0 + lane;
+        const bool keep = i < cnt && wt[i] > 0.0;
+        const unsigned bal = __ballot_sync(0xffffffffu, keep);
+        if (keep) nz[base + __popc(bal & ((1u << lane) - 1u))] = i;
+        base += __popc(bal);
+      }
+    if (lane == 0) s_nnz = base;
+  } else if (wid == 1) {
     double s0 = 0.0, c = 0.0, sf = 0.0;
     if (!failed)
-      for (int i = 0; i < cnt; ++i) {
+      for (int i = lane; i < cnt; i += 32) {
         s0 += wt[i];
         if (isfinite(tot[i])) {
           c += 1.0;
           sf += tot[i];
         }
       }
-    rec[0] = c > 0.0 ? mb : CUDART_INF;
-    rec[1] = s0;
-    rec[2] = c;
-    rec[3] = sf;
-    rec[4] = (double)a.status[b];
-    rec[5] = (double)a.bad[b];
+    s0 = warp_sum(s0);
+    c = warp_sum(c);
+    sf = warp_sum(sf);
+    if (lane == 0) {
+      rec[0] = c > 0.0 ? mb : CUDART_INF;
+      rec[1] = s0;
+      rec[2] = c;
+      rec[3] = sf;
+      rec[4] = (double)a.status[b];
+      rec[5] = (double)a.bad[b];
+    }
   }
+  __syncthreads();
+  const int nnz = s_nnz;
   for (int o = threadIdx.x; o < HD; o += blockDim.x) {
     double s1 = 0.0, s2 = 0.0;
     if (!failed) {
@@ -680,19 +720,25 @@ __global__ void __launch_bounds__(kStatsThreads) stats_kernel(const __grid_const
       const int hs = a.shift ? h + 1 : h;
       const double mo = hs < H ? a.means[(size_t)b * HD + hs * D + j] : a.tail_mean;
       const double so = hs < H ? a.sd[(size_t)b * HD + hs * D + j] : a.tail_sd;
-      for (int i = 0; i < cnt; ++i) {
-        const double w = wt[i];
-        if (w == 0.0) continue;
-        const int ng = n0 + i + a.particle_offset;
-        double dv;
-        if (ng < a.null_count)
-          dv = 0.0 - mo;
-        else if (ng == a.null_count)
-          dv = 0.0;
-        else
-          dv = (mo + so * a.eps[(size_t)(n0 + i) * HD + o]) - mo;
-        s1 += w * dv;
-        s2 += w * dv * dv;
+      const double* ep = a.eps + (size_t)n0 * HD + o;
+      constexpr int PD = 8;
+      for (int k0 = 0; k0 < nnz; k0 += PD) {
+        double e[PD];
+        int ii[PD];
+#pragma unroll
+        for (int u = 0; u < PD; ++u) {
+          ii[u] = k0 + u < nnz ? nz[k0 + u] : -1;
+          e[u] = ii[u] >= 0 ? __ldg(ep + (size_t)ii[u] * HD) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < PD; ++u) {
+          if (ii[u] < 0) break;
+          const int ng = n0 + ii[u] + a.particle_offset;
+          const double dv = ng < a.null_count ? 0.0 - mo : (ng == a.null_count ? 0.0 : (mo + so * e[u]) - mo);
+          const double w = wt[ii[u]];
+          s1 += w * dv;
+          s2 += w * dv * dv;
+        }
       }
     }
     rec[kRecHead + o] = s1;

@@ -15,7 +15,8 @@ template <typename R>
 cudaError_t launch_finalize(const StatsArgs<R>& s, const double* recs, int count, cudaStream_t st);
 
 inline size_t stats_smem_bytes(int ppb, int nblk, int HD) {
-  return sizeof(double) * (2 * (size_t)ppb + 32 + (nblk > 8 ? nblk : 8) + (kRecHead + 2 * HD) + HD);
+  return sizeof(double) * (2 * (size_t)ppb + 32 + (nblk > 8 ? nblk : 8) + (kRecHead + 2 * HD) + HD) +
+         sizeof(int) * ((size_t)ppb + 2);
 }
 
 #ifdef MPPI_LAUNCH_IMPL

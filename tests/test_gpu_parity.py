@@ -130,8 +130,11 @@ def test_mlp_forward_matches_reference():
 
     g = golden("mlp")
     d = load_arm7_surrogate().distance(g["q"])
-    # FP16-split x3 tensor-core product, FP32 accumulate: |d| error ~1e-6 m
-    np.testing.assert_allclose(d, g["dist"], atol=2e-5)
+    # FP16-split x3 tensor-core product, FP32 accumulate (~3.5e-7 m)
+    err = np.abs(d - g["dist"]).max()
+    print(f"mlp max |d - ref| = {err:.3e}")
+    assert err < 2e-6, err
+    assert np.array_equal(d > 0, g["dist"] > 0) or np.abs(g["dist"][(d > 0) != (g["dist"] > 0)]).max() < 2e-6
 
 
 # ---------------------------------------------------------------- fused controller
