@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -165,19 +166,16 @@ struct mppi_plan {
   DevBuf<unsigned> counters;
   DevBuf<int> status, bad;
   DevBuf<mppi_step_info> info;
-  DevBuf<unsigned long long> stepctr;
   int nblk = 1, ppb = 64;
   int dump = 0;  // bundle dumps for instance 0
   DevBuf<double> d_pos, d_vel, d_acc, d_terms, d_step, d_w;
   // pinned staging
-  // pinned, mapped host staging: the step graph's prologue kernel reads the
-  // state straight from h_state, the finalize writes h_cmd / h_info directly
+  // pinned host staging: one H2D node copies h_state (+ step counter) into the
+  // graph; h_cmd / h_info are mapped and written directly by the finalize
   double* h_state = nullptr;          // (B,2D)
-  unsigned long long* h_ctr = nullptr;
   double* h_cmd = nullptr;            // (B,D)
   mppi_step_info* h_info = nullptr;   // (B)
   double* m_state = nullptr;          // device aliases of the above
-  unsigned long long* m_ctr = nullptr;
   double* m_cmd = nullptr;
   mppi_step_info* m_info = nullptr;
   std::vector<double> goal_host;
@@ -185,6 +183,7 @@ struct mppi_plan {
   cudaGraphExec_t graph = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   std::vector<cudaEvent_t> stage_ev;
+  bool stage_events = true;
   unsigned long long step_counter = 0;
   int sharded_iter = 0;
   // eval scratch
@@ -331,6 +330,7 @@ int enqueue_iteration(mppi_plan* p, int it, bool inline_final, double* out_recor
   s.nblk = p->nblk;
   s.shift = it == 0;
   s.finalize_inline = inline_final;
+  s.reset_status = inline_final && it == p->iters - 1;
   s.step = reinterpret_cast<const R*>(p->stepbuf.p);
   s.mlp_d = p->learned() ? p->mlp_d.p : nullptr;
   s.eps = p->eps.p;
@@ -362,7 +362,9 @@ int enqueue_sampling(mppi_plan* p, int it, cudaStream_t st) {
   // device copy of the input block so the captured graph stays valid.
   const long long rows = p->N;  // pseudorandom rows are local (no centring)
   const long long nz = rows * p->Kn * p->D;
-  knots_ptr_kernel<<<grid_for(nz, 256), 256, 0, st>>>(p->z.p, rows, p->Kn, p->D, p->seed, p->stepctr.p,
+  knots_ptr_kernel<<<grid_for(nz, 256), 256, 0, st>>>(p->z.p, rows, p->Kn, p->D, p->seed,
+                                                      reinterpret_cast<const unsigned long long*>(
+                                                          p->state.p + (size_t)p->B * 2 * p->D),
                                                       (unsigned long long)p->iters, it, p->offset,
                                                       p->status.p);
   CK(cudaGetLastError());
@@ -376,13 +378,18 @@ int enqueue_sampling(mppi_plan* p, int it, cudaStream_t st) {
 
 int enqueue_step_body(mppi_plan* p, cudaStream_t st) {
   const int B = p->B, D = p->D;
-  step_prologue_kernel<<<grid_for((long long)B * 2 * D, 256, 148), 256, 0, st>>>(
-      p->m_state, p->m_ctr, p->state.p, p->stepctr.p, p->status.p, p->bad.p, B, 2 * D);
-  CK(cudaGetLastError());
+  // one H2D node: the (B,2d) state followed by the step counter (pseudorandom
+  // generator). Status words were re-armed by the previous step's finalize.
+  CK(cudaMemcpyAsync(p->state.p, p->h_state, sizeof(double) * (B * 2 * D + 1), cudaMemcpyHostToDevice, st));
   // event-record nodes between the stages give per-kernel device times of
   // every replayed step (mppi_step_info.*_ms)
+  static const bool stage_events = [] {
+    const char* e = getenv("MPPI_STAGE_EVENTS");
+    return !(e && e[0] == '0');
+  }();
+  p->stage_events = stage_events;
   auto mark = [&](int i) -> int {
-    CK(cudaEventRecordWithFlags(p->stage_ev[i], st, cudaEventRecordExternal));
+    if (stage_events) CK(cudaEventRecordWithFlags(p->stage_ev[i], st, cudaEventRecordExternal));
     return MPPI_OK;
   };
   for (int it = 0; it < p->iters; ++it) {
@@ -540,7 +547,7 @@ int mppi_plan_create(const mppi_chain_desc* chain, const mppi_cost_desc* costs,
     CKR(p->prev_means.alloc(B * HD));
     CKR(p->prev_sd.alloc(B * HD));
     CKR(p->goal.alloc((size_t)B * 16));
-    CKR(p->state.alloc((size_t)B * 2 * D));
+    CKR(p->state.alloc((size_t)B * 2 * D + 1));  // + step counter slot
     CKR(p->stepbuf.alloc((size_t)B * N * H * rsz));
     CKR(p->totals.alloc((size_t)B * N));
     CKR(p->records.alloc((size_t)B * p->nblk * reclen));
@@ -553,7 +560,6 @@ int mppi_plan_create(const mppi_chain_desc* chain, const mppi_cost_desc* costs,
     CK(cudaMemset(p->status.p, 0, sizeof(int) * B));
     CK(cudaMemset(p->bad.p, 0x7f, sizeof(int) * B));
     CKR(p->info.alloc(B));
-    CKR(p->stepctr.alloc(1));
     if (p->dump) {
       CKR(p->d_pos.alloc((size_t)N * HD));
       CKR(p->d_vel.alloc((size_t)N * HD));
@@ -580,16 +586,13 @@ int mppi_plan_create(const mppi_chain_desc* chain, const mppi_cost_desc* costs,
       p->goal_host[b * 16 + 0] = p->goal_host[b * 16 + 4] = p->goal_host[b * 16 + 8] = 1.0;
     }
     CK(cudaMemcpy(p->goal.p, p->goal_host.data(), sizeof(double) * B * 16, cudaMemcpyHostToDevice));
-    CK(cudaHostAlloc(&p->h_state, sizeof(double) * B * 2 * D, cudaHostAllocMapped));
-    CK(cudaHostAlloc(&p->h_ctr, sizeof(unsigned long long), cudaHostAllocMapped));
+    CK(cudaHostAlloc(&p->h_state, sizeof(double) * (B * 2 * D + 1), cudaHostAllocMapped));
     CK(cudaHostAlloc(&p->h_cmd, sizeof(double) * B * D, cudaHostAllocMapped));
     CK(cudaHostAlloc(&p->h_info, sizeof(mppi_step_info) * B, cudaHostAllocMapped));
     CK(cudaHostGetDevicePointer((void**)&p->m_state, p->h_state, 0));
-    CK(cudaHostGetDevicePointer((void**)&p->m_ctr, p->h_ctr, 0));
     CK(cudaHostGetDevicePointer((void**)&p->m_cmd, p->h_cmd, 0));
     CK(cudaHostGetDevicePointer((void**)&p->m_info, p->h_info, 0));
     memset(p->h_state, 0, sizeof(double) * B * 2 * D);
-    *p->h_ctr = 0;
     if (p->generator == MPPI_GEN_PSEUDORANDOM) {
       CKR(p->z.alloc((size_t)N * p->Kn * D));
       if (p->smoothing == MPPI_SMOOTH_BSPLINE) {
@@ -636,10 +639,8 @@ int mppi_plan_destroy(mppi_plan* p) {
   p->bad.release();
   p->e_status.release();
   p->info.release();
-  p->stepctr.release();
   mlp_release(p->mlp);
   if (p->h_state) cudaFreeHost(p->h_state);
-  if (p->h_ctr) cudaFreeHost(p->h_ctr);
   if (p->h_cmd) cudaFreeHost(p->h_cmd);
   if (p->h_info) cudaFreeHost(p->h_info);
   if (p->ev0) cudaEventDestroy(p->ev0);
@@ -860,7 +861,10 @@ int mppi_step(mppi_plan* p, const double* theta, const double* theta_dot, double
     memcpy(p->h_state + (size_t)b * 2 * D, theta + (size_t)b * D, sizeof(double) * D);
     memcpy(p->h_state + (size_t)b * 2 * D + D, theta_dot + (size_t)b * D, sizeof(double) * D);
   }
-  *p->h_ctr = p->step_counter++;
+  {
+    const unsigned long long ctr = p->step_counter++;
+    memcpy(p->h_state + (size_t)B * 2 * D, &ctr, sizeof(ctr));
+  }
   CK(cudaEventRecord(p->ev0, p->stream));
   CK(cudaGraphLaunch(p->graph, p->stream));
   CK(cudaEventRecord(p->ev1, p->stream));
@@ -871,7 +875,7 @@ int mppi_step(mppi_plan* p, const double* theta, const double* theta_dot, double
   if (info) {
     memcpy(info, p->h_info, sizeof(mppi_step_info) * B);
     double stg[4] = {0, 0, 0, 0};
-    for (int it = 0; it < p->iters; ++it)
+    for (int it = 0; it < (p->stage_events ? p->iters : 0); ++it)
       for (int sg = 0; sg < 4; ++sg) {
         float t = 0.f;
         CK(cudaEventElapsedTime(&t, p->stage_ev[4 * it + sg], p->stage_ev[4 * it + sg + 1]));
@@ -1062,10 +1066,9 @@ int mppi_stats_dev(mppi_plan* p, const double* theta, const double* theta_dot, v
     if (!theta || !theta_dot) return fail(MPPI_E_BAD_ARGUMENT, "state missing");
     memcpy(p->h_state, theta, sizeof(double) * D);
     memcpy(p->h_state + D, theta_dot, sizeof(double) * D);
-    *p->h_ctr = p->step_counter++;
-    step_prologue_kernel<<<1, 256, 0, st>>>(p->m_state, p->m_ctr, p->state.p, p->stepctr.p, p->status.p,
-                                            p->bad.p, 1, 2 * D);
-    CK(cudaGetLastError());
+    const unsigned long long ctr = p->step_counter++;
+    memcpy(p->h_state + 2 * D, &ctr, sizeof(ctr));
+    CK(cudaMemcpyAsync(p->state.p, p->h_state, sizeof(double) * (2 * D + 1), cudaMemcpyHostToDevice, st));
   }
   CKR(enqueue_sampling(p, it, st));
   double* rec = reinterpret_cast<double*>(record_dev);
@@ -1098,6 +1101,7 @@ int mppi_finalize_dev(mppi_plan* p, const void* records_dev, int32_t n_records, 
     s.bad = p->bad.p;
     s.cmd = p->m_cmd;
     s.info = p->m_info;
+    s.reset_status = it == p->iters - 1;
     CK(launch_finalize<R>(s, (const double*)records_dev, n_records, st));
     return MPPI_OK;
   };

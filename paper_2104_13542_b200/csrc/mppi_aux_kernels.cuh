@@ -446,23 +446,6 @@ __global__ void knots_ptr_kernel(double* z, long long rows, int K, int d, uint64
   (void)err;
 }
 
-// Step prologue: pull the (B, 2d) joint state and the step counter out of
-// mapped pinned host memory and reset the per-instance status words.
-__global__ void step_prologue_kernel(const double* __restrict__ h_state, const unsigned long long* h_ctr,
-                                     double* state, unsigned long long* ctr, int* status, int* bad, int B,
-                                     int per) {
-  const long long n = (long long)B * per;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
-       i += (long long)gridDim.x * blockDim.x)
-    state[i] = h_state[i];
-  for (long long b = blockIdx.x * (long long)blockDim.x + threadIdx.x; b < B;
-       b += (long long)gridDim.x * blockDim.x) {
-    status[b] = 0;
-    bad[b] = 0x7f7f7f7f;
-  }
-  if (blockIdx.x == 0 && threadIdx.x == 0) *ctr = *h_ctr;
-}
-
 __global__ void halton_points_kernel(double* out, long long count, int dims) {
   const long long total = count * dims;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;

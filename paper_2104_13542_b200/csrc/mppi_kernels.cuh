@@ -415,6 +415,7 @@ template <typename R>
 struct StatsArgs {
   int H, N, B, D, null_count, particle_offset, ppb, nblk;
   int shift, learned, totals_only, finalize_inline, isotropic, raw_step;
+  int reset_status;  // last iteration of a step: re-arm status/bad for the next step
   double beta, alpha_mu, alpha_sigma, smin, smax, a_coll;
   double tail_mean, tail_var, tail_sd;
   double disc[MAXH];   // gamma^h (numpy power), h < H-1
@@ -475,6 +476,7 @@ static __device__ void combine_records(const double* recs, int count, int reclen
   __syncthreads();
   if (threadIdx.x == 0) {
     double s0 = 0.0, cnt = 0.0, sf = 0.0, stt = 0.0, bad = 2147483647.0;
+#pragma unroll 4
     for (int k = 0; k < count; ++k) {
       const double* r = recs + (size_t)k * reclen;
       s0 += scale_smem[k] * r[1];
@@ -491,10 +493,17 @@ static __device__ void combine_records(const double* recs, int count, int reclen
     out[5] = bad;
   }
   for (int o = threadIdx.x; o < 2 * HD; o += blockDim.x) {
+    // branch-free, 8 independent record loads in flight (records of empty
+    // blocks hold zeros, so scale 0 contributes exactly 0)
     double s = 0.0;
-    for (int k = 0; k < count; ++k) {
-      const double sc = scale_smem[k];
-      if (sc != 0.0) s += sc * recs[(size_t)k * reclen + kRecHead + o];
+    const double* col = recs + kRecHead + o;
+    for (int k0 = 0; k0 < count; k0 += 8) {
+      double v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = k0 + u < count ? col[(size_t)(k0 + u) * reclen] : 0.0;
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (k0 + u < count) s += scale_smem[k0 + u] * v[u];
     }
     out[kRecHead + o] = s;
   }
@@ -591,6 +600,13 @@ static __device__ void finalize_policy(const StatsArgs<R>& a, int b, const doubl
     }
   }
   if (s_status == 0 && o < D && a.cmd) a.cmd[(size_t)b * D + o] = mu_new;  // next_command "mean"
+  if (a.reset_status) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      a.status[b] = 0;
+      a.bad[b] = 0x7f7f7f7f;
+    }
+  }
 }
 
 template <typename R, int D>
