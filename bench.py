@@ -306,6 +306,88 @@ def run_ours(args):
     return 0
 
 
+def run_batched(args):
+    """Config 4: B independent controllers, instances sharded over ranks, no
+    data-path collective. value = whole-job particle-steps/s."""
+    ws, rank, local = _dist_env()
+    dist = _maybe_init_dist(ws, local)
+    import torch
+
+    torch.cuda.set_device(local)
+    from paper_2104_13542_b200 import configs
+    from paper_2104_13542_b200 import _native as N
+    from paper_2104_13542_b200 import roofline as RL
+    from paper_2104_13542_b200.batched import BatchedController, shard_instances
+    from paper_2104_13542_b200.kinematics import load_chain
+    from paper_2104_13542_b200.surrogate import load_arm7_surrogate
+
+    N.require_device()
+    peaks, peaks_kind = _peaks()
+    B = args.instances
+    a, b = shard_instances(B, ws, rank)
+    goals, th0 = configs.batched_problem(b - a, first=a)
+    kw = dict(configs.CONTROLLER_KW)
+    kw.pop("seed")
+    kw["particles"] = args.particles
+    bc = BatchedController(load_chain("arm7.chain"), goals, weights=configs.make_weights(2),
+                           self_collision=load_arm7_surrogate(), precision=args.precision, device=local, **kw)
+    thd = np.zeros_like(th0)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=f"cuda:{local}")
+    for _ in range(max(3, args.warmup)):
+        bc.control_step(th0, thd)
+    dev_ms, stages = [], {"sample": [], "rollout": [], "mlp": [], "update": []}
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            _flush_l2(flush)
+            torch.cuda.synchronize()
+            _, diag = bc.control_step(th0, thd)
+            dev_ms.append(diag.device_ms)
+            for k in stages:
+                stages[k].append(diag.stage_ms[k])
+        torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
+    step_ms = _max_over_ranks(dist, float(np.mean(dev_ms)), local)
+    units = B * args.particles * 30
+    value = units / (step_ms * 1e-3)
+    e2e = []
+    for _ in range(max(3, args.steps // 4)):
+        _flush_l2(flush)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        bc.control_step(th0, thd)
+        e2e.append((time.perf_counter() - t0) * 1e3)
+    e2e_ms = _max_over_ranks(dist, float(np.mean(e2e)), local)
+    st_mean = {k: float(np.mean(v)) for k, v in stages.items()}
+    roof = RL.step_roofline(st_mean, rows=(b - a) * args.particles * 30, particles=(b - a) * args.particles,
+                            horizon=30, dof=7, config=2, peaks=peaks, peaks_kind=peaks_kind)
+    line = {
+        "metric": METRIC, "value": value, "unit": "particle-steps/s", "n_gpus": ws, "steps": args.steps,
+        "warmup": max(3, args.warmup), "ms_per_step": step_ms, "higher_is_better": True, "scaling": "weak"
+        if args.weak else "strong", "vs_baseline": None, "dtype": args.precision.replace("fp", "f"),
+        "data": "synthetic (goal_i = FK(q_i), q_i, theta0_i from default_rng(i), default_rng(10000+i))",
+        "config": {"workload": f"config4: {B} arm7 controllers x {args.particles} particles x H30, "
+                               "config-2 cost stack (learned MLP), instance-sharded",
+                   "instances": B, "instances_per_gpu": b - a, "particles": args.particles, "horizon": 30,
+                   "parallelism": f"instance-sharded x{ws}", "l2": "flushed before every timed step"},
+        "stage_ms": st_mean,
+        "e2e": {"value": units / (e2e_ms * 1e-3), "unit": "particle-steps/s",
+                "h2d_bytes_per_step": B * 14 * 8 // ws, "d2h_bytes_per_step": B * (7 * 8 + 80) // ws,
+                "ms_per_step": e2e_ms, "api": "BatchedController.control_step"},
+        "gpu_launches": args.steps * 3,
+        "roofline": roof,
+        "clocks": clk.summary(),
+    }
+    if rank == 0:
+        print(json.dumps(line))
+    if dist is not None:
+        dist.destroy_process_group()
+    return 0
+
+
 def _cpu_baseline(args):
     if not _have_reference():
         return {"value": None, "unit": "ms", "cores": os.cpu_count(), "kind": "reference",
@@ -322,13 +404,19 @@ def main():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="c2", choices=["c1", "c2"])
+    ap.add_argument("--workload", default="c2", choices=["c1", "c2", "c4"])
+    ap.add_argument("--instances", type=int, default=4096, help="config 4: total controllers")
+    ap.add_argument("--weak", action="store_true", help="config 4: --instances per GPU (weak scaling)")
     ap.add_argument("--particles", type=int, default=500)
     ap.add_argument("--precision", default="fp32", choices=["fp32", "fp64"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
+    if args.workload == "c4":
+        if args.weak:
+            args.instances *= int(os.environ.get("WORLD_SIZE", "1"))
+        return run_batched(args)
     return run_ours(args)
 
 

@@ -239,7 +239,11 @@ int mppi_get_noise(mppi_plan* plan, double* eps /* (N,H,d) host */);
 int mppi_set_goal(mppi_plan* plan, int32_t instance /* -1: all */,
                   const double* rotation /* (3,3) */, const double* translation /* (3,) */,
                   int32_t mode);
-int mppi_set_world(mppi_plan* plan, const double* spheres, int32_t n_spheres,
+/* All instances at once (config 4): rotations (count,3,3), translations
+ * (count,3), modes (count,) for instances [first, first+count). */
+int mppi_set_goals(mppi_plan* plan, int32_t first, int32_t count, const double* rotations,
+                   const double* translations, const int32_t* modes);
+int mppi_set_world(mppi_plan* plan,const double* spheres, int32_t n_spheres,
                    const double* boxes, int32_t n_boxes);
 /* Occupancy grid (nx,ny,nz) uint8, voxel (i,j,k) covers
  * origin + [i,i+1)*voxel ... ; narrow phase against boxes (nb,6) that tile

@@ -446,6 +446,43 @@ def shifted(means, variances, tail_mean: float, tail_var: float):
     return m, v
 
 
+def shard_record(totals, dev, beta: float) -> np.ndarray:
+    """Restatement of one rank's statistics record for the particle-sharded
+    update: [m_k, S0_k, count_k, sumfinite_k, status, bad,
+    S1_k (H*d), S2_k (H*d)] with weights relative to the LOCAL minimum and
+    deviations dev = u - mu_old (n_local, H, d)."""
+    ok = np.isfinite(totals)
+    m = totals[ok].min() if ok.any() else np.inf
+    w = np.zeros_like(totals)
+    if ok.any():
+        w[ok] = np.exp(-(totals[ok] - m) / beta)
+    s1 = np.einsum("n,nhd->hd", w, dev).ravel()
+    s2 = np.einsum("n,nhd->hd", w, dev * dev).ravel()
+    head = [m, w.sum(), float(ok.sum()), float(totals[ok].sum()), 0.0, 2147483647.0]
+    return np.concatenate([head, s1, s2])
+
+
+def combine_and_update(records, means, variances, alpha_mu, alpha_sigma, smin, smax, beta,
+                       isotropic=False):
+    """Fixed-order combine of rank records + update_mean/update_covariance,
+    algebraically equal to blend_policy over the concatenated particles."""
+    records = np.asarray(records)
+    HD = means.size
+    ok = records[:, 2] > 0
+    m = records[ok, 0].min()
+    scale = np.where(ok, np.exp(-(records[:, 0] - m) / beta), 0.0)
+    S0 = (scale * records[:, 1]).sum()
+    S1 = (scale[:, None] * records[:, 6:6 + HD]).sum(0).reshape(means.shape)
+    S2 = (scale[:, None] * records[:, 6 + HD:6 + 2 * HD]).sum(0).reshape(means.shape)
+    mu = (1.0 - alpha_mu) * means + alpha_mu * (means + S1 / S0)
+    delta = mu - means
+    emp = S2 / S0 - 2.0 * delta * (S1 / S0) + delta * delta
+    if isotropic:
+        emp = emp.mean(axis=1)
+    var = np.clip((1.0 - alpha_sigma) * variances + alpha_sigma * emp, smin, smax)
+    return mu, var
+
+
 class OracleController:
     """Controller.control_step (controller.py:198-260) restated: shift, K x
     (perturb, shape, rollout, weights, mean, covariance), command = means[0].

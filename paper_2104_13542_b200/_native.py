@@ -110,6 +110,7 @@ _SIGS = {
     "mppi_set_noise": (C.c_int, [_vp, _dp]),
     "mppi_get_noise": (C.c_int, [_vp, _dp]),
     "mppi_set_goal": (C.c_int, [_vp, C.c_int32, _dp, _dp, C.c_int32]),
+    "mppi_set_goals": (C.c_int, [_vp, C.c_int32, C.c_int32, _dp, _dp, C.POINTER(C.c_int32)]),
     "mppi_set_world": (C.c_int, [_vp, _dp, C.c_int32, _dp, C.c_int32]),
     "mppi_set_voxel_world": (C.c_int, [_vp, C.POINTER(C.c_uint8), C.c_int32, C.c_int32, C.c_int32,
                                        _dp, C.c_double, _dp, C.c_int32]),

@@ -67,6 +67,26 @@ def make_controller(config: int = 2, **overrides):
                       self_collision=provider, **kw)
 
 
+def batched_problem(instances: int, first: int = 0, chain=None):
+    """Config 4 goals and start states for instances [first, first+instances):
+    goal_i = FK(q_i) (full pose), q_i ~ U(k_jl-shrunk limits) from default_rng(i);
+    theta0_i ~ U(shrunk limits) from default_rng(10000 + i)."""
+    from .costs import FULL_POSE, GoalSpec
+    from .kinematics import Pose, fk_batch, load_chain
+
+    chain = chain or load_chain("arm7.chain")
+    lo, hi = chain.joint_limits[:, 0], chain.joint_limits[:, 1]
+    k = WEIGHTS[2].get("k_jl", 0.1)
+    lo_s, hi_s = lo + k * (hi - lo), hi - k * (hi - lo)
+    idx = range(first, first + instances)
+    q = np.stack([np.random.default_rng(i).uniform(lo_s, hi_s) for i in idx])
+    th0 = np.stack([np.random.default_rng(10000 + i).uniform(lo_s, hi_s) for i in idx])
+    rot, trans = fk_batch(chain, q)
+    goals = [GoalSpec(target_pose=Pose(rotation=rot[i, -1], translation=trans[i, -1]), mode=FULL_POSE)
+             for i in range(instances)]
+    return goals, th0
+
+
 def start_state():
     from .rollout import JointState
 

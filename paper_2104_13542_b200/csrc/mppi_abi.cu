@@ -728,6 +728,23 @@ int mppi_set_goal(mppi_plan* p, int32_t inst, const double* R, const double* t, 
   return MPPI_OK;
 }
 
+int mppi_set_goals(mppi_plan* p, int32_t first, int32_t count, const double* R, const double* t,
+                   const int32_t* modes) {
+  if (!p || !R || !t || !modes) return fail(MPPI_E_BAD_ARGUMENT, "null argument");
+  if (first < 0 || count < 1 || first + count > p->B) return fail(MPPI_E_BAD_ARGUMENT, "instance range");
+  CKR(set_device(p));
+  for (int i = 0; i < count; ++i) {
+    double* g = &p->goal_host[(size_t)(first + i) * 16];
+    for (int k = 0; k < 9; ++k) g[k] = R[(size_t)i * 9 + k];
+    for (int k = 0; k < 3; ++k) g[9 + k] = t[(size_t)i * 3 + k];
+    g[12] = (double)modes[i];
+  }
+  CK(cudaMemcpyAsync(p->goal.p + (size_t)first * 16, &p->goal_host[(size_t)first * 16],
+                     sizeof(double) * 16 * count, cudaMemcpyHostToDevice, p->stream));
+  CK(cudaStreamSynchronize(p->stream));
+  return MPPI_OK;
+}
+
 int mppi_set_world(mppi_plan* p, const double* spheres, int32_t ns, const double* boxes, int32_t nb) {
   if (!p || ns < 0 || nb < 0) return fail(MPPI_E_BAD_ARGUMENT, "bad world arguments");
   CKR(set_device(p));

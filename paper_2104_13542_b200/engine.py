@@ -166,6 +166,13 @@ class Plan:
         t = N.f64(translation, (3,))
         N.check(self.lib.mppi_set_goal(self.handle, int(instance), N.dptr(R), N.dptr(t), int(mode)))
 
+    def set_goals(self, rotations, translations, modes, first: int = 0):
+        R = N.f64(rotations).reshape(-1, 9)
+        t = N.f64(translations).reshape(-1, 3)
+        m = np.ascontiguousarray(np.asarray(modes, dtype=np.int32).reshape(-1))
+        N.check(self.lib.mppi_set_goals(self.handle, int(first), R.shape[0], N.dptr(R), N.dptr(t),
+                                        m.ctypes.data_as(C.POINTER(C.c_int32))))
+
     def set_world(self, world):
         grid = getattr(world, "voxel_grid", None)
         sp = N.f64(world.spheres).reshape(-1, 4)

@@ -1,0 +1,102 @@
+"""Config 4 (batched independent controllers) and config 5 (particle-sharded
+single controller) on the GPU, against independent oracle controllers and the
+unsharded device controller."""
+
+import numpy as np
+import pytest
+
+from oracle import mppi_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+def _oracle_for(goal, theta0, config=2, particles=128, **extra):
+    from paper_2104_13542_b200 import configs
+    from paper_2104_13542_b200.kinematics import load_chain
+    from paper_2104_13542_b200.surrogate import ARM7_SURROGATE
+
+    kw = dict(configs.CONTROLLER_KW)
+    kw.pop("seed")
+    kw["particles"] = particles
+    kw.update(extra)
+    mlp = None
+    if config == 2:
+        with np.load(ARM7_SURROGATE) as z:
+            mlp = {k: z[k] for k in z.files if k.startswith(("W", "b"))}
+    return O.OracleController(load_chain("arm7.chain"), configs.make_weights(config), goal.target_pose.rotation,
+                              goal.target_pose.translation, goal.mode != "position_only",
+                              provider="learned" if config == 2 else None, mlp_state=mlp, **kw)
+
+
+@pytest.mark.parametrize("precision,tol", [("fp64", 1e-6), ("fp32", 1e-3)])
+def test_batched_instances_match_independent_controllers(precision, tol):
+    from paper_2104_13542_b200 import configs
+    from paper_2104_13542_b200.batched import BatchedController
+    from paper_2104_13542_b200.kinematics import load_chain
+    from paper_2104_13542_b200.surrogate import load_arm7_surrogate
+
+    B, n = 5, 128
+    goals, th0 = configs.batched_problem(B)
+    kw = dict(configs.CONTROLLER_KW)
+    kw.pop("seed")
+    kw["particles"] = n
+    bc = BatchedController(load_chain("arm7.chain"), goals, weights=configs.make_weights(2),
+                           self_collision=load_arm7_surrogate(), precision=precision, **kw)
+    oracles = [_oracle_for(goals[b], th0[b], particles=n) for b in range(B)]
+    theta = th0.copy()
+    thetad = np.zeros_like(theta)
+    for _ in range(2):
+        cmds, diag = bc.control_step(theta, thetad)
+        assert (diag.status == 0).all()
+        for b in range(B):
+            ref = oracles[b].step(theta[b], thetad[b])
+            np.testing.assert_allclose(cmds[b], ref, atol=tol, err_msg=f"instance {b}")
+            np.testing.assert_allclose(bc.policy(b).means, oracles[b].means, atol=tol)
+        thetad = thetad + 0.05 * cmds
+        theta = theta + 0.05 * thetad
+
+
+def test_emulated_particle_shards_match_unsharded():
+    """R plans holding disjoint particle shards on one GPU; their records are
+    concatenated on the device exactly as the all-gather would, and every
+    shard's finalize must reproduce the unsharded controller."""
+    import torch
+
+    from paper_2104_13542_b200 import configs
+    from paper_2104_13542_b200.engine import Plan, PlanSpec
+    from paper_2104_13542_b200.kinematics import load_chain
+    from paper_2104_13542_b200.sharded import particle_shard
+    from paper_2104_13542_b200 import _native as N
+
+    total, R = 600, 3
+    ref = configs.make_controller(1, particles=total, precision="fp64")
+    chain = load_chain("arm7.chain")
+    goal = configs.make_goal(1)
+    plans = []
+    for r in range(R):
+        off, cnt = particle_shard(total, R, r)
+        spec = PlanSpec(horizon=30, particles=cnt, dts=ref.sched.dts, null_count=2, precision=N.FP64,
+                        particle_offset=off, particles_total=total, gamma=0.99, beta=1.0, alpha_mu=0.9,
+                        alpha_sigma=0.5, sigma0_sq=0.5, sigma_sq_min=0.01, sigma_sq_max=0.5, knots=5)
+        p = Plan(chain, configs.make_weights(1), spec)
+        p.init_noise()
+        p.set_goal(goal.target_pose.rotation, goal.target_pose.translation, goal.mode_code, 0)
+        plans.append(p)
+    # the shards' noise rows are exactly the unsharded block's rows
+    full = ref.plan.get_noise()
+    for r, p in enumerate(plans):
+        off, cnt = particle_shard(total, R, r)
+        np.testing.assert_array_equal(p.get_noise(), full[off:off + cnt])
+    L = plans[0].record_len()
+    recs = torch.zeros(R * L, dtype=torch.float64, device="cuda:0")
+    st = configs.start_state()
+    for _ in range(3):
+        cmd_ref, _ = ref.control_step(st)
+        for r, p in enumerate(plans):
+            p.stats_dev(st.theta, st.theta_dot, recs.data_ptr() + r * L * 8)
+        torch.cuda.synchronize()
+        outs = [p.finalize_dev(recs.data_ptr(), R)[0] for p in plans]
+        for c in outs:
+            np.testing.assert_allclose(c, cmd_ref, atol=1e-9)
+        np.testing.assert_array_equal(outs[0], outs[1])
+        np.testing.assert_allclose(plans[0].get_policy(0)[1], ref.plan.get_policy(0)[1], atol=1e-9)
