@@ -334,3 +334,44 @@ def test_pseudorandom_generator_runs_and_is_seeded():
         outs.append(cmd)
     np.testing.assert_array_equal(outs[0], outs[1])
     assert not np.array_equal(outs[0], outs[2])
+
+
+def test_cuda_backend_in_unmodified_reference():
+    """INTEGRATION.md tier 2: install the six seam kernels into the reference's
+    own kernel table (oracle/_ref, unmodified) and run ITS Controller."""
+    import sys
+    from pathlib import Path
+
+    ref_root = Path(__file__).resolve().parents[1] / "oracle" / "_ref"
+    if not (ref_root / "jointmpc").exists():
+        pytest.skip("oracle/_ref not built")
+    sys.path.insert(0, str(ref_root))
+    import jointmpc.kernels as RK
+    from jointmpc.controller import Controller as RefController
+    from jointmpc.costs import CostWeights as RefWeights
+    from jointmpc.costs import goal_at_position as ref_goal
+    from jointmpc.kinematics import load_chain as ref_load
+    from jointmpc.rollout import JointState as RefState
+
+    from paper_2104_13542_b200 import kernels as cuda_backend
+
+    saved = cuda_backend.install_into(RK)
+    try:
+        chain = ref_load("arm7.chain")
+        c = RefController(chain, ref_goal([0.4, 0.2, 0.5]), particles=64, horizon=20, weights=RefWeights(), seed=0)
+        st = RefState(theta=np.array([0.0, -0.5, 0.0, -1.8, 0.0, 1.4, 0.0]), theta_dot=np.zeros(7),
+                      theta_ddot=np.zeros(7))
+        cmd, diag = c.control_step(st)
+        assert RK.BACKEND_NAME in ("numba", "numpy")  # the table was rebound, not the module swapped
+        assert RK.fk_batch is cuda_backend.fk_batch
+    finally:
+        for k, fn in saved.items():
+            setattr(RK, k, fn)
+    # the same step with the oracle (float64, same kwargs) — defaults of Controller / CostWeights
+    from paper_2104_13542_b200.costs import CostWeights
+    from paper_2104_13542_b200.kinematics import load_chain
+
+    oc = O.OracleController(load_chain("arm7.chain"), CostWeights(), np.eye(3), np.array([0.4, 0.2, 0.5]), False,
+                            particles=64, horizon=20, provider="oracle")
+    ocmd = oc.step(st.theta, st.theta_dot)
+    np.testing.assert_allclose(cmd, ocmd, atol=1e-9)
