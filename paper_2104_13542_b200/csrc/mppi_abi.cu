@@ -164,6 +164,7 @@ struct mppi_plan {
   DevBuf<float> mlp_x, mlp_d;
   DevBuf<double> totals, records, out_record, cmd, counters_pad;
   DevBuf<unsigned> counters;
+  DevBuf<unsigned long long> dbg;  // MPPI_DEBUG_TIMERS=1: stats-kernel phase stamps
   DevBuf<int> status, bad;
   DevBuf<mppi_step_info> info;
   int nblk = 1, ppb = 64;
@@ -345,6 +346,7 @@ int enqueue_iteration(mppi_plan* p, int it, bool inline_final, double* out_recor
   s.counters = p->counters.p;
   s.status = p->status.p;
   s.bad = p->bad.p;
+  s.dbg = p->dbg.p;
   s.cmd = p->m_cmd;   // mapped host memory: no D2H copy node
   s.info = p->m_info;
   if (p->dump) {
@@ -560,6 +562,10 @@ int mppi_plan_create(const mppi_chain_desc* chain, const mppi_cost_desc* costs,
     CK(cudaMemset(p->status.p, 0, sizeof(int) * B));
     CK(cudaMemset(p->bad.p, 0x7f, sizeof(int) * B));
     CKR(p->info.alloc(B));
+    if (getenv("MPPI_DEBUG_TIMERS")) {
+      CKR(p->dbg.alloc((size_t)16 * p->nblk));
+      CK(cudaMemset(p->dbg.p, 0, sizeof(unsigned long long) * 16 * p->nblk));
+    }
     if (p->dump) {
       CKR(p->d_pos.alloc((size_t)N * HD));
       CKR(p->d_vel.alloc((size_t)N * HD));
@@ -634,6 +640,7 @@ int mppi_plan_destroy(mppi_plan* p) {
   p->stepbuf.release();
   p->e_stepbuf.release();
   p->counters.release();
+  p->dbg.release();
   p->e_counters.release();
   p->status.release();
   p->bad.release();
@@ -889,6 +896,17 @@ int mppi_step(mppi_plan* p, const double* theta, const double* theta_dot, double
   float ms = 0.f;
   CK(cudaEventElapsedTime(&ms, p->ev0, p->ev1));
   memcpy(command_out, p->h_cmd, sizeof(double) * B * D);
+  if (p->dbg.p) {  // debug: stats-kernel phase timeline of instance 0, relative to block 0 start
+    std::vector<unsigned long long> t((size_t)16 * p->nblk);
+    CK(cudaMemcpy(t.data(), p->dbg.p, sizeof(unsigned long long) * t.size(), cudaMemcpyDeviceToHost));
+    const unsigned long long t0 = t[0];
+    for (int k = 0; k < p->nblk; ++k) {
+      fprintf(stderr, "stats blk %2d:", k);
+      for (int j = 0; j < 7; ++j)
+        fprintf(stderr, " %8.2f", t[k * 16 + j] ? (double)(long long)(t[k * 16 + j] - t0) * 1e-3 : -1.0);
+      fprintf(stderr, "\n");
+    }
+  }
   if (info) {
     memcpy(info, p->h_info, sizeof(mppi_step_info) * B);
     double stg[4] = {0, 0, 0, 0};

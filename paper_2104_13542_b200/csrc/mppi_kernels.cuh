@@ -439,6 +439,7 @@ struct StatsArgs {
   double* dump_step;   // (N,H) instance 0
   double* dump_terms;  // (6,N,H) instance 0 (selfcoll row written for learned)
   double* dump_weights;  // (N) instance 0
+  unsigned long long* dbg;  // debug phase timers (globaltimer ns), NULL in production
 };
 
 __device__ __forceinline__ double block_min_d(double v, double* red) {
@@ -462,51 +463,83 @@ __device__ __forceinline__ double block_min_d(double v, double* red) {
 // minimum) into one record relative to the global minimum. Deterministic:
 // every sum runs in record order. (§8(e): rescale by exp(-(m_k - m)/beta).)
 static __device__ void combine_records(const double* recs, int count, int reclen, int HD, double beta,
-                                double* out, double* scale_smem, double* red) {
-  double m = CUDART_INF;
-  for (int k = threadIdx.x; k < count; k += blockDim.x) {
-    const double* r = recs + (size_t)k * reclen;
-    if (r[2] > 0.0) m = fmin(m, r[0]);
-  }
-  m = block_min_d(m, red);
-  for (int k = threadIdx.x; k < count; k += blockDim.x) {
-    const double* r = recs + (size_t)k * reclen;
-    scale_smem[k] = r[2] > 0.0 ? exp(-(r[0] - m) / beta) : 0.0;
+                                       double* out, double* scale_smem, double* red) {
+  // Latency-oriented: ONE parallel load of every record head into shared
+  // memory, the record columns are preloaded (16 in flight per thread) while
+  // warp 0 derives the global minimum and the rescale factors.
+  double* hs = scale_smem + max(count, 8);  // record heads follow the scales (host sizes both)
+  for (int t = threadIdx.x; t < count * kRecHead; t += blockDim.x)
+    hs[t] = recs[(size_t)(t / kRecHead) * reclen + (t % kRecHead)];
+  constexpr int CB = 16;
+  const int o0 = threadIdx.x, o1 = threadIdx.x + blockDim.x;
+  double v0[CB], v1[CB];
+#pragma unroll
+  for (int u = 0; u < CB; ++u) {
+    v0[u] = (u < count && o0 < 2 * HD) ? recs[(size_t)u * reclen + kRecHead + o0] : 0.0;
+    v1[u] = (u < count && o1 < 2 * HD) ? recs[(size_t)u * reclen + kRecHead + o1] : 0.0;
   }
   __syncthreads();
-  if (threadIdx.x == 0) {
+  if (threadIdx.x < 32) {
+    const int lane = threadIdx.x;
+    double m = CUDART_INF;
+    for (int k = lane; k < count; k += 32)
+      if (hs[k * kRecHead + 2] > 0.0) m = fmin(m, hs[k * kRecHead + 0]);
+    for (int off = 16; off > 0; off >>= 1) m = fmin(m, __shfl_xor_sync(0xffffffffu, m, off));
     double s0 = 0.0, cnt = 0.0, sf = 0.0, stt = 0.0, bad = 2147483647.0;
-#pragma unroll 4
-    for (int k = 0; k < count; ++k) {
-      const double* r = recs + (size_t)k * reclen;
-      s0 += scale_smem[k] * r[1];
+    for (int k = lane; k < count; k += 32) {
+      const double* r = hs + k * kRecHead;
+      const double sc = r[2] > 0.0 ? exp(-(r[0] - m) / beta) : 0.0;
+      scale_smem[k] = sc;
+      s0 += sc * r[1];
       cnt += r[2];
       sf += r[3];
       stt = fmax(stt, r[4]);
       bad = fmin(bad, r[5]);
     }
-    out[0] = m;
-    out[1] = s0;
-    out[2] = cnt;
-    out[3] = sf;
-    out[4] = stt;
-    out[5] = bad;
-  }
-  for (int o = threadIdx.x; o < 2 * HD; o += blockDim.x) {
-    // branch-free, 8 independent record loads in flight (records of empty
-    // blocks hold zeros, so scale 0 contributes exactly 0)
-    double s = 0.0;
-    const double* col = recs + kRecHead + o;
-    for (int k0 = 0; k0 < count; k0 += 8) {
-      double v[8];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) v[u] = k0 + u < count ? col[(size_t)(k0 + u) * reclen] : 0.0;
-#pragma unroll
-      for (int u = 0; u < 8; ++u)
-        if (k0 + u < count) s += scale_smem[k0 + u] * v[u];
+    s0 = warp_sum(s0);
+    cnt = warp_sum(cnt);
+    sf = warp_sum(sf);
+    for (int off = 16; off > 0; off >>= 1) {
+      stt = fmax(stt, __shfl_xor_sync(0xffffffffu, stt, off));
+      bad = fmin(bad, __shfl_xor_sync(0xffffffffu, bad, off));
     }
+    if (lane == 0) {
+      out[0] = m;
+      out[1] = s0;
+      out[2] = cnt;
+      out[3] = sf;
+      out[4] = stt;
+      out[5] = bad;
+    }
+  }
+  __syncthreads();
+  double s_0 = 0.0, s_1 = 0.0;
+#pragma unroll
+  for (int u = 0; u < CB; ++u)
+    if (u < count) {
+      s_0 += scale_smem[u] * v0[u];
+      s_1 += scale_smem[u] * v1[u];
+    }
+  for (int k0 = CB; k0 < count; k0 += CB) {  // more than 16 records (large N): further batches
+#pragma unroll
+    for (int u = 0; u < CB; ++u) {
+      v0[u] = (k0 + u < count && o0 < 2 * HD) ? recs[(size_t)(k0 + u) * reclen + kRecHead + o0] : 0.0;
+      v1[u] = (k0 + u < count && o1 < 2 * HD) ? recs[(size_t)(k0 + u) * reclen + kRecHead + o1] : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < CB; ++u)
+      if (k0 + u < count) {
+        s_0 += scale_smem[k0 + u] * v0[u];
+        s_1 += scale_smem[k0 + u] * v1[u];
+      }
+  }
+  for (int o = 2 * blockDim.x; o < 2 * HD; o += blockDim.x) {  // only if 2HD > 2*blockDim
+    double s = 0.0;
+    for (int k = 0; k < count; ++k) s += scale_smem[k] * recs[(size_t)k * reclen + kRecHead + o];
     out[kRecHead + o] = s;
   }
+  if (o0 < 2 * HD) out[kRecHead + o0] = s_0;
+  if (o1 < 2 * HD) out[kRecHead + o1] = s_1;
   __syncthreads();
 }
 
@@ -620,15 +653,22 @@ __global__ void __launch_bounds__(kStatsThreads) stats_kernel(const __grid_const
   double* tot = sm;             // [ppb]
   double* wt = sm + a.ppb;      // [ppb]
   double* red = wt + a.ppb;     // [32]
-  double* scale = red + 32;     // [max(nblk, 8)]
+  double* scale = red + 32;     // [max(nblk, 8)] scales + [max(nblk, 8) * kRecHead] heads
   const int reclen = kRecHead + 2 * HD;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const bool failed = (a.status[b] != 0);
+#define MPPI_STAMP(k)                                                                        \
+  if (a.dbg && threadIdx.x == 0 && b == 0) {                                                  \
+    unsigned long long t_;                                                                   \
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                                   \
+    a.dbg[blk * 16 + (k)] = t_;                                                              \
+  }
+  MPPI_STAMP(0);
 
   // ---- phase A: discounted totals, quarantine (rollout.py:111-171) ---------
   // Each warp takes PA particles at a time and issues all their loads before
   // the first reduction, so the HBM/L2 latency is paid once per batch.
-  if (!failed || a.totals_only) {
+  {  // runs even when the step already failed: cheap, and the status load overlaps it
     constexpr int PA = 4;
     for (int i0 = wid * PA; i0 < cnt; i0 += nw * PA) {
       double cv[PA], dv[PA];
@@ -675,6 +715,7 @@ __global__ void __launch_bounds__(kStatsThreads) stats_kernel(const __grid_const
   }
   if (a.totals_only) return;
   __syncthreads();
+  MPPI_STAMP(1);
 
   // ---- phase B/C: block min, weights relative to it (policy.py:103-121) ----
   double mloc = CUDART_INF;
@@ -688,11 +729,18 @@ __global__ void __launch_bounds__(kStatsThreads) stats_kernel(const __grid_const
   __syncthreads();
 
   // ---- phase D: weighted sufficient statistics around the old mean ---------
+  double mo_pre = 0.0, so_pre = 0.0;  // this thread's policy entry, loaded before the barriers
+  if (threadIdx.x < HD) {
+    const int h = threadIdx.x / D, j = threadIdx.x - h * D;
+    const int hs = a.shift ? h + 1 : h;
+    mo_pre = hs < H ? a.means[(size_t)b * HD + hs * D + j] : a.tail_mean;
+    so_pre = hs < H ? a.sd[(size_t)b * HD + hs * D + j] : a.tail_sd;
+  }
   // Particles whose weight underflowed to exactly 0 contribute nothing; warp 0
   // compacts the others (ascending, so the summation order is fixed) and every
   // output then runs a branch-free loop with PD independent eps loads in flight.
   double* rec = a.records + ((size_t)b * a.nblk + blk) * reclen;
-  int* nz = reinterpret_cast<int*>(sm + 2 * a.ppb + 32 + max(a.nblk, 8) + reclen + HD);
+  int* nz = reinterpret_cast<int*>(sm + 2 * a.ppb + 32 + max(a.nblk, 8) * (1 + kRecHead) + reclen + HD);
   __shared__ int s_nnz;
   if (wid == 0) {
     int base = 0;
@@ -729,15 +777,13 @@ __global__ void __launch_bounds__(kStatsThreads) stats_kernel(const __grid_const
   }
   __syncthreads();
   const int nnz = s_nnz;
-  for (int o = threadIdx.x; o < HD; o += blockDim.x) {
+  MPPI_STAMP(2);
+  if (threadIdx.x < HD) {  // H*d <= 256 = blockDim: one policy entry per thread
+    const int o = threadIdx.x;
     double s1 = 0.0, s2 = 0.0;
     if (!failed) {
-      const int h = o / D, j = o - h * D;
-      const int hs = a.shift ? h + 1 : h;
-      const double mo = hs < H ? a.means[(size_t)b * HD + hs * D + j] : a.tail_mean;
-      const double so = hs < H ? a.sd[(size_t)b * HD + hs * D + j] : a.tail_sd;
       const double* ep = a.eps + (size_t)n0 * HD + o;
-      constexpr int PD = 8;
+      constexpr int PD = 16;
       for (int k0 = 0; k0 < nnz; k0 += PD) {
         double e[PD];
         int ii[PD];
@@ -750,7 +796,8 @@ __global__ void __launch_bounds__(kStatsThreads) stats_kernel(const __grid_const
         for (int u = 0; u < PD; ++u) {
           if (ii[u] < 0) break;
           const int ng = n0 + ii[u] + a.particle_offset;
-          const double dv = ng < a.null_count ? 0.0 - mo : (ng == a.null_count ? 0.0 : (mo + so * e[u]) - mo);
+          const double dv = ng < a.null_count ? 0.0 - mo_pre
+                                              : (ng == a.null_count ? 0.0 : (mo_pre + so_pre * e[u]) - mo_pre);
           const double w = wt[ii[u]];
           s1 += w * dv;
           s2 += w * dv * dv;
@@ -763,6 +810,7 @@ __global__ void __launch_bounds__(kStatsThreads) stats_kernel(const __grid_const
 
   // ---- last block of this instance combines + finalizes --------------------
   __shared__ bool s_last;
+  MPPI_STAMP(3);
   __threadfence();
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -771,15 +819,19 @@ __global__ void __launch_bounds__(kStatsThreads) stats_kernel(const __grid_const
   }
   __syncthreads();
   if (!s_last) return;
+  MPPI_STAMP(4);
   __threadfence();
   if (threadIdx.x == 0) a.counters[b] = 0u;
-  double* comb = a.finalize_inline ? (sm + 2 * a.ppb + 32 + max(a.nblk, 8))
+  double* comb = a.finalize_inline ? (sm + 2 * a.ppb + 32 + max(a.nblk, 8) * (1 + kRecHead))
                                    : a.out_record + (size_t)b * reclen;
   combine_records(a.records + (size_t)b * a.nblk * reclen, a.nblk, reclen, HD, a.beta, comb, scale,
                   red);
+  MPPI_STAMP(5);
   if (!a.finalize_inline) return;
   double* emp = comb + reclen;
   finalize_policy(a, b, comb, emp);
+  __syncthreads();
+  MPPI_STAMP(6);
   if (b == 0 && a.dump_weights && a.status[0] == 0) {
     __syncthreads();
     const double m = comb[0];
@@ -798,7 +850,7 @@ __global__ void __launch_bounds__(kStatsThreads)
   const int HD = a.H * a.D, reclen = kRecHead + 2 * HD;
   double* red = sm;
   double* scale = sm + 32;
-  double* comb = scale + max(count, 8);
+  double* comb = scale + max(count, 8) * (1 + kRecHead);
   double* emp = comb + reclen;
   combine_records(recs, count, reclen, HD, a.beta, comb, scale, red);
   finalize_policy(a, 0, comb, emp);

@@ -15,7 +15,8 @@ template <typename R>
 cudaError_t launch_finalize(const StatsArgs<R>& s, const double* recs, int count, cudaStream_t st);
 
 inline size_t stats_smem_bytes(int ppb, int nblk, int HD) {
-  return sizeof(double) * (2 * (size_t)ppb + 32 + (nblk > 8 ? nblk : 8) + (kRecHead + 2 * HD) + HD) +
+  return sizeof(double) * (2 * (size_t)ppb + 32 + (size_t)(nblk > 8 ? nblk : 8) * (1 + kRecHead) +
+                           (kRecHead + 2 * HD) + HD) +
          sizeof(int) * ((size_t)ppb + 2);
 }
 
@@ -69,7 +70,7 @@ cudaError_t launch_stats_any(const StatsArgs<R>& s, int D, cudaStream_t st) {
 template <typename R>
 cudaError_t launch_finalize(const StatsArgs<R>& s, const double* recs, int count, cudaStream_t st) {
   const int HD = s.H * s.D;
-  const size_t smem = sizeof(double) * (32 + (count > 8 ? count : 8) + kRecHead + 2 * HD + HD);
+  const size_t smem = sizeof(double) * (32 + (size_t)(count > 8 ? count : 8) * (1 + kRecHead) + kRecHead + 2 * HD + HD);
   finalize_kernel<R><<<1, kStatsThreads, smem, st>>>(s, recs, count);
   return cudaGetLastError();
 }
