@@ -388,6 +388,132 @@ def run_batched(args):
     return 0
 
 
+def run_tracking(args):
+    """Config 3: moving-target tracking with the 64^3 voxel world, closed loop
+    (goal from the TargetScript at t = i*dt, plant = semi-implicit Euler)."""
+    ws, rank, local = _dist_env()
+    import torch
+
+    torch.cuda.set_device(local)
+    from paper_2104_13542_b200 import configs
+    from paper_2104_13542_b200 import _native as N
+    from paper_2104_13542_b200 import roofline as RL
+    from paper_2104_13542_b200.controller import Controller
+    from paper_2104_13542_b200.kinematics import load_chain
+    from paper_2104_13542_b200.simworld import target_at
+
+    N.require_device()
+    peaks, peaks_kind = _peaks()
+    script, world = configs.tracking_problem()
+    kw = dict(configs.CONTROLLER_KW)
+    kw["particles"] = args.particles
+    ctrl = Controller(load_chain("arm7.chain"), target_at(script, 0.0), weights=configs.make_weights(3),
+                      world=world, precision=args.precision, device=local, **kw)
+    st = configs.start_state()
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=f"cuda:{local}")
+    dev_ms, e2e, stages = [], [], {"sample": [], "rollout": [], "mlp": [], "update": []}
+    total = max(3, args.warmup) + args.steps
+    for i in range(total):
+        ctrl.set_goal(target_at(script, i * 0.05))
+        _flush_l2(flush)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        cmd, diag = ctrl.control_step(st)
+        wall = (time.perf_counter() - t0) * 1e3
+        if i >= total - args.steps:
+            e2e.append(wall)
+            inf = ctrl.plan._info[0]
+            dev_ms.append(inf.device_ms)
+            for k, v in (("sample", inf.sample_ms), ("rollout", inf.rollout_ms), ("mlp", inf.mlp_ms),
+                         ("update", inf.update_ms)):
+                stages[k].append(v)
+        st.theta_dot = st.theta_dot + 0.05 * cmd
+        st.theta = st.theta + 0.05 * st.theta_dot
+    st_mean = {k: float(np.mean(v)) for k, v in stages.items()}
+    value = float(np.mean(dev_ms))
+    line = {
+        "metric": METRIC, "value": value, "unit": "ms", "n_gpus": ws, "steps": args.steps,
+        "warmup": max(3, args.warmup), "ms_per_step": value, "higher_is_better": False, "scaling": "weak",
+        "vs_baseline": None, "dtype": args.precision.replace("fp", "f"), "data": "synthetic",
+        "config": {"workload": f"config3: moving-target tracking, 64^3 voxel world ({world.boxes.shape[0]} boxes), "
+                               f"{args.particles} x H30, closed loop", "particles": args.particles,
+                   "horizon": 30, "l2": "flushed before every timed step"},
+        "stage_ms": st_mean,
+        "e2e": {"value": float(np.mean(e2e)), "unit": "ms", "h2d_bytes_per_step": 112 + 16 * 8,
+                "d2h_bytes_per_step": 136, "api": "Controller.control_step + set_goal"},
+        "gpu_launches": args.steps * 2,
+        "roofline": RL.step_roofline(st_mean, rows=args.particles * 30, particles=args.particles, horizon=30,
+                                     dof=7, config=1, peaks=peaks, peaks_kind=peaks_kind),
+    }
+    if rank == 0:
+        print(json.dumps(line))
+    return 0
+
+
+def run_sweep(args):
+    """Config 5: one controller, N particles; 1 GPU = plain Controller, N GPUs =
+    particle-sharded with one record all-gather per iteration."""
+    ws, rank, local = _dist_env()
+    dist = _maybe_init_dist(ws, local)
+    import torch
+
+    torch.cuda.set_device(local)
+    from paper_2104_13542_b200 import configs
+    from paper_2104_13542_b200 import _native as N
+    from paper_2104_13542_b200.kinematics import load_chain
+    from paper_2104_13542_b200.surrogate import load_arm7_surrogate
+
+    N.require_device()
+    Np = args.particles
+    st = configs.start_state()
+    if ws == 1:
+        ctrl = configs.make_controller(2, particles=Np, precision=args.precision, device=local)
+        step = lambda: ctrl.control_step(st)  # noqa: E731
+    else:
+        from paper_2104_13542_b200.sharded import RecordExchange, ShardedController
+
+        kw = dict(configs.CONTROLLER_KW)
+        kw.pop("particles")
+        ctrl = ShardedController(load_chain("arm7.chain"), configs.make_goal(2), particles=Np, world_size=ws,
+                                 rank=rank, device=local, exchange=RecordExchange(),
+                                 weights=configs.make_weights(2), self_collision=load_arm7_surrogate(),
+                                 precision=args.precision, **kw)
+        step = lambda: ctrl.control_step(st)  # noqa: E731
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=f"cuda:{local}")
+    for _ in range(max(3, args.warmup)):
+        step()
+    times = []
+    s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if dist is not None:
+        dist.barrier()
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            _flush_l2(flush)
+            torch.cuda.synchronize()
+            s0.record()
+            step()
+            s1.record()
+            torch.cuda.synchronize()
+            times.append(s0.elapsed_time(s1))
+    ms = _max_over_ranks(dist, float(np.mean(times)), local)
+    line = {
+        "metric": METRIC, "value": Np * 30 / (ms * 1e-3), "unit": "particle-steps/s", "n_gpus": ws,
+        "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": args.precision.replace("fp", "f"), "data": "synthetic",
+        "config": {"workload": f"config5: one controller, {Np} particles x H30, config-2 costs, "
+                               + ("particle-sharded, 1 all-gather/iteration" if ws > 1 else "single GPU"),
+                   "particles": Np, "horizon": 30, "l2": "flushed before every timed step"},
+        "e2e": {"value": Np * 30 / (ms * 1e-3), "unit": "particle-steps/s", "h2d_bytes_per_step": 112,
+                "d2h_bytes_per_step": 136, "api": "Controller / ShardedController.control_step"},
+        "gpu_launches": args.steps * 3, "clocks": clk.summary(),
+    }
+    if rank == 0:
+        print(json.dumps(line))
+    if dist is not None:
+        dist.destroy_process_group()
+    return 0
+
+
 def _cpu_baseline(args):
     if not _have_reference():
         return {"value": None, "unit": "ms", "cores": os.cpu_count(), "kind": "reference",
@@ -404,7 +530,7 @@ def main():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="c2", choices=["c1", "c2", "c4"])
+    ap.add_argument("--workload", default="c2", choices=["c1", "c2", "c3", "c4", "c5"])
     ap.add_argument("--instances", type=int, default=4096, help="config 4: total controllers")
     ap.add_argument("--weak", action="store_true", help="config 4: --instances per GPU (weak scaling)")
     ap.add_argument("--particles", type=int, default=500)
@@ -413,6 +539,10 @@ def main():
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
+    if args.workload == "c3":
+        return run_tracking(args)
+    if args.workload == "c5":
+        return run_sweep(args)
     if args.workload == "c4":
         if args.weak:
             args.instances *= int(os.environ.get("WORLD_SIZE", "1"))

@@ -87,6 +87,39 @@ def batched_problem(instances: int, first: int = 0, chain=None):
     return goals, th0
 
 
+def tracking_problem(seed: int = 0, n_boxes: int = 8, dims: int = 64):
+    """Config 3: moving target (TargetScript, linear, 5 waypoints = FK of seeded
+    in-limit q, one every 3 s, position_only) and a 64^3 grid over [-1,1]^3
+    built from 8 seeded voxel-aligned boxes that do not touch the start pose's
+    capsules."""
+    from .kinematics import fk_batch, load_chain
+    from .simworld import TargetScript, seeded_box_grid
+
+    chain = load_chain("arm7.chain")
+    rng = np.random.default_rng(seed)
+    lo, hi = chain.joint_limits[:, 0], chain.joint_limits[:, 1]
+    q = rng.uniform(lo + 0.1 * (hi - lo), hi - 0.1 * (hi - lo), size=(5, 7))
+    _, trans = fk_batch(chain, q)
+    script = TargetScript(times=np.arange(5) * 3.0, positions=trans[:, -1], interpolation="linear",
+                          mode="position_only")
+    rot0, tr0 = fk_batch(chain, REACH_START[None])
+    caps0 = [(rot0[0, l] @ p0 + tr0[0, l], rot0[0, l] @ p1 + tr0[0, l], r)
+             for p0, p1, r, l in zip(chain.cap_p0, chain.cap_p1, chain.cap_r, chain.cap_link)]
+
+    def keep_clear(box):
+        lo_b, hi_b = box[:3], box[3:]
+        for a, b, r in caps0:
+            for t in np.linspace(0.0, 1.0, 9):
+                p = a + t * (b - a)
+                gap = np.maximum(lo_b - p, 0.0) + np.maximum(p - hi_b, 0.0)
+                if np.sqrt((gap * gap).sum()) < r + 0.05:
+                    return False
+        return True
+
+    world = seeded_box_grid(n_boxes=n_boxes, dims=dims, seed=seed, keep_clear=keep_clear)
+    return script, world
+
+
 def start_state():
     from .rollout import JointState
 
