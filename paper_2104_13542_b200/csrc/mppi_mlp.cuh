@@ -160,22 +160,19 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
   for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
 
-__device__ __forceinline__ uint32_t pack_h2(__half a, __half b) {
-  return (uint32_t)__half_as_ushort(a) | ((uint32_t)__half_as_ushort(b) << 16);
-}
-
-// Split 16 fp32 activations of one row into fp16 hi/lo and store them as two
-// 16-byte core-matrix rows each (k0 multiple of 16) of a K-wide operand.
+// Split 16 fp32 activations of one row into fp16 hi/lo (packed cvt.rn.f16x2)
+// and store them as two 16-byte core-matrix rows each (k0 multiple of 16) of a
+// K-wide K-major operand.
 __device__ __forceinline__ void store_split16(unsigned char* sm, uint32_t off_h, uint32_t off_l,
                                               uint32_t row, uint32_t k0, uint32_t K, const float* y) {
   uint32_t h[8], l[8];
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
-    const __half h0 = __float2half_rn(y[2 * i]), h1 = __float2half_rn(y[2 * i + 1]);
-    const __half l0 = __float2half_rn(y[2 * i] - __half2float(h0));
-    const __half l1 = __float2half_rn(y[2 * i + 1] - __half2float(h1));
-    h[i] = pack_h2(h0, h1);
-    l[i] = pack_h2(l0, l1);
+    const __half2 hh = __floats2half2_rn(y[2 * i], y[2 * i + 1]);
+    const float2 hf = __half22float2(hh);
+    const __half2 ll = __floats2half2_rn(y[2 * i] - hf.x, y[2 * i + 1] - hf.y);
+    h[i] = *reinterpret_cast<const uint32_t*>(&hh);
+    l[i] = *reinterpret_cast<const uint32_t*>(&ll);
   }
 #pragma unroll
   for (int c = 0; c < 2; ++c) {
@@ -185,18 +182,42 @@ __device__ __forceinline__ void store_split16(unsigned char* sm, uint32_t off_h,
   }
 }
 
+// 8 fp32 -> one hi and one lo 16-byte core-matrix row.
+__device__ __forceinline__ void store_split8(unsigned char* sm, uint32_t off_h, uint32_t off_l, uint32_t o,
+                                             const float* y) {
+  uint32_t h[4], l[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const __half2 hh = __floats2half2_rn(y[2 * i], y[2 * i + 1]);
+    const float2 hf = __half22float2(hh);
+    const __half2 ll = __floats2half2_rn(y[2 * i] - hf.x, y[2 * i + 1] - hf.y);
+    h[i] = *reinterpret_cast<const uint32_t*>(&hh);
+    l[i] = *reinterpret_cast<const uint32_t*>(&ll);
+  }
+  *reinterpret_cast<uint4*>(sm + off_h + o) = make_uint4(h[0], h[1], h[2], h[3]);
+  *reinterpret_cast<uint4*>(sm + off_l + o) = make_uint4(l[0], l[1], l[2], l[3]);
+}
+
 // ------------------------------------------------------------------ the kernel
+// 16 warps: warp w serves TMEM lane quadrant q = w % 4 (rows 32q..32q+31 of
+// the tile) and column group cg = w / 4 (16 of every 64 accumulator columns),
+// so the epilogue instruction stream is spread over 4 warps per scheduler.
+constexpr int kMlpThreads = 512;
+
 // x: (M_pad,16) fp32 positional encodings; out: (M) fp32 distances.
-__global__ void __launch_bounds__(128, 1)
+__global__ void __launch_bounds__(kMlpThreads, 1)
     mlp_tcgen05_kernel(const float* __restrict__ x, long long M, const unsigned char* __restrict__ img,
                        float* __restrict__ out) {
   extern __shared__ __align__(1024) unsigned char mlp_smem[];
   unsigned char* sm = mlp_smem;
-  const int tid = threadIdx.x, warp = tid >> 5;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int quad = warp & 3, cg = warp >> 2;
+  const int row_in_tile = quad * 32 + lane;
   const uint32_t sb = smem_u32(sm);
   const uint32_t barW0 = sb + OFF_BAR, barW1 = barW0 + 8, barW2 = barW0 + 16;
   const uint32_t barL1a = barW0 + 24, barL1b = barW0 + 32, barL2 = barW0 + 40, barL3 = barW0 + 48;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sm + OFF_TMEMPTR);
+  float* red = reinterpret_cast<float*>(sm + OFF_AH);  // final 64->1 partials reuse the A buffer
 
   if (tid == 0) {
     for (int i = 0; i < 7; ++i) mbar_init(barW0 + 8 * i, 1);
@@ -213,7 +234,7 @@ __global__ void __launch_bounds__(128, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   const uint32_t acc1[2] = {tmem, tmem + 64}, acc2 = tmem + 128, acc3 = tmem + 256;
-  const uint32_t lane_base = (uint32_t)(warp * 32) << 16;
+  const uint32_t lane_base = (uint32_t)(quad * 32) << 16;
 
   if (tid == 0) {  // weights: three bulk-copy segments, each on its own barrier
     mbar_expect_tx(barW0, kSeg0);
@@ -235,94 +256,96 @@ __global__ void __launch_bounds__(128, 1)
   bool weights_ready = false;
   const long long ntiles = (M + 127) / 128;
 
-  for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    const long long row = tile * 128 + tid;
-    {  // X tile: fp32 -> fp16 hi/lo, K-major core-matrix layout
-      float xv[16];
-      if (row < M) {
-        const float4* src = reinterpret_cast<const float4*>(x + row * 16);
+  // X loader: threads < 256 own (row = tid % 128, 8 of the 16 columns)
+  auto load_x = [&](long long tile, float* xv) {
+    const long long r = tile * 128 + (tid & 127);
+    if (tid < 256 && r < M) {
+      const float4* src = reinterpret_cast<const float4*>(x + r * 16 + (tid >> 7) * 8);
+      const float4 f0 = __ldg(src), f1 = __ldg(src + 1);
+      xv[0] = f0.x; xv[1] = f0.y; xv[2] = f0.z; xv[3] = f0.w;
+      xv[4] = f1.x; xv[5] = f1.y; xv[6] = f1.z; xv[7] = f1.w;
+    } else {
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const float4 f = __ldg(src + i);
-          xv[4 * i] = f.x;
-          xv[4 * i + 1] = f.y;
-          xv[4 * i + 2] = f.z;
-          xv[4 * i + 3] = f.w;
-        }
-      } else {
-#pragma unroll
-        for (int i = 0; i < 16; ++i) xv[i] = 0.f;
-      }
-      store_split16(sm, OFF_XH, OFF_XL, tid, 0, 16, xv);
+      for (int i = 0; i < 8; ++i) xv[i] = 0.f;
     }
+  };
+  auto store_x = [&](const float* xv) {
+    if (tid < 256) store_split8(sm, OFF_XH, OFF_XL, umma_off(tid & 127, (tid >> 7) * 8, 16), xv);
+  };
+  auto issue_l1 = [&](int c) {  // acc1[c%2] = X . W0t[64c:64c+64]^T   (N = 64)
+    const uint64_t xh = umma_desc(sb + OFF_XH, 128, 256), xl = umma_desc(sb + OFF_XL, 128, 256);
+    const uint64_t wh = umma_desc(sb + OFF_W0H + umma_off(64 * c, 0, 16), 128, 256);
+    const uint64_t wl = umma_desc(sb + OFF_W0L + umma_off(64 * c, 0, 16), 128, 256);
+    umma_f16(acc1[c & 1], xh, wh, id64, 0);
+    umma_f16(acc1[c & 1], xh, wl, id64, 1);
+    umma_f16(acc1[c & 1], xl, wh, id64, 1);
+    umma_commit((c & 1) ? barL1b : barL1a);
+  };
+  auto issue_l2 = [&](int c) {  // acc2 += A_c . W1t[:, 64c:64c+64]^T   (N = 128)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const uint64_t ah = umma_desc(sb + OFF_AH + j * 256, 128, 1024);
+      const uint64_t al = umma_desc(sb + OFF_AL + j * 256, 128, 1024);
+      const uint64_t wh = umma_desc(sb + OFF_W1H + (8 * c + 2 * j) * 128, 128, 4096);
+      const uint64_t wl = umma_desc(sb + OFF_W1L + (8 * c + 2 * j) * 128, 128, 4096);
+      umma_f16(acc2, ah, wh, id128, (c | j) ? 1u : 0u);
+      umma_f16(acc2, ah, wl, id128, 1);
+      umma_f16(acc2, al, wh, id128, 1);
+    }
+    umma_commit(barL2);
+  };
+  auto issue_l3 = [&](int hh) {  // acc3 += A_h . W2t[:, 64h:64h+64]^T   (N = 64)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const uint64_t ah = umma_desc(sb + OFF_AH + j * 256, 128, 1024);
+      const uint64_t al = umma_desc(sb + OFF_AL + j * 256, 128, 1024);
+      const uint64_t wh = umma_desc(sb + OFF_W2H + (8 * hh + 2 * j) * 128, 128, 2048);
+      const uint64_t wl = umma_desc(sb + OFF_W2L + (8 * hh + 2 * j) * 128, 128, 2048);
+      umma_f16(acc3, ah, wh, id64, (hh | j) ? 1u : 0u);
+      umma_f16(acc3, ah, wl, id64, 1);
+      umma_f16(acc3, al, wh, id64, 1);
+    }
+    umma_commit(barL3);
+  };
+
+  float xnext[8];
+  long long tile = blockIdx.x;
+  if (tile < ntiles) {
+    load_x(tile, xnext);
+    store_x(xnext);
     fence_async_smem();
-    if (!weights_ready) mbar_wait(barW0, 0);  // W0 + biases; W1/W2 still streaming
+    mbar_wait(barW0, 0);  // W0 + biases; W1/W2 still streaming
     __syncthreads();
     tc_fence_after();
-
-    auto issue_l1 = [&](int c) {  // acc1[c%2] = X . W0t[64c:64c+64]^T   (N = 64)
-      const uint64_t xh = umma_desc(sb + OFF_XH, 128, 256), xl = umma_desc(sb + OFF_XL, 128, 256);
-      const uint64_t wh = umma_desc(sb + OFF_W0H + umma_off(64 * c, 0, 16), 128, 256);
-      const uint64_t wl = umma_desc(sb + OFF_W0L + umma_off(64 * c, 0, 16), 128, 256);
-      umma_f16(acc1[c & 1], xh, wh, id64, 0);
-      umma_f16(acc1[c & 1], xh, wl, id64, 1);
-      umma_f16(acc1[c & 1], xl, wh, id64, 1);
-      umma_commit((c & 1) ? barL1b : barL1a);
-    };
-    auto issue_l2 = [&](int c) {  // acc2 += A_c . W1t[:, 64c:64c+64]^T   (N = 128)
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const uint64_t ah = umma_desc(sb + OFF_AH + j * 256, 128, 1024);
-        const uint64_t al = umma_desc(sb + OFF_AL + j * 256, 128, 1024);
-        const uint64_t wh = umma_desc(sb + OFF_W1H + (8 * c + 2 * j) * 128, 128, 4096);
-        const uint64_t wl = umma_desc(sb + OFF_W1L + (8 * c + 2 * j) * 128, 128, 4096);
-        umma_f16(acc2, ah, wh, id128, (c | j) ? 1u : 0u);
-        umma_f16(acc2, ah, wl, id128, 1);
-        umma_f16(acc2, al, wh, id128, 1);
-      }
-      umma_commit(barL2);
-    };
-    auto issue_l3 = [&](int hh) {  // acc3 += A_h . W2t[:, 64h:64h+64]^T   (N = 64)
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const uint64_t ah = umma_desc(sb + OFF_AH + j * 256, 128, 1024);
-        const uint64_t al = umma_desc(sb + OFF_AL + j * 256, 128, 1024);
-        const uint64_t wh = umma_desc(sb + OFF_W2H + (8 * hh + 2 * j) * 128, 128, 2048);
-        const uint64_t wl = umma_desc(sb + OFF_W2L + (8 * hh + 2 * j) * 128, 128, 2048);
-        umma_f16(acc3, ah, wh, id64, (hh | j) ? 1u : 0u);
-        umma_f16(acc3, ah, wl, id64, 1);
-        umma_f16(acc3, al, wh, id64, 1);
-      }
-      umma_commit(barL3);
-    };
-
     if (tid == 0) {
       issue_l1(0);
       issue_l1(1);
     }
-    const float s0 = par[kMlpH0 + kMlpH1 + 2 * kMlpH2 + 1];
-    const float s1 = par[kMlpH0 + kMlpH1 + 2 * kMlpH2 + 2];
-    const float s2 = par[kMlpH0 + kMlpH1 + 2 * kMlpH2 + 3];
+  }
+  const float s0 = par[kMlpH0 + kMlpH1 + 2 * kMlpH2 + 1];
+  const float s1 = par[kMlpH0 + kMlpH1 + 2 * kMlpH2 + 2];
+  const float s2 = par[kMlpH0 + kMlpH1 + 2 * kMlpH2 + 3];
 
-    // ---- layer 1 (4 chunks of 64) feeding layer 2
+  for (; tile < ntiles; tile += gridDim.x) {
+    const long long next = tile + gridDim.x;
+    const bool has_next = next < ntiles;
+    if (has_next) load_x(next, xnext);  // in flight during layer 1
+
+    // ---- layer 1 (4 chunks of 64 outputs) feeding layer 2
     for (int c = 0; c < 4; ++c) {
       mbar_wait((c & 1) ? barL1b : barL1a, phL1[c & 1]);
       phL1[c & 1] ^= 1;
       tc_fence_after();
-      float y[64];
+      float y[16];
+      tmem_ld16(acc1[c & 1] + lane_base + 16 * cg, y);
 #pragma unroll
-      for (int q = 0; q < 4; ++q) tmem_ld16(acc1[c & 1] + lane_base + 16 * q, y + 16 * q);
-#pragma unroll
-      for (int i = 0; i < 64; ++i) {
-        const float t = fmaf(y[i], s0, b0[64 * c + i]);
-        y[i] = t > 0.f ? t : 0.f;
-      }
+      for (int i = 0; i < 16; ++i) y[i] = fmaxf(fmaf(y[i], s0, b0[64 * c + 16 * cg + i]), 0.f);
       if (c > 0) {  // layer-2 MMAs of the previous chunk must be done reading A
         mbar_wait(barL2, phL2);
         phL2 ^= 1;
       }
-#pragma unroll
-      for (int q = 0; q < 4; ++q) store_split16(sm, OFF_AH, OFF_AL, tid, 16 * q, 64, y + 16 * q);
+      store_split16(sm, OFF_AH, OFF_AL, row_in_tile, 16 * cg, 64, y);
+      if (c == 3 && has_next) store_x(xnext);  // every layer-1 MMA of this tile is complete
       fence_async_smem();
       tc_fence_before();
       __syncthreads();
@@ -331,6 +354,10 @@ __global__ void __launch_bounds__(128, 1)
         if (!weights_ready && c == 0) mbar_wait(barW1, 0);
         issue_l2(c);
         if (c + 2 < 4) issue_l1(c + 2);
+        if (c == 3 && has_next) {  // next tile's first two layer-1 chunks overlap this tile's tail
+          issue_l1(0);
+          issue_l1(1);
+        }
       }
     }
     mbar_wait(barL2, phL2);
@@ -339,20 +366,15 @@ __global__ void __launch_bounds__(128, 1)
 
     // ---- layer 2 output (2 K-chunks of 64) feeding layer 3
     for (int hh = 0; hh < 2; ++hh) {
-      float y[64];
+      float y[16];
+      tmem_ld16(acc2 + lane_base + 64 * hh + 16 * cg, y);
 #pragma unroll
-      for (int q = 0; q < 4; ++q) tmem_ld16(acc2 + lane_base + 64 * hh + 16 * q, y + 16 * q);
-#pragma unroll
-      for (int i = 0; i < 64; ++i) {
-        const float t = fmaf(y[i], s1, b1[64 * hh + i]);
-        y[i] = t > 0.f ? t : 0.f;
-      }
+      for (int i = 0; i < 16; ++i) y[i] = fmaxf(fmaf(y[i], s1, b1[64 * hh + 16 * cg + i]), 0.f);
       if (hh > 0) {
         mbar_wait(barL3, phL3);
         phL3 ^= 1;
       }
-#pragma unroll
-      for (int q = 0; q < 4; ++q) store_split16(sm, OFF_AH, OFF_AL, tid, 16 * q, 64, y + 16 * q);
+      store_split16(sm, OFF_AH, OFF_AL, row_in_tile, 16 * cg, 64, y);
       fence_async_smem();
       tc_fence_before();
       __syncthreads();
@@ -368,22 +390,24 @@ __global__ void __launch_bounds__(128, 1)
     tc_fence_after();
 
     // ---- layer 3 epilogue + the 64 -> 1 output layer on the CUDA cores
-    float o = par[kMlpH0 + kMlpH1 + 2 * kMlpH2];  // b3
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
+    float part = 0.f;
+    {
       float y[16];
-      tmem_ld16(acc3 + lane_base + 16 * q, y);
+      tmem_ld16(acc3 + lane_base + 16 * cg, y);
 #pragma unroll
-      for (int i = 0; i < 16; ++i) {
-        float t = fmaf(y[i], s2, b2[16 * q + i]);
-        t = t > 0.f ? t : 0.f;
-        o = fmaf(t, w3[16 * q + i], o);
-      }
+      for (int i = 0; i < 16; ++i) part = fmaf(fmaxf(fmaf(y[i], s2, b2[16 * cg + i]), 0.f), w3[16 * cg + i], part);
     }
-    if (row < M) out[row] = o;
+    red[cg * 128 + row_in_tile] = part;  // A buffer is free: every L3 MMA has completed
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
+    if (cg == 0) {
+      const long long row = tile * 128 + row_in_tile;
+      const float o = par[kMlpH0 + kMlpH1 + 2 * kMlpH2] + red[row_in_tile] + red[128 + row_in_tile] +
+                      red[256 + row_in_tile] + red[384 + row_in_tile];
+      if (row < M) out[row] = o;
+    }
+    __syncthreads();  // red (A buffer) is rewritten by the next tile's first epilogue
   }
   if (!weights_ready && tid == 0) {  // CTA got no tile: drain the weight copies before exit
     mbar_wait(barW0, 0);
@@ -461,7 +485,7 @@ inline cudaError_t mlp_forward(const MlpWeights& m, const float* x, long long ro
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const long long tiles = (rows + 127) / 128;
   const unsigned grid = (unsigned)(tiles < sms ? tiles : sms);
-  mlp_tcgen05_kernel<<<grid, 128, kMlpSmem, st>>>(x, rows, m.img, out);
+  mlp_tcgen05_kernel<<<grid, kMlpThreads, kMlpSmem, st>>>(x, rows, m.img, out);
   return cudaGetLastError();
 }
 
