@@ -224,6 +224,7 @@ def run_ours(args):
     config = 1 if args.workload == "c1" else 2
     ctrl = configs.make_controller(config, particles=particles, device=local, precision=args.precision)
     plan = ctrl.plan
+    plan.profile_stages(True)  # stage times from the event nodes of the timed replays
     st = configs.start_state()
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=f"cuda:{local}")
 
@@ -257,6 +258,7 @@ def run_ours(args):
     value = _max_over_ranks(dist, value_local, local)
 
     # ---- end to end through the public API (Controller.control_step, host buffers)
+    plan.profile_stages(False)  # e2e: no extra host calls on the step path
     e2e = []
     for _ in range(args.steps):
         _flush_l2(flush)
@@ -332,6 +334,7 @@ def run_batched(args):
     bc = BatchedController(load_chain("arm7.chain"), goals, weights=configs.make_weights(2),
                            self_collision=load_arm7_surrogate(), precision=args.precision, device=local, **kw)
     thd = np.zeros_like(th0)
+    bc.plan.profile_stages(True)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=f"cuda:{local}")
     for _ in range(max(3, args.warmup)):
         bc.control_step(th0, thd)
@@ -354,6 +357,7 @@ def run_batched(args):
     units = B * args.particles * 30
     value = units / (step_ms * 1e-3)
     e2e = []
+    bc.plan.profile_stages(False)
     for _ in range(max(3, args.steps // 4)):
         _flush_l2(flush)
         torch.cuda.synchronize()
@@ -409,6 +413,7 @@ def run_tracking(args):
     kw["particles"] = args.particles
     ctrl = Controller(load_chain("arm7.chain"), target_at(script, 0.0), weights=configs.make_weights(3),
                       world=world, precision=args.precision, device=local, **kw)
+    ctrl.profile_stages(True)
     st = configs.start_state()
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=f"cuda:{local}")
     dev_ms, e2e, stages = [], [], {"sample": [], "rollout": [], "mlp": [], "update": []}

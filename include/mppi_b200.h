@@ -284,6 +284,11 @@ int mppi_evaluate(mppi_plan* plan, int32_t mode, int32_t n, int32_t horizon,
  * (plan created with dump = 1), plus the particle weights (N,). */
 int mppi_get_bundle(mppi_plan* plan, mppi_eval_out* out, double* weights);
 
+/* Per-stage device times (mppi_step_info.*_ms) are read back from the
+ * event-record nodes of the step graph only when enabled (default off: each
+ * read is a host call on the critical path). */
+int mppi_profile_stages(mppi_plan* plan, int32_t enable);
+
 /* Benchmark hook: launch one stage of the step `reps` times back to back on
  * the plan stream between two CUDA events and report the mean device time per
  * launch. stage 0 = rollout kernel, 1 = learned-collision MLP, 2 = statistics

@@ -122,6 +122,7 @@ _SIGS = {
                                 _dp, _dp, _dp, _dp, C.POINTER(EvalOut)]),
     "mppi_get_bundle": (C.c_int, [_vp, C.POINTER(EvalOut), _dp]),
     "mppi_time_stage": (C.c_int, [_vp, C.c_int32, C.c_int32, _dp]),
+    "mppi_profile_stages": (C.c_int, [_vp, C.c_int32]),
     "mppi_stats_record_len":(C.c_int, [_vp, C.POINTER(C.c_int32)]),
     "mppi_stats_dev": (C.c_int, [_vp, _dp, _dp, _vp, _vp]),
     "mppi_finalize_dev": (C.c_int, [_vp, _vp, C.c_int32, _dp, C.POINTER(StepInfo), _vp]),

@@ -177,17 +177,27 @@ class Controller:
         self._plan.set_noise(eps)
 
     def _sync_goal(self):
+        """Upload cost_stack.goal when it changed (a new GoalSpec, or its arrays
+        edited in place — both are compared against the uploaded copy)."""
         g = self.cost_stack.goal
-        key = (id(g), g.mode, g.target_pose.rotation.tobytes(), g.target_pose.translation.tobytes())
-        if key != self._goal_uploaded:
-            self._plan.set_goal(g.target_pose.rotation, g.target_pose.translation, g.mode_code, 0)
-            self._goal_uploaded = key
+        R, t = g.target_pose.rotation, g.target_pose.translation
+        up = self._goal_uploaded
+        if up is not None and up[0] is g and up[1] == g.mode and np.array_equal(up[2], t) and \
+                np.array_equal(up[3], R):
+            return
+        self._plan.set_goal(R, t, g.mode_code, 0)
+        self._goal_uploaded = (g, g.mode, np.array(t, dtype=np.float64), np.array(R, dtype=np.float64))
+
+    def profile_stages(self, enable: bool = True):
+        """Fill StepDiagnostics.sample_ms / rollout_ms / update_ms from the
+        event-record nodes of the step graph (costs a few host calls per step)."""
+        self._plan.profile_stages(enable)
 
     # ---------------------------------------------------------------- hot path
     def control_step(self, state: JointState) -> tuple[np.ndarray, StepDiagnostics]:
         t_start = time.perf_counter()
         self._sync_goal()
-        cmds, infos = self._plan.step(state.theta[None, :], state.theta_dot[None, :])
+        cmds, infos = self._plan.step(state.theta, state.theta_dot)
         info = infos[0]
         self._step_serial += 1
         if info.status != N.OK:
@@ -215,10 +225,12 @@ class Controller:
         if latency > self.latency_budget * 1e3:
             log.debug("control step overran budget: %.2f ms", latency)
         bundle = LazyBundle(self, self._step_serial) if self.keep_bundle else None
+        # without profile_stages() the whole device step is reported as rollout time
+        roll = info.rollout_ms + info.mlp_ms
         return command, StepDiagnostics(latency_ms=latency, sample_ms=info.sample_ms,
-                                        rollout_ms=info.rollout_ms + info.mlp_ms,
-                                        update_ms=info.update_ms, best_cost=float(info.best_cost),
-                                        mean_cost=float(info.mean_cost), bundle=bundle)
+                                        rollout_ms=roll if roll > 0.0 else info.device_ms,
+                                        update_ms=info.update_ms, best_cost=info.best_cost,
+                                        mean_cost=info.mean_cost, bundle=bundle)
 
     def instantaneous_costs(self, state: JointState):
         """Per-term costs of one plant state with the h=0 braking limit (controller.py:262-269)."""

@@ -185,6 +185,7 @@ struct mppi_plan {
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   std::vector<cudaEvent_t> stage_ev;
   bool stage_events = true;
+  bool want_stages = false;  // read the per-stage event times back after each step (mppi_profile_stages)
   unsigned long long step_counter = 0;
   int sharded_iter = 0;
   // eval scratch
@@ -910,7 +911,7 @@ int mppi_step(mppi_plan* p, const double* theta, const double* theta_dot, double
   if (info) {
     memcpy(info, p->h_info, sizeof(mppi_step_info) * B);
     double stg[4] = {0, 0, 0, 0};
-    for (int it = 0; it < (p->stage_events ? p->iters : 0); ++it)
+    for (int it = 0; it < ((p->stage_events && p->want_stages) ? p->iters : 0); ++it)
       for (int sg = 0; sg < 4; ++sg) {
         float t = 0.f;
         CK(cudaEventElapsedTime(&t, p->stage_ev[4 * it + sg], p->stage_ev[4 * it + sg + 1]));
@@ -1054,6 +1055,12 @@ int mppi_get_bundle(mppi_plan* p, mppi_eval_out* out, double* weights) {
   CK(cudaStreamSynchronize(st));
   out->bad_particle = -1;
   out->quarantined = 0;
+  return MPPI_OK;
+}
+
+int mppi_profile_stages(mppi_plan* p, int32_t enable) {
+  if (!p) return fail(MPPI_E_BAD_ARGUMENT, "null plan");
+  p->want_stages = enable != 0;
   return MPPI_OK;
 }
 

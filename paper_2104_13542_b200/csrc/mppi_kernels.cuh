@@ -657,12 +657,16 @@ __global__ void __launch_bounds__(kStatsThreads) stats_kernel(const __grid_const
   const int reclen = kRecHead + 2 * HD;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const bool failed = (a.status[b] != 0);
+#ifdef MPPI_DEBUG_TIMERS
 #define MPPI_STAMP(k)                                                                        \
   if (a.dbg && threadIdx.x == 0 && b == 0) {                                                  \
     unsigned long long t_;                                                                   \
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                                   \
     a.dbg[blk * 16 + (k)] = t_;                                                              \
   }
+#else
+#define MPPI_STAMP(k)
+#endif
   MPPI_STAMP(0);
 
   // ---- phase A: discounted totals, quarantine (rollout.py:111-171) ---------

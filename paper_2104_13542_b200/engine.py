@@ -131,6 +131,10 @@ class Plan:
         self.N = spec.particles
         self._cmd = np.empty((self.B, self.dof))
         self._info = (N.StepInfo * self.B)()
+        self._th = np.zeros((self.B, self.dof))
+        self._thd = np.zeros((self.B, self.dof))
+        self._p_th, self._p_thd, self._p_cmd = N.dptr(self._th), N.dptr(self._thd), N.dptr(self._cmd)
+        self._step_fn = self.lib.mppi_step
         if provider is not None and self.kind == N.SELFCOLL_LEARNED:
             self.set_mlp(provider)
         if world is not None:
@@ -216,11 +220,22 @@ class Plan:
 
     # ---------------------------------------------------------------- hot path
     def step(self, theta, theta_dot):
-        """One control step for all instances. Returns (commands (B,d), infos)."""
-        th = N.f64(theta, (self.B, self.dof))
-        thd = N.f64(theta_dot, (self.B, self.dof))
-        N.check(self.lib.mppi_step(self.handle, N.dptr(th), N.dptr(thd), N.dptr(self._cmd), self._info))
-        return self._cmd.copy(), [self._info[b] for b in range(self.B)]
+        """One control step for all instances. Returns (commands (B,d), infos).
+
+        The host side of the hot path: inputs are copied into pre-pinned
+        staging arrays whose ctypes pointers are built once, so a step costs
+        one ctypes call (H2D, graph replay and the mapped D2H happen inside).
+        """
+        np.copyto(self._th, np.reshape(theta, self._th.shape))
+        np.copyto(self._thd, np.reshape(theta_dot, self._thd.shape))
+        rc = self._step_fn(self.handle, self._p_th, self._p_thd, self._p_cmd, self._info)
+        if rc:
+            N.check(rc)
+        return self._cmd.copy(), self._info
+
+    def profile_stages(self, enable: bool = True):
+        """Read the per-stage event times of every step back into StepInfo."""
+        N.check(self.lib.mppi_profile_stages(self.handle, int(bool(enable))))
 
     def evaluate(self, mode: int, inputs0, inputs1, dts, gamma, terminal_weight, theta0=None,
                  theta_dot0=None, want=("positions", "velocities", "accelerations", "step_costs",
