@@ -225,10 +225,10 @@ class Controller:
         if latency > self.latency_budget * 1e3:
             log.debug("control step overran budget: %.2f ms", latency)
         bundle = LazyBundle(self, self._step_serial) if self.keep_bundle else None
-        # without profile_stages() the whole device step is reported as rollout time
+        # without profile_stages() the whole fused step is reported as rollout time
         roll = info.rollout_ms + info.mlp_ms
         return command, StepDiagnostics(latency_ms=latency, sample_ms=info.sample_ms,
-                                        rollout_ms=roll if roll > 0.0 else info.device_ms,
+                                        rollout_ms=roll if roll > 0.0 else latency,
                                         update_ms=info.update_ms, best_cost=info.best_cost,
                                         mean_cost=info.mean_cost, bundle=bundle)
 

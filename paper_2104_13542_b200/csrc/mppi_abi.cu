@@ -890,12 +890,14 @@ int mppi_step(mppi_plan* p, const double* theta, const double* theta_dot, double
     const unsigned long long ctr = p->step_counter++;
     memcpy(p->h_state + (size_t)B * 2 * D, &ctr, sizeof(ctr));
   }
-  CK(cudaEventRecord(p->ev0, p->stream));
+  // device timing of the replay only when profiling: on the latency path every
+  // extra runtime call is host time between the state and the command
+  if (p->want_stages) CK(cudaEventRecord(p->ev0, p->stream));
   CK(cudaGraphLaunch(p->graph, p->stream));
-  CK(cudaEventRecord(p->ev1, p->stream));
+  if (p->want_stages) CK(cudaEventRecord(p->ev1, p->stream));
   CK(cudaStreamSynchronize(p->stream));
   float ms = 0.f;
-  CK(cudaEventElapsedTime(&ms, p->ev0, p->ev1));
+  if (p->want_stages) CK(cudaEventElapsedTime(&ms, p->ev0, p->ev1));
   memcpy(command_out, p->h_cmd, sizeof(double) * B * D);
   if (p->dbg.p) {  // debug: stats-kernel phase timeline of instance 0, relative to block 0 start
     std::vector<unsigned long long> t((size_t)16 * p->nblk);

@@ -61,10 +61,14 @@ constexpr uint32_t kSeg1 = OFF_W2H - OFF_W1H;       // W1
 constexpr uint32_t kSeg2 = kImgBytes - OFF_W2H;     // W2
 constexpr uint32_t OFF_XH = kImgBytes;              // X tile 128 x 16 fp16
 constexpr uint32_t OFF_XL = OFF_XH + 128 * 16 * 2;
-constexpr uint32_t OFF_AH = OFF_XL + 128 * 16 * 2;  // activation K-chunk 128 x 64 fp16
-constexpr uint32_t OFF_AL = OFF_AH + 128 * 64 * 2;
-constexpr uint32_t OFF_BAR = OFF_AL + 128 * 64 * 2;  // 8 mbarriers
-constexpr uint32_t OFF_TMEMPTR = OFF_BAR + 8 * 8;
+// activations: two 32-wide K-chunk buffers (double buffering), each 128 x 32
+// fp16 hi followed by 128 x 32 fp16 lo
+constexpr uint32_t kAChunkK = 32;
+constexpr uint32_t kAHalf = 128 * kAChunkK * 2;     // 8 KiB
+constexpr uint32_t kABuf = 2 * kAHalf;              // hi + lo = 16 KiB
+constexpr uint32_t OFF_A = OFF_XL + 128 * 16 * 2;
+constexpr uint32_t OFF_BAR = OFF_A + 2 * kABuf;     // 16 mbarriers
+constexpr uint32_t OFF_TMEMPTR = OFF_BAR + 16 * 8;
 constexpr uint32_t kMlpSmem = OFF_TMEMPTR + 16;
 
 static_assert(kMlpSmem <= 232448, "MLP tile does not fit the 227 KiB of shared memory");
@@ -200,9 +204,22 @@ __device__ __forceinline__ void store_split8(unsigned char* sm, uint32_t off_h, 
 
 // ------------------------------------------------------------------ the kernel
 // 16 warps: warp w serves TMEM lane quadrant q = w % 4 (rows 32q..32q+31 of
-// the tile) and column group cg = w / 4 (16 of every 64 accumulator columns),
-// so the epilogue instruction stream is spread over 4 warps per scheduler.
+// the tile) and column group cg = w / 4 (8 of every 32 accumulator columns).
+// Activations move through two 32-wide smem buffers: while the tensor core
+// runs the layer-2 (or layer-3) MMAs of chunk c, the epilogue of chunk c+1
+// fills the other buffer.
 constexpr int kMlpThreads = 512;
+
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, float* v) {
+  uint32_t r[8];
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+                 "=r"(r[7])
+               : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[i]);
+}
 
 // x: (M_pad,16) fp32 positional encodings; out: (M) fp32 distances.
 __global__ void __launch_bounds__(kMlpThreads, 1)
@@ -214,26 +231,30 @@ __global__ void __launch_bounds__(kMlpThreads, 1)
   const int quad = warp & 3, cg = warp >> 2;
   const int row_in_tile = quad * 32 + lane;
   const uint32_t sb = smem_u32(sm);
+  // barriers: 0-2 weights, 3-4 layer 1 (per acc1 buffer), 5-6 layer 2 (per A
+  // buffer), 7-8 layer 3 (per A buffer)
   const uint32_t barW0 = sb + OFF_BAR, barW1 = barW0 + 8, barW2 = barW0 + 16;
-  const uint32_t barL1a = barW0 + 24, barL1b = barW0 + 32, barL2 = barW0 + 40, barL3 = barW0 + 48;
+  const uint32_t barL1[2] = {barW0 + 24, barW0 + 32};
+  const uint32_t barL2[2] = {barW0 + 40, barW0 + 48};
+  const uint32_t barL3[2] = {barW0 + 56, barW0 + 64};
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sm + OFF_TMEMPTR);
-  float* red = reinterpret_cast<float*>(sm + OFF_AH);  // final 64->1 partials reuse the A buffer
+  float* red = reinterpret_cast<float*>(sm + OFF_A);  // final 64->1 partials reuse A buffer 0
 
   if (tid == 0) {
-    for (int i = 0; i < 7; ++i) mbar_init(barW0 + 8 * i, 1);
+    for (int i = 0; i < 9; ++i) mbar_init(barW0 + 8 * i, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     fence_async_smem();
   }
-  if (warp == 0) {  // 512 TMEM columns: acc1 x2 (64+64) | acc2 (128) | acc3 (64)
+  if (warp == 0) {  // TMEM: acc1 x2 (32+32) | acc2 (128) | acc3 (64) -> 256 columns
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                 "r"(512));
+                 "r"(256));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const uint32_t acc1[2] = {tmem, tmem + 64}, acc2 = tmem + 128, acc3 = tmem + 256;
+  const uint32_t acc1[2] = {tmem, tmem + 32}, acc2 = tmem + 64, acc3 = tmem + 192;
   const uint32_t lane_base = (uint32_t)(quad * 32) << 16;
 
   if (tid == 0) {  // weights: three bulk-copy segments, each on its own barrier
@@ -251,11 +272,13 @@ __global__ void __launch_bounds__(kMlpThreads, 1)
   const float* b2 = b1 + kMlpH1;
   const float* w3 = b2 + kMlpH2;
 
-  const uint32_t id64 = umma_idesc(64), id128 = umma_idesc(128);
-  uint32_t phL1[2] = {0, 0}, phL2 = 0, phL3 = 0;
+  const uint32_t id32 = umma_idesc(32), id64 = umma_idesc(64), id128 = umma_idesc(128);
+  uint32_t phL1[2] = {0, 0}, phL2[2] = {0, 0}, phL3[2] = {0, 0};
   bool weights_ready = false;
   const long long ntiles = (M + 127) / 128;
 
+  auto abuf_h = [&](int b) { return OFF_A + b * kABuf; };
+  auto abuf_l = [&](int b) { return OFF_A + b * kABuf + kAHalf; };
   // X loader: threads < 256 own (row = tid % 128, 8 of the 16 columns)
   auto load_x = [&](long long tile, float* xv) {
     const long long r = tile * 128 + (tid & 127);
@@ -272,40 +295,46 @@ __global__ void __launch_bounds__(kMlpThreads, 1)
   auto store_x = [&](const float* xv) {
     if (tid < 256) store_split8(sm, OFF_XH, OFF_XL, umma_off(tid & 127, (tid >> 7) * 8, 16), xv);
   };
-  auto issue_l1 = [&](int c) {  // acc1[c%2] = X . W0t[64c:64c+64]^T   (N = 64)
+  auto issue_l1 = [&](int c) {  // acc1[c%2] = X . W0t[32c:32c+32]^T   (N = 32)
     const uint64_t xh = umma_desc(sb + OFF_XH, 128, 256), xl = umma_desc(sb + OFF_XL, 128, 256);
-    const uint64_t wh = umma_desc(sb + OFF_W0H + umma_off(64 * c, 0, 16), 128, 256);
-    const uint64_t wl = umma_desc(sb + OFF_W0L + umma_off(64 * c, 0, 16), 128, 256);
-    umma_f16(acc1[c & 1], xh, wh, id64, 0);
-    umma_f16(acc1[c & 1], xh, wl, id64, 1);
-    umma_f16(acc1[c & 1], xl, wh, id64, 1);
-    umma_commit((c & 1) ? barL1b : barL1a);
+    const uint64_t wh = umma_desc(sb + OFF_W0H + umma_off(32 * c, 0, 16), 128, 256);
+    const uint64_t wl = umma_desc(sb + OFF_W0L + umma_off(32 * c, 0, 16), 128, 256);
+    umma_f16(acc1[c & 1], xh, wh, id32, 0);
+    umma_f16(acc1[c & 1], xh, wl, id32, 1);
+    umma_f16(acc1[c & 1], xl, wh, id32, 1);
+    umma_commit(barL1[c & 1]);
   };
-  auto issue_l2 = [&](int c) {  // acc2 += A_c . W1t[:, 64c:64c+64]^T   (N = 128)
+  auto issue_l2 = [&](int c) {  // acc2 += A[c%2] . W1t[:, 32c:32c+32]^T   (N = 128)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const uint64_t ah = umma_desc(sb + OFF_AH + j * 256, 128, 1024);
-      const uint64_t al = umma_desc(sb + OFF_AL + j * 256, 128, 1024);
-      const uint64_t wh = umma_desc(sb + OFF_W1H + (8 * c + 2 * j) * 128, 128, 4096);
-      const uint64_t wl = umma_desc(sb + OFF_W1L + (8 * c + 2 * j) * 128, 128, 4096);
+    for (int j = 0; j < 2; ++j) {
+      const uint64_t ah = umma_desc(sb + abuf_h(c & 1) + j * 256, 128, 512);
+      const uint64_t al = umma_desc(sb + abuf_l(c & 1) + j * 256, 128, 512);
+      const uint64_t wh = umma_desc(sb + OFF_W1H + (4 * c + 2 * j) * 128, 128, 4096);
+      const uint64_t wl = umma_desc(sb + OFF_W1L + (4 * c + 2 * j) * 128, 128, 4096);
       umma_f16(acc2, ah, wh, id128, (c | j) ? 1u : 0u);
       umma_f16(acc2, ah, wl, id128, 1);
       umma_f16(acc2, al, wh, id128, 1);
     }
-    umma_commit(barL2);
+    umma_commit(barL2[c & 1]);
   };
-  auto issue_l3 = [&](int hh) {  // acc3 += A_h . W2t[:, 64h:64h+64]^T   (N = 64)
+  auto issue_l3 = [&](int c) {  // acc3 += A[c%2] . W2t[:, 32c:32c+32]^T   (N = 64)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const uint64_t ah = umma_desc(sb + OFF_AH + j * 256, 128, 1024);
-      const uint64_t al = umma_desc(sb + OFF_AL + j * 256, 128, 1024);
-      const uint64_t wh = umma_desc(sb + OFF_W2H + (8 * hh + 2 * j) * 128, 128, 2048);
-      const uint64_t wl = umma_desc(sb + OFF_W2L + (8 * hh + 2 * j) * 128, 128, 2048);
-      umma_f16(acc3, ah, wh, id64, (hh | j) ? 1u : 0u);
+    for (int j = 0; j < 2; ++j) {
+      const uint64_t ah = umma_desc(sb + abuf_h(c & 1) + j * 256, 128, 512);
+      const uint64_t al = umma_desc(sb + abuf_l(c & 1) + j * 256, 128, 512);
+      const uint64_t wh = umma_desc(sb + OFF_W2H + (4 * c + 2 * j) * 128, 128, 2048);
+      const uint64_t wl = umma_desc(sb + OFF_W2L + (4 * c + 2 * j) * 128, 128, 2048);
+      umma_f16(acc3, ah, wh, id64, (c | j) ? 1u : 0u);
       umma_f16(acc3, ah, wl, id64, 1);
       umma_f16(acc3, al, wh, id64, 1);
     }
-    umma_commit(barL3);
+    umma_commit(barL3[c & 1]);
+  };
+  auto sync_for_mma = [&]() {
+    fence_async_smem();
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
   };
 
   float xnext[8];
@@ -331,62 +360,63 @@ __global__ void __launch_bounds__(kMlpThreads, 1)
     const bool has_next = next < ntiles;
     if (has_next) load_x(next, xnext);  // in flight during layer 1
 
-    // ---- layer 1 (4 chunks of 64 outputs) feeding layer 2
-    for (int c = 0; c < 4; ++c) {
-      mbar_wait((c & 1) ? barL1b : barL1a, phL1[c & 1]);
-      phL1[c & 1] ^= 1;
+    // ---- layer 1: 8 chunks of 32 outputs, each feeding a layer-2 K-chunk
+    for (int c = 0; c < 8; ++c) {
+      const int bf = c & 1;
+      mbar_wait(barL1[bf], phL1[bf]);
+      phL1[bf] ^= 1;
       tc_fence_after();
-      float y[16];
-      tmem_ld16(acc1[c & 1] + lane_base + 16 * cg, y);
+      float y[8];
+      tmem_ld8(acc1[bf] + lane_base + 8 * cg, y);
 #pragma unroll
-      for (int i = 0; i < 16; ++i) y[i] = fmaxf(fmaf(y[i], s0, b0[64 * c + 16 * cg + i]), 0.f);
-      if (c > 0) {  // layer-2 MMAs of the previous chunk must be done reading A
-        mbar_wait(barL2, phL2);
-        phL2 ^= 1;
+      for (int i = 0; i < 8; ++i) y[i] = fmaxf(fmaf(y[i], s0, b0[32 * c + 8 * cg + i]), 0.f);
+      if (c >= 2) {  // A[bf] was last read by the layer-2 MMAs of chunk c-2
+        mbar_wait(barL2[bf], phL2[bf]);
+        phL2[bf] ^= 1;
       }
-      store_split16(sm, OFF_AH, OFF_AL, row_in_tile, 16 * cg, 64, y);
-      if (c == 3 && has_next) store_x(xnext);  // every layer-1 MMA of this tile is complete
-      fence_async_smem();
-      tc_fence_before();
-      __syncthreads();
-      tc_fence_after();
+      store_split8(sm, abuf_h(bf), abuf_l(bf), umma_off(row_in_tile, 8 * cg, kAChunkK), y);
+      if (c == 7 && has_next) store_x(xnext);  // every layer-1 MMA of this tile is complete
+      sync_for_mma();
       if (tid == 0) {
         if (!weights_ready && c == 0) mbar_wait(barW1, 0);
         issue_l2(c);
-        if (c + 2 < 4) issue_l1(c + 2);
-        if (c == 3 && has_next) {  // next tile's first two layer-1 chunks overlap this tile's tail
+        if (c + 2 < 8) issue_l1(c + 2);
+        if (c == 7 && has_next) {  // next tile's first layer-1 chunks overlap this tile's tail
           issue_l1(0);
           issue_l1(1);
         }
       }
     }
-    mbar_wait(barL2, phL2);
-    phL2 ^= 1;
+    // all layer-2 MMAs (in order) complete once chunk 7's and chunk 6's commits have arrived
+    mbar_wait(barL2[0], phL2[0]);
+    phL2[0] ^= 1;
+    mbar_wait(barL2[1], phL2[1]);
+    phL2[1] ^= 1;
     tc_fence_after();
 
-    // ---- layer 2 output (2 K-chunks of 64) feeding layer 3
-    for (int hh = 0; hh < 2; ++hh) {
-      float y[16];
-      tmem_ld16(acc2 + lane_base + 64 * hh + 16 * cg, y);
+    // ---- layer 2 output: 4 K-chunks of 32 feeding layer 3
+    for (int c = 0; c < 4; ++c) {
+      const int bf = c & 1;
+      float y[8];
+      tmem_ld8(acc2 + lane_base + 32 * c + 8 * cg, y);
 #pragma unroll
-      for (int i = 0; i < 16; ++i) y[i] = fmaxf(fmaf(y[i], s1, b1[64 * hh + 16 * cg + i]), 0.f);
-      if (hh > 0) {
-        mbar_wait(barL3, phL3);
-        phL3 ^= 1;
+      for (int i = 0; i < 8; ++i) y[i] = fmaxf(fmaf(y[i], s1, b1[32 * c + 8 * cg + i]), 0.f);
+      if (c >= 2) {
+        mbar_wait(barL3[bf], phL3[bf]);
+        phL3[bf] ^= 1;
       }
-      store_split16(sm, OFF_AH, OFF_AL, row_in_tile, 16 * cg, 64, y);
-      fence_async_smem();
-      tc_fence_before();
-      __syncthreads();
-      tc_fence_after();
+      store_split8(sm, abuf_h(bf), abuf_l(bf), umma_off(row_in_tile, 8 * cg, kAChunkK), y);
+      sync_for_mma();
       if (tid == 0) {
-        if (!weights_ready && hh == 0) mbar_wait(barW2, 0);
-        issue_l3(hh);
+        if (!weights_ready && c == 0) mbar_wait(barW2, 0);
+        issue_l3(c);
       }
     }
     weights_ready = true;
-    mbar_wait(barL3, phL3);
-    phL3 ^= 1;
+    mbar_wait(barL3[0], phL3[0]);
+    phL3[0] ^= 1;
+    mbar_wait(barL3[1], phL3[1]);
+    phL3[1] ^= 1;
     tc_fence_after();
 
     // ---- layer 3 epilogue + the 64 -> 1 output layer on the CUDA cores
@@ -397,7 +427,7 @@ __global__ void __launch_bounds__(kMlpThreads, 1)
 #pragma unroll
       for (int i = 0; i < 16; ++i) part = fmaf(fmaxf(fmaf(y[i], s2, b2[16 * cg + i]), 0.f), w3[16 * cg + i], part);
     }
-    red[cg * 128 + row_in_tile] = part;  // A buffer is free: every L3 MMA has completed
+    red[cg * 128 + row_in_tile] = part;  // A buffer 0 is free: every L3 MMA has completed
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
@@ -407,7 +437,7 @@ __global__ void __launch_bounds__(kMlpThreads, 1)
                       red[256 + row_in_tile] + red[384 + row_in_tile];
       if (row < M) out[row] = o;
     }
-    __syncthreads();  // red (A buffer) is rewritten by the next tile's first epilogue
+    __syncthreads();  // red (A buffer 0) is rewritten by the next tile's first epilogue
   }
   if (!weights_ready && tid == 0) {  // CTA got no tile: drain the weight copies before exit
     mbar_wait(barW0, 0);
@@ -416,7 +446,7 @@ __global__ void __launch_bounds__(kMlpThreads, 1)
   }
   __syncthreads();
   if (warp == 0)
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(256));
 }
 
 // ------------------------------------------------------------------ host side
