@@ -68,7 +68,7 @@ constexpr uint32_t kAHalf = 128 * kAChunkK * 2;     // 8 KiB
 constexpr uint32_t kABuf = 2 * kAHalf;              // hi + lo = 16 KiB
 constexpr uint32_t OFF_A = OFF_XL + 128 * 16 * 2;
 constexpr uint32_t OFF_BAR = OFF_A + 2 * kABuf;     // 16 mbarriers
-constexpr uint32_t OFF_TMEMPTR = OFF_BAR + 16 * 8;
+constexpr uint32_t OFF_TMEMPTR = OFF_BAR + 16 * 8;  // 12 used
 constexpr uint32_t kMlpSmem = OFF_TMEMPTR + 16;
 
 static_assert(kMlpSmem <= 232448, "MLP tile does not fit the 227 KiB of shared memory");
@@ -203,12 +203,14 @@ __device__ __forceinline__ void store_split8(unsigned char* sm, uint32_t off_h, 
 }
 
 // ------------------------------------------------------------------ the kernel
-// 16 warps: warp w serves TMEM lane quadrant q = w % 4 (rows 32q..32q+31 of
-// the tile) and column group cg = w / 4 (8 of every 32 accumulator columns).
-// Activations move through two 32-wide smem buffers: while the tensor core
-// runs the layer-2 (or layer-3) MMAs of chunk c, the epilogue of chunk c+1
-// fills the other buffer.
-constexpr int kMlpThreads = 512;
+// Warp-specialised: warps 0-15 are the epilogue (warp w serves TMEM lane
+// quadrant q = w % 4, i.e. rows 32q..32q+31 of the tile, and column group
+// cg = w / 4: 8 of every 32 accumulator columns); warp 16 is the producer:
+// it issues the weight TMA and every tcgen05.mma. Activations move through two
+// 32-wide smem buffers; the hand-off is mbarrier-only:
+//   epilogue --aready[b] (16 arrivals)--> issuer --tcgen05.commit--> epilogue
+constexpr int kMlpEpiWarps = 16;
+constexpr int kMlpThreads = (kMlpEpiWarps + 1) * 32;
 
 __device__ __forceinline__ void tmem_ld8(uint32_t taddr, float* v) {
   uint32_t r[8];
@@ -221,6 +223,14 @@ __device__ __forceinline__ void tmem_ld8(uint32_t taddr, float* v) {
   for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+
+__device__ __forceinline__ void epi_barrier() {  // named barrier over the 512 epilogue threads
+  asm volatile("bar.sync 1, %0;" ::"n"(kMlpEpiWarps * 32) : "memory");
+}
+
 // x: (M_pad,16) fp32 positional encodings; out: (M) fp32 distances.
 __global__ void __launch_bounds__(kMlpThreads, 1)
     mlp_tcgen05_kernel(const float* __restrict__ x, long long M, const unsigned char* __restrict__ img,
@@ -228,20 +238,22 @@ __global__ void __launch_bounds__(kMlpThreads, 1)
   extern __shared__ __align__(1024) unsigned char mlp_smem[];
   unsigned char* sm = mlp_smem;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int quad = warp & 3, cg = warp >> 2;
-  const int row_in_tile = quad * 32 + lane;
   const uint32_t sb = smem_u32(sm);
-  // barriers: 0-2 weights, 3-4 layer 1 (per acc1 buffer), 5-6 layer 2 (per A
-  // buffer), 7-8 layer 3 (per A buffer)
+  // barriers: 0-2 weights, 3-4 L1 done (per acc1 buffer), 5-6 L2 done (per A
+  // buffer), 7-8 L3 done (per A buffer), 9-10 A ready (per A buffer), 11 X ready
   const uint32_t barW0 = sb + OFF_BAR, barW1 = barW0 + 8, barW2 = barW0 + 16;
   const uint32_t barL1[2] = {barW0 + 24, barW0 + 32};
   const uint32_t barL2[2] = {barW0 + 40, barW0 + 48};
   const uint32_t barL3[2] = {barW0 + 56, barW0 + 64};
+  const uint32_t barA[2] = {barW0 + 72, barW0 + 80};
+  const uint32_t barX = barW0 + 88;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sm + OFF_TMEMPTR);
-  float* red = reinterpret_cast<float*>(sm + OFF_A);  // final 64->1 partials reuse A buffer 0
 
   if (tid == 0) {
     for (int i = 0; i < 9; ++i) mbar_init(barW0 + 8 * i, 1);
+    mbar_init(barA[0], kMlpEpiWarps);
+    mbar_init(barA[1], kMlpEpiWarps);
+    mbar_init(barX, kMlpEpiWarps);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     fence_async_smem();
   }
@@ -255,198 +267,207 @@ __global__ void __launch_bounds__(kMlpThreads, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   const uint32_t acc1[2] = {tmem, tmem + 32}, acc2 = tmem + 64, acc3 = tmem + 192;
-  const uint32_t lane_base = (uint32_t)(quad * 32) << 16;
-
-  if (tid == 0) {  // weights: three bulk-copy segments, each on its own barrier
-    mbar_expect_tx(barW0, kSeg0);
-    bulk_g2s(sb + 0, img, kSeg0, barW0);
-    mbar_expect_tx(barW1, kSeg1);
-    for (uint32_t o = 0; o < kSeg1; o += 32768)
-      bulk_g2s(sb + OFF_W1H + o, img + OFF_W1H + o, min(32768u, kSeg1 - o), barW1);
-    mbar_expect_tx(barW2, kSeg2);
-    bulk_g2s(sb + OFF_W2H, img + OFF_W2H, kSeg2, barW2);
-  }
-  const float* par = reinterpret_cast<const float*>(sm + OFF_PAR);
-  const float* b0 = par;
-  const float* b1 = par + kMlpH0;
-  const float* b2 = b1 + kMlpH1;
-  const float* w3 = b2 + kMlpH2;
-
-  const uint32_t id32 = umma_idesc(32), id64 = umma_idesc(64), id128 = umma_idesc(128);
-  uint32_t phL1[2] = {0, 0}, phL2[2] = {0, 0}, phL3[2] = {0, 0};
-  bool weights_ready = false;
   const long long ntiles = (M + 127) / 128;
 
-  auto abuf_h = [&](int b) { return OFF_A + b * kABuf; };
-  auto abuf_l = [&](int b) { return OFF_A + b * kABuf + kAHalf; };
-  // X loader: threads < 256 own (row = tid % 128, 8 of the 16 columns)
-  auto load_x = [&](long long tile, float* xv) {
-    const long long r = tile * 128 + (tid & 127);
-    if (tid < 256 && r < M) {
-      const float4* src = reinterpret_cast<const float4*>(x + r * 16 + (tid >> 7) * 8);
-      const float4 f0 = __ldg(src), f1 = __ldg(src + 1);
-      xv[0] = f0.x; xv[1] = f0.y; xv[2] = f0.z; xv[3] = f0.w;
-      xv[4] = f1.x; xv[5] = f1.y; xv[6] = f1.z; xv[7] = f1.w;
-    } else {
-#pragma unroll
-      for (int i = 0; i < 8; ++i) xv[i] = 0.f;
-    }
-  };
-  auto store_x = [&](const float* xv) {
-    if (tid < 256) store_split8(sm, OFF_XH, OFF_XL, umma_off(tid & 127, (tid >> 7) * 8, 16), xv);
-  };
-  auto issue_l1 = [&](int c) {  // acc1[c%2] = X . W0t[32c:32c+32]^T   (N = 32)
-    const uint64_t xh = umma_desc(sb + OFF_XH, 128, 256), xl = umma_desc(sb + OFF_XL, 128, 256);
-    const uint64_t wh = umma_desc(sb + OFF_W0H + umma_off(32 * c, 0, 16), 128, 256);
-    const uint64_t wl = umma_desc(sb + OFF_W0L + umma_off(32 * c, 0, 16), 128, 256);
-    umma_f16(acc1[c & 1], xh, wh, id32, 0);
-    umma_f16(acc1[c & 1], xh, wl, id32, 1);
-    umma_f16(acc1[c & 1], xl, wh, id32, 1);
-    umma_commit(barL1[c & 1]);
-  };
-  auto issue_l2 = [&](int c) {  // acc2 += A[c%2] . W1t[:, 32c:32c+32]^T   (N = 128)
-#pragma unroll
-    for (int j = 0; j < 2; ++j) {
-      const uint64_t ah = umma_desc(sb + abuf_h(c & 1) + j * 256, 128, 512);
-      const uint64_t al = umma_desc(sb + abuf_l(c & 1) + j * 256, 128, 512);
-      const uint64_t wh = umma_desc(sb + OFF_W1H + (4 * c + 2 * j) * 128, 128, 4096);
-      const uint64_t wl = umma_desc(sb + OFF_W1L + (4 * c + 2 * j) * 128, 128, 4096);
-      umma_f16(acc2, ah, wh, id128, (c | j) ? 1u : 0u);
-      umma_f16(acc2, ah, wl, id128, 1);
-      umma_f16(acc2, al, wh, id128, 1);
-    }
-    umma_commit(barL2[c & 1]);
-  };
-  auto issue_l3 = [&](int c) {  // acc3 += A[c%2] . W2t[:, 32c:32c+32]^T   (N = 64)
-#pragma unroll
-    for (int j = 0; j < 2; ++j) {
-      const uint64_t ah = umma_desc(sb + abuf_h(c & 1) + j * 256, 128, 512);
-      const uint64_t al = umma_desc(sb + abuf_l(c & 1) + j * 256, 128, 512);
-      const uint64_t wh = umma_desc(sb + OFF_W2H + (4 * c + 2 * j) * 128, 128, 2048);
-      const uint64_t wl = umma_desc(sb + OFF_W2L + (4 * c + 2 * j) * 128, 128, 2048);
-      umma_f16(acc3, ah, wh, id64, (c | j) ? 1u : 0u);
-      umma_f16(acc3, ah, wl, id64, 1);
-      umma_f16(acc3, al, wh, id64, 1);
-    }
-    umma_commit(barL3[c & 1]);
-  };
-  auto sync_for_mma = [&]() {
-    fence_async_smem();
-    tc_fence_before();
-    __syncthreads();
-    tc_fence_after();
-  };
-
-  float xnext[8];
-  long long tile = blockIdx.x;
-  if (tile < ntiles) {
-    load_x(tile, xnext);
-    store_x(xnext);
-    fence_async_smem();
-    mbar_wait(barW0, 0);  // W0 + biases; W1/W2 still streaming
-    __syncthreads();
-    tc_fence_after();
-    if (tid == 0) {
-      issue_l1(0);
-      issue_l1(1);
-    }
-  }
-  const float s0 = par[kMlpH0 + kMlpH1 + 2 * kMlpH2 + 1];
-  const float s1 = par[kMlpH0 + kMlpH1 + 2 * kMlpH2 + 2];
-  const float s2 = par[kMlpH0 + kMlpH1 + 2 * kMlpH2 + 3];
-
-  for (; tile < ntiles; tile += gridDim.x) {
-    const long long next = tile + gridDim.x;
-    const bool has_next = next < ntiles;
-    if (has_next) load_x(next, xnext);  // in flight during layer 1
-
-    // ---- layer 1: 8 chunks of 32 outputs, each feeding a layer-2 K-chunk
-    for (int c = 0; c < 8; ++c) {
-      const int bf = c & 1;
-      mbar_wait(barL1[bf], phL1[bf]);
-      phL1[bf] ^= 1;
-      tc_fence_after();
-      float y[8];
-      tmem_ld8(acc1[bf] + lane_base + 8 * cg, y);
-#pragma unroll
-      for (int i = 0; i < 8; ++i) y[i] = fmaxf(fmaf(y[i], s0, b0[32 * c + 8 * cg + i]), 0.f);
-      if (c >= 2) {  // A[bf] was last read by the layer-2 MMAs of chunk c-2
-        mbar_wait(barL2[bf], phL2[bf]);
-        phL2[bf] ^= 1;
-      }
-      store_split8(sm, abuf_h(bf), abuf_l(bf), umma_off(row_in_tile, 8 * cg, kAChunkK), y);
-      if (c == 7 && has_next) store_x(xnext);  // every layer-1 MMA of this tile is complete
-      sync_for_mma();
-      if (tid == 0) {
-        if (!weights_ready && c == 0) mbar_wait(barW1, 0);
-        issue_l2(c);
-        if (c + 2 < 8) issue_l1(c + 2);
-        if (c == 7 && has_next) {  // next tile's first layer-1 chunks overlap this tile's tail
+  if (warp == kMlpEpiWarps) {
+    // ======================= producer / MMA issuer ==========================
+    if (lane == 0) {
+      mbar_expect_tx(barW0, kSeg0);
+      bulk_g2s(sb + 0, img, kSeg0, barW0);
+      mbar_expect_tx(barW1, kSeg1);
+      for (uint32_t o = 0; o < kSeg1; o += 32768)
+        bulk_g2s(sb + OFF_W1H + o, img + OFF_W1H + o, min(32768u, kSeg1 - o), barW1);
+      mbar_expect_tx(barW2, kSeg2);
+      bulk_g2s(sb + OFF_W2H, img + OFF_W2H, kSeg2, barW2);
+      const uint32_t id32 = umma_idesc(32), id64 = umma_idesc(64), id128 = umma_idesc(128);
+      // descriptors are built once; per-chunk operands differ only in the
+      // start-address field (bits 0-13, 16-byte units, no carry: smem < 256 KiB)
+      const uint64_t dXH = umma_desc(sb + OFF_XH, 128, 256), dXL = umma_desc(sb + OFF_XL, 128, 256);
+      const uint64_t dW0H = umma_desc(sb + OFF_W0H, 128, 256), dW0L = umma_desc(sb + OFF_W0L, 128, 256);
+      const uint64_t dAH = umma_desc(sb + OFF_A, 128, 512), dAL = umma_desc(sb + OFF_A + kAHalf, 128, 512);
+      const uint64_t dW1H = umma_desc(sb + OFF_W1H, 128, 4096), dW1L = umma_desc(sb + OFF_W1L, 128, 4096);
+      const uint64_t dW2H = umma_desc(sb + OFF_W2H, 128, 2048), dW2L = umma_desc(sb + OFF_W2L, 128, 2048);
+      auto issue_l1 = [&](int c) {
+        const uint64_t wo = umma_off(32 * c, 0, 16) >> 4;
+        umma_f16(acc1[c & 1], dXH, dW0H + wo, id32, 0);
+        umma_f16(acc1[c & 1], dXH, dW0L + wo, id32, 1);
+        umma_f16(acc1[c & 1], dXL, dW0H + wo, id32, 1);
+        umma_commit(barL1[c & 1]);
+      };
+      uint32_t phA[2] = {0, 0}, phX = 0;
+      bool first = true;
+      for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const bool has_next = tile + gridDim.x < ntiles;
+        if (first) {
+          mbar_wait(barX, phX);
+          phX ^= 1;
+          mbar_wait(barW0, 0);
+          tc_fence_after();
           issue_l1(0);
           issue_l1(1);
         }
-      }
-    }
-    // all layer-2 MMAs (in order) complete once chunk 7's and chunk 6's commits have arrived
-    mbar_wait(barL2[0], phL2[0]);
-    phL2[0] ^= 1;
-    mbar_wait(barL2[1], phL2[1]);
-    phL2[1] ^= 1;
-    tc_fence_after();
-
-    // ---- layer 2 output: 4 K-chunks of 32 feeding layer 3
-    for (int c = 0; c < 4; ++c) {
-      const int bf = c & 1;
-      float y[8];
-      tmem_ld8(acc2 + lane_base + 32 * c + 8 * cg, y);
+        for (int c = 0; c < 8; ++c) {
+          const int bf = c & 1;
+          mbar_wait(barA[bf], phA[bf]);
+          phA[bf] ^= 1;
+          if (first && c == 0) mbar_wait(barW1, 0);
+          tc_fence_after();
+          const uint64_t ao = (uint64_t)(bf * kABuf) >> 4;
 #pragma unroll
-      for (int i = 0; i < 8; ++i) y[i] = fmaxf(fmaf(y[i], s1, b1[32 * c + 8 * cg + i]), 0.f);
-      if (c >= 2) {
-        mbar_wait(barL3[bf], phL3[bf]);
-        phL3[bf] ^= 1;
-      }
-      store_split8(sm, abuf_h(bf), abuf_l(bf), umma_off(row_in_tile, 8 * cg, kAChunkK), y);
-      sync_for_mma();
-      if (tid == 0) {
-        if (!weights_ready && c == 0) mbar_wait(barW2, 0);
-        issue_l3(c);
-      }
-    }
-    weights_ready = true;
-    mbar_wait(barL3[0], phL3[0]);
-    phL3[0] ^= 1;
-    mbar_wait(barL3[1], phL3[1]);
-    phL3[1] ^= 1;
-    tc_fence_after();
-
-    // ---- layer 3 epilogue + the 64 -> 1 output layer on the CUDA cores
-    float part = 0.f;
-    {
-      float y[16];
-      tmem_ld16(acc3 + lane_base + 16 * cg, y);
+          for (int j = 0; j < 2; ++j) {
+            const uint64_t aj = ao + (uint64_t)(j * 256 >> 4), wj = (uint64_t)((4 * c + 2 * j) * 128 >> 4);
+            umma_f16(acc2, dAH + aj, dW1H + wj, id128, (c | j) ? 1u : 0u);
+            umma_f16(acc2, dAH + aj, dW1L + wj, id128, 1);
+            umma_f16(acc2, dAL + aj, dW1H + wj, id128, 1);
+          }
+          umma_commit(barL2[bf]);
+          if (c + 2 < 8) issue_l1(c + 2);
+          if (c == 7 && has_next) {  // the next tile's X is in smem once the epilogue saw L1(7)
+            mbar_wait(barX, phX);
+            phX ^= 1;
+            tc_fence_after();
+            issue_l1(0);
+            issue_l1(1);
+          }
+        }
+        for (int c = 0; c < 4; ++c) {
+          const int bf = c & 1;
+          mbar_wait(barA[bf], phA[bf]);
+          phA[bf] ^= 1;
+          if (first && c == 0) mbar_wait(barW2, 0);
+          tc_fence_after();
+          const uint64_t ao = (uint64_t)(bf * kABuf) >> 4;
 #pragma unroll
-      for (int i = 0; i < 16; ++i) part = fmaf(fmaxf(fmaf(y[i], s2, b2[16 * cg + i]), 0.f), w3[16 * cg + i], part);
+          for (int j = 0; j < 2; ++j) {
+            const uint64_t aj = ao + (uint64_t)(j * 256 >> 4), wj = (uint64_t)((4 * c + 2 * j) * 128 >> 4);
+            umma_f16(acc3, dAH + aj, dW2H + wj, id64, (c | j) ? 1u : 0u);
+            umma_f16(acc3, dAH + aj, dW2L + wj, id64, 1);
+            umma_f16(acc3, dAL + aj, dW2H + wj, id64, 1);
+          }
+          umma_commit(barL3[bf]);
+        }
+        first = false;
+      }
+      if (first) {  // no tile for this CTA: drain the weight copies before exit
+        mbar_wait(barW0, 0);
+        mbar_wait(barW1, 0);
+        mbar_wait(barW2, 0);
+      }
     }
-    red[cg * 128 + row_in_tile] = part;  // A buffer 0 is free: every L3 MMA has completed
-    tc_fence_before();
-    __syncthreads();
-    tc_fence_after();
-    if (cg == 0) {
-      const long long row = tile * 128 + row_in_tile;
-      const float o = par[kMlpH0 + kMlpH1 + 2 * kMlpH2] + red[row_in_tile] + red[128 + row_in_tile] +
-                      red[256 + row_in_tile] + red[384 + row_in_tile];
-      if (row < M) out[row] = o;
+  } else {
+    // ============================ epilogue warps ============================
+    const int quad = warp & 3, cg = warp >> 2;
+    const int row_in_tile = quad * 32 + lane;
+    const uint32_t lane_base = (uint32_t)(quad * 32) << 16;
+    float* red = reinterpret_cast<float*>(sm + OFF_A);  // final partials reuse A buffer 0
+    const float* par = reinterpret_cast<const float*>(sm + OFF_PAR);
+    const float* b0 = par;
+    const float* b1 = par + kMlpH0;
+    const float* b2 = b1 + kMlpH1;
+    const float* w3 = b2 + kMlpH2;
+    uint32_t phL1[2] = {0, 0}, phL2[2] = {0, 0}, phL3[2] = {0, 0};
+    auto load_x = [&](long long tile, float* xv) {  // threads < 256: row tid % 128, 8 of 16 columns
+      const long long r = tile * 128 + (tid & 127);
+      if (tid < 256 && r < M) {
+        const float4* src = reinterpret_cast<const float4*>(x + r * 16 + (tid >> 7) * 8);
+        const float4 f0 = __ldg(src), f1 = __ldg(src + 1);
+        xv[0] = f0.x; xv[1] = f0.y; xv[2] = f0.z; xv[3] = f0.w;
+        xv[4] = f1.x; xv[5] = f1.y; xv[6] = f1.z; xv[7] = f1.w;
+      } else {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) xv[i] = 0.f;
+      }
+    };
+    auto publish = [&](uint32_t bar) {  // generic-proxy smem writes -> async proxy, then arrive
+      fence_async_smem();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(bar);
+    };
+    float xnext[8];
+    long long tile = blockIdx.x;
+    if (tile < ntiles) {
+      load_x(tile, xnext);
+      if (tid < 256) store_split8(sm, OFF_XH, OFF_XL, umma_off(tid & 127, (tid >> 7) * 8, 16), xnext);
+      publish(barX);
+      mbar_wait(barW0, 0);  // biases live in the W0 segment
     }
-    __syncthreads();  // red (A buffer 0) is rewritten by the next tile's first epilogue
-  }
-  if (!weights_ready && tid == 0) {  // CTA got no tile: drain the weight copies before exit
-    mbar_wait(barW0, 0);
-    mbar_wait(barW1, 0);
-    mbar_wait(barW2, 0);
+    const float s0 = par[kMlpH0 + kMlpH1 + 2 * kMlpH2 + 1];
+    const float s1 = par[kMlpH0 + kMlpH1 + 2 * kMlpH2 + 2];
+    const float s2 = par[kMlpH0 + kMlpH1 + 2 * kMlpH2 + 3];
+    for (; tile < ntiles; tile += gridDim.x) {
+      const bool has_next = tile + gridDim.x < ntiles;
+      if (has_next) load_x(tile + gridDim.x, xnext);  // in flight during layer 1
+      for (int c = 0; c < 8; ++c) {
+        const int bf = c & 1;
+        mbar_wait(barL1[bf], phL1[bf]);
+        phL1[bf] ^= 1;
+        tc_fence_after();
+        float y[8];
+        tmem_ld8(acc1[bf] + lane_base + 8 * cg, y);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) y[i] = fmaxf(fmaf(y[i], s0, b0[32 * c + 8 * cg + i]), 0.f);
+        if (c >= 2) {  // A[bf] was last read by the layer-2 MMAs of chunk c-2
+          mbar_wait(barL2[bf], phL2[bf]);
+          phL2[bf] ^= 1;
+        }
+        store_split8(sm, OFF_A + bf * kABuf, OFF_A + bf * kABuf + kAHalf,
+                     umma_off(row_in_tile, 8 * cg, kAChunkK), y);
+        publish(barA[bf]);
+        if (c == 7 && has_next) {  // every layer-1 MMA of this tile is complete: reuse X
+          if (tid < 256) store_split8(sm, OFF_XH, OFF_XL, umma_off(tid & 127, (tid >> 7) * 8, 16), xnext);
+          publish(barX);
+        }
+      }
+      mbar_wait(barL2[0], phL2[0]);  // chunk 6's and chunk 7's layer-2 MMAs: all of layer 2
+      phL2[0] ^= 1;
+      mbar_wait(barL2[1], phL2[1]);
+      phL2[1] ^= 1;
+      tc_fence_after();
+      for (int c = 0; c < 4; ++c) {
+        const int bf = c & 1;
+        float y[8];
+        tmem_ld8(acc2 + lane_base + 32 * c + 8 * cg, y);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) y[i] = fmaxf(fmaf(y[i], s1, b1[32 * c + 8 * cg + i]), 0.f);
+        if (c >= 2) {
+          mbar_wait(barL3[bf], phL3[bf]);
+          phL3[bf] ^= 1;
+        }
+        store_split8(sm, OFF_A + bf * kABuf, OFF_A + bf * kABuf + kAHalf,
+                     umma_off(row_in_tile, 8 * cg, kAChunkK), y);
+        publish(barA[bf]);
+      }
+      mbar_wait(barL3[0], phL3[0]);
+      phL3[0] ^= 1;
+      mbar_wait(barL3[1], phL3[1]);
+      phL3[1] ^= 1;
+      tc_fence_after();
+      float part = 0.f;
+      {
+        float y[16];
+        tmem_ld16(acc3 + lane_base + 16 * cg, y);
+#pragma unroll
+        for (int i = 0; i < 16; ++i)
+          part = fmaf(fmaxf(fmaf(y[i], s2, b2[16 * cg + i]), 0.f), w3[16 * cg + i], part);
+      }
+      red[cg * 128 + row_in_tile] = part;  // A buffer 0 is free: every L3 MMA has completed
+      epi_barrier();
+      if (cg == 0) {
+        const long long row = tile * 128 + row_in_tile;
+        const float o = par[kMlpH0 + kMlpH1 + 2 * kMlpH2] + red[row_in_tile] + red[128 + row_in_tile] +
+                        red[256 + row_in_tile] + red[384 + row_in_tile];
+        if (row < M) out[row] = o;
+      }
+      tc_fence_before();
+      epi_barrier();  // red (A buffer 0) is rewritten by the next tile's first epilogue
+    }
   }
   __syncthreads();
-  if (warp == 0)
+  if (warp == 0) {
+    tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(256));
+  }
 }
 
 // ------------------------------------------------------------------ host side
