@@ -257,16 +257,16 @@ __global__ void __launch_bounds__(kMlpThreads, 1)
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     fence_async_smem();
   }
-  if (warp == 0) {  // TMEM: acc1 x2 (32+32) | acc2 (128) | acc3 (64) -> 256 columns
+  if (warp == 0) {  // TMEM: acc1 8 x 32 (all of layer 1) | acc2 (128) | acc3 (64) -> 448 of 512 columns
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                 "r"(256));
+                 "r"(512));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const uint32_t acc1[2] = {tmem, tmem + 32}, acc2 = tmem + 64, acc3 = tmem + 192;
+  const uint32_t acc2 = tmem + 256, acc3 = tmem + 384;  // acc1 chunk c at tmem + 32c
   const long long ntiles = (M + 127) / 128;
 
   if (warp == kMlpEpiWarps) {
@@ -287,12 +287,15 @@ __global__ void __launch_bounds__(kMlpThreads, 1)
       const uint64_t dAH = umma_desc(sb + OFF_A, 128, 512), dAL = umma_desc(sb + OFF_A + kAHalf, 128, 512);
       const uint64_t dW1H = umma_desc(sb + OFF_W1H, 128, 4096), dW1L = umma_desc(sb + OFF_W1L, 128, 4096);
       const uint64_t dW2H = umma_desc(sb + OFF_W2H, 128, 2048), dW2L = umma_desc(sb + OFF_W2L, 128, 2048);
-      auto issue_l1 = [&](int c) {
-        const uint64_t wo = umma_off(32 * c, 0, 16) >> 4;
-        umma_f16(acc1[c & 1], dXH, dW0H + wo, id32, 0);
-        umma_f16(acc1[c & 1], dXH, dW0L + wo, id32, 1);
-        umma_f16(acc1[c & 1], dXL, dW0H + wo, id32, 1);
-        umma_commit(barL1[c & 1]);
+      auto issue_l1_all = [&]() {  // the whole of layer 1: 8 chunks of N=32, two commits
+        for (int c = 0; c < 8; ++c) {
+          const uint64_t wo = umma_off(32 * c, 0, 16) >> 4;
+          umma_f16(tmem + 32 * c, dXH, dW0H + wo, id32, 0);
+          umma_f16(tmem + 32 * c, dXH, dW0L + wo, id32, 1);
+          umma_f16(tmem + 32 * c, dXL, dW0H + wo, id32, 1);
+          if (c == 3) umma_commit(barL1[0]);
+        }
+        umma_commit(barL1[1]);
       };
       uint32_t phA[2] = {0, 0}, phX = 0;
       bool first = true;
@@ -303,8 +306,7 @@ __global__ void __launch_bounds__(kMlpThreads, 1)
           phX ^= 1;
           mbar_wait(barW0, 0);
           tc_fence_after();
-          issue_l1(0);
-          issue_l1(1);
+          issue_l1_all();
         }
         for (int c = 0; c < 8; ++c) {
           const int bf = c & 1;
@@ -321,13 +323,11 @@ __global__ void __launch_bounds__(kMlpThreads, 1)
             umma_f16(acc2, dAL + aj, dW1H + wj, id128, 1);
           }
           umma_commit(barL2[bf]);
-          if (c + 2 < 8) issue_l1(c + 2);
-          if (c == 7 && has_next) {  // the next tile's X is in smem once the epilogue saw L1(7)
+          if (c == 7 && has_next) {  // every acc1 chunk consumed and the next X in smem
             mbar_wait(barX, phX);
             phX ^= 1;
             tc_fence_after();
-            issue_l1(0);
-            issue_l1(1);
+            issue_l1_all();  // runs behind this tile's layer 2, under its layer-2/3 epilogues
           }
         }
         for (int c = 0; c < 4; ++c) {
@@ -400,11 +400,13 @@ __global__ void __launch_bounds__(kMlpThreads, 1)
       if (has_next) load_x(tile + gridDim.x, xnext);  // in flight during layer 1
       for (int c = 0; c < 8; ++c) {
         const int bf = c & 1;
-        mbar_wait(barL1[bf], phL1[bf]);
-        phL1[bf] ^= 1;
-        tc_fence_after();
+        if ((c & 3) == 0) {  // layer-1 chunks 0-3 and 4-7 complete on separate barriers
+          mbar_wait(barL1[c >> 2], phL1[c >> 2]);
+          phL1[c >> 2] ^= 1;
+          tc_fence_after();
+        }
         float y[8];
-        tmem_ld8(acc1[bf] + lane_base + 8 * cg, y);
+        tmem_ld8(tmem + 32 * c + lane_base + 8 * cg, y);
 #pragma unroll
         for (int i = 0; i < 8; ++i) y[i] = fmaxf(fmaf(y[i], s0, b0[32 * c + 8 * cg + i]), 0.f);
         if (c >= 2) {  // A[bf] was last read by the layer-2 MMAs of chunk c-2
