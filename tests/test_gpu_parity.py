@@ -375,3 +375,114 @@ def test_cuda_backend_in_unmodified_reference():
                             particles=64, horizon=20, provider="oracle")
     ocmd = oc.step(st.theta, st.theta_dot)
     np.testing.assert_allclose(cmd, ocmd, atol=1e-9)
+
+
+def _random_chain(d, seed):
+    from paper_2104_13542_b200.kinematics import chain_from_dict
+
+    rng = np.random.default_rng(seed)
+    joints = []
+    for k in range(d):
+        ax = rng.standard_normal(3)
+        ax /= np.linalg.norm(ax)
+        joints.append({"type": "prismatic" if (k % 3 == 2) else "revolute", "axis": ax.tolist(),
+                       "origin": {"xyz": (rng.standard_normal(3) * 0.2).tolist(),
+                                  "rpy": (rng.standard_normal(3) * 0.5).tolist()}})
+    caps = [{"link": int(l), "p0": (rng.standard_normal(3) * 0.05).tolist(),
+             "p1": (rng.standard_normal(3) * 0.1).tolist(), "radius": 0.04} for l in range(d)]
+    pairs = [[i, j] for i in range(d) for j in range(i + 2, d)][:8]
+    return chain_from_dict({"name": f"rand{d}", "task_dim": 3, "joints": joints,
+                            "limits": {"position": [[-2.0, 2.0]] * d, "velocity": [3.0] * d,
+                                       "acceleration": [10.0] * d},
+                            "capsules": caps, "self_collision_pairs": pairs})
+
+
+@pytest.mark.parametrize("d", [1, 2, 3, 4, 5, 6, 7, 8])
+def test_fused_rollout_generic_chains(d):
+    """Every dof instantiation of the fused kernel (d = 8 exercises the
+    re-orthonormalisation of jit.py:190), prismatic joints, non-identity origin
+    rotations, all cost terms incl. capsules and a world, vs the oracle."""
+    from paper_2104_13542_b200.costs import CostStack, CostWeights, goal_at_position
+    from paper_2104_13542_b200.kinematics import Pose
+    from paper_2104_13542_b200.costs import GoalSpec, FULL_POSE
+    from paper_2104_13542_b200.rollout import evaluate_rollouts, make_dt_schedule, zero_state
+    from paper_2104_13542_b200.simworld import world_from_dict
+    from paper_2104_13542_b200 import kernels as K
+
+    chain = _random_chain(d, 100 + d)
+    rng = np.random.default_rng(d)
+    q = rng.uniform(-1, 1, size=(64, d))
+    rot, trans = K.fk_batch(q, chain.axes, chain.origin_rot, chain.origin_trans, chain.jtype)
+    orot, otrans = O.link_poses(q, chain)
+    np.testing.assert_allclose(rot, orot, atol=1e-12)
+    np.testing.assert_allclose(trans, otrans, atol=1e-12)
+    world = world_from_dict({"obstacles": [{"type": "sphere", "center": [0.2, 0.1, 0.3], "radius": 0.15},
+                                           {"type": "box", "min": [-0.4, -0.3, 0.0], "max": [-0.1, 0.2, 0.4]}]})
+    Rg = O._rodrigues(np.array([0.0, 0.0, 1.0]), np.array([0.3]))[0]
+    goal = GoalSpec(target_pose=Pose(rotation=Rg, translation=np.array([0.2, -0.1, 0.3])), mode=FULL_POSE)
+    w = CostWeights(alpha_stop=5.0, alpha_joint=10.0, alpha_manip=3.0, alpha_coll=10.0, k_m=0.02)
+    stack = CostStack(chain=chain, weights=w, goal=goal, world=world)
+    sched = make_dt_schedule(12, 0.05, "linear")
+    u = rng.standard_normal((96, 12, d)) * 2.0
+    x0 = zero_state(d)
+    ref = O.rollout_scores(x0.theta, x0.theta_dot, u, sched.dts, chain, w, Rg, goal.target_pose.translation, True,
+                           0.97, 2.0, provider="oracle" if chain.pair_a.size else None, spheres=world.spheres,
+                           boxes=world.boxes)
+    b = evaluate_rollouts(x0, u, chain, stack, sched, gamma=0.97, terminal_weight=2.0)  # FP64 plan
+    np.testing.assert_allclose(b.positions, ref["positions"], atol=1e-12)
+    for name in O.TERMS:
+        np.testing.assert_allclose(b.term_breakdown[name], ref["terms"][name], rtol=1e-9, atol=1e-9, err_msg=name)
+    np.testing.assert_allclose(b.total_per_particle, ref["totals"], rtol=1e-10)
+
+
+@pytest.mark.parametrize("mode,horizon,iso", [("comb", 12, False), ("none", 8, True), ("bspline", 8, False)])
+def test_controller_smoothing_modes_vs_oracle(planar2, mode, horizon, iso):
+    """Halton set built on the device for every smoothing mode (sampling.py:240-265)
+    and short horizons, planar2 (the reference's controller test chain)."""
+    from paper_2104_13542_b200.controller import Controller
+    from paper_2104_13542_b200.costs import CostWeights, goal_at_position
+    from paper_2104_13542_b200.rollout import JointState
+    from paper_2104_13542_b200.sampling import SmoothingSpec
+
+    spec = SmoothingSpec(mode=mode)
+    kw = dict(horizon=horizon, particles=24, beta=0.5, sigma0_sq=1.0, alpha_mu=0.9, alpha_sigma=0.5,
+              policy_mode="isotropic" if iso else "per_joint_diagonal")
+    c = Controller(planar2, goal_at_position([1.2, 0.8]), smoothing=spec, precision="fp64", seed=7, **kw)
+    oc = O.OracleController(planar2, CostWeights(), np.eye(3), np.array([1.2, 0.8, 0.0]), False,
+                            provider="oracle", smoothing=mode, isotropic=iso, **{k: v for k, v in kw.items()
+                                                                                 if k != "policy_mode"})
+    np.testing.assert_allclose(c._fixed_eps, oc.eps_source(), atol=1e-12)
+    st = JointState(theta=np.array([0.3, -0.2]), theta_dot=np.zeros(2), theta_ddot=np.zeros(2))
+    for _ in range(4):
+        cmd, d = c.control_step(st)
+        ocmd = oc.step(st.theta, st.theta_dot)
+        np.testing.assert_allclose(cmd, ocmd, atol=1e-8)
+        st = JointState(theta=st.theta + 0.05 * (st.theta_dot + 0.05 * cmd), theta_dot=st.theta_dot + 0.05 * cmd,
+                        theta_ddot=cmd)
+
+
+def test_failure_in_second_iteration_keeps_first_update():
+    """iterations=2: a poisoned policy makes iteration 1 fail -> the shifted
+    policy stands (controller.py:200, 224); status is re-armed for the next step."""
+    from paper_2104_13542_b200 import configs
+
+    c = configs.make_controller(1, particles=64, iterations=2, precision="fp64")
+    st = configs.start_state()
+    cmd0, d0 = c.control_step(st)
+    assert d0.fallback == ""
+    pol = c.policy
+    pol.variances[3, 2] = np.nan  # NaN variance: finite-check fails on the shaped controls
+    c.policy = pol
+    before = c.policy
+    _, d1 = c.control_step(st)
+    assert d1.fallback == "reissue"
+    after = c.policy
+    # the failed step still shifted the policy (and changed nothing else)
+    np.testing.assert_array_equal(after.means[:-1], before.means[1:])
+    np.testing.assert_array_equal(after.means[-1], 0.0)
+    # recovery: a healthy policy steps normally again
+    from paper_2104_13542_b200.policy import make_policy
+
+    c.policy = make_policy(30, 7, 0.5)
+    _, d2 = c.control_step(st)
+    assert d2.fallback == ""
