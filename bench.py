@@ -8,12 +8,13 @@ braking envelope, manipulability, learned self-collision MLP), Halton +
 B-spline sampling, FP32 fused rollout. A "step" is one Controller.control_step
 (shift + sample + rollout/costs + MLP + weights/update + command).
 
-* value: mean device time of the step's CUDA-graph replay (CUDA events on the
-  plan stream), L2 flushed (256 MiB memset) before every timed step.
+* value: mean device time of the lean step graph's replay (two CUDA events on
+  the plan stream around it), L2 flushed (256 MiB memset) before every step.
 * e2e: mean wall time of Controller.control_step (the public API) with host
-  buffers: H2D of the joint state, graph replay, D2H of command + status.
-* roofline: dominant kernel of the step, timed by event-record nodes inside
-  the same timed graph replays.
+  buffers: H2D of the joint state, graph replay, mapped D2H of command + status.
+* roofline / stage_ms: per-kernel device times from a second timed pass over
+  the instrumented copy of the graph (event-record nodes between the stages;
+  `instrumented_step_ms` is that pass's step time — the nodes cost ~3.5 us each).
 * cpu_baseline: the unmodified reference (oracle/_ref, numba backend) timed
   on this host on a bounded sample of the same workload.
 
@@ -64,6 +65,31 @@ class ClockSampler:
         self.lines = []
 
     def __enter__(self):
+        # NVML polled from a thread every 5 ms (nvidia-smi's -lms floor is too coarse
+        # for sub-second timed regions); nvidia-smi is the fallback
+        self._stop = threading.Event()
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.gpu)
+            bits = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20,
+                    "sw_power_cap": 0x4}
+
+            def poll():
+                mx = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+                while not self._stop.is_set():
+                    sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+                    r = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                    act = ["Active" if r & b else "Not Active" for b in bits.values()]
+                    self.lines.append(f"{sm}, {mx}, {r}, " + ", ".join(act))
+                    time.sleep(0.005)
+
+            self.t = threading.Thread(target=poll, daemon=True)
+            self.t.start()
+            return self
+        except Exception:
+            pass
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
@@ -79,6 +105,9 @@ class ClockSampler:
             self.lines.append(line.strip())
 
     def __exit__(self, *exc):
+        self._stop.set()
+        if getattr(self, "t", None) is not None and self.proc is None:
+            self.t.join(timeout=1)
         if self.proc is not None:
             self.proc.terminate()
             try:
@@ -224,41 +253,54 @@ def run_ours(args):
     config = 1 if args.workload == "c1" else 2
     ctrl = configs.make_controller(config, particles=particles, device=local, precision=args.precision)
     plan = ctrl.plan
-    plan.profile_stages(True)  # stage times from the event nodes of the timed replays
     st = configs.start_state()
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=f"cuda:{local}")
 
     for _ in range(max(3, args.warmup)):
         ctrl.control_step(st)
 
-    # ---- device-timed loop (value): graph replay between CUDA events, L2 flushed before each step
-    dev_ms, stages = [], {"sample": [], "rollout": [], "mlp": [], "update": []}
+    # ---- device-timed loop (value): the lean step graph between two CUDA
+    # events on the plan stream, L2 flushed before each step
+    theta = st.theta[None, :]
+    thetad = st.theta_dot[None, :]
+    plan.profile_stages(1)
+    dev_ms = []
     if dist is not None:
         dist.barrier()
     torch.cuda.synchronize()
-    theta = st.theta[None, :]
-    thetad = st.theta_dot[None, :]
     with ClockSampler(local) as clk:
         t_wall0 = time.perf_counter()
         for _ in range(args.steps):
             _flush_l2(flush)
             torch.cuda.synchronize()
             _, infos = plan.step(theta, thetad)
-            inf = infos[0]
-            dev_ms.append(inf.device_ms)
-            stages["sample"].append(inf.sample_ms)
-            stages["rollout"].append(inf.rollout_ms)
-            stages["mlp"].append(inf.mlp_ms)
-            stages["update"].append(inf.update_ms)
+            dev_ms.append(infos[0].device_ms)
         torch.cuda.synchronize()
         t_wall = time.perf_counter() - t_wall0
     if dist is not None:
         dist.barrier()
+    # ---- kernel attribution: the same steps through the instrumented graph
+    # (event-record nodes between the stages), separately timed
+    plan.profile_stages(2)
+    for _ in range(3):
+        plan.step(theta, thetad)
+    stages = {"sample": [], "rollout": [], "mlp": [], "update": []}
+    prof_ms = []
+    for _ in range(args.steps):
+        _flush_l2(flush)
+        torch.cuda.synchronize()
+        _, infos = plan.step(theta, thetad)
+        inf = infos[0]
+        prof_ms.append(inf.device_ms)
+        stages["sample"].append(inf.sample_ms)
+        stages["rollout"].append(inf.rollout_ms)
+        stages["mlp"].append(inf.mlp_ms)
+        stages["update"].append(inf.update_ms)
+    plan.profile_stages(0)
     value_local = float(np.mean(dev_ms))
     value = _max_over_ranks(dist, value_local, local)
 
-    # ---- end to end through the public API (Controller.control_step, host buffers)
-    plan.profile_stages(False)  # e2e: no extra host calls on the step path
+    # ---- end to end through the public API (Controller.control_step, host buffers), lean graph
     e2e = []
     for _ in range(args.steps):
         _flush_l2(flush)
@@ -291,6 +333,7 @@ def run_ours(args):
         "particle_steps_per_s": ws * particles * 30 / (value * 1e-3),
         "median_ms": float(np.median(dev_ms)), "p99_ms": float(np.percentile(dev_ms, 99)),
         "stage_ms": st_mean,
+        "instrumented_step_ms": float(np.mean(prof_ms)),
         "e2e": {"value": e2e_v, "unit": "ms", "h2d_bytes_per_step": 2 * 7 * 8,
                 "d2h_bytes_per_step": 7 * 8 + 80, "median_ms": float(np.median(e2e)),
                 "api": "Controller.control_step"},
@@ -336,7 +379,7 @@ def run_batched(args):
     bc = BatchedController(load_chain("arm7.chain"), goals, weights=configs.make_weights(2),
                            self_collision=load_arm7_surrogate(), precision=args.precision, device=local, **kw)
     thd = np.zeros_like(th0)
-    bc.plan.profile_stages(True)
+    bc.plan.profile_stages(2)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=f"cuda:{local}")
     for _ in range(max(3, args.warmup)):
         bc.control_step(th0, thd)
@@ -359,7 +402,7 @@ def run_batched(args):
     units = B * args.particles * 30
     value = units / (step_ms * 1e-3)
     e2e = []
-    bc.plan.profile_stages(False)
+    bc.plan.profile_stages(0)
     for _ in range(max(3, args.steps // 4)):
         _flush_l2(flush)
         torch.cuda.synchronize()
@@ -415,7 +458,7 @@ def run_tracking(args):
     kw["particles"] = args.particles
     ctrl = Controller(load_chain("arm7.chain"), target_at(script, 0.0), weights=configs.make_weights(3),
                       world=world, precision=args.precision, device=local, **kw)
-    ctrl.profile_stages(True)
+    ctrl.profile_stages(2)
     st = configs.start_state()
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=f"cuda:{local}")
     dev_ms, e2e, stages = [], [], {"sample": [], "rollout": [], "mlp": [], "update": []}
@@ -539,7 +582,7 @@ def _scale_roofline(args, local, peaks, peaks_kind, instances=256, steps=5):
     kw.pop("seed")
     bc = BatchedController(load_chain("arm7.chain"), goals, weights=configs.make_weights(2),
                            self_collision=load_arm7_surrogate(), precision=args.precision, device=local, **kw)
-    bc.plan.profile_stages(True)
+    bc.plan.profile_stages(2)
     thd = np.zeros_like(th0)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=f"cuda:{local}")
     for _ in range(3):

@@ -284,10 +284,13 @@ int mppi_evaluate(mppi_plan* plan, int32_t mode, int32_t n, int32_t horizon,
  * (plan created with dump = 1), plus the particle weights (N,). */
 int mppi_get_bundle(mppi_plan* plan, mppi_eval_out* out, double* weights);
 
-/* Per-stage device times (mppi_step_info.*_ms) are read back from the
- * event-record nodes of the step graph only when enabled (default off: each
- * read is a host call on the critical path). */
-int mppi_profile_stages(mppi_plan* plan, int32_t enable);
+/* Step timing level. 0 (default): the lean step graph, no timing calls on the
+ * latency path. 1: two stream events around the lean graph fill
+ * mppi_step_info.device_ms. 2: an instrumented copy of the graph with
+ * event-record nodes between the stages fills sample/rollout/mlp/update_ms
+ * (the nodes serialise the replay and cost ~3.5 us each, so level 2 is for
+ * attributing time to kernels, not for measuring the step). */
+int mppi_profile_stages(mppi_plan* plan, int32_t level);
 
 /* Benchmark hook: launch one stage of the step `reps` times back to back on
  * the plan stream between two CUDA events and report the mean device time per

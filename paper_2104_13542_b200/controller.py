@@ -188,10 +188,11 @@ class Controller:
         self._plan.set_goal(R, t, g.mode_code, 0)
         self._goal_uploaded = (g, g.mode, np.array(t, dtype=np.float64), np.array(R, dtype=np.float64))
 
-    def profile_stages(self, enable: bool = True):
-        """Fill StepDiagnostics.sample_ms / rollout_ms / update_ms from the
-        event-record nodes of the step graph (costs a few host calls per step)."""
-        self._plan.profile_stages(enable)
+    def profile_stages(self, level: int = 2):
+        """Fill StepDiagnostics.sample_ms / rollout_ms / update_ms from device
+        events (level 2: instrumented graph with per-stage events; 1: whole-step
+        device time; 0: off, the default)."""
+        self._plan.profile_stages(int(level))
 
     # ---------------------------------------------------------------- hot path
     def control_step(self, state: JointState) -> tuple[np.ndarray, StepDiagnostics]:

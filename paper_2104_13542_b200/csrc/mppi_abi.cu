@@ -181,11 +181,11 @@ struct mppi_plan {
   mppi_step_info* m_info = nullptr;
   std::vector<double> goal_host;
   // graph
-  cudaGraphExec_t graph = nullptr;
+  cudaGraphExec_t graph = nullptr;       // lean step graph (production)
+  cudaGraphExec_t graph_prof = nullptr;  // same step + event-record nodes between the stages
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   std::vector<cudaEvent_t> stage_ev;
-  bool stage_events = true;
-  bool want_stages = false;  // read the per-stage event times back after each step (mppi_profile_stages)
+  int profile_level = 0;  // 0 none, 1 device time of the lean graph, 2 instrumented graph (stage times)
   unsigned long long step_counter = 0;
   int sharded_iter = 0;
   // eval scratch
@@ -210,7 +210,9 @@ int set_device(mppi_plan* p) {
 
 void invalidate_graph(mppi_plan* p) {
   if (p->graph) cudaGraphExecDestroy(p->graph);
+  if (p->graph_prof) cudaGraphExecDestroy(p->graph_prof);
   p->graph = nullptr;
+  p->graph_prof = nullptr;
 }
 
 template <typename R>
@@ -379,18 +381,15 @@ int enqueue_sampling(mppi_plan* p, int it, cudaStream_t st) {
   return MPPI_OK;
 }
 
-int enqueue_step_body(mppi_plan* p, cudaStream_t st) {
+int enqueue_step_body(mppi_plan* p, cudaStream_t st, bool stage_events) {
   const int B = p->B, D = p->D;
   // one H2D node: the (B,2d) state followed by the step counter (pseudorandom
   // generator). Status words were re-armed by the previous step's finalize.
   CK(cudaMemcpyAsync(p->state.p, p->h_state, sizeof(double) * (B * 2 * D + 1), cudaMemcpyHostToDevice, st));
   // event-record nodes between the stages give per-kernel device times of
   // every replayed step (mppi_step_info.*_ms)
-  static const bool stage_events = [] {
-    const char* e = getenv("MPPI_STAGE_EVENTS");
-    return !(e && e[0] == '0');
-  }();
-  p->stage_events = stage_events;
+  // event-record nodes between the stages (instrumented graph only: each node
+  // serialises the replay, ~3.5 us apiece on B200)
   auto mark = [&](int i) -> int {
     if (stage_events) CK(cudaEventRecordWithFlags(p->stage_ev[i], st, cudaEventRecordExternal));
     return MPPI_OK;
@@ -410,20 +409,21 @@ int enqueue_step_body(mppi_plan* p, cudaStream_t st) {
   return MPPI_OK;
 }
 
-int ensure_graph(mppi_plan* p) {
-  if (p->graph) return MPPI_OK;
+int ensure_graph(mppi_plan* p, bool prof = false) {
+  cudaGraphExec_t* slot = prof ? &p->graph_prof : &p->graph;
+  if (*slot) return MPPI_OK;
   if (p->learned() && !p->mlp_ready)
     return fail(MPPI_E_CONFIG, "learned self-collision selected but mppi_set_mlp was not called");
   cudaGraph_t g = nullptr;
   CK(cudaStreamBeginCapture(p->stream, cudaStreamCaptureModeThreadLocal));
-  int rc = enqueue_step_body(p, p->stream);
+  int rc = enqueue_step_body(p, p->stream, prof);
   cudaError_t e = cudaStreamEndCapture(p->stream, &g);
   if (rc != MPPI_OK) {
     if (g) cudaGraphDestroy(g);
     return rc;
   }
   if (e != cudaSuccess) return fail(MPPI_E_CUDA, std::string("graph capture: ") + cudaGetErrorString(e));
-  e = cudaGraphInstantiate(&p->graph, g, 0);
+  e = cudaGraphInstantiate(slot, g, 0);
   cudaGraphDestroy(g);
   if (e != cudaSuccess) return fail(MPPI_E_CUDA, std::string("graph instantiate: ") + cudaGetErrorString(e));
   return MPPI_OK;
@@ -892,12 +892,14 @@ int mppi_step(mppi_plan* p, const double* theta, const double* theta_dot, double
   }
   // device timing of the replay only when profiling: on the latency path every
   // extra runtime call is host time between the state and the command
-  if (p->want_stages) CK(cudaEventRecord(p->ev0, p->stream));
-  CK(cudaGraphLaunch(p->graph, p->stream));
-  if (p->want_stages) CK(cudaEventRecord(p->ev1, p->stream));
+  const bool prof = p->profile_level >= 2;
+  if (prof) CKR(ensure_graph(p, true));
+  if (p->profile_level) CK(cudaEventRecord(p->ev0, p->stream));
+  CK(cudaGraphLaunch(prof ? p->graph_prof : p->graph, p->stream));
+  if (p->profile_level) CK(cudaEventRecord(p->ev1, p->stream));
   CK(cudaStreamSynchronize(p->stream));
   float ms = 0.f;
-  if (p->want_stages) CK(cudaEventElapsedTime(&ms, p->ev0, p->ev1));
+  if (p->profile_level) CK(cudaEventElapsedTime(&ms, p->ev0, p->ev1));
   memcpy(command_out, p->h_cmd, sizeof(double) * B * D);
   if (p->dbg.p) {  // debug: stats-kernel phase timeline of instance 0, relative to block 0 start
     std::vector<unsigned long long> t((size_t)16 * p->nblk);
@@ -913,7 +915,7 @@ int mppi_step(mppi_plan* p, const double* theta, const double* theta_dot, double
   if (info) {
     memcpy(info, p->h_info, sizeof(mppi_step_info) * B);
     double stg[4] = {0, 0, 0, 0};
-    for (int it = 0; it < ((p->stage_events && p->want_stages) ? p->iters : 0); ++it)
+    for (int it = 0; it < (prof ? p->iters : 0); ++it)
       for (int sg = 0; sg < 4; ++sg) {
         float t = 0.f;
         CK(cudaEventElapsedTime(&t, p->stage_ev[4 * it + sg], p->stage_ev[4 * it + sg + 1]));
@@ -1062,7 +1064,7 @@ int mppi_get_bundle(mppi_plan* p, mppi_eval_out* out, double* weights) {
 
 int mppi_profile_stages(mppi_plan* p, int32_t enable) {
   if (!p) return fail(MPPI_E_BAD_ARGUMENT, "null plan");
-  p->want_stages = enable != 0;
+  p->profile_level = enable < 0 ? 0 : (enable > 2 ? 2 : enable);
   return MPPI_OK;
 }
 

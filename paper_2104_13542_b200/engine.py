@@ -233,9 +233,10 @@ class Plan:
             N.check(rc)
         return self._cmd.copy(), self._info
 
-    def profile_stages(self, enable: bool = True):
-        """Read the per-stage event times of every step back into StepInfo."""
-        N.check(self.lib.mppi_profile_stages(self.handle, int(bool(enable))))
+    def profile_stages(self, level: int = 2):
+        """0: lean graph, no timing; 1: device_ms of the lean graph; 2: the
+        instrumented graph with per-stage event times (see mppi_profile_stages)."""
+        N.check(self.lib.mppi_profile_stages(self.handle, int(level)))
 
     def evaluate(self, mode: int, inputs0, inputs1, dts, gamma, terminal_weight, theta0=None,
                  theta_dot0=None, want=("positions", "velocities", "accelerations", "step_costs",

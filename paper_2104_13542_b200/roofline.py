@@ -44,6 +44,9 @@ def step_roofline(stage_ms: dict, rows: int, particles: int, horizon: int, dof: 
     event-record nodes of the timed graph replays)."""
     stage = max(("rollout", "mlp", "update"), key=lambda k: stage_ms.get(k, 0.0))
     t = stage_ms[stage] * 1e-3
+    if not t > 0.0:  # stage events disabled (MPPI_STAGE_EVENTS=0): no per-kernel time
+        return {"kernel": None, "bound": None, "achieved": None, "peak": None, "unit": None, "frac": None,
+                "traffic": None, "note": "stage events disabled"}
     sm_mhz = peaks.get("sm_max_mhz", 1965.0)
     if stage == "mlp":
         achieved = MLP_TENSOR_FLOPS_PER_ROW * rows / t / 1e12
