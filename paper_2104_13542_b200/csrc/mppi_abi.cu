@@ -280,8 +280,11 @@ void stats_static(mppi_plan* p, int H, double gamma, double tw, StatsArgs<R>& s)
 
 void choose_blocks(int N, int& ppb, int& nblk) {
   // 32 particles per block (latency: more blocks pull eps/step costs in
-  // parallel), at most 296 blocks per instance (the combine is linear in it)
+  // parallel); up to 1024 particles grow the block to keep one <= 16-CTA
+  // cluster per instance (stats_cluster_kernel); beyond that at most 296
+  // blocks per instance (the record combine is linear in it)
   ppb = 32;
+  if (N > 16 * 32 && N <= 16 * 64) ppb = (N + 15) / 16;
   nblk = (N + ppb - 1) / ppb;
   if (nblk > 296) {
     nblk = 296;

@@ -15,6 +15,8 @@
 //                     (policy.py:170-177).
 #pragma once
 
+#include <cooperative_groups.h>
+
 #include "mppi_common.cuh"
 
 namespace mppi {
@@ -844,6 +846,211 @@ __global__ void __launch_bounds__(kStatsThreads) stats_kernel(const __grid_const
       a.dump_weights[n] = isfinite(t) ? exp(-(t - m) / a.beta) : 0.0;
     }
   }
+}
+
+// Cluster statistics (latency path, N <= 16 * kClusterMaxPPB): the nblk <= 16
+// CTAs of one instance form one thread-block cluster. They agree on the global
+// best finite total through distributed shared memory BEFORE computing
+// weights (so weights are exactly exp(-(c - min)/beta), policy.py:113-114, with
+// no rescaling), and the rank-0 CTA reduces the per-CTA statistics straight out
+// of its peers' shared memory: no global records, fences, atomics or last-block
+// hand-off. Cluster barriers replace the grid-level round trips.
+constexpr int kClusterMax = 16;
+constexpr int kClusterMaxPPB = 64;
+
+template <typename R, int D>
+__global__ void __launch_bounds__(kStatsThreads) stats_cluster_kernel(const __grid_constant__ StatsArgs<R> a) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cluster = cg::this_cluster();
+  extern __shared__ __align__(16) double sm[];
+  const int b = blockIdx.y;
+  const int blk = (int)cluster.block_rank();
+  const int nblk = (int)cluster.num_blocks();
+  const int H = a.H, HD = H * D, N = a.N;
+  const int n0 = blk * a.ppb;
+  const int cnt = max(0, min(N, n0 + a.ppb) - n0);
+  double* tot = sm;                 // [ppb]
+  double* wt = tot + a.ppb;         // [ppb]
+  double* red = wt + a.ppb;         // [32]
+  double* part = red + 32;          // [2*HD] this CTA's S1 | S2
+  double* head = part + 2 * HD;     // [8]: local min, S0, count, sumfinite
+  double* rec = head + 8;           // [kRecHead + 2*HD] (rank 0: the combined record)
+  double* emp = rec + kRecHead + 2 * HD;  // [HD]
+  int* nz = reinterpret_cast<int*>(emp + HD);  // [ppb]
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int status0 = a.status[b];
+  const bool failed = status0 != 0;
+
+  double mo_pre = 0.0, so_pre = 0.0;
+  if (threadIdx.x < HD) {
+    const int h = threadIdx.x / D, j = threadIdx.x - h * D;
+    const int hs = a.shift ? h + 1 : h;
+    mo_pre = hs < H ? a.means[(size_t)b * HD + hs * D + j] : a.tail_mean;
+    so_pre = hs < H ? a.sd[(size_t)b * HD + hs * D + j] : a.tail_sd;
+  }
+
+  // ---- totals (rollout.py:111-171), 4 particles per warp, loads batched -----
+  {
+    constexpr int PA = 4;
+    for (int i0 = wid * PA; i0 < cnt; i0 += nw * PA) {
+      double cv[PA], dv[PA];
+#pragma unroll
+      for (int u = 0; u < PA; ++u) {
+        cv[u] = 0.0;
+        dv[u] = 0.0;
+        if (i0 + u < cnt && lane < H) {
+          const size_t m = ((size_t)b * N + n0 + i0 + u) * H + lane;
+          cv[u] = (double)a.step[m];
+          if (a.learned) dv[u] = (double)a.mlp_d[m];
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < PA; ++u) {
+        const int i = i0 + u;
+        if (i >= cnt) break;
+        const int n = n0 + i;
+        double c = 0.0, dself = 0.0;
+        bool fin = true;
+        if (lane < H) {
+          c = cv[u];
+          if (a.learned) {
+            dself = dv[u] > 0.0 ? dv[u] : 0.0;
+            c = c + a.a_coll * dself;
+          }
+          fin = isfinite(c);
+        }
+        const bool allfin = __all_sync(0xffffffffu, fin);
+        double contrib = 0.0;
+        if (lane < H) contrib = (lane < H - 1 ? a.disc[lane] : a.dlast) * c;
+        double total = warp_sum(contrib);
+        if (!allfin) total = CUDART_INF;
+        if (lane == 0) {
+          tot[i] = total;
+          if (a.totals) a.totals[(size_t)b * N + n] = total;
+        }
+        if (b == 0 && lane < H) {
+          if (a.dump_step) a.dump_step[(size_t)n * H + lane] = allfin ? c : 0.0;
+          if (a.dump_terms && a.learned) a.dump_terms[(size_t)T_SELF * N * H + (size_t)n * H + lane] = dself;
+        }
+      }
+    }
+  }
+  __syncthreads();
+  // ---- cluster-wide best finite total ---------------------------------------
+  double mloc = CUDART_INF;
+  for (int i = threadIdx.x; i < cnt; i += blockDim.x)
+    if (isfinite(tot[i])) mloc = fmin(mloc, tot[i]);
+  mloc = block_min_d(mloc, red);
+  if (threadIdx.x == 0) head[0] = mloc;
+  cluster.sync();
+  double m = CUDART_INF;
+  if (wid == 0) {
+    double v = lane < nblk ? *cluster.map_shared_rank(&head[0], lane) : CUDART_INF;
+    for (int off = 16; off > 0; off >>= 1) v = fmin(v, __shfl_xor_sync(0xffffffffu, v, off));
+    if (lane == 0) red[0] = v;
+  }
+  __syncthreads();
+  m = red[0];
+  // ---- weights (policy.py:103-121), compaction, local sums ------------------
+  for (int i = threadIdx.x; i < cnt; i += blockDim.x)
+    wt[i] = (!failed && isfinite(tot[i])) ? exp(-(tot[i] - m) / a.beta) : 0.0;
+  __syncthreads();
+  __shared__ int s_nnz;
+  if (wid == 0) {
+    int base = 0;
+    for (int c0 = 0; c0 < cnt; c0 += 32) {
+      const int i = c0 + lane;
+      const bool keep = i < cnt && wt[i] > 0.0;
+      const unsigned bal = __ballot_sync(0xffffffffu, keep);
+      if (keep) nz[base + __popc(bal & ((1u << lane) - 1u))] = i;
+      base += __popc(bal);
+    }
+    if (lane == 0) s_nnz = base;
+  } else if (wid == 1) {
+    double s0 = 0.0, c = 0.0, sf = 0.0;
+    for (int i = lane; i < cnt; i += 32) {
+      s0 += wt[i];
+      if (isfinite(tot[i])) {
+        c += 1.0;
+        sf += tot[i];
+      }
+    }
+    s0 = warp_sum(s0);
+    c = warp_sum(c);
+    sf = warp_sum(sf);
+    if (lane == 0) {
+      head[1] = s0;
+      head[2] = c;
+      head[3] = sf;
+    }
+  }
+  __syncthreads();
+  const int nnz = s_nnz;
+  // ---- weighted sufficient statistics around the old mean -------------------
+  if (threadIdx.x < HD) {
+    const int o = threadIdx.x;
+    double s1 = 0.0, s2 = 0.0;
+    if (!failed) {
+      const double* ep = a.eps + (size_t)n0 * HD + o;
+      constexpr int PD = 16;
+      for (int k0 = 0; k0 < nnz; k0 += PD) {
+        double e[PD];
+        int ii[PD];
+#pragma unroll
+        for (int u = 0; u < PD; ++u) {
+          ii[u] = k0 + u < nnz ? nz[k0 + u] : -1;
+          e[u] = ii[u] >= 0 ? __ldg(ep + (size_t)ii[u] * HD) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < PD; ++u) {
+          if (ii[u] < 0) break;
+          const int ng = n0 + ii[u] + a.particle_offset;
+          const double dv = ng < a.null_count ? 0.0 - mo_pre
+                                              : (ng == a.null_count ? 0.0 : (mo_pre + so_pre * e[u]) - mo_pre);
+          const double w = wt[ii[u]];
+          s1 += w * dv;
+          s2 += w * dv * dv;
+        }
+      }
+    }
+    part[o] = s1;
+    part[HD + o] = s2;
+  }
+  if (b == 0 && a.dump_weights && !failed)
+    for (int i = threadIdx.x; i < cnt; i += blockDim.x) a.dump_weights[n0 + i] = wt[i];
+  cluster.sync();
+  // ---- rank 0 reduces the cluster's statistics in rank order ----------------
+  if (blk == 0) {
+    double* out = a.finalize_inline ? rec : a.out_record + (size_t)b * (kRecHead + 2 * HD);
+    for (int o = threadIdx.x; o < 2 * HD; o += blockDim.x) {
+      double v[kClusterMax];
+#pragma unroll
+      for (int k = 0; k < kClusterMax; ++k) v[k] = k < nblk ? *cluster.map_shared_rank(&part[o], k) : 0.0;
+      double s = 0.0;
+#pragma unroll
+      for (int k = 0; k < kClusterMax; ++k)
+        if (k < nblk) s += v[k];
+      out[kRecHead + o] = s;
+    }
+    if (threadIdx.x == 0) {
+      double s0 = 0.0, c = 0.0, sf = 0.0;
+      for (int k = 0; k < nblk; ++k) {
+        const double* hk = cluster.map_shared_rank(head, k);
+        s0 += hk[1];
+        c += hk[2];
+        sf += hk[3];
+      }
+      out[0] = c > 0.0 ? m : CUDART_INF;
+      out[1] = s0;
+      out[2] = c;
+      out[3] = sf;
+      out[4] = (double)status0;
+      out[5] = (double)a.bad[b];
+    }
+  }
+  cluster.sync();  // peers' shared memory stays alive until rank 0 has read it
+  if (blk != 0 || !a.finalize_inline) return;
+  finalize_policy(a, b, rec, emp);
 }
 
 // Finalize from R rank records (config 5, after the all-gather).

@@ -3,6 +3,8 @@
 // mppi_launch_f64.cu) so the eight dof variants compile in parallel.
 #pragma once
 
+#include <cstdlib>
+
 #include "mppi_kernels.cuh"
 
 namespace mppi {
@@ -35,7 +37,35 @@ cudaError_t launch_rollout_d(const RolloutArgs<R>& a, long long warps, cudaStrea
 }
 
 template <typename R, int D>
+cudaError_t launch_stats_cluster_d(const StatsArgs<R>& s, cudaStream_t st) {
+  const int HD = s.H * D;
+  const size_t smem = sizeof(double) * (2 * (size_t)s.ppb + 32 + 2 * HD + 8 + kRecHead + 2 * HD + HD) +
+                      sizeof(int) * (size_t)s.ppb;
+  auto kern = stats_cluster_kernel<R, D>;
+  if (s.nblk > 8) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (e != cudaSuccess) return e;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(s.nblk, s.B, 1);
+  cfg.blockDim = dim3(kStatsThreads, 1, 1);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = s.nblk;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, s);
+}
+
+template <typename R, int D>
 cudaError_t launch_stats_d(const StatsArgs<R>& s, cudaStream_t st) {
+  // latency path: one cluster per instance when the particles fit 16 CTAs
+  if (!s.totals_only && s.nblk <= kClusterMax && s.ppb <= kClusterMaxPPB && getenv("MPPI_NO_CLUSTER") == nullptr)
+    return launch_stats_cluster_d<R, D>(s, st);
   const size_t smem = stats_smem_bytes(s.ppb, s.nblk, s.H * D);
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(stats_kernel<R, D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
