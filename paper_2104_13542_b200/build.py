@@ -24,7 +24,7 @@ OBJ = ROOT / "build" / "obj"
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
-         f"-I{ROOT / 'include'}"]
+         f"-I{ROOT / 'include'}"] + os.environ.get("MPPI_NVCC_FLAGS", "").split()
 SOURCES = ["mppi_abi.cu", "mppi_launch_f32.cu", "mppi_launch_f64.cu"]
 
 

@@ -660,6 +660,7 @@ __global__ void __launch_bounds__(kStatsThreads) stats_kernel(const __grid_const
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const bool failed = (a.status[b] != 0);
 #ifdef MPPI_DEBUG_TIMERS
+#undef MPPI_STAMP
 #define MPPI_STAMP(k)                                                                        \
   if (a.dbg && threadIdx.x == 0 && b == 0) {                                                  \
     unsigned long long t_;                                                                   \
@@ -880,6 +881,7 @@ __global__ void __launch_bounds__(kStatsThreads) stats_cluster_kernel(const __gr
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const int status0 = a.status[b];
   const bool failed = status0 != 0;
+  MPPI_STAMP(0);
 
   double mo_pre = 0.0, so_pre = 0.0;
   if (threadIdx.x < HD) {
@@ -890,6 +892,9 @@ __global__ void __launch_bounds__(kStatsThreads) stats_cluster_kernel(const __gr
   }
 
   // ---- totals (rollout.py:111-171), 4 particles per warp, loads batched -----
+  // the discount row is read per lane: take it from a register, not from the
+  // (address-serialising) constant bank inside the loop
+  const double disc_l = lane < H - 1 ? a.disc[lane] : a.dlast;
   {
     constexpr int PA = 4;
     for (int i0 = wid * PA; i0 < cnt; i0 += nw * PA) {
@@ -921,7 +926,7 @@ __global__ void __launch_bounds__(kStatsThreads) stats_cluster_kernel(const __gr
         }
         const bool allfin = __all_sync(0xffffffffu, fin);
         double contrib = 0.0;
-        if (lane < H) contrib = (lane < H - 1 ? a.disc[lane] : a.dlast) * c;
+        if (lane < H) contrib = disc_l * c;
         double total = warp_sum(contrib);
         if (!allfin) total = CUDART_INF;
         if (lane == 0) {
@@ -936,6 +941,7 @@ __global__ void __launch_bounds__(kStatsThreads) stats_cluster_kernel(const __gr
     }
   }
   __syncthreads();
+  MPPI_STAMP(1);
   // ---- cluster-wide best finite total ---------------------------------------
   double mloc = CUDART_INF;
   for (int i = threadIdx.x; i < cnt; i += blockDim.x)
@@ -951,6 +957,7 @@ __global__ void __launch_bounds__(kStatsThreads) stats_cluster_kernel(const __gr
   }
   __syncthreads();
   m = red[0];
+  MPPI_STAMP(2);
   // ---- weights (policy.py:103-121), compaction, local sums ------------------
   for (int i = threadIdx.x; i < cnt; i += blockDim.x)
     wt[i] = (!failed && isfinite(tot[i])) ? exp(-(tot[i] - m) / a.beta) : 0.0;
@@ -986,13 +993,14 @@ __global__ void __launch_bounds__(kStatsThreads) stats_cluster_kernel(const __gr
   }
   __syncthreads();
   const int nnz = s_nnz;
+  MPPI_STAMP(3);
   // ---- weighted sufficient statistics around the old mean -------------------
   if (threadIdx.x < HD) {
     const int o = threadIdx.x;
     double s1 = 0.0, s2 = 0.0;
     if (!failed) {
       const double* ep = a.eps + (size_t)n0 * HD + o;
-      constexpr int PD = 16;
+      constexpr int PD = 32;
       for (int k0 = 0; k0 < nnz; k0 += PD) {
         double e[PD];
         int ii[PD];
@@ -1018,7 +1026,9 @@ __global__ void __launch_bounds__(kStatsThreads) stats_cluster_kernel(const __gr
   }
   if (b == 0 && a.dump_weights && !failed)
     for (int i = threadIdx.x; i < cnt; i += blockDim.x) a.dump_weights[n0 + i] = wt[i];
+  MPPI_STAMP(4);
   cluster.sync();
+  MPPI_STAMP(5);
   // ---- rank 0 reduces the cluster's statistics in rank order ----------------
   if (blk == 0) {
     double* out = a.finalize_inline ? rec : a.out_record + (size_t)b * (kRecHead + 2 * HD);
@@ -1032,25 +1042,33 @@ __global__ void __launch_bounds__(kStatsThreads) stats_cluster_kernel(const __gr
         if (k < nblk) s += v[k];
       out[kRecHead + o] = s;
     }
-    if (threadIdx.x == 0) {
+    if (wid == 7) {  // one lane per peer CTA, then a fixed-order warp tree
       double s0 = 0.0, c = 0.0, sf = 0.0;
-      for (int k = 0; k < nblk; ++k) {
-        const double* hk = cluster.map_shared_rank(head, k);
-        s0 += hk[1];
-        c += hk[2];
-        sf += hk[3];
+      if (lane < nblk) {
+        const double* hk = cluster.map_shared_rank(head, lane);
+        s0 = hk[1];
+        c = hk[2];
+        sf = hk[3];
       }
-      out[0] = c > 0.0 ? m : CUDART_INF;
-      out[1] = s0;
-      out[2] = c;
-      out[3] = sf;
-      out[4] = (double)status0;
-      out[5] = (double)a.bad[b];
+      s0 = warp_sum(s0);
+      c = warp_sum(c);
+      sf = warp_sum(sf);
+      if (lane == 0) {
+        out[0] = c > 0.0 ? m : CUDART_INF;
+        out[1] = s0;
+        out[2] = c;
+        out[3] = sf;
+        out[4] = (double)status0;
+        out[5] = (double)a.bad[b];
+      }
     }
   }
   cluster.sync();  // peers' shared memory stays alive until rank 0 has read it
+  MPPI_STAMP(6);
   if (blk != 0 || !a.finalize_inline) return;
   finalize_policy(a, b, rec, emp);
+  __syncthreads();
+  MPPI_STAMP(7);
 }
 
 // Finalize from R rank records (config 5, after the all-gather).

@@ -64,7 +64,8 @@ cudaError_t launch_stats_cluster_d(const StatsArgs<R>& s, cudaStream_t st) {
 template <typename R, int D>
 cudaError_t launch_stats_d(const StatsArgs<R>& s, cudaStream_t st) {
   // latency path: one cluster per instance when the particles fit 16 CTAs
-  if (!s.totals_only && s.nblk <= kClusterMax && s.ppb <= kClusterMaxPPB && getenv("MPPI_NO_CLUSTER") == nullptr)
+  if (!s.totals_only && s.B <= 8 && s.nblk <= kClusterMax && s.ppb <= kClusterMaxPPB &&
+      getenv("MPPI_NO_CLUSTER") == nullptr)
     return launch_stats_cluster_d<R, D>(s, st);
   const size_t smem = stats_smem_bytes(s.ppb, s.nblk, s.H * D);
   if (smem > 48 * 1024) {
