@@ -12,6 +12,7 @@
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <type_traits>
 #include <vector>
 
 #include "mppi_aux_kernels.cuh"
@@ -308,6 +309,8 @@ int enqueue_iteration(mppi_plan* p, int it, bool inline_final, double* out_recor
   a.shift = it == 0;
   a.check_var = 1;
   a.skip_on_status = 1;
+  a.pdl_early = (pdl_mask() & PDL_EARLY) ? 1 : 0;
+  a.dbg = p->dbg.p ? p->dbg.p + 16 * p->nblk : nullptr;
   a.tail_mean = p->tail;
   a.tail_sd = std::sqrt(p->sigma0_sq);
   a.eps = p->eps.p;
@@ -325,8 +328,27 @@ int enqueue_iteration(mppi_plan* p, int it, bool inline_final, double* out_recor
     a.out_acc = p->d_acc.p;
     a.out_terms = p->d_terms.p;
   }
-  if (stages & 1u) CK(launch_rollout_any<R>(a, p->D, (long long)p->B * p->N, st));
-  if ((stages & 2u) && p->learned()) CK(mlp_forward(p->mlp, p->mlp_x.p, (long long)p->B * p->N * p->H, p->mlp_d.p, st));
+  // Rollout + MLP in one kernel (mppi_fused.cuh) when the particles fit one
+  // wave. Opt-in (MPPI_FUSE=1): measured 1.5-2 us slower per cold-L2 step than
+  // the two kernels on B200.
+  bool fused = false;
+  if constexpr (std::is_same<R, float>::value) {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    fused = p->learned() && getenv("MPPI_FUSE") != nullptr &&
+            ((long long)p->B * p->N + 3) / 4 <= sms && fused_cap_bytes_f32(a) <= 2 * kABuf;
+    if (fused) {
+      a.mlp_x = nullptr;
+      if (stages & 1u) CK(launch_rollout_mlp_any(a, p->D, p->mlp.img, p->mlp_d.p, st));
+    }
+  }
+  if (!fused) {
+    if (stages & 1u) CK(launch_rollout_any<R>(a, p->D, (long long)p->B * p->N, st));
+    if ((stages & 2u) && p->learned())
+      CK(mlp_forward(p->mlp, p->mlp_x.p, (long long)p->B * p->N * p->H, p->mlp_d.p, st,
+                     p->dbg.p ? p->dbg.p + 16 * p->nblk + 16 * 128 : nullptr));
+  }
   StatsArgs<R> s;
   stats_static<R>(p, p->H, p->gamma, p->tw, s);
   s.N = p->N;
@@ -567,8 +589,9 @@ int mppi_plan_create(const mppi_chain_desc* chain, const mppi_cost_desc* costs,
     CK(cudaMemset(p->bad.p, 0x7f, sizeof(int) * B));
     CKR(p->info.alloc(B));
     if (getenv("MPPI_DEBUG_TIMERS")) {
-      CKR(p->dbg.alloc((size_t)16 * p->nblk));
-      CK(cudaMemset(p->dbg.p, 0, sizeof(unsigned long long) * 16 * p->nblk));
+      // stats phases (16 per stats block) + fused rollout/MLP phases (8 per CTA, <= 256 CTAs)
+      CKR(p->dbg.alloc((size_t)16 * p->nblk + 16 * 256));
+      CK(cudaMemset(p->dbg.p, 0, sizeof(unsigned long long) * (16 * p->nblk + 16 * 256)));
     }
     if (p->dump) {
       CKR(p->d_pos.alloc((size_t)N * HD));
@@ -905,9 +928,33 @@ int mppi_step(mppi_plan* p, const double* theta, const double* theta_dot, double
   if (p->profile_level) CK(cudaEventElapsedTime(&ms, p->ev0, p->ev1));
   memcpy(command_out, p->h_cmd, sizeof(double) * B * D);
   if (p->dbg.p) {  // debug: stats-kernel phase timeline of instance 0, relative to block 0 start
-    std::vector<unsigned long long> t((size_t)16 * p->nblk);
+    std::vector<unsigned long long> t((size_t)16 * p->nblk + 16 * 256);
     CK(cudaMemcpy(t.data(), p->dbg.p, sizeof(unsigned long long) * t.size(), cudaMemcpyDeviceToHost));
-    const unsigned long long t0 = t[0];
+    const unsigned long long* f = t.data() + 16 * p->nblk;
+    unsigned long long t0 = t[0];
+    if (f[0]) {  // fused rollout + MLP: phase stamps relative to the earliest CTA start
+      for (int k = 0; k < 256; ++k)
+        if (f[16 * k] && f[16 * k] < t0) t0 = f[16 * k];
+      double mx[12] = {0};
+      for (int k = 0; k < 256; ++k)
+        for (int j = 0; j < 12; ++j)
+          if (f[16 * k + j]) mx[j] = std::max(mx[j], (double)(long long)(f[16 * k + j] - t0) * 1e-3);
+      for (int k : {0, 1, 2, 3, 64, 124}) {
+        fprintf(stderr, "fused blk %3d:", k);
+        for (int j = 0; j < 12; ++j)
+          fprintf(stderr, " %7.2f", f[16 * k + j] ? (double)(long long)(f[16 * k + j] - t0) * 1e-3 : -1.0);
+        fprintf(stderr, "\n");
+      }
+      for (int k : {128, 129, 200}) {
+        fprintf(stderr, "mlp   blk %3d:", k - 128);
+        for (int j = 0; j < 12; ++j)
+          fprintf(stderr, " %7.2f", f[16 * k + j] ? (double)(long long)(f[16 * k + j] - t0) * 1e-3 : -1.0);
+        fprintf(stderr, "\n");
+      }
+      fprintf(stderr, "fused max    :");
+      for (int j = 0; j < 12; ++j) fprintf(stderr, " %7.2f", mx[j]);
+      fprintf(stderr, "\n");
+    }
     for (int k = 0; k < p->nblk; ++k) {
       fprintf(stderr, "stats blk %2d:", k);
       for (int j = 0; j < 8; ++j)

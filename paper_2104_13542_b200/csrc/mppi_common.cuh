@@ -9,6 +9,7 @@
 #include <cuda_runtime.h>
 #include <math_constants.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include "../../include/mppi_b200.h"
 
@@ -227,6 +228,37 @@ __device__ __forceinline__ bool capsule_hits_sphere(const R* P0, const R* P1, R 
   const R ez = P0[2] + t * dz - sph[2];
   return sqrt(ex * ex + ey * ey + ez * ez) < rcap + sph[3];
 }
+
+// ---------------------------------------------------------------- programmatic dependent launch
+// The step's kernels are chained with programmatic stream serialisation: a
+// dependent grid may start (and run its prologue) while its predecessor
+// drains, and blocks in pdl_wait() until the predecessor has completed and its
+// writes are visible. pdl_trigger() lets the dependent grid be scheduled early.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+// host side: which PDL features are on (MPPI_PDL bit mask, A/B switch):
+// 1 = MLP after rollout, 2 = statistics after MLP/rollout, 4 = early triggers
+enum { PDL_MLP = 1, PDL_STATS = 2, PDL_EARLY = 4 };
+inline int pdl_mask() {
+  static const int m = getenv("MPPI_PDL") ? atoi(getenv("MPPI_PDL")) : 0;
+  return m;
+}
+
+// debug phase stamp (globaltimer ns) into dbg[k], compiled in with -DMPPI_DEBUG_TIMERS
+#ifdef MPPI_DEBUG_TIMERS
+#define MPPI_TSTAMP(ptr, k)                                      \
+  do {                                                           \
+    if ((ptr) != nullptr) {                                      \
+      unsigned long long t_;                                     \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));     \
+      (ptr)[k] = t_;                                             \
+    }                                                            \
+  } while (0)
+#else
+#define MPPI_TSTAMP(ptr, k) \
+  do {                      \
+  } while (0)
+#endif
 
 // ---------------------------------------------------------------- warp helpers
 template <typename T>

@@ -37,6 +37,7 @@ struct RolloutArgs {
   int shift;      // read the stored policy through the shift view
   int check_var;  // PolicyStateError check of build_control_batch (sampling.py:282)
   int skip_on_status;
+  int pdl_early;  // trigger the dependent grid at entry
   double tail_mean, tail_sd;
   const double* eps;     // (N,H,d)
   const double* means;   // (B,H,d)
@@ -53,6 +54,7 @@ struct RolloutArgs {
   double* out_vel;
   double* out_acc;
   double* out_terms;     // (6,n,H)
+  unsigned long long* dbg;  // debug phase stamps of the fused kernel (MPPI_DEBUG_TIMERS), else NULL
 };
 
 // Any capsule of this lane's configuration penetrates the world (costs.py:235-240).
@@ -108,16 +110,24 @@ __device__ __forceinline__ bool env_any_hit(const WorldT<R>& w, const ChainT<R>&
   return false;
 }
 
+// Capsule endpoints are staged in shared memory only when a cost term reads
+// them (world collision, capsule self-collision).
+template <typename R>
+__host__ __device__ __forceinline__ bool rollout_needs_caps(const CostT<R>& cs) {
+  return cs.use_env || cs.selfcoll == MPPI_SELFCOLL_ORACLE;
+}
+
+// Rollout + cost stack of particle g (one warp, lane = horizon step h), the
+// body of rollout_kernel and of the fused rollout + MLP kernel. `cap` is this
+// warp's [cap][6][32] staging area; `enc` (16 floats, may be NULL) receives the
+// lane's positional encoding [sin q, cos q, 0...] (surrogate.py:24-28).
+// Returns false when the instance already failed (nothing written).
 template <typename R, int D>
-__global__ void __launch_bounds__(kRolloutWarps * 32)
-    rollout_kernel(const __grid_constant__ RolloutArgs<R> a) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  const long long g = (long long)blockIdx.x * kRolloutWarps + wib;
-  if (g >= (long long)a.B * a.N) return;  // warp-uniform exit
+__device__ __forceinline__ bool rollout_particle(const RolloutArgs<R>& a, long long g, int lane, R* cap,
+                                                 float* enc) {
   const int b = (int)(g / a.N);
   const int n = (int)(g - (long long)b * a.N);
-  if (a.skip_on_status && a.status[b] != 0) return;
+  if (a.skip_on_status && a.status[b] != 0) return false;
   const int H = a.H;
   const bool act = lane < H;
   const int h = act ? lane : H - 1;
@@ -187,8 +197,7 @@ __global__ void __launch_bounds__(kRolloutWarps * 32)
   R tw[3] = {R(0), R(0), R(0)};
   R ja[D][3], jp[D][3];  // Jacobian column data: world axis, joint origin
   R sq[D], cq[D];
-  const int nc = ch.n_caps;
-  R* cap = reinterpret_cast<R*>(smem_raw) + (size_t)wib * nc * 6 * 32;
+  const int nc = rollout_needs_caps(cs) ? ch.n_caps : 0;
 #pragma unroll
   for (int j = 0; j < 3; ++j) {
     ja[0][j] = ch.axes[0][j];
@@ -392,6 +401,13 @@ __global__ void __launch_bounds__(kRolloutWarps * 32)
 #pragma unroll
       for (int k = 2 * D; k < 16; ++k) x[k] = 0.f;
     }
+    if (enc != nullptr) {
+#pragma unroll
+      for (int k = 0; k < D; ++k) {
+        enc[k] = (float)sq[k];
+        enc[D + k] = (float)cq[k];
+      }
+    }
     if (a.out_pos != nullptr && b == 0) {
 #pragma unroll
       for (int j = 0; j < D; ++j) {
@@ -410,6 +426,23 @@ __global__ void __launch_bounds__(kRolloutWarps * 32)
       a.out_terms[T_ENV * nh + o] = (double)envc;
     }
   }
+  return true;
+}
+
+template <typename R, int D>
+__global__ void __launch_bounds__(kRolloutWarps * 32)
+    rollout_kernel(const __grid_constant__ RolloutArgs<R> a) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  if (a.pdl_early) pdl_trigger();  // the MLP / statistics grids may be scheduled as SMs free up
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const long long g = (long long)blockIdx.x * kRolloutWarps + wib;
+  if (g >= (long long)a.B * a.N) return;  // warp-uniform exit
+  unsigned long long* dbg =
+      (a.dbg != nullptr && threadIdx.x == 0 && blockIdx.x < 256) ? a.dbg + 16 * blockIdx.x : nullptr;
+  MPPI_TSTAMP(dbg, 0);
+  R* cap = reinterpret_cast<R*>(smem_raw) + (size_t)wib * a.chain.n_caps * 6 * 32;
+  rollout_particle<R, D>(a, g, lane, cap, nullptr);
+  MPPI_TSTAMP(dbg, 1);
 }
 
 // ============================================================== statistics
@@ -658,6 +691,7 @@ __global__ void __launch_bounds__(kStatsThreads) stats_kernel(const __grid_const
   double* scale = red + 32;     // [max(nblk, 8)] scales + [max(nblk, 8) * kRecHead] heads
   const int reclen = kRecHead + 2 * HD;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  pdl_wait();  // rollout / MLP outputs and the status word are ready past this point
   const bool failed = (a.status[b] != 0);
 #ifdef MPPI_DEBUG_TIMERS
 #undef MPPI_STAMP
@@ -879,10 +913,8 @@ __global__ void __launch_bounds__(kStatsThreads) stats_cluster_kernel(const __gr
   double* emp = rec + kRecHead + 2 * HD;  // [HD]
   int* nz = reinterpret_cast<int*>(emp + HD);  // [ppb]
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  const int status0 = a.status[b];
-  const bool failed = status0 != 0;
-  MPPI_STAMP(0);
-
+  // prologue under the predecessor's tail: the policy was written by the
+  // previous step, not by the kernels this one depends on
   double mo_pre = 0.0, so_pre = 0.0;
   if (threadIdx.x < HD) {
     const int h = threadIdx.x / D, j = threadIdx.x - h * D;
@@ -890,11 +922,16 @@ __global__ void __launch_bounds__(kStatsThreads) stats_cluster_kernel(const __gr
     mo_pre = hs < H ? a.means[(size_t)b * HD + hs * D + j] : a.tail_mean;
     so_pre = hs < H ? a.sd[(size_t)b * HD + hs * D + j] : a.tail_sd;
   }
+  const double disc_pre = lane < H - 1 ? a.disc[lane] : a.dlast;
+  pdl_wait();
+  const int status0 = a.status[b];
+  const bool failed = status0 != 0;
+  MPPI_STAMP(0);
 
   // ---- totals (rollout.py:111-171), 4 particles per warp, loads batched -----
   // the discount row is read per lane: take it from a register, not from the
   // (address-serialising) constant bank inside the loop
-  const double disc_l = lane < H - 1 ? a.disc[lane] : a.dlast;
+  const double disc_l = disc_pre;
   {
     constexpr int PA = 4;
     for (int i0 = wid * PA; i0 < cnt; i0 += nw * PA) {

@@ -15,6 +15,10 @@ template <typename R>
 cudaError_t launch_stats_any(const StatsArgs<R>& s, int D, cudaStream_t st);
 template <typename R>
 cudaError_t launch_finalize(const StatsArgs<R>& s, const double* recs, int count, cudaStream_t st);
+// fused rollout + learned-collision MLP (mppi_fused.cuh), float only
+cudaError_t launch_rollout_mlp_any(const RolloutArgs<float>& a, int D, const unsigned char* img, float* out_d,
+                                   cudaStream_t st);
+size_t fused_cap_bytes_f32(const RolloutArgs<float>& a);
 
 inline size_t stats_smem_bytes(int ppb, int nblk, int HD) {
   return sizeof(double) * (2 * (size_t)ppb + 32 + (size_t)(nblk > 8 ? nblk : 8) * (1 + kRecHead) +
@@ -25,7 +29,7 @@ inline size_t stats_smem_bytes(int ppb, int nblk, int HD) {
 #ifdef MPPI_LAUNCH_IMPL
 template <typename R, int D>
 cudaError_t launch_rollout_d(const RolloutArgs<R>& a, long long warps, cudaStream_t st) {
-  const size_t smem = (size_t)kRolloutWarps * a.chain.n_caps * 6 * 32 * sizeof(R);
+  const size_t smem = rollout_needs_caps(a.cost) ? (size_t)kRolloutWarps * a.chain.n_caps * 6 * 32 * sizeof(R) : 0;
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(rollout_kernel<R, D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem);
@@ -51,13 +55,15 @@ cudaError_t launch_stats_cluster_d(const StatsArgs<R>& s, cudaStream_t st) {
   cfg.blockDim = dim3(kStatsThreads, 1, 1);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = s.nblk;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = (pdl_mask() & PDL_STATS) != 0;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = 2;
   return cudaLaunchKernelEx(&cfg, kern, s);
 }
 
@@ -73,8 +79,17 @@ cudaError_t launch_stats_d(const StatsArgs<R>& s, cudaStream_t st) {
                                          (int)smem);
     if (e != cudaSuccess) return e;
   }
-  stats_kernel<R, D><<<dim3(s.nblk, s.B), kStatsThreads, smem, st>>>(s);
-  return cudaGetLastError();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(s.nblk, s.B, 1);
+  cfg.blockDim = dim3(kStatsThreads, 1, 1);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = (pdl_mask() & PDL_STATS) != 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, stats_kernel<R, D>, s);
 }
 
 #define MPPI_LAUNCH_SWITCH(FN, ...)                 \

@@ -29,6 +29,8 @@
 #pragma once
 
 #include <cuda_fp16.h>
+
+#include "mppi_common.cuh"
 #include <cuda_runtime.h>
 
 #include <cmath>
@@ -232,27 +234,31 @@ __device__ __forceinline__ void epi_barrier() {  // named barrier over the 512 e
 }
 
 // x: (M_pad,16) fp32 positional encodings; out: (M) fp32 distances.
-__global__ void __launch_bounds__(kMlpThreads, 1)
+// 88 registers: 544 x 88 + a 128-thread rollout CTA (128 registers) fit one
+// SM's 64K register file, so with programmatic dependent launch the MLP CTAs
+// become resident next to the rollout and load their weights under it.
+static __global__ void __maxnreg__(88)
     mlp_tcgen05_kernel(const float* __restrict__ x, long long M, const unsigned char* __restrict__ img,
-                       float* __restrict__ out) {
+                       float* __restrict__ out, int early, unsigned long long* dbg_base) {
   extern __shared__ __align__(1024) unsigned char mlp_smem[];
   unsigned char* sm = mlp_smem;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  // debug stamps (MPPI_DEBUG_TIMERS): 0 start, 1 X stored, 2 W0, 3 L1 epi, 4 L2 epi, 5 L3, 6 end
+  unsigned long long* dbg = (dbg_base != nullptr && tid == 0 && blockIdx.x < 128) ? dbg_base + 16 * blockIdx.x : nullptr;
+  MPPI_TSTAMP(dbg, 0);
   const uint32_t sb = smem_u32(sm);
   // barriers: 0-2 weights, 3-4 L1 done (per acc1 buffer), 5-6 L2 done (per A
   // buffer), 7-8 L3 done (per A buffer), 9-10 A ready (per A buffer), 11 X ready
   const uint32_t barW0 = sb + OFF_BAR, barW1 = barW0 + 8, barW2 = barW0 + 16;
-  const uint32_t barL1[2] = {barW0 + 24, barW0 + 32};
-  const uint32_t barL2[2] = {barW0 + 40, barW0 + 48};
-  const uint32_t barL3[2] = {barW0 + 56, barW0 + 64};
-  const uint32_t barA[2] = {barW0 + 72, barW0 + 80};
+  // barrier pairs 8 bytes apart, [0] and [1] per buffer
+  const uint32_t barL10 = barW0 + 24, barL20 = barW0 + 40, barL30 = barW0 + 56, barA0 = barW0 + 72;
   const uint32_t barX = barW0 + 88;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sm + OFF_TMEMPTR);
 
   if (tid == 0) {
     for (int i = 0; i < 9; ++i) mbar_init(barW0 + 8 * i, 1);
-    mbar_init(barA[0], kMlpEpiWarps);
-    mbar_init(barA[1], kMlpEpiWarps);
+    mbar_init(barA0, kMlpEpiWarps);
+    mbar_init(barA0 + 8, kMlpEpiWarps);
     mbar_init(barX, kMlpEpiWarps);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     fence_async_smem();
@@ -287,17 +293,19 @@ __global__ void __launch_bounds__(kMlpThreads, 1)
       const uint64_t dAH = umma_desc(sb + OFF_A, 128, 512), dAL = umma_desc(sb + OFF_A + kAHalf, 128, 512);
       const uint64_t dW1H = umma_desc(sb + OFF_W1H, 128, 4096), dW1L = umma_desc(sb + OFF_W1L, 128, 4096);
       const uint64_t dW2H = umma_desc(sb + OFF_W2H, 128, 2048), dW2L = umma_desc(sb + OFF_W2L, 128, 2048);
+      pdl_wait();  // sleep (rather than spin on barX) while the rollout still runs
       auto issue_l1_all = [&]() {  // the whole of layer 1: 8 chunks of N=32, two commits
+#pragma unroll
         for (int c = 0; c < 8; ++c) {
           const uint64_t wo = umma_off(32 * c, 0, 16) >> 4;
           umma_f16(tmem + 32 * c, dXH, dW0H + wo, id32, 0);
           umma_f16(tmem + 32 * c, dXH, dW0L + wo, id32, 1);
           umma_f16(tmem + 32 * c, dXL, dW0H + wo, id32, 1);
-          if (c == 3) umma_commit(barL1[0]);
+          if (c == 3) umma_commit(barL10);
         }
-        umma_commit(barL1[1]);
+        umma_commit(barL10 + 8);
       };
-      uint32_t phA[2] = {0, 0}, phX = 0;
+      uint32_t phA = 0, phX = 0;  // parity bits
       bool first = true;
       for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         const bool has_next = tile + gridDim.x < ntiles;
@@ -308,10 +316,11 @@ __global__ void __launch_bounds__(kMlpThreads, 1)
           tc_fence_after();
           issue_l1_all();
         }
+#pragma unroll
         for (int c = 0; c < 8; ++c) {
           const int bf = c & 1;
-          mbar_wait(barA[bf], phA[bf]);
-          phA[bf] ^= 1;
+          mbar_wait(barA0 + 8 * bf, (phA >> bf) & 1u);
+          phA ^= 1u << bf;
           if (first && c == 0) mbar_wait(barW1, 0);
           tc_fence_after();
           const uint64_t ao = (uint64_t)(bf * kABuf) >> 4;
@@ -322,7 +331,7 @@ __global__ void __launch_bounds__(kMlpThreads, 1)
             umma_f16(acc2, dAH + aj, dW1L + wj, id128, 1);
             umma_f16(acc2, dAL + aj, dW1H + wj, id128, 1);
           }
-          umma_commit(barL2[bf]);
+          umma_commit(barL20 + 8 * bf);
           if (c == 7 && has_next) {  // every acc1 chunk consumed and the next X in smem
             mbar_wait(barX, phX);
             phX ^= 1;
@@ -330,10 +339,11 @@ __global__ void __launch_bounds__(kMlpThreads, 1)
             issue_l1_all();  // runs behind this tile's layer 2, under its layer-2/3 epilogues
           }
         }
+#pragma unroll
         for (int c = 0; c < 4; ++c) {
           const int bf = c & 1;
-          mbar_wait(barA[bf], phA[bf]);
-          phA[bf] ^= 1;
+          mbar_wait(barA0 + 8 * bf, (phA >> bf) & 1u);
+          phA ^= 1u << bf;
           if (first && c == 0) mbar_wait(barW2, 0);
           tc_fence_after();
           const uint64_t ao = (uint64_t)(bf * kABuf) >> 4;
@@ -344,7 +354,7 @@ __global__ void __launch_bounds__(kMlpThreads, 1)
             umma_f16(acc3, dAH + aj, dW2L + wj, id64, 1);
             umma_f16(acc3, dAL + aj, dW2H + wj, id64, 1);
           }
-          umma_commit(barL3[bf]);
+          umma_commit(barL30 + 8 * bf);
         }
         first = false;
       }
@@ -365,7 +375,9 @@ __global__ void __launch_bounds__(kMlpThreads, 1)
     const float* b1 = par + kMlpH0;
     const float* b2 = b1 + kMlpH1;
     const float* w3 = b2 + kMlpH2;
-    uint32_t phL1[2] = {0, 0}, phL2[2] = {0, 0}, phL3[2] = {0, 0};
+    uint32_t phL1 = 0, phL2 = 0, phL3 = 0;  // parity bits per buffer
+    // (chunk loops fully unrolled: rolling them shrinks the cold-L2 code
+    // fetch but costs 25% of the steady-state tile rate at scale)
     auto load_x = [&](long long tile, float* xv) {  // threads < 256: row tid % 128, 8 of 16 columns
       const long long r = tile * 128 + (tid & 127);
       if (tid < 256 && r < M) {
@@ -386,11 +398,15 @@ __global__ void __launch_bounds__(kMlpThreads, 1)
     };
     float xnext[8];
     long long tile = blockIdx.x;
+    if (early) pdl_trigger();
+    pdl_wait();  // the rollout's positional encodings are complete past this point
     if (tile < ntiles) {
       load_x(tile, xnext);
       if (tid < 256) store_split8(sm, OFF_XH, OFF_XL, umma_off(tid & 127, (tid >> 7) * 8, 16), xnext);
       publish(barX);
+      MPPI_TSTAMP(dbg, 1);
       mbar_wait(barW0, 0);  // biases live in the W0 segment
+      MPPI_TSTAMP(dbg, 2);
     }
     const float s0 = par[kMlpH0 + kMlpH1 + 2 * kMlpH2 + 1];
     const float s1 = par[kMlpH0 + kMlpH1 + 2 * kMlpH2 + 2];
@@ -398,11 +414,13 @@ __global__ void __launch_bounds__(kMlpThreads, 1)
     for (; tile < ntiles; tile += gridDim.x) {
       const bool has_next = tile + gridDim.x < ntiles;
       if (has_next) load_x(tile + gridDim.x, xnext);  // in flight during layer 1
+#pragma unroll
       for (int c = 0; c < 8; ++c) {
         const int bf = c & 1;
         if ((c & 3) == 0) {  // layer-1 chunks 0-3 and 4-7 complete on separate barriers
-          mbar_wait(barL1[c >> 2], phL1[c >> 2]);
-          phL1[c >> 2] ^= 1;
+          const int hb = c >> 2;
+          mbar_wait(barL10 + 8 * hb, (phL1 >> hb) & 1u);
+          phL1 ^= 1u << hb;
           tc_fence_after();
         }
         float y[8];
@@ -410,22 +428,23 @@ __global__ void __launch_bounds__(kMlpThreads, 1)
 #pragma unroll
         for (int i = 0; i < 8; ++i) y[i] = fmaxf(fmaf(y[i], s0, b0[32 * c + 8 * cg + i]), 0.f);
         if (c >= 2) {  // A[bf] was last read by the layer-2 MMAs of chunk c-2
-          mbar_wait(barL2[bf], phL2[bf]);
-          phL2[bf] ^= 1;
+          mbar_wait(barL20 + 8 * bf, (phL2 >> bf) & 1u);
+          phL2 ^= 1u << bf;
         }
         store_split8(sm, OFF_A + bf * kABuf, OFF_A + bf * kABuf + kAHalf,
                      umma_off(row_in_tile, 8 * cg, kAChunkK), y);
-        publish(barA[bf]);
+        publish(barA0 + 8 * bf);
         if (c == 7 && has_next) {  // every layer-1 MMA of this tile is complete: reuse X
           if (tid < 256) store_split8(sm, OFF_XH, OFF_XL, umma_off(tid & 127, (tid >> 7) * 8, 16), xnext);
           publish(barX);
         }
       }
-      mbar_wait(barL2[0], phL2[0]);  // chunk 6's and chunk 7's layer-2 MMAs: all of layer 2
-      phL2[0] ^= 1;
-      mbar_wait(barL2[1], phL2[1]);
-      phL2[1] ^= 1;
+      MPPI_TSTAMP(dbg, 3);
+      mbar_wait(barL20, phL2 & 1u);  // chunk 6's and chunk 7's layer-2 MMAs: all of layer 2
+      mbar_wait(barL20 + 8, (phL2 >> 1) & 1u);
+      phL2 ^= 3u;
       tc_fence_after();
+#pragma unroll
       for (int c = 0; c < 4; ++c) {
         const int bf = c & 1;
         float y[8];
@@ -433,17 +452,18 @@ __global__ void __launch_bounds__(kMlpThreads, 1)
 #pragma unroll
         for (int i = 0; i < 8; ++i) y[i] = fmaxf(fmaf(y[i], s1, b1[32 * c + 8 * cg + i]), 0.f);
         if (c >= 2) {
-          mbar_wait(barL3[bf], phL3[bf]);
-          phL3[bf] ^= 1;
+          mbar_wait(barL30 + 8 * bf, (phL3 >> bf) & 1u);
+          phL3 ^= 1u << bf;
         }
         store_split8(sm, OFF_A + bf * kABuf, OFF_A + bf * kABuf + kAHalf,
                      umma_off(row_in_tile, 8 * cg, kAChunkK), y);
-        publish(barA[bf]);
+        publish(barA0 + 8 * bf);
       }
-      mbar_wait(barL3[0], phL3[0]);
-      phL3[0] ^= 1;
-      mbar_wait(barL3[1], phL3[1]);
-      phL3[1] ^= 1;
+      MPPI_TSTAMP(dbg, 4);
+      mbar_wait(barL30, phL3 & 1u);
+      mbar_wait(barL30 + 8, (phL3 >> 1) & 1u);
+      phL3 ^= 3u;
+      MPPI_TSTAMP(dbg, 5);
       tc_fence_after();
       float part = 0.f;
       {
@@ -463,6 +483,7 @@ __global__ void __launch_bounds__(kMlpThreads, 1)
       }
       tc_fence_before();
       epi_barrier();  // red (A buffer 0) is rewritten by the next tile's first epilogue
+      MPPI_TSTAMP(dbg, 6);
     }
   }
   __syncthreads();
@@ -525,7 +546,7 @@ inline cudaError_t mlp_upload(MlpWeights& m, int in_dim, const double* W0, const
 }
 
 inline cudaError_t mlp_forward(const MlpWeights& m, const float* x, long long rows, float* out,
-                               cudaStream_t st) {
+                               cudaStream_t st, unsigned long long* dbg = nullptr) {
   static bool attr_set[64] = {};
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
@@ -538,8 +559,18 @@ inline cudaError_t mlp_forward(const MlpWeights& m, const float* x, long long ro
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const long long tiles = (rows + 127) / 128;
   const unsigned grid = (unsigned)(tiles < sms ? tiles : sms);
-  mlp_tcgen05_kernel<<<grid, kMlpThreads, kMlpSmem, st>>>(x, rows, m.img, out);
-  return cudaGetLastError();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid, 1, 1);
+  cfg.blockDim = dim3(kMlpThreads, 1, 1);
+  cfg.dynamicSmemBytes = kMlpSmem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = (pdl_mask() & PDL_MLP) != 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, mlp_tcgen05_kernel, x, rows, (const unsigned char*)m.img, out,
+                            (pdl_mask() & PDL_EARLY) ? 1 : 0, dbg);
 }
 
 inline void mlp_release(MlpWeights& m) {

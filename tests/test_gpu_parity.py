@@ -486,3 +486,30 @@ def test_failure_in_second_iteration_keeps_first_update():
     c.policy = make_policy(30, 7, 0.5)
     _, d2 = c.control_step(st)
     assert d2.fallback == ""
+
+
+@pytest.mark.gpu
+def test_fused_rollout_mlp_matches_two_kernel_path(monkeypatch):
+    """The opt-in fused rollout + MLP kernel (MPPI_FUSE=1, mppi_fused.cuh)
+    computes exactly what rollout_kernel + mlp_tcgen05_kernel compute."""
+    from paper_2104_13542_b200 import configs
+
+    st = configs.start_state()
+    outs = []
+    for fuse in (False, True):
+        if fuse:
+            monkeypatch.setenv("MPPI_FUSE", "1")
+        else:
+            monkeypatch.delenv("MPPI_FUSE", raising=False)
+        c = configs.make_controller(2, particles=500)
+        seq = []
+        for _ in range(3):
+            cmd, d = c.control_step(st)
+            seq.append((cmd.copy(), d.best_cost, d.mean_cost))
+        outs.append((seq, c.policy.means.copy(), c.policy.variances.copy()))
+    (s0, m0, v0), (s1, m1, v1) = outs
+    for (c0, b0, mc0), (c1, b1, mc1) in zip(s0, s1):
+        np.testing.assert_array_equal(c0, c1)
+        assert b0 == b1 and mc0 == mc1
+    np.testing.assert_array_equal(m0, m1)
+    np.testing.assert_array_equal(v0, v1)
