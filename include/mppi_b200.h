@@ -76,7 +76,7 @@
 extern "C" {
 #endif
 
-#define MPPI_ABI_VERSION 1
+#define MPPI_ABI_VERSION 2
 
 /* Compile-time capacity of the fused kernels. */
 #define MPPI_MAX_DOF      8   /* kernels are instantiated for dof 1..8      */
@@ -93,7 +93,8 @@ enum mppi_status {
   MPPI_E_BAD_ARGUMENT = 4,
   MPPI_E_CUDA = 5,
   MPPI_E_NONPOSITIVE_VARIANCE = 6,
-  MPPI_E_CONFIG = 7
+  MPPI_E_CONFIG = 7,
+  MPPI_E_SKIPPED = 8           /* step not run: the on-device episode aborted */
 };
 
 enum mppi_goal_mode {          /* costs.py:20-22 */
@@ -114,6 +115,9 @@ enum mppi_generator {
 };
 
 enum mppi_smoothing { MPPI_SMOOTH_BSPLINE = 0, MPPI_SMOOTH_COMB = 1, MPPI_SMOOTH_NONE = 2 };
+enum mppi_goal_source { MPPI_GOAL_FIXED = 0, MPPI_GOAL_SCRIPT = 1 };  /* run_episode goal_source */
+enum mppi_interp { MPPI_INTERP_HOLD = 0, MPPI_INTERP_LINEAR = 1 };    /* TargetScript.interpolation */
+enum mppi_fallback { MPPI_FALLBACK_NONE = 0, MPPI_FALLBACK_REISSUE = 1, MPPI_FALLBACK_BRAKE = 2 };
 enum mppi_policy_mode { MPPI_POLICY_PER_JOINT = 0, MPPI_POLICY_ISOTROPIC = 1 };
 enum mppi_precision { MPPI_FP32 = 0, MPPI_FP64 = 1 };
 
@@ -283,6 +287,69 @@ int mppi_evaluate(mppi_plan* plan, int32_t mode, int32_t n, int32_t horizon,
 /* Instance 0's RolloutBundle of the last iteration of the last mppi_step
  * (plan created with dump = 1), plus the particle weights (N,). */
 int mppi_get_bundle(mppi_plan* plan, mppi_eval_out* out, double* weights);
+
+/* ---- closed-loop episode on the device -------------
+ * run_episode (controller.py:331-416) without a host round trip per step: for
+ * i < steps, on the plan stream,
+ *   goal  = target_at(script, i*dt) (simworld.py:175-197) or the plan goal,
+ *   est   = i > 0 ? filter_state(plant, filter, dt) : plant (controller.py:63-78),
+ *   cmd   = control_step(est) with the fallback ladder (controller.py:224-241),
+ *   costs = instantaneous_costs(plant) (controller.py:262-269), EE pose = FK,
+ *   plant = sim_step(plant, cmd, dt, noise) (simworld.py:108-127);
+ * a non-finite plant state ends the episode after logging that row (the
+ * remaining replays leave the policy untouched, status MPPI_E_SKIPPED).
+ * Plant noise is not drawn on the device: pass the reference's draws
+ * (rng.normal(0, sigma, d) for the position, then for the velocity, per step)
+ * as `noise` so the episode is the reference's bit-for-bit input. Requires
+ * instances == 1 and command_mode "mean". */
+typedef struct mppi_episode_desc {
+  int32_t steps;              /* S                                          */
+  int32_t goal_source;        /* enum mppi_goal_source                      */
+  int32_t interpolation;      /* enum mppi_interp (script goals)            */
+  int32_t script_mode;        /* enum mppi_goal_mode of the script goals    */
+  int32_t waypoints;          /* W (script goals)                           */
+  int32_t _pad;
+  double dt;                  /* Controller.control_period                  */
+  double filter_lambda;       /* FilterState.lam                            */
+  const double* times;        /* (W,) strictly increasing                   */
+  const double* positions;    /* (W,3)                                      */
+  const double* noise;        /* (S,2d) or NULL                             */
+} mppi_episode_desc;
+
+/* EpisodeLog columns (controller.py:273-291), caller-owned host arrays of
+ * `steps` rows; rows past *steps_done are left untouched. */
+typedef struct mppi_episode_log {
+  double* t;                  /* (S,)   */
+  double* theta;              /* (S,d)  plant state at the start of the step */
+  double* theta_dot;          /* (S,d)  */
+  double* command;            /* (S,d)  */
+  double* goal;               /* (S,3)  */
+  double* goal_rot;           /* (S,9)  */
+  double* ee;                 /* (S,3)  */
+  double* ee_rot;             /* (S,9)  */
+  double* cost_total;         /* (S,)   */
+  double* cost_terms;         /* (6,S)  pose stop joint manip selfcoll envcoll */
+  int32_t* collision;         /* (S,)   envcoll > 0                         */
+  int32_t* fallback;          /* (S,)   enum mppi_fallback                  */
+  int32_t* status;            /* (S,)   enum mppi_status of the control step */
+} mppi_episode_log;
+
+/* The filter / fallback state a host-side Controller mirrors. */
+typedef struct mppi_episode_state {
+  double last_estimate[2 * MPPI_MAX_DOF]; /* theta, theta_dot              */
+  double last_command[MPPI_MAX_DOF];
+  double prev_command[MPPI_MAX_DOF];      /* Controller._prev_command      */
+  double plant[2 * MPPI_MAX_DOF];         /* plant state after the last step */
+  int32_t fallback_armed;
+  int32_t aborted;
+} mppi_episode_state;
+
+/* The filter starts from last_estimate = x0, last_command = 0 as run_episode
+ * sets it (controller.py:354-355); prev_command and fallback_armed are read
+ * from `state` (the Controller's); every field is written back at the end. */
+int mppi_episode(mppi_plan* plan, const mppi_episode_desc* desc, const double* theta0,
+                 const double* theta_dot0, mppi_episode_state* state, mppi_episode_log* log,
+                 int32_t* steps_done, double* device_ms);
 
 /* Step timing level. 0 (default): the lean step graph, no timing calls on the
  * latency path. 1: two stream events around the lean graph fill

@@ -28,6 +28,7 @@ E_BAD_ARGUMENT = 4
 E_CUDA = 5
 E_NONPOSITIVE_VARIANCE = 6
 E_CONFIG = 7
+E_SKIPPED = 8  # the on-device episode aborted before this step
 
 GOAL_POSITION_ONLY = 0
 GOAL_FULL_POSE = 1
@@ -36,6 +37,9 @@ GEN_HALTON, GEN_PSEUDORANDOM, GEN_EXTERNAL = 0, 1, 2
 SMOOTH_BSPLINE, SMOOTH_COMB, SMOOTH_NONE = 0, 1, 2
 POLICY_PER_JOINT, POLICY_ISOTROPIC = 0, 1
 FP32, FP64 = 0, 1
+GOAL_FIXED, GOAL_SCRIPT = 0, 1
+INTERP_HOLD, INTERP_LINEAR = 0, 1
+FALLBACK_NONE, FALLBACK_REISSUE, FALLBACK_BRAKE = 0, 1, 2
 
 MAX_DOF = 8
 MAX_HORIZON = 32
@@ -96,6 +100,32 @@ class EvalOut(C.Structure):
     ]
 
 
+_ip = C.POINTER(C.c_int32)
+
+
+class EpisodeDesc(C.Structure):
+    _fields_ = [
+        ("steps", C.c_int32), ("goal_source", C.c_int32), ("interpolation", C.c_int32),
+        ("script_mode", C.c_int32), ("waypoints", C.c_int32), ("_pad", C.c_int32),
+        ("dt", C.c_double), ("filter_lambda", C.c_double),
+        ("times", _dp), ("positions", _dp), ("noise", _dp),
+    ]
+
+
+class EpisodeLogC(C.Structure):
+    _fields_ = [(n, _dp) for n in ("t", "theta", "theta_dot", "command", "goal", "goal_rot", "ee",
+                                   "ee_rot", "cost_total", "cost_terms")] + \
+               [(n, _ip) for n in ("collision", "fallback", "status")]
+
+
+class EpisodeState(C.Structure):
+    _fields_ = [
+        ("last_estimate", C.c_double * (2 * MAX_DOF)), ("last_command", C.c_double * MAX_DOF),
+        ("prev_command", C.c_double * MAX_DOF), ("plant", C.c_double * (2 * MAX_DOF)),
+        ("fallback_armed", C.c_int32), ("aborted", C.c_int32),
+    ]
+
+
 # name -> (restype, argtypes); every function returns int status unless noted
 _vp = C.c_void_p
 _SIGS = {
@@ -121,6 +151,8 @@ _SIGS = {
     "mppi_evaluate": (C.c_int, [_vp, C.c_int32, C.c_int32, C.c_int32, _dp, C.c_double, C.c_double,
                                 _dp, _dp, _dp, _dp, C.POINTER(EvalOut)]),
     "mppi_get_bundle": (C.c_int, [_vp, C.POINTER(EvalOut), _dp]),
+    "mppi_episode": (C.c_int, [_vp, C.POINTER(EpisodeDesc), _dp, _dp, C.POINTER(EpisodeState),
+                               C.POINTER(EpisodeLogC), _ip, _dp]),
     "mppi_time_stage": (C.c_int, [_vp, C.c_int32, C.c_int32, _dp]),
     "mppi_profile_stages": (C.c_int, [_vp, C.c_int32]),
     "mppi_stats_record_len":(C.c_int, [_vp, C.POINTER(C.c_int32)]),
@@ -169,7 +201,7 @@ def load_library(path: str | os.PathLike | None = None) -> C.CDLL:
         fn = getattr(lib, name)
         fn.restype = res
         fn.argtypes = args
-    if lib.mppi_abi_version() != 1:
+    if lib.mppi_abi_version() != 2:
         raise DeviceError("native library ABI version mismatch")
     if path is None:
         _lib = lib

@@ -6,6 +6,11 @@ call = one H2D of the joint state, one CUDA-graph replay of
 mean/covariance update)], one D2H of the command and status. The policy lives
 on the device; ``controller.policy`` reads it back on access.
 
+The episode driver around it (controller.py:53-78, 273-416: FilterState,
+filter_state, EpisodeLog, run_episode) is here too; run_episode runs the whole
+closed loop on the device (mppi_episode) when the controller's command mode
+allows it.
+
 Differences from the reference, by design:
   * ``workers`` is accepted and ignored (particles map to warps, not threads);
   * ``diag.bundle`` is a lazily fetched view of the last iteration's device
@@ -15,6 +20,8 @@ Differences from the reference, by design:
 
 from __future__ import annotations
 
+import csv
+import io
 import logging
 import time
 from dataclasses import dataclass
@@ -29,8 +36,36 @@ from .kinematics import KinematicChain
 from .policy import ISOTROPIC, PER_JOINT, PolicyParams, UpdateConfig
 from .rollout import DtSchedule, JointState, RolloutBundle, make_dt_schedule
 from .sampling import HALTON, PSEUDORANDOM, SmoothingSpec, smoothing_code
+from .simworld import HOLD, LINEAR, TargetScript, sim_step, target_at
 
 log = logging.getLogger(__name__)
+
+
+@dataclass
+class FilterState:
+    """Measurement/prediction blend state (controller.py:53-60)."""
+
+    lam: float
+    last_command: np.ndarray
+    last_estimate: JointState
+
+    def __post_init__(self):
+        if not 0.0 <= self.lam <= 1.0:
+            raise ContractError("filter blend must lie in [0, 1]")
+
+
+def filter_state(raw: JointState, filt: FilterState, dt: float) -> JointState:
+    """Blend the measurement with the model prediction from the last command
+    (controller.py:63-78); updates filt.last_estimate."""
+    if dt <= 0.0:
+        raise ContractError("dt must be positive")
+    pv = filt.last_estimate.theta_dot + dt * filt.last_command
+    pp = filt.last_estimate.theta + dt * pv
+    lam = filt.lam
+    est = JointState(theta=(1.0 - lam) * pp + lam * raw.theta, theta_dot=(1.0 - lam) * pv + lam * raw.theta_dot,
+                     theta_ddot=filt.last_command.copy(), stamp=raw.stamp)
+    filt.last_estimate = est
+    return est
 
 
 @dataclass
@@ -145,6 +180,9 @@ class Controller:
         self._fallback_armed = False
         self._step_serial = 0
         self.keep_bundle = keep_bundle
+        z = np.zeros(chain.dof)
+        self.filter = FilterState(lam=filter_lambda, last_command=z.copy(),
+                                  last_estimate=JointState(theta=z.copy(), theta_dot=z.copy(), theta_ddot=z.copy()))
 
     # ---------------------------------------------------------------- state
     @property
@@ -211,6 +249,7 @@ class Controller:
             else:
                 command, mode = np.zeros(self.chain.dof), "brake"
             log.warning("control step failed (%s); falling back to %s", exc, mode)
+            self.filter.last_command = command.copy()
             latency = (time.perf_counter() - t_start) * 1e3
             return command, StepDiagnostics(latency_ms=latency, sample_ms=0.0, rollout_ms=info.device_ms,
                                             update_ms=0.0, best_cost=float("nan"),
@@ -222,6 +261,7 @@ class Controller:
             pol = self.policy
             command = self.rng.normal(pol.means[0], pol.stddev()[0])
         self._prev_command = command.copy()
+        self.filter.last_command = command.copy()
         latency = (time.perf_counter() - t_start) * 1e3
         if latency > self.latency_budget * 1e3:
             log.debug("control step overran budget: %.2f ms", latency)
@@ -267,3 +307,183 @@ class LazyBundle:
     def materialize(self) -> RolloutBundle:
         d = self._load()
         return RolloutBundle(**{k: d[k] for k in self._FIELDS if k != "weights"})
+
+
+# ---------------------------------------------------------------- episodes
+@dataclass
+class EpisodeLog:
+    """Step-indexed record of one simulated episode (controller.py:273-328);
+    the CSV rendering is the external interface."""
+
+    chain: KinematicChain
+    t: np.ndarray
+    theta: np.ndarray
+    theta_dot: np.ndarray
+    command: np.ndarray
+    goal: np.ndarray
+    ee: np.ndarray
+    cost_total: np.ndarray
+    cost_terms: dict
+    collision: np.ndarray
+    latency_ms: np.ndarray
+    aborted: bool = False
+    goal_rotations: np.ndarray | None = None
+    ee_rotations: np.ndarray | None = None
+
+    @property
+    def steps(self) -> int:
+        return self.t.shape[0]
+
+    def header(self) -> list:
+        d = self.chain.dof
+        return (["t"] + [f"theta_{k}" for k in range(d)] + [f"thetadot_{k}" for k in range(d)]
+                + [f"u_{k}" for k in range(d)] + [f"goal_{k}" for k in range(3)]
+                + ["cost_total"] + [f"cost_{k}" for k in TERMS] + ["collision", "latency_ms"])
+
+    def to_csv(self, path=None) -> str:
+        buf = io.StringIO()
+        w = csv.writer(buf, lineterminator="\n")
+        w.writerow(self.header())
+        g = lambda v: f"{v:.17g}"  # noqa: E731
+        for i in range(self.steps):
+            w.writerow([g(self.t[i])] + [g(v) for v in self.theta[i]] + [g(v) for v in self.theta_dot[i]]
+                       + [g(v) for v in self.command[i]] + [g(v) for v in self.goal[i]]
+                       + [g(self.cost_total[i])] + [g(self.cost_terms[k][i]) for k in TERMS]
+                       + [str(int(self.collision[i])), g(self.latency_ms[i])])
+        text = buf.getvalue()
+        if path is not None:
+            with open(path, "w") as fh:
+                fh.write(text)
+        return text
+
+
+TERMS = ("pose", "stop", "joint", "manip", "selfcoll", "envcoll")
+
+
+def run_episode(controller: Controller, x0: JointState, goal_source, steps: int, noise_sigma: float = 0.0,
+                sim_seed: int = 0, *, device_loop: bool | None = None) -> EpisodeLog:
+    """Alternate control and plant steps (controller.py:331-416).
+
+    goal_source is a GoalSpec or a TargetScript; a non-finite plant state
+    ends the episode after logging that step. By default the whole loop runs
+    on the device (mppi_episode: one graph replay per step, no host round
+    trip; latency_ms is then the device time per step), with the plant noise
+    drawn here from default_rng(sim_seed) in the reference's order so the
+    inputs are the reference's. command_mode "sample" draws commands from the
+    host rng and so runs the host loop (device_loop=False forces it)."""
+    if device_loop is None:
+        device_loop = controller.command_mode == "mean"
+    if device_loop and controller.command_mode != "mean":
+        raise ContractError("the device episode loop issues mean commands only")
+    if device_loop:
+        return _run_episode_device(controller, x0, goal_source, steps, noise_sigma, sim_seed)
+    return _run_episode_host(controller, x0, goal_source, steps, noise_sigma, sim_seed)
+
+
+def _episode_log(chain, cols: dict, aborted: bool) -> EpisodeLog:
+    n = len(cols["t"])
+    return EpisodeLog(
+        chain=chain, t=np.asarray(cols["t"], dtype=np.float64),
+        theta=np.asarray(cols["theta"]).reshape(n, chain.dof),
+        theta_dot=np.asarray(cols["theta_dot"]).reshape(n, chain.dof),
+        command=np.asarray(cols["command"]).reshape(n, chain.dof),
+        goal=np.asarray(cols["goal"]).reshape(n, 3), ee=np.asarray(cols["ee"]).reshape(n, 3),
+        cost_total=np.asarray(cols["cost_total"], dtype=np.float64),
+        cost_terms={k: np.asarray(v, dtype=np.float64) for k, v in cols["terms"].items()},
+        collision=np.asarray(cols["collision"], dtype=bool),
+        latency_ms=np.asarray(cols["latency_ms"], dtype=np.float64), aborted=aborted,
+        goal_rotations=np.asarray(cols["goal_rot"]).reshape(n, 3, 3),
+        ee_rotations=np.asarray(cols["ee_rot"]).reshape(n, 3, 3))
+
+
+def _run_episode_host(controller, x0, goal_source, steps, noise_sigma, sim_seed) -> EpisodeLog:
+    """The reference's loop over this package's Controller (one control_step
+    per plant step, each a host round trip)."""
+    from .kinematics import fk_batch
+
+    chain, dt = controller.chain, controller.control_period
+    rng = np.random.default_rng(sim_seed) if noise_sigma > 0.0 else None
+    cols = {k: [] for k in ("t", "theta", "theta_dot", "command", "goal", "goal_rot", "ee", "ee_rot",
+                            "cost_total", "collision", "latency_ms")}
+    cols["terms"] = {k: [] for k in TERMS}
+    controller.filter.last_estimate = x0
+    controller.filter.last_command = np.zeros(chain.dof)
+    state, aborted = x0, False
+    for i in range(steps):
+        t_now = i * dt
+        goal = target_at(goal_source, t_now) if isinstance(goal_source, TargetScript) else goal_source
+        controller.set_goal(goal)
+        est = filter_state(state, controller.filter, dt) if i > 0 else state
+        command, diag = controller.control_step(est)
+        total, terms = controller.instantaneous_costs(state)
+        rot, trans = fk_batch(chain, state.theta[None, :])
+        for k, v in (("t", t_now), ("theta", state.theta.copy()), ("theta_dot", state.theta_dot.copy()),
+                     ("command", command.copy()), ("goal", goal.target_pose.translation.copy()),
+                     ("goal_rot", goal.target_pose.rotation.copy()), ("ee", trans[0, -1].copy()),
+                     ("ee_rot", rot[0, -1].copy()), ("cost_total", total),
+                     ("collision", bool(terms["envcoll"] > 0.0)), ("latency_ms", diag.latency_ms)):
+            cols[k].append(v)
+        for k in TERMS:
+            cols["terms"][k].append(terms[k])
+        try:
+            state = sim_step(state, command, dt, noise_sigma=noise_sigma, rng=rng)
+        except ContractError:
+            log.error("plant diverged at step %d; aborting episode", i)
+            aborted = True
+            break
+    return _episode_log(chain, cols, aborted)
+
+
+def _run_episode_device(controller, x0, goal_source, steps, noise_sigma, sim_seed) -> EpisodeLog:
+    from .costs import goal_at_position
+
+    chain, dt, d = controller.chain, controller.control_period, controller.chain.dof
+    if steps < 0:
+        raise ContractError("negative episode length")
+    noise = None
+    if noise_sigma > 0.0 and steps > 0:
+        rng = np.random.default_rng(sim_seed)
+        noise = np.empty((steps, 2 * d))
+        for i in range(steps):  # sim_step's draw order: positions, then velocities
+            noise[i, :d] = rng.normal(0.0, noise_sigma, size=d)
+            noise[i, d:] = rng.normal(0.0, noise_sigma, size=d)
+    script = None
+    if isinstance(goal_source, TargetScript):
+        mode_code = goal_at_position(goal_source.positions[0], mode=goal_source.mode).mode_code
+        script = (goal_source.times, goal_source.positions,
+                  N.INTERP_LINEAR if goal_source.interpolation == LINEAR else N.INTERP_HOLD, mode_code)
+    else:
+        controller.set_goal(goal_source)
+    r = controller.plan.episode(steps, dt, controller.filter.lam, x0.theta, x0.theta_dot,
+                                prev_command=controller._prev_command, fallback_armed=controller._fallback_armed,
+                                script=script, noise=noise)
+    n = r["steps_done"]
+    # the Controller's host-side state as the reference loop leaves it
+    controller._step_serial += n
+    controller._prev_command = r["prev_command"].copy()
+    controller._fallback_armed = r["fallback_armed"]
+    controller.filter.last_command = r["last_command"].copy()
+    if n > 1:
+        est = r["last_estimate"]
+        controller.filter.last_estimate = JointState(theta=est[:d].copy(), theta_dot=est[d:].copy(),
+                                                     theta_ddot=r["command"][n - 2].copy(),
+                                                     stamp=x0.stamp + (n - 1) * dt)
+    else:
+        controller.filter.last_estimate = x0
+    if script is not None and n > 0:
+        goal = target_at(goal_source, (n - 1) * dt)
+        controller.cost_stack.goal = goal
+        controller._goal_uploaded = (goal, goal.mode, np.array(goal.target_pose.translation),
+                                     np.array(goal.target_pose.rotation))
+    for i in np.flatnonzero(r["fallback"] != N.FALLBACK_NONE):
+        mode = "reissue" if r["fallback"][i] == N.FALLBACK_REISSUE else "brake"
+        log.warning("control step %d failed (%s); fell back to %s", i,
+                    N.status_exception(int(r["status"][i])), mode)
+    if r["aborted"]:
+        log.error("plant diverged at step %d; aborting episode", n - 1)
+    per_step = r["device_ms"] / max(n, 1)
+    cols = {"t": r["t"], "theta": r["theta"], "theta_dot": r["theta_dot"], "command": r["command"],
+            "goal": r["goal"], "goal_rot": r["goal_rot"], "ee": r["ee"], "ee_rot": r["ee_rot"],
+            "cost_total": r["cost_total"], "collision": r["collision"] != 0,
+            "latency_ms": np.full(n, per_step), "terms": {k: r["cost_terms"][i] for i, k in enumerate(TERMS)}}
+    return _episode_log(chain, cols, r["aborted"])

@@ -18,6 +18,7 @@
 #include "mppi_aux_kernels.cuh"
 #include "mppi_launch.cuh"
 #include "mppi_mlp.cuh"
+#include "mppi_episode.cuh"
 
 using namespace mppi;
 
@@ -196,6 +197,23 @@ struct mppi_plan {
   DevBuf<int> e_status;
   DevBuf<double> e_records;
   DevBuf<unsigned> e_counters;
+  // closed-loop episode (mppi_episode): device state, log, script, noise,
+  // the step's command/info (device instead of mapped host) and the
+  // instantaneous-cost evaluation of the plant state (n = 1, H = 1)
+  DevBuf<double> ep_state, ep_log, ep_script, ep_noise, ep_cmd;
+  DevBuf<int> ep_ilog;
+  DevBuf<mppi_step_info> ep_info;
+  DevBuf<double> ev_in, ev_out, ev_records;
+  DevBuf<unsigned char> ev_stepbuf;
+  DevBuf<float> ev_x, ev_d;
+  DevBuf<int> ev_status;
+  DevBuf<unsigned> ev_counters;
+  double* cmd_dst = nullptr;             // finalize outputs while capturing an episode
+  mppi_step_info* info_dst = nullptr;
+  cudaStream_t stream2 = nullptr;        // the episode's cost-evaluation branch
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  cudaGraphExec_t ep_graph = nullptr;    // last episode graph, reused while its arguments match
+  std::vector<unsigned char> ep_key;
 
   bool learned() const {
     return costs.self_collision == MPPI_SELFCOLL_LEARNED && costs.alpha_coll > 0.0;
@@ -212,6 +230,8 @@ int set_device(mppi_plan* p) {
 void invalidate_graph(mppi_plan* p) {
   if (p->graph) cudaGraphExecDestroy(p->graph);
   if (p->graph_prof) cudaGraphExecDestroy(p->graph_prof);
+  if (p->ep_graph) cudaGraphExecDestroy(p->ep_graph);
+  p->ep_graph = nullptr;
   p->graph = nullptr;
   p->graph_prof = nullptr;
 }
@@ -375,8 +395,8 @@ int enqueue_iteration(mppi_plan* p, int it, bool inline_final, double* out_recor
   s.status = p->status.p;
   s.bad = p->bad.p;
   s.dbg = p->dbg.p;
-  s.cmd = p->m_cmd;   // mapped host memory: no D2H copy node
-  s.info = p->m_info;
+  s.cmd = p->cmd_dst ? p->cmd_dst : p->m_cmd;  // mapped host memory: no D2H copy node
+  s.info = p->info_dst ? p->info_dst : p->m_info;
   if (p->dump) {
     s.dump_step = p->d_step.p;
     s.dump_terms = p->d_terms.p;
@@ -406,11 +426,13 @@ int enqueue_sampling(mppi_plan* p, int it, cudaStream_t st) {
   return MPPI_OK;
 }
 
-int enqueue_step_body(mppi_plan* p, cudaStream_t st, bool stage_events) {
+int enqueue_step_body(mppi_plan* p, cudaStream_t st, bool stage_events, bool h2d = true) {
   const int B = p->B, D = p->D;
   // one H2D node: the (B,2d) state followed by the step counter (pseudorandom
   // generator). Status words were re-armed by the previous step's finalize.
-  CK(cudaMemcpyAsync(p->state.p, p->h_state, sizeof(double) * (B * 2 * D + 1), cudaMemcpyHostToDevice, st));
+  // (The episode graph writes the state on the device instead.)
+  if (h2d)
+    CK(cudaMemcpyAsync(p->state.p, p->h_state, sizeof(double) * (B * 2 * D + 1), cudaMemcpyHostToDevice, st));
   // event-record nodes between the stages give per-kernel device times of
   // every replayed step (mppi_step_info.*_ms)
   // event-record nodes between the stages (instrumented graph only: each node
@@ -492,6 +514,108 @@ int copy_chain(const mppi_chain_desc* c, HostChain& h) {
 }  // namespace
 
 // ================================================================== C ABI
+// ---------------------------------------------------------------- episode
+namespace {
+
+constexpr int kEpisodeUnroll = 16;  // episode steps per captured graph
+
+// instantaneous_costs (controller.py:262-269) of the plant state in ev_in:
+// CostStack.evaluate with one step whose braking time is the whole horizon.
+template <typename R>
+int enqueue_instant_costs(mppi_plan* p, cudaStream_t st) {
+  const int D = p->D;
+  double horizon_time = 0.0;
+  for (double x : p->dts) horizon_time += x;
+  RolloutArgs<R> a;
+  rollout_static<R>(p, 1, &horizon_time, a);
+  a.N = 1;
+  a.B = 1;
+  a.mode = 2;  // positions (in0) and velocities (in1) given
+  a.skip_on_status = 1;
+  a.state = p->ev_in.p;
+  a.goal = p->goal.p;
+  a.in0 = p->ev_in.p;
+  a.in1 = p->ev_in.p + D;
+  a.step = reinterpret_cast<R*>(p->ev_stepbuf.p);
+  a.mlp_x = p->learned() ? p->ev_x.p : nullptr;
+  a.status = p->ev_status.p;
+  a.bad = p->ev_status.p + 1;
+  a.out_terms = p->ev_out.p + 1;
+  CK(launch_rollout_any<R>(a, D, 1, st));
+  if (p->learned()) CK(mlp_forward(p->mlp, p->ev_x.p, 1, p->ev_d.p, st));
+  StatsArgs<R> s;
+  stats_static<R>(p, 1, p->gamma, 1.0, s);
+  s.N = 1;
+  s.B = 1;
+  s.ppb = 1;
+  s.nblk = 1;
+  s.totals_only = 1;
+  s.raw_step = 1;
+  s.step = reinterpret_cast<const R*>(p->ev_stepbuf.p);
+  s.mlp_d = p->learned() ? p->ev_d.p : nullptr;
+  s.totals = p->ev_out.p + 7;
+  s.records = p->ev_records.p;
+  s.counters = p->ev_counters.p;
+  s.status = p->ev_status.p;
+  s.bad = p->ev_status.p + 1;
+  s.dump_step = p->ev_out.p;       // raw step cost (total_cost incl. the learned term)
+  s.dump_terms = p->ev_out.p + 1;  // selfcoll row rewritten for the learned provider
+  CK(launch_stats_any<R>(s, D, st));
+  return MPPI_OK;
+}
+
+// `unroll` episode steps in one graph: pre -> {control step || cost
+// evaluation} -> post, per step. Sections past the last step do nothing.
+int capture_episode_graph(mppi_plan* p, const EpisodeArgs& ea, int unroll, cudaGraphExec_t* exec) {
+  cudaStream_t st = p->stream;
+  if (!p->stream2) {
+    CK(cudaStreamCreateWithFlags(&p->stream2, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&p->ev_fork, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&p->ev_join, cudaEventDisableTiming));
+  }
+  cudaGraph_t g = nullptr;
+  CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+  int rc = MPPI_OK;
+  auto launched = [&](const char* what) {
+    if (rc == MPPI_OK && cudaGetLastError() != cudaSuccess) rc = fail(MPPI_E_CUDA, std::string(what) + " launch");
+  };
+  for (int u = 0; u < unroll && rc == MPPI_OK; ++u) {
+    episode_pre_kernel<<<1, 32, 0, st>>>(ea);
+    launched("episode_pre_kernel");
+    // fork: the plant-state cost evaluation runs beside the control step
+    if (rc == MPPI_OK && (cudaEventRecord(p->ev_fork, st) != cudaSuccess ||
+                          cudaStreamWaitEvent(p->stream2, p->ev_fork, 0) != cudaSuccess))
+      rc = fail(MPPI_E_CUDA, "episode fork");
+    if (rc == MPPI_OK)
+      rc = p->precision == MPPI_FP64 ? enqueue_instant_costs<double>(p, p->stream2)
+                                     : enqueue_instant_costs<float>(p, p->stream2);
+    if (rc == MPPI_OK && cudaEventRecord(p->ev_join, p->stream2) != cudaSuccess)
+      rc = fail(MPPI_E_CUDA, "episode join");
+    p->cmd_dst = p->ep_cmd.p;
+    p->info_dst = p->ep_info.p;
+    if (rc == MPPI_OK) rc = enqueue_step_body(p, st, false, false);
+    p->cmd_dst = nullptr;
+    p->info_dst = nullptr;
+    if (rc == MPPI_OK && cudaStreamWaitEvent(st, p->ev_join, 0) != cudaSuccess) rc = fail(MPPI_E_CUDA, "episode join");
+    if (rc == MPPI_OK) {
+      episode_post_kernel<<<1, 32, 0, st>>>(ea);
+      launched("episode_post_kernel");
+    }
+  }
+  cudaError_t e = cudaStreamEndCapture(st, &g);
+  if (rc != MPPI_OK) {
+    if (g) cudaGraphDestroy(g);
+    return rc;
+  }
+  if (e != cudaSuccess) return fail(MPPI_E_CUDA, std::string("episode capture: ") + cudaGetErrorString(e));
+  e = cudaGraphInstantiate(exec, g, 0);
+  cudaGraphDestroy(g);
+  if (e != cudaSuccess) return fail(MPPI_E_CUDA, std::string("episode instantiate: ") + cudaGetErrorString(e));
+  return MPPI_OK;
+}
+
+}  // namespace
+
 extern "C" {
 
 int32_t mppi_abi_version(void) { return MPPI_ABI_VERSION; }
@@ -655,7 +779,9 @@ int mppi_plan_destroy(mppi_plan* p) {
                            &p->totals, &p->records, &p->out_record, &p->cmd, &p->counters_pad,
                            &p->e_in0, &p->e_in1, &p->e_pos, &p->e_vel, &p->e_acc, &p->e_terms,
                            &p->e_step, &p->e_tot, &p->e_state, &p->e_dts, &p->e_records,
-                           &p->d_pos, &p->d_vel, &p->d_acc, &p->d_terms, &p->d_step, &p->d_w};
+                           &p->d_pos, &p->d_vel, &p->d_acc, &p->d_terms, &p->d_step, &p->d_w,
+                           &p->ep_state, &p->ep_log, &p->ep_script, &p->ep_noise, &p->ep_cmd,
+                           &p->ev_in, &p->ev_out, &p->ev_records};
   for (auto* b : dbl) b->release();
   p->sph_f.release();
   p->box_f.release();
@@ -673,6 +799,13 @@ int mppi_plan_destroy(mppi_plan* p) {
   p->bad.release();
   p->e_status.release();
   p->info.release();
+  p->ep_ilog.release();
+  p->ep_info.release();
+  p->ev_stepbuf.release();
+  p->ev_x.release();
+  p->ev_d.release();
+  p->ev_status.release();
+  p->ev_counters.release();
   mlp_release(p->mlp);
   if (p->h_state) cudaFreeHost(p->h_state);
   if (p->h_cmd) cudaFreeHost(p->h_cmd);
@@ -681,6 +814,9 @@ int mppi_plan_destroy(mppi_plan* p) {
   if (p->ev1) cudaEventDestroy(p->ev1);
   for (auto e : p->stage_ev) cudaEventDestroy(e);
   if (p->stream) cudaStreamDestroy(p->stream);
+  if (p->stream2) cudaStreamDestroy(p->stream2);
+  if (p->ev_fork) cudaEventDestroy(p->ev_fork);
+  if (p->ev_join) cudaEventDestroy(p->ev_join);
   delete p;
   return MPPI_OK;
 }
@@ -1109,6 +1245,180 @@ int mppi_get_bundle(mppi_plan* p, mppi_eval_out* out, double* weights) {
   CK(cudaStreamSynchronize(st));
   out->bad_particle = -1;
   out->quarantined = 0;
+  return MPPI_OK;
+}
+
+
+int mppi_episode(mppi_plan* p, const mppi_episode_desc* d, const double* theta0, const double* theta_dot0,
+                 mppi_episode_state* es, mppi_episode_log* lg, int32_t* steps_done, double* device_ms) {
+  if (!p || !d || !theta0 || !theta_dot0 || !es || !lg) return fail(MPPI_E_BAD_ARGUMENT, "null argument");
+  if (p->B != 1) return fail(MPPI_E_CONFIG, "an episode drives a single-instance plan");
+  if (d->steps < 0) return fail(MPPI_E_BAD_ARGUMENT, "negative episode length");
+  if (!(d->dt > 0.0)) return fail(MPPI_E_BAD_ARGUMENT, "dt must be positive");
+  if (!(d->filter_lambda >= 0.0 && d->filter_lambda <= 1.0))
+    return fail(MPPI_E_BAD_ARGUMENT, "filter blend must lie in [0, 1]");
+  const bool script = d->goal_source == MPPI_GOAL_SCRIPT;
+  if (d->goal_source != MPPI_GOAL_FIXED && !script) return fail(MPPI_E_BAD_ARGUMENT, "unknown goal source");
+  if (script) {
+    if (d->waypoints < 1 || !d->times || !d->positions)
+      return fail(MPPI_E_BAD_ARGUMENT, "target script needs at least one waypoint");
+    for (int w = 1; w < d->waypoints; ++w)
+      if (!(d->times[w] > d->times[w - 1])) return fail(MPPI_E_BAD_ARGUMENT, "waypoint times must increase");
+    if (d->interpolation != MPPI_INTERP_HOLD && d->interpolation != MPPI_INTERP_LINEAR)
+      return fail(MPPI_E_BAD_ARGUMENT, "unknown interpolation");
+  }
+  if (p->learned() && !p->mlp_ready) return fail(MPPI_E_CONFIG, "learned provider without weights");
+  if (steps_done) *steps_done = 0;
+  if (device_ms) *device_ms = 0.0;
+  const int S = d->steps, D = p->D;
+  if (S == 0) return MPPI_OK;
+  CKR(set_device(p));
+  cudaStream_t st = p->stream;
+  // ---- buffers
+  const size_t flog = (size_t)S * (1 + 3 * D + 3 + 9 + 3 + 9 + 1 + N_TERMS);
+  CKR(p->ep_state.alloc((sizeof(EpisodeDev) + 7) / 8));
+  CKR(p->ep_log.alloc(flog));
+  CKR(p->ep_ilog.alloc((size_t)3 * S));
+  CKR(p->ep_cmd.alloc(MPPI_MAX_DOF));
+  CKR(p->ep_info.alloc(1));
+  CKR(p->ev_in.alloc(2 * MPPI_MAX_DOF));
+  CKR(p->ev_out.alloc(8));
+  CKR(p->ev_records.alloc(kRecHead + 2 * D));
+  CKR(p->ev_stepbuf.alloc(sizeof(double)));
+  CKR(p->ev_status.alloc(2));
+  CKR(p->ev_counters.alloc(1));
+  if (p->learned()) {
+    CKR(p->ev_x.alloc(128 * 16));
+    CKR(p->ev_d.alloc(128));
+    CK(cudaMemsetAsync(p->ev_x.p, 0, sizeof(float) * 128 * 16, st));
+  }
+  CK(cudaMemsetAsync(p->ev_status.p, 0, sizeof(int), st));
+  CK(cudaMemsetAsync(p->ev_status.p + 1, 0x7f, sizeof(int), st));
+  CK(cudaMemsetAsync(p->ev_counters.p, 0, sizeof(unsigned), st));
+  if (script) {
+    CKR(p->ep_script.alloc((size_t)4 * d->waypoints));
+    CK(cudaMemcpyAsync(p->ep_script.p, d->times, sizeof(double) * d->waypoints, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(p->ep_script.p + d->waypoints, d->positions, sizeof(double) * 3 * d->waypoints,
+                       cudaMemcpyHostToDevice, st));
+  }
+  if (d->noise) {
+    CKR(p->ep_noise.alloc((size_t)2 * D * S));
+    CK(cudaMemcpyAsync(p->ep_noise.p, d->noise, sizeof(double) * 2 * D * S, cudaMemcpyHostToDevice, st));
+  }
+  EpisodeDev h;
+  memset(&h, 0, sizeof(h));
+  h.armed = es->fallback_armed;
+  h.ctr_base = p->step_counter;
+  for (int j = 0; j < D; ++j) {
+    h.plant[j] = h.est[j] = theta0[j];
+    h.plant[D + j] = h.est[D + j] = theta_dot0[j];
+    h.prev_cmd[j] = es->prev_command[j];
+  }
+  CK(cudaMemcpyAsync(p->ep_state.p, &h, sizeof(h), cudaMemcpyHostToDevice, st));
+  // ---- graph of one episode step
+  EpisodeArgs ea;
+  memset(&ea, 0, sizeof(ea));
+  ea.ep = reinterpret_cast<EpisodeDev*>(p->ep_state.p);
+  ea.S = S;
+  ea.D = D;
+  ea.goal_source = d->goal_source;
+  ea.interp = d->interpolation;
+  ea.script_mode = d->script_mode;
+  ea.W = d->waypoints;
+  ea.has_noise = d->noise != nullptr;
+  ea.dt = d->dt;
+  ea.lam = d->filter_lambda;
+  ea.times = script ? p->ep_script.p : nullptr;
+  ea.positions = script ? p->ep_script.p + d->waypoints : nullptr;
+  ea.noise = d->noise ? p->ep_noise.p : nullptr;
+  ea.state = p->state.p;
+  ea.goal = p->goal.p;
+  ea.status = p->status.p;
+  ea.step_cmd = p->ep_cmd.p;
+  ea.step_info = p->ep_info.p;
+  ea.ev_pos = p->ev_in.p;
+  ea.ev_vel = p->ev_in.p + D;
+  ea.ev_status = p->ev_status.p;
+  ea.ev_step = p->ev_out.p;
+  ea.ev_terms = p->ev_out.p + 1;
+  fill_chain(p->chain, p->costs.k_jl, ea.chain);
+  double* L = p->ep_log.p;
+  ea.t = L;
+  ea.theta = ea.t + S;
+  ea.theta_dot = ea.theta + (size_t)S * D;
+  ea.command = ea.theta_dot + (size_t)S * D;
+  ea.goalp = ea.command + (size_t)S * D;
+  ea.goal_rot = ea.goalp + (size_t)3 * S;
+  ea.ee = ea.goal_rot + (size_t)9 * S;
+  ea.ee_rot = ea.ee + (size_t)3 * S;
+  ea.cost_total = ea.ee_rot + (size_t)9 * S;
+  ea.cost_terms = ea.cost_total + S;
+  ea.collision = p->ep_ilog.p;
+  ea.fallback = p->ep_ilog.p + S;
+  ea.stat = p->ep_ilog.p + 2 * S;
+  const int unroll = std::min(S, kEpisodeUnroll);
+  // the graph bakes in the arguments (buffer pointers, sizes, dt, ...): reuse
+  // the previous one when they are the same, recapture otherwise
+  std::vector<unsigned char> key(sizeof(ea) + sizeof(int));
+  memcpy(key.data(), &ea, sizeof(ea));
+  memcpy(key.data() + sizeof(ea), &unroll, sizeof(int));
+  if (!p->ep_graph || key != p->ep_key) {
+    if (p->ep_graph) cudaGraphExecDestroy(p->ep_graph);
+    p->ep_graph = nullptr;
+    CKR(capture_episode_graph(p, ea, unroll, &p->ep_graph));
+    p->ep_key = key;
+  }
+  cudaGraphExec_t exec = p->ep_graph;
+  // ---- ceil(S / unroll) replays back to back, one synchronisation
+  cudaError_t e = cudaEventRecord(p->ev0, st);
+  for (int i = 0; i < S && e == cudaSuccess; i += unroll) e = cudaGraphLaunch(exec, st);
+  if (e == cudaSuccess) e = cudaEventRecord(p->ev1, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) return fail(MPPI_E_CUDA, std::string("episode: ") + cudaGetErrorString(e));
+  float ms = 0.f;
+  CK(cudaEventElapsedTime(&ms, p->ev0, p->ev1));
+  CK(cudaMemcpy(&h, p->ep_state.p, sizeof(h), cudaMemcpyDeviceToHost));
+  const int done = h.i;
+  // ---- log and state back to the caller
+  std::vector<double> fl(flog);
+  std::vector<int> il((size_t)3 * S);
+  CK(cudaMemcpy(fl.data(), L, sizeof(double) * flog, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(il.data(), p->ep_ilog.p, sizeof(int) * 3 * S, cudaMemcpyDeviceToHost));
+  auto col = [&](double* dst, const double* src, size_t width) {
+    if (dst) memcpy(dst, src, sizeof(double) * width * done);
+  };
+  const double* F = fl.data();
+  col(lg->t, F, 1);
+  col(lg->theta, F + S, D);
+  col(lg->theta_dot, F + (size_t)S * (1 + D), D);
+  col(lg->command, F + (size_t)S * (1 + 2 * D), D);
+  col(lg->goal, F + (size_t)S * (1 + 3 * D), 3);
+  col(lg->goal_rot, F + (size_t)S * (4 + 3 * D), 9);
+  col(lg->ee, F + (size_t)S * (13 + 3 * D), 3);
+  col(lg->ee_rot, F + (size_t)S * (16 + 3 * D), 9);
+  col(lg->cost_total, F + (size_t)S * (25 + 3 * D), 1);
+  if (lg->cost_terms)
+    for (int k = 0; k < N_TERMS; ++k)
+      memcpy(lg->cost_terms + (size_t)k * S, F + (size_t)S * (26 + 3 * D + k), sizeof(double) * done);
+  if (lg->collision) memcpy(lg->collision, il.data(), sizeof(int) * done);
+  if (lg->fallback) memcpy(lg->fallback, il.data() + S, sizeof(int) * done);
+  if (lg->status) memcpy(lg->status, il.data() + 2 * S, sizeof(int) * done);
+  for (int j = 0; j < 2 * D; ++j) {
+    es->last_estimate[j] = h.est[j];
+    es->plant[j] = h.plant[j];
+  }
+  for (int j = 0; j < D; ++j) {
+    es->last_command[j] = h.last_cmd[j];
+    es->prev_command[j] = h.prev_cmd[j];
+  }
+  es->fallback_armed = h.armed;
+  es->aborted = h.aborted;
+  p->step_counter += (unsigned long long)done;
+  if (script && done > 0) {  // the plan goal is the last script goal; keep goal_host in step
+    CK(cudaMemcpy(p->goal_host.data(), p->goal.p, sizeof(double) * 16, cudaMemcpyDeviceToHost));
+  }
+  if (steps_done) *steps_done = done;
+  if (device_ms) *device_ms = ms;
   return MPPI_OK;
 }
 

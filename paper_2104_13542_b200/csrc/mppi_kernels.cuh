@@ -644,7 +644,7 @@ static __device__ void finalize_policy(const StatsArgs<R>& a, int b, const doubl
         var[o] = vo;
         sd[o] = so;
       }
-    } else if (a.shift) {  // failure: the shift of controller.py:200 still stands
+    } else if (a.shift && s_status != MPPI_E_SKIPPED) {  // failure: the shift of controller.py:200 still stands
       means[o] = mo;
       var[o] = vo;
       sd[o] = so;

@@ -278,6 +278,69 @@ class Plan:
                 "term_breakdown": {nm: res["terms"][i] for i, nm in enumerate(TERM_NAMES)},
                 "total_per_particle": res["totals"], "weights": res["weights"]}
 
+    def episode(self, steps: int, dt: float, filter_lambda: float, theta0, theta_dot0, *,
+                prev_command=None, fallback_armed: bool = False, script=None, noise=None) -> dict:
+        """Closed-loop episode on the device (mppi_episode). ``script`` is
+        (times (W,), positions (W,3), interpolation code, goal-mode code) or
+        None for the plan's current goal; ``noise`` (steps, 2d) are the plant
+        noise draws. Returns the log columns trimmed to the steps run, the
+        final filter / fallback / plant state and the device time."""
+        d, S = self.dof, int(steps)
+        desc = N.EpisodeDesc()
+        desc.steps = S
+        desc.dt = float(dt)
+        desc.filter_lambda = float(filter_lambda)
+        keep = []
+        if script is not None:
+            times, positions, interp, mode = script
+            times = N.f64(times)
+            positions = N.f64(positions).reshape(-1, 3)
+            keep += [times, positions]
+            desc.goal_source = N.GOAL_SCRIPT
+            desc.interpolation = int(interp)
+            desc.script_mode = int(mode)
+            desc.waypoints = times.shape[0]
+            desc.times = N.dptr(times)
+            desc.positions = N.dptr(positions)
+        if noise is not None:
+            noise = N.f64(noise).reshape(S, 2 * d)
+            keep.append(noise)
+            desc.noise = N.dptr(noise)
+        st = N.EpisodeState()
+        if prev_command is not None:
+            for j in range(d):
+                st.prev_command[j] = float(prev_command[j])
+        st.fallback_armed = int(bool(fallback_armed))
+        S1 = max(S, 1)
+        cols = {"t": np.zeros(S1), "theta": np.zeros((S1, d)), "theta_dot": np.zeros((S1, d)),
+                "command": np.zeros((S1, d)), "goal": np.zeros((S1, 3)), "goal_rot": np.zeros((S1, 9)),
+                "ee": np.zeros((S1, 3)), "ee_rot": np.zeros((S1, 9)), "cost_total": np.zeros(S1),
+                "cost_terms": np.zeros((6, S1))}
+        icols = {k: np.zeros(S1, dtype=np.int32) for k in ("collision", "fallback", "status")}
+        lg = N.EpisodeLogC()
+        for k, v in cols.items():
+            setattr(lg, k, N.dptr(v))
+        for k, v in icols.items():
+            setattr(lg, k, v.ctypes.data_as(C.POINTER(C.c_int32)))
+        done = C.c_int32(0)
+        ms = C.c_double(0.0)
+        th0 = N.f64(theta0, (d,))
+        thd0 = N.f64(theta_dot0, (d,))
+        N.check(self.lib.mppi_episode(self.handle, C.byref(desc), N.dptr(th0), N.dptr(thd0), C.byref(st),
+                                      C.byref(lg), C.byref(done), C.byref(ms)))
+        n = int(done.value)
+        out = {k: (v[:, :n] if k == "cost_terms" else v[:n]) for k, v in cols.items()}
+        out.update({k: v[:n] for k, v in icols.items()})
+        out["steps_done"] = n
+        out["device_ms"] = float(ms.value)
+        out["aborted"] = bool(st.aborted)
+        out["fallback_armed"] = bool(st.fallback_armed)
+        out["last_estimate"] = np.array(st.last_estimate[:2 * d])
+        out["last_command"] = np.array(st.last_command[:d])
+        out["prev_command"] = np.array(st.prev_command[:d])
+        out["plant"] = np.array(st.plant[:2 * d])
+        return out
+
     def time_stage(self, stage: int, reps: int = 50) -> float:
         """Mean device ms per launch of one stage (0 rollout, 1 MLP, 2 stats, 3 whole graph)."""
         ms = C.c_double(0.0)

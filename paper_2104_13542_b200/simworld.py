@@ -199,3 +199,51 @@ def target_at(script: TargetScript, t: float):
     from .costs import goal_at_position
 
     return goal_at_position(target_position_at(script, t), mode=script.mode)
+
+
+def script_from_waypoints(waypoints, interpolation: str = HOLD, mode: str = "position_only") -> TargetScript:
+    """TargetScript from (time, position) pairs or flat [time, x, y(, z)] rows (simworld.py:152-165)."""
+    times, positions = [], []
+    for w in waypoints:
+        times.append(float(w[0]))
+        positions.append(_pad3(w[1] if len(w) == 2 and np.ndim(w[1]) == 1 else w[1:]))
+    return TargetScript(times=np.array(times), positions=np.array(positions),
+                        interpolation=interpolation, mode=mode)
+
+
+def _pad3(p) -> np.ndarray:
+    """Planar positions get z = 0 (simworld.py:168-172)."""
+    p = np.asarray(p, dtype=np.float64).ravel()
+    return np.array([p[0], p[1], 0.0]) if p.size == 2 else p
+
+
+# ---------------------------------------------------------------- plant (host form)
+def sim_step(state, command, dt: float, noise_sigma: float = 0.0, rng=None):
+    """One plant step (simworld.py:108-127): the rollouts' semi-implicit Euler
+    plus optional Gaussian state noise drawn from ``rng`` (position first, then
+    velocity). run_episode's device loop consumes the same draws."""
+    from .rollout import JointState
+
+    if dt <= 0.0:
+        raise ContractError("dt must be positive")
+    u = np.asarray(command, dtype=np.float64)
+    vel = state.theta_dot + dt * u
+    pos = state.theta + dt * vel
+    if noise_sigma > 0.0:
+        if rng is None:
+            raise ContractError("state noise requires an rng")
+        pos = pos + rng.normal(0.0, noise_sigma, size=pos.shape)
+        vel = vel + rng.normal(0.0, noise_sigma, size=vel.shape)
+    return JointState(theta=pos, theta_dot=vel, theta_ddot=u.copy(), stamp=state.stamp + dt)
+
+
+def collision_query(world: WorldModel, chain, rot, trans):
+    """(collided, first obstacle index) of one configuration's link poses
+    through the operator seam's env_collision_batch (simworld.py:200-212)."""
+    from . import kernels
+
+    rot = np.asarray(rot, dtype=np.float64).reshape(1, chain.dof, 3, 3)
+    trans = np.asarray(trans, dtype=np.float64).reshape(1, chain.dof, 3)
+    hit = kernels.env_collision_batch(rot, trans, chain.cap_p0, chain.cap_p1, chain.cap_r, chain.cap_link,
+                                      world.spheres, world.boxes)[0]
+    return bool(hit >= 0), int(hit)

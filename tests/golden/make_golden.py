@@ -31,7 +31,8 @@ from jointmpc.policy import (UpdateConfig, make_policy, particle_weights, shift,
 from jointmpc.rollout import JointState, evaluate_rollouts, make_dt_schedule  # noqa: E402
 from jointmpc.sampling import (HALTON, SmoothingSpec, bspline_basis, gaussianize,  # noqa: E402
                                halton_points, smooth_sequences)
-from jointmpc.simworld import WorldModel, sim_step  # noqa: E402
+from jointmpc.controller import FilterState, filter_state, run_episode  # noqa: E402
+from jointmpc.simworld import TargetScript, WorldModel, sim_step, target_position_at  # noqa: E402
 from jointmpc.surrogate import LearnedSelfCollision  # noqa: E402
 
 from paper_2104_13542_b200 import configs  # noqa: E402  (numbers only)
@@ -198,6 +199,74 @@ def world_fixture():
          term_stop=b.term_breakdown["stop"], term_pose=b.term_breakdown["pose"])
 
 
+def episode_parts():
+    """Small known answers of the episode driver's pieces: target_position_at
+    (hold / linear, before / inside / after the script), filter_state, sim_step
+    with noise."""
+    times = np.array([0.0, 0.3, 0.5, 1.2])
+    pos = np.array([[0.1, 0.2, 0.3], [0.4, -0.2, 0.6], [0.0, 0.0, 0.9], [-0.3, 0.5, 0.2]])
+    ts = np.array([0.0, 0.05, 0.3, 0.31, 0.499, 0.5, 0.9, 1.2, 1.5, 7.0])
+    hold = np.array([target_position_at(TargetScript(times, pos, "hold"), t) for t in ts])
+    lin = np.array([target_position_at(TargetScript(times, pos, "linear"), t) for t in ts])
+    rng = np.random.default_rng(11)
+    raw = JointState(theta=rng.normal(size=7), theta_dot=rng.normal(size=7), theta_ddot=np.zeros(7))
+    filt = FilterState(lam=0.3, last_command=rng.normal(size=7),
+                       last_estimate=JointState(theta=rng.normal(size=7), theta_dot=rng.normal(size=7),
+                                                theta_ddot=np.zeros(7)))
+    le_th, le_thd, lc = filt.last_estimate.theta.copy(), filt.last_estimate.theta_dot.copy(), filt.last_command.copy()
+    est = filter_state(raw, filt, 0.05)
+    u = rng.normal(size=7)
+    nxt = sim_step(raw, u, 0.05, noise_sigma=0.01, rng=np.random.default_rng(5))
+    save("episode_parts", times=times, positions=pos, ts=ts, hold=hold, linear=lin,
+         raw_theta=raw.theta, raw_theta_dot=raw.theta_dot, le_theta=le_th, le_theta_dot=le_thd,
+         last_command=lc, est_theta=est.theta, est_theta_dot=est.theta_dot, u=u,
+         sim_theta=nxt.theta, sim_theta_dot=nxt.theta_dot)
+
+
+def episode_fixture(name, config, steps, particles=500, script=None, goal=None, noise_sigma=0.0,
+                    sim_seed=0, world=None):
+    """Reference run_episode (controller.py:331-416): every EpisodeLog column
+    plus the controller state it leaves behind."""
+    c = reach_controller(config, particles, world=world)
+    x0 = JointState(theta=configs.REACH_START.copy(), theta_dot=np.zeros(7), theta_ddot=np.zeros(7))
+    lg = run_episode(c, x0, script if script is not None else goal, steps, noise_sigma=noise_sigma,
+                     sim_seed=sim_seed)
+    rec = dict(t=lg.t, theta=lg.theta, theta_dot=lg.theta_dot, command=lg.command, goal=lg.goal, ee=lg.ee,
+               cost_total=lg.cost_total, collision=lg.collision, aborted=np.array(lg.aborted),
+               goal_rotations=lg.goal_rotations, ee_rotations=lg.ee_rotations,
+               final_means=c.policy.means, final_variances=c.policy.variances,
+               filt_last_command=c.filter.last_command, filt_theta=c.filter.last_estimate.theta,
+               filt_theta_dot=c.filter.last_estimate.theta_dot, noise_sigma=np.array(noise_sigma),
+               sim_seed=np.array(sim_seed), steps=np.array(steps), particles=np.array(particles),
+               csv=np.array(lg.to_csv()))
+    for k, v in lg.cost_terms.items():
+        rec[f"term_{k}"] = v
+    if script is not None:
+        rec.update(script_times=script.times, script_positions=script.positions,
+                   script_interp=np.array(script.interpolation), script_mode=np.array(script.mode))
+    if world is not None:
+        rec.update(boxes=world.boxes, spheres=world.spheres)
+    save(name, **rec)
+
+
+def episode_fixtures():
+    lin = TargetScript(times=np.array([0.0, 0.2, 0.45]),
+                       positions=np.array([[0.45, 0.1, 0.55], [0.35, -0.2, 0.6], [0.5, 0.05, 0.4]]),
+                       interpolation="linear", mode="position_only")
+    episode_fixture("episode_c1", 1, steps=12, script=lin, noise_sigma=0.002, sim_seed=7)
+    goal = GoalSpec(target_pose=Pose(rotation=_rpy_matrix(*configs.REACH_GOAL_RPY),
+                                     translation=configs.REACH_GOAL_POS.copy()), mode=FULL_POSE)
+    episode_fixture("episode_c2", 2, steps=6, goal=goal)
+    from paper_2104_13542_b200.simworld import seeded_box_grid
+
+    grid_world = seeded_box_grid(n_boxes=8, dims=64, seed=3, max_extent=10)
+    world = WorldModel(spheres=np.array([[0.35, 0.25, 0.55, 0.08]]), boxes=grid_world.boxes,
+                       bounds_min=np.full(3, -1.0), bounds_max=np.full(3, 1.0))
+    hold = TargetScript(times=np.array([0.0, 0.1]), positions=np.array([[0.45, 0.1, 0.55], [0.4, 0.2, 0.5]]),
+                        interpolation="hold", mode="position_only")
+    episode_fixture("episode_c3", 3, steps=5, particles=128, script=hold, world=world)
+
+
 if __name__ == "__main__":
     which = set(sys.argv[1:])
     jobs = {"sampling": sampling_fixtures, "kinematics": kinematics_fixtures, "mlp": mlp_fixtures,
@@ -206,7 +275,7 @@ if __name__ == "__main__":
             "step_c2": lambda: step_fixture("step_c2", 2),
             "step_c2_iso_k2": lambda: step_fixture("step_c2_iso_k2", 2, particles=256, steps=2,
                                                    policy_mode="isotropic", iterations=2),
-            "step_world": world_fixture}
+            "step_world": world_fixture, "episode_parts": episode_parts, "episodes": episode_fixtures}
     for name, fn in jobs.items():
         if not which or name in which:
             fn()
