@@ -216,15 +216,17 @@ class Controller:
 
     def _sync_goal(self):
         """Upload cost_stack.goal when it changed (a new GoalSpec, or its arrays
-        edited in place — both are compared against the uploaded copy)."""
+        edited in place — both are compared, as bytes, against the uploaded copy)."""
         g = self.cost_stack.goal
-        R, t = g.target_pose.rotation, g.target_pose.translation
+        pose = g.target_pose
         up = self._goal_uploaded
-        if up is not None and up[0] is g and up[1] == g.mode and np.array_equal(up[2], t) and \
-                np.array_equal(up[3], R):
+        if up is not None and up[0] is g and up[1] == g.mode and up[2] == pose.translation.tobytes() and \
+                up[3] == pose.rotation.tobytes():
             return
+        R = np.ascontiguousarray(pose.rotation, dtype=np.float64)
+        t = np.ascontiguousarray(pose.translation, dtype=np.float64)
         self._plan.set_goal(R, t, g.mode_code, 0)
-        self._goal_uploaded = (g, g.mode, np.array(t, dtype=np.float64), np.array(R, dtype=np.float64))
+        self._goal_uploaded = (g, g.mode, pose.translation.tobytes(), pose.rotation.tobytes())
 
     def profile_stages(self, level: int = 2):
         """Fill StepDiagnostics.sample_ms / rollout_ms / update_ms from device
@@ -236,8 +238,7 @@ class Controller:
     def control_step(self, state: JointState) -> tuple[np.ndarray, StepDiagnostics]:
         t_start = time.perf_counter()
         self._sync_goal()
-        cmds, infos = self._plan.step(state.theta, state.theta_dot)
-        info = infos[0]
+        cmd_view, info = self._plan.step_single(state.theta, state.theta_dot)
         self._step_serial += 1
         if info.status != N.OK:
             exc = N.status_exception(info.status, info.bad_particle)
@@ -256,7 +257,7 @@ class Controller:
                                             mean_cost=float("nan"), fallback=mode)
         self._fallback_armed = False
         if self.command_mode == "mean":
-            command = cmds[0]
+            command = cmd_view.copy()
         else:  # host rng, as next_command(policy, "sample", rng) (policy.py:174-176)
             pol = self.policy
             command = self.rng.normal(pol.means[0], pol.stddev()[0])
@@ -473,8 +474,8 @@ def _run_episode_device(controller, x0, goal_source, steps, noise_sigma, sim_see
     if script is not None and n > 0:
         goal = target_at(goal_source, (n - 1) * dt)
         controller.cost_stack.goal = goal
-        controller._goal_uploaded = (goal, goal.mode, np.array(goal.target_pose.translation),
-                                     np.array(goal.target_pose.rotation))
+        controller._goal_uploaded = (goal, goal.mode, goal.target_pose.translation.tobytes(),
+                                     goal.target_pose.rotation.tobytes())
     for i in np.flatnonzero(r["fallback"] != N.FALLBACK_NONE):
         mode = "reissue" if r["fallback"][i] == N.FALLBACK_REISSUE else "brake"
         log.warning("control step %d failed (%s); fell back to %s", i,

@@ -17,6 +17,8 @@ import numpy as np
 from . import _native as N
 from .errors import ConfigError
 
+_F64 = np.dtype(np.float64)
+
 
 @dataclass
 class PlanSpec:
@@ -135,6 +137,11 @@ class Plan:
         self._thd = np.zeros((self.B, self.dof))
         self._p_th, self._p_thd, self._p_cmd = N.dptr(self._th), N.dptr(self._thd), N.dptr(self._cmd)
         self._step_fn = self.lib.mppi_step
+        # address-level entry for the single-controller latency path: caller
+        # arrays go straight to mppi_step (it copies them into pinned staging)
+        proto = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p)
+        self._step_raw = proto(C.cast(self.lib.mppi_step, C.c_void_p).value)
+        self._a_cmd, self._a_info = self._cmd.ctypes.data, C.addressof(self._info)
         if provider is not None and self.kind == N.SELFCOLL_LEARNED:
             self.set_mlp(provider)
         if world is not None:
@@ -232,6 +239,21 @@ class Plan:
         if rc:
             N.check(rc)
         return self._cmd.copy(), self._info
+
+    def step_single(self, theta, theta_dot):
+        """step() for B = 1 with float64 (d,) inputs: no staging copies on the
+        Python side. Returns (command (d,) view of the plan's output buffer,
+        info of instance 0); the view is overwritten by the next step."""
+        if (type(theta) is np.ndarray and type(theta_dot) is np.ndarray and theta.dtype == _F64
+                and theta_dot.dtype == _F64 and theta.size == self.dof and theta_dot.size == self.dof
+                and theta.flags.c_contiguous and theta_dot.flags.c_contiguous):
+            rc = self._step_raw(self.handle.value, theta.ctypes.data, theta_dot.ctypes.data, self._a_cmd,
+                                self._a_info)
+            if rc:
+                N.check(rc)
+            return self._cmd[0], self._info[0]
+        cmds, infos = self.step(theta, theta_dot)
+        return self._cmd[0], infos[0]
 
     def profile_stages(self, level: int = 2):
         """0: lean graph, no timing; 1: device_ms of the lean graph; 2: the
