@@ -17,7 +17,7 @@ import numpy as np
 
 from .errors import ConfigError, ContractError, DeviceError, PolicyStateError
 
-LIB_PATH = Path(__file__).resolve().parent / "_mppi_b200.so"
+LIB_PATH = Path(os.environ.get("MPPI_LIB") or Path(__file__).resolve().parent / "_mppi_b200.so")  # MPPI_LIB: A/B builds
 
 # enum mppi_status
 OK = 0
