@@ -351,6 +351,47 @@ int mppi_episode(mppi_plan* plan, const mppi_episode_desc* desc, const double* t
                  const double* theta_dot0, mppi_episode_state* state, mppi_episode_log* log,
                  int32_t* steps_done, double* device_ms);
 
+/* ---- surrogate training on the device --------------
+ * train_collision_surrogate (surrogate.py:146-206) in float64: mini-batch MSE
+ * on the (2d -> 256 -> 128 -> 64 -> 1) ReLU MLP, Adam (0.9, 0.999, 1e-8) with
+ * the per-epoch step size lr[e], then the holdout MAE and sign agreement.
+ * The caller supplies what the reference draws from its numpy generator —
+ * the encoded samples, the labels, the per-epoch permutations, the He
+ * initialisation (in weights / biases, overwritten with the trained values)
+ * — and the Adam bias corrections 1 - beta^t per step, so the device trains
+ * on the reference's inputs bit for bit. */
+typedef struct mppi_train_desc {
+  int32_t in_dim;             /* 2d                                         */
+  int32_t n_train;
+  int32_t n_hold;
+  int32_t epochs;
+  int32_t batch_size;         /* <= 1024                                    */
+  int32_t _pad;
+  const double* x_train;      /* (n_train, in_dim) positional encodings     */
+  const double* y_train;      /* (n_train,) oracle distances                */
+  const double* x_hold;       /* (n_hold, in_dim)                           */
+  const double* y_hold;       /* (n_hold,)                                  */
+  const int64_t* order;       /* (epochs, n_train) rng.permutation per epoch */
+  const double* lr;           /* (epochs,) step size of each epoch          */
+  const double* bias_corr1;   /* (epochs * ceil(n_train / batch)) 1 - 0.9^t   */
+  const double* bias_corr2;   /* same, 1 - 0.999^t                          */
+} mppi_train_desc;
+
+typedef struct mppi_train_result {
+  int64_t steps;              /* optimiser steps taken                      */
+  int32_t diverged_epoch;     /* epoch of the first non-finite loss, or -1  */
+  int32_t _pad;
+  double last_finite_loss;
+  double holdout_mae;
+  double sign_agreement;
+  double device_ms;           /* the training loop on the device            */
+  double* losses;             /* optional out (epochs * batches) or NULL    */
+} mppi_train_result;
+
+/* weights[l] (dims[l], dims[l+1]) and biases[l] (dims[l+1]), l = 0..3. */
+int mppi_train_mlp(const mppi_train_desc* desc, double* const* weights, double* const* biases,
+                   mppi_train_result* result);
+
 /* Step timing level. 0 (default): the lean step graph, no timing calls on the
  * latency path. 1: two stream events around the lean graph fill
  * mppi_step_info.device_ms. 2: an instrumented copy of the graph with

@@ -126,6 +126,23 @@ class EpisodeState(C.Structure):
     ]
 
 
+class TrainDesc(C.Structure):
+    _fields_ = [
+        ("in_dim", C.c_int32), ("n_train", C.c_int32), ("n_hold", C.c_int32), ("epochs", C.c_int32),
+        ("batch_size", C.c_int32), ("_pad", C.c_int32),
+        ("x_train", _dp), ("y_train", _dp), ("x_hold", _dp), ("y_hold", _dp),
+        ("order", C.POINTER(C.c_int64)), ("lr", _dp), ("bias_corr1", _dp), ("bias_corr2", _dp),
+    ]
+
+
+class TrainResult(C.Structure):
+    _fields_ = [
+        ("steps", C.c_int64), ("diverged_epoch", C.c_int32), ("_pad", C.c_int32),
+        ("last_finite_loss", C.c_double), ("holdout_mae", C.c_double), ("sign_agreement", C.c_double),
+        ("device_ms", C.c_double), ("losses", _dp),
+    ]
+
+
 # name -> (restype, argtypes); every function returns int status unless noted
 _vp = C.c_void_p
 _SIGS = {
@@ -153,6 +170,7 @@ _SIGS = {
     "mppi_get_bundle": (C.c_int, [_vp, C.POINTER(EvalOut), _dp]),
     "mppi_episode": (C.c_int, [_vp, C.POINTER(EpisodeDesc), _dp, _dp, C.POINTER(EpisodeState),
                                C.POINTER(EpisodeLogC), _ip, _dp]),
+    "mppi_train_mlp": (C.c_int, [C.POINTER(TrainDesc), C.POINTER(_dp), C.POINTER(_dp), C.POINTER(TrainResult)]),
     "mppi_time_stage": (C.c_int, [_vp, C.c_int32, C.c_int32, _dp]),
     "mppi_profile_stages": (C.c_int, [_vp, C.c_int32]),
     "mppi_stats_record_len":(C.c_int, [_vp, C.POINTER(C.c_int32)]),

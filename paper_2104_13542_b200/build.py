@@ -25,7 +25,7 @@ OBJ = ROOT / "build" / "obj"
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
          f"-I{ROOT / 'include'}"] + os.environ.get("MPPI_NVCC_FLAGS", "").split()
-SOURCES = ["mppi_abi.cu", "mppi_launch_f32.cu", "mppi_launch_f64.cu"]
+SOURCES = ["mppi_abi.cu", "mppi_launch_f32.cu", "mppi_launch_f64.cu", "mppi_train.cu"]
 
 
 def nvcc() -> str:

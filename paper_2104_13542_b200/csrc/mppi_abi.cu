@@ -622,6 +622,9 @@ int32_t mppi_abi_version(void) { return MPPI_ABI_VERSION; }
 
 const char* mppi_last_error(void) { return g_last_error.c_str(); }
 
+// error hand-off from the other translation units (mppi_train.cu); not part of the public header
+int mppi_internal_fail(int code, const char* msg) { return fail(code, msg); }
+
 const char* mppi_build_info(void) {
 #define MPPI_STR2(x) #x
 #define MPPI_STR(x) MPPI_STR2(x)

@@ -267,6 +267,29 @@ def episode_fixtures():
     episode_fixture("episode_c3", 3, steps=5, particles=128, script=hold, world=world)
 
 
+def training_fixtures():
+    """Reference train_collision_surrogate runs (surrogate.py:146-206): a short
+    one (3 epochs) for weight-level parity, one through both step-size halvings
+    (80 epochs), and the acceptance configuration's metrics (50k samples, 100
+    epochs, seed 0; test_acceptance.py:267-279)."""
+    import time
+
+    from jointmpc.surrogate import train_collision_surrogate
+
+    arm7 = load_chain("arm7.chain")
+    for name, samples, seed, epochs in (("train_short", 2000, 3, 3), ("train_sched", 3000, 5, 80)):
+        m = train_collision_surrogate(arm7, samples, seed, epochs=epochs)
+        rec = {f"W{i}": w for i, w in enumerate(m.net.weights)}
+        rec.update({f"b{i}": v for i, v in enumerate(m.net.biases)})
+        save(name, samples=np.array(samples), seed=np.array(seed), epochs=np.array(epochs),
+             holdout_mae=np.array(m.holdout_mae), sign_agreement=np.array(m.sign_agreement), **rec)
+    t0 = time.perf_counter()
+    m = train_collision_surrogate(arm7, 50_000, 0)
+    save("train_accept", samples=np.array(50_000), seed=np.array(0), epochs=np.array(100),
+         holdout_mae=np.array(m.holdout_mae), sign_agreement=np.array(m.sign_agreement),
+         cpu_seconds=np.array(time.perf_counter() - t0))
+
+
 if __name__ == "__main__":
     which = set(sys.argv[1:])
     jobs = {"sampling": sampling_fixtures, "kinematics": kinematics_fixtures, "mlp": mlp_fixtures,
@@ -275,7 +298,8 @@ if __name__ == "__main__":
             "step_c2": lambda: step_fixture("step_c2", 2),
             "step_c2_iso_k2": lambda: step_fixture("step_c2_iso_k2", 2, particles=256, steps=2,
                                                    policy_mode="isotropic", iterations=2),
-            "step_world": world_fixture, "episode_parts": episode_parts, "episodes": episode_fixtures}
+            "step_world": world_fixture, "episode_parts": episode_parts, "episodes": episode_fixtures,
+            "training": training_fixtures}
     for name, fn in jobs.items():
         if not which or name in which:
             fn()
