@@ -392,6 +392,12 @@ typedef struct mppi_train_result {
 int mppi_train_mlp(const mppi_train_desc* desc, double* const* weights, double* const* biases,
                    mppi_train_result* result);
 
+/* Telemetry: the k (<= 64) best rollouts of instance 0's last iteration
+ * (bridge.py:196-203 — argsort of the totals, then the end-effector path of
+ * each): particle indices (k), their totals (k) and end-effector positions
+ * (k, H, 3). Ties go to the lower index. Needs a plan created with dump = 1. */
+int mppi_top_rollouts(mppi_plan* plan, int32_t k, int32_t* index_out, double* totals_out, double* ee_out);
+
 /* Step timing level. 0 (default): the lean step graph, no timing calls on the
  * latency path. 1: two stream events around the lean graph fill
  * mppi_step_info.device_ms. 2: an instrumented copy of the graph with

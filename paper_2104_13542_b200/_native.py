@@ -170,6 +170,7 @@ _SIGS = {
     "mppi_get_bundle": (C.c_int, [_vp, C.POINTER(EvalOut), _dp]),
     "mppi_episode": (C.c_int, [_vp, C.POINTER(EpisodeDesc), _dp, _dp, C.POINTER(EpisodeState),
                                C.POINTER(EpisodeLogC), _ip, _dp]),
+    "mppi_top_rollouts": (C.c_int, [_vp, C.c_int32, _ip, _dp, _dp]),
     "mppi_train_mlp": (C.c_int, [C.POINTER(TrainDesc), C.POINTER(_dp), C.POINTER(_dp), C.POINTER(TrainResult)]),
     "mppi_time_stage": (C.c_int, [_vp, C.c_int32, C.c_int32, _dp]),
     "mppi_profile_stages": (C.c_int, [_vp, C.c_int32]),

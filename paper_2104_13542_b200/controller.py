@@ -274,6 +274,23 @@ class Controller:
                                         update_ms=info.update_ms, best_cost=info.best_cost,
                                         mean_cost=info.mean_cost, bundle=bundle)
 
+    def top_rollouts(self, k: int):
+        """The k best rollouts of the last step for telemetry (bridge.py:196-203):
+        (particle indices (k,), totals (k,), end-effector paths (k, H, coords)),
+        selected and run through FK on the device. Needs keep_bundle=True."""
+        import ctypes as C
+
+        if not self.keep_bundle:
+            raise ContractError("top_rollouts needs keep_bundle=True")
+        k = int(k)
+        idx = np.empty(k, dtype=np.int32)
+        tot = np.empty(k)
+        ee = np.empty((k, self.horizon, 3))
+        N.check(self._plan.lib.mppi_top_rollouts(self._plan.handle, k, idx.ctypes.data_as(C.POINTER(C.c_int32)),
+                                                 N.dptr(tot), N.dptr(ee)))
+        coords = 2 if self.chain.task_dim == 2 else 3
+        return idx.astype(np.int64), tot, ee[:, :, :coords]
+
     def instantaneous_costs(self, state: JointState):
         """Per-term costs of one plant state with the h=0 braking limit (controller.py:262-269)."""
         one = DtSchedule(dts=np.array([self.sched.dts.sum()]))

@@ -1425,6 +1425,34 @@ int mppi_episode(mppi_plan* p, const mppi_episode_desc* d, const double* theta0,
   return MPPI_OK;
 }
 
+int mppi_top_rollouts(mppi_plan* p, int32_t k, int32_t* index_out, double* totals_out, double* ee_out) {
+  if (!p || !index_out || !totals_out || !ee_out) return fail(MPPI_E_BAD_ARGUMENT, "null argument");
+  if (k < 1 || k > 64 || k > p->N) return fail(MPPI_E_BAD_ARGUMENT, "k must lie in [1, min(64, particles)]");
+  if (!p->dump) return fail(MPPI_E_CONFIG, "top rollouts need the bundle dump (plan created with dump = 1)");
+  CKR(set_device(p));
+  cudaStream_t st = p->stream;
+  const int N = p->N, H = p->H, D = p->D;
+  DevBuf<int> idx;
+  DevBuf<double> out;
+  DevBuf<unsigned char> taken;
+  CKR(idx.alloc(k));
+  CKR(out.alloc((size_t)k + (size_t)k * H * 3));
+  CKR(taken.alloc(N));
+  ChainT<double> ch;
+  fill_chain(p->chain, p->costs.k_jl, ch);
+  topk_rollouts_kernel<<<1, 512, 0, st>>>(p->totals.p, N, k, p->d_pos.p, H, D, ch, idx.p, out.p, out.p + k,
+                                          taken.p);
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(index_out, idx.p, sizeof(int) * k, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(totals_out, out.p, sizeof(double) * k, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(ee_out, out.p + k, sizeof(double) * k * H * 3, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  idx.release();
+  out.release();
+  taken.release();
+  return MPPI_OK;
+}
+
 int mppi_profile_stages(mppi_plan* p, int32_t enable) {
   if (!p) return fail(MPPI_E_BAD_ARGUMENT, "null plan");
   p->profile_level = enable < 0 ? 0 : (enable > 2 ? 2 : enable);

@@ -91,6 +91,94 @@ __device__ inline void target_position(const EpisodeArgs& a, double t, double* p
     p[k] = add_(mul_(1.0 - frac, a.positions[3 * lo + k]), mul_(frac, a.positions[3 * hi + k]));
 }
 
+// End-effector frame of one configuration (the last link of fk_batch,
+// jit.py:89-111), float64.
+__device__ inline void ee_frame(const ChainT<double>& ch, const double* q, int D, double* Rw, double* tw) {
+  for (int r = 0; r < 9; ++r) Rw[r] = (r % 4 == 0) ? 1.0 : 0.0;
+  for (int r = 0; r < 3; ++r) tw[r] = 0.0;
+  for (int k = 0; k < D; ++k) {
+    double Rmo[9], tmo[3];
+    if (ch.jtype[k] == 0) {
+      double s, c, Rm[9];
+      sincos(q[k], &s, &c);
+      axis_rotation(ch.axes[k], s, 1.0 - c, Rm);
+      mat33_mul(Rm, ch.orot[k], Rmo);
+      mat33_vec(Rm, ch.otrans[k], tmo);
+    } else {
+      for (int r = 0; r < 9; ++r) Rmo[r] = ch.orot[k][r];
+      for (int r = 0; r < 3; ++r) tmo[r] = q[k] * ch.axes[k][r] + ch.otrans[k][r];
+    }
+    double dtw[3], Rn[9];
+    mat33_vec(Rw, tmo, dtw);
+    for (int r = 0; r < 3; ++r) tw[r] = tw[r] + dtw[r];
+    mat33_mul(Rw, Rmo, Rn);
+    for (int r = 0; r < 9; ++r) Rw[r] = Rn[r];
+    if ((k + 1) % REORTHO_EVERY == 0) orthonormalize(Rw);
+  }
+}
+
+// Top-k rollouts for telemetry (bridge.py:196-203): the k lowest totals of
+// instance 0 (ties to the lower particle index; +inf quarantined rows last),
+// then the end-effector path of each selected particle from the bundle dump.
+// One block: k rounds of a block-wide (total, index) argmin, then k x H FKs.
+__global__ void topk_rollouts_kernel(const double* __restrict__ totals, int N, int k, const double* __restrict__ pos,
+                                     int H, int D, const ChainT<double> ch, int* __restrict__ idx_out,
+                                     double* __restrict__ tot_out, double* __restrict__ ee_out,
+                                     unsigned char* __restrict__ taken) {
+  __shared__ double sv[32];
+  __shared__ int si[32];
+  __shared__ int chosen[64];
+  for (int n = threadIdx.x; n < N; n += blockDim.x) taken[n] = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int r = 0; r < k; ++r) {
+    double bv = CUDART_INF;
+    int bi = 0x7fffffff;
+    for (int n = threadIdx.x; n < N; n += blockDim.x) {
+      if (taken[n]) continue;
+      double v = totals[n];
+      if (isnan(v)) v = CUDART_INF;  // argsort puts NaN last as well
+      if (v < bv || (v == bv && n < bi)) {
+        bv = v;
+        bi = n;
+      }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ov < bv || (ov == bv && oi < bi)) {
+        bv = ov;
+        bi = oi;
+      }
+    }
+    if (lane == 0) {
+      sv[w] = bv;
+      si[w] = bi;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double v = sv[0];
+      int b = si[0];
+      for (int q = 1; q < nw; ++q)
+        if (sv[q] < v || (sv[q] == v && si[q] < b)) {
+          v = sv[q];
+          b = si[q];
+        }
+      chosen[r] = b;
+      idx_out[r] = b;
+      tot_out[r] = totals[b];
+      taken[b] = 1;
+    }
+    __syncthreads();
+  }
+  for (int t = threadIdx.x; t < k * H; t += blockDim.x) {
+    const int r = t / H, h = t - r * H;
+    double Rw[9], tw[3];
+    ee_frame(ch, pos + ((size_t)chosen[r] * H + h) * D, D, Rw, tw);
+    for (int c = 0; c < 3; ++c) ee_out[(size_t)t * 3 + c] = tw[c];
+  }
+}
+
 // aborted, or the section is past the episode's last step
 __device__ __forceinline__ bool episode_over(const EpisodeArgs& a) { return a.ep->aborted || a.ep->i >= a.S; }
 
@@ -172,28 +260,8 @@ __global__ void episode_post_kernel(const __grid_constant__ EpisodeArgs a) {
   for (int k = 0; k < N_TERMS; ++k) a.cost_terms[(size_t)k * S + i] = a.ev_terms[k];
   a.collision[i] = a.ev_terms[T_ENV] > 0.0 ? 1 : 0;
   // end-effector frame: fk_batch(chain, theta)[.., -1] (jit.py:89-111)
-  const ChainT<double>& ch = a.chain;
-  double Rw[9] = {1, 0, 0, 0, 1, 0, 0, 0, 1}, tw[3] = {0, 0, 0};
-  for (int k = 0; k < D; ++k) {
-    double Rmo[9], tmo[3];
-    const double q = ep->plant[k];
-    if (ch.jtype[k] == 0) {
-      double s, c, Rm[9];
-      sincos(q, &s, &c);
-      axis_rotation(ch.axes[k], s, 1.0 - c, Rm);
-      mat33_mul(Rm, ch.orot[k], Rmo);
-      mat33_vec(Rm, ch.otrans[k], tmo);
-    } else {
-      for (int r = 0; r < 9; ++r) Rmo[r] = ch.orot[k][r];
-      for (int r = 0; r < 3; ++r) tmo[r] = q * ch.axes[k][r] + ch.otrans[k][r];
-    }
-    double dtw[3], Rn[9];
-    mat33_vec(Rw, tmo, dtw);
-    for (int r = 0; r < 3; ++r) tw[r] = tw[r] + dtw[r];
-    mat33_mul(Rw, Rmo, Rn);
-    for (int r = 0; r < 9; ++r) Rw[r] = Rn[r];
-    if ((k + 1) % REORTHO_EVERY == 0) orthonormalize(Rw);
-  }
+  double Rw[9], tw[3];
+  ee_frame(a.chain, ep->plant, D, Rw, tw);
   for (int r = 0; r < 3; ++r) a.ee[3 * i + r] = tw[r];
   for (int r = 0; r < 9; ++r) a.ee_rot[9 * i + r] = Rw[r];
   // sim_step: semi-implicit Euler + the caller's noise draws

@@ -513,3 +513,24 @@ def test_fused_rollout_mlp_matches_two_kernel_path(monkeypatch):
         assert b0 == b1 and mc0 == mc1
     np.testing.assert_array_equal(m0, m1)
     np.testing.assert_array_equal(v0, v1)
+
+
+@pytest.mark.gpu
+def test_top_rollouts_match_bundle_argsort(arm7):
+    """Telemetry top-k (bridge.py:196-203): the device selection and FK of the
+    k best paths equal argsort of the bundle totals + fk_batch on the host."""
+    from paper_2104_13542_b200 import configs
+    from paper_2104_13542_b200.kinematics import fk_batch
+
+    c = configs.make_controller(2, particles=500, keep_bundle=True)
+    st = configs.start_state()
+    for _ in range(2):
+        cmd, diag = c.control_step(st)
+    b = diag.bundle
+    tot = b.total_per_particle
+    idx, got_tot, ee = c.top_rollouts(8)
+    order = np.argsort(tot, kind="stable")[:8]
+    np.testing.assert_array_equal(idx, order)
+    np.testing.assert_array_equal(got_tot, tot[order])
+    _, trans = fk_batch(arm7, b.positions[order].reshape(-1, 7))
+    np.testing.assert_allclose(ee, trans[:, -1].reshape(8, 30, 3), atol=1e-12)
