@@ -101,6 +101,38 @@ __device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
 }
 
+__device__ __forceinline__ bool mbar_try(uint32_t bar, uint32_t phase) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, P1;\n}"
+      : "=r"(ok)
+      : "r"(bar), "r"(phase)
+      : "memory");
+  return ok != 0;
+}
+
+// non-blocking probe of a phase (the two-slot issuer polls several barriers)
+__device__ __forceinline__ bool mbar_test(uint32_t bar, uint32_t phase) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, P1;\n}"
+      : "=r"(ok)
+      : "r"(bar), "r"(phase)
+      : "memory");
+  return ok != 0;
+}
+
+#ifdef MPPI_WATCHDOG
+// development builds: a barrier that never completes traps instead of hanging the GPU
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t phase) {
+  for (long long i = 0; !mbar_try(bar, phase); ++i)
+    if (i > (1ll << 24)) __trap();
+}
+#else
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t phase) {
   asm volatile(
       "{\n\t.reg .pred P1;\n"
@@ -110,6 +142,7 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t phase) {
       "r"(phase)
       : "memory");
 }
+#endif
 
 __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
   asm volatile(
