@@ -127,13 +127,30 @@ __device__ __forceinline__ bool rollout_particle(const RolloutArgs<R>& a, long l
                                                  float* enc) {
   const int b = (int)(g / a.N);
   const int n = (int)(g - (long long)b * a.N);
-  if (a.skip_on_status && a.status[b] != 0) return false;
+  // Every global input of the warp is requested up front and the status word
+  // is tested only once the control loads are in flight: after an L2 flush
+  // each of these is an HBM round trip, and taken one after another they
+  // were the largest part of the rollout's latency.
+  const int status_b = a.skip_on_status ? a.status[b] : 0;
   const int H = a.H;
   const bool act = lane < H;
   const int h = act ? lane : H - 1;
   const ChainT<R>& ch = a.chain;
   const CostT<R>& cs = a.cost;
   const double* st = a.state + (size_t)b * 2 * D;
+  R st_p[D], st_v[D];
+#pragma unroll
+  for (int j = 0; j < D; ++j) {
+    st_p[j] = (R)st[j];
+    st_v[j] = (R)st[D + j];
+  }
+  const double* gl = a.goal + (size_t)b * 16;
+  R Rg[9], tg[3];
+#pragma unroll
+  for (int i = 0; i < 9; ++i) Rg[i] = (R)gl[i];
+#pragma unroll
+  for (int i = 0; i < 3; ++i) tg[i] = (R)gl[9 + i];
+  const int gmode = (int)gl[12];
 
   // ---- controls -> positions / velocities --------------------------------
   R p[D], v[D], u[D];
@@ -145,6 +162,7 @@ __device__ __forceinline__ bool rollout_particle(const RolloutArgs<R>& a, long l
       v[j] = (R)a.in1[row + j];
       u[j] = R(0);
     }
+    if (status_b != 0) return false;
   } else {
     bool bad = false, varbad = false;
     const int ng = n + a.particle_offset;
@@ -175,6 +193,7 @@ __device__ __forceinline__ bool rollout_particle(const RolloutArgs<R>& a, long l
         u[j] = (R)uu;
       }
     }
+    if (status_b != 0) return false;  // the instance already failed (an earlier iteration)
     const unsigned badm = __ballot_sync(0xffffffffu, act && bad);
     const unsigned varm = __ballot_sync(0xffffffffu, act && varbad);
     if (lane == 0 && a.status != nullptr) {
@@ -187,11 +206,16 @@ __device__ __forceinline__ bool rollout_particle(const RolloutArgs<R>& a, long l
     // semi-implicit Euler as two inclusive warp scans over the horizon
     const R dt = act ? a.dts[h] : R(0);
 #pragma unroll
-    for (int j = 0; j < D; ++j) v[j] = (R)st[D + j] + warp_inclusive_scan(dt * u[j], lane);
+    for (int j = 0; j < D; ++j) v[j] = st_v[j] + warp_inclusive_scan(dt * u[j], lane);
 #pragma unroll
-    for (int j = 0; j < D; ++j) p[j] = (R)st[j] + warp_inclusive_scan(dt * v[j], lane);
+    for (int j = 0; j < D; ++j) p[j] = st_p[j] + warp_inclusive_scan(dt * v[j], lane);
   }
 
+#ifdef MPPI_DEBUG_TIMERS
+  unsigned long long* pdbg = (a.dbg != nullptr && threadIdx.x == 0 && blockIdx.x < 256) ? a.dbg + 16 * blockIdx.x
+                                                                                         : nullptr;
+#endif
+  MPPI_TSTAMP(pdbg, 2);  // controls and integration issued
   // ---- forward kinematics, link by link in registers ----------------------
   R Rw[9] = {R(1), R(0), R(0), R(0), R(1), R(0), R(0), R(0), R(1)};
   R tw[3] = {R(0), R(0), R(0)};
@@ -249,15 +273,9 @@ __device__ __forceinline__ bool rollout_particle(const RolloutArgs<R>& a, long l
   }
   __syncwarp();
 
+  MPPI_TSTAMP(pdbg, 3);  // forward kinematics
   // ---- cost terms -----------------------------------------------------------
   // pose (costs.py:76-95)
-  const double* gl = a.goal + (size_t)b * 16;
-  R Rg[9], tg[3];
-#pragma unroll
-  for (int i = 0; i < 9; ++i) Rg[i] = (R)gl[i];
-#pragma unroll
-  for (int i = 0; i < 3; ++i) tg[i] = (R)gl[9 + i];
-  const int gmode = (int)gl[12];
   R pose;
   {
     const R e0 = tw[0] - tg[0], e1 = tw[1] - tg[1], e2 = tw[2] - tg[2];
@@ -384,6 +402,7 @@ __device__ __forceinline__ bool rollout_particle(const RolloutArgs<R>& a, long l
   R envc = R(0);
   if (cs.use_env) envc = env_any_hit(a.world, ch, cap, lane) ? R(1) : R(0);
 
+  MPPI_TSTAMP(pdbg, 4);  // cost terms
   // total_cost (costs.py:176-187) minus the learned self-collision term
   const R stepc = pose + cs.a_stop * stop + cs.a_joint * joint + cs.a_manip * manip +
                   cs.a_coll * (selfc + envc);
