@@ -410,15 +410,18 @@ __device__ __forceinline__ bool rollout_particle(const RolloutArgs<R>& a, long l
   if (act) {
     const size_t m = (size_t)g * H + h;
     a.step[m] = stepc;
-    if (a.mlp_x != nullptr) {
-      float* x = a.mlp_x + m * 16;
+    if (a.mlp_x != nullptr) {  // one 64-byte row, four 16-byte stores
+      float xr[16];
 #pragma unroll
       for (int k = 0; k < D; ++k) {
-        x[k] = (float)sq[k];
-        x[D + k] = (float)cq[k];
+        xr[k] = (float)sq[k];
+        xr[D + k] = (float)cq[k];
       }
 #pragma unroll
-      for (int k = 2 * D; k < 16; ++k) x[k] = 0.f;
+      for (int k = 2 * D; k < 16; ++k) xr[k] = 0.f;
+      float4* x4 = reinterpret_cast<float4*>(a.mlp_x + m * 16);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) x4[q] = make_float4(xr[4 * q], xr[4 * q + 1], xr[4 * q + 2], xr[4 * q + 3]);
     }
     if (enc != nullptr) {
 #pragma unroll
