@@ -154,14 +154,13 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
       MPPI_TSTAMP(pdbg, 8);
       tc_fence_after();
 #pragma unroll
-      for (int c = 0; c < 8; ++c) {
-        const uint64_t wo = umma_off(32 * c, 0, 16) >> 4;
-        umma_f16(tmem + 32 * c, dXH, dW0H + wo, id32, 0);
-        umma_f16(tmem + 32 * c, dXH, dW0L + wo, id32, 1);
-        umma_f16(tmem + 32 * c, dXL, dW0H + wo, id32, 1);
-        if (c == 3) umma_commit(barL1[0]);
+      for (int hf = 0; hf < 2; ++hf) {  // layer 1 as two N=128 halves
+        const uint64_t wo = umma_off(128 * hf, 0, 16) >> 4;
+        umma_f16(tmem + 128 * hf, dXH, dW0H + wo, id128, 0);
+        umma_f16(tmem + 128 * hf, dXH, dW0L + wo, id128, 1);
+        umma_f16(tmem + 128 * hf, dXL, dW0H + wo, id128, 1);
+        umma_commit(barL1[hf]);
       }
-      umma_commit(barL1[1]);
       uint32_t phA = 0;  // parity bit per A buffer
 #pragma unroll
       for (int c = 0; c < 8; ++c) {

@@ -327,16 +327,15 @@ static __global__ void __maxnreg__(88)
       const uint64_t dW1H = umma_desc(sb + OFF_W1H, 128, 4096), dW1L = umma_desc(sb + OFF_W1L, 128, 4096);
       const uint64_t dW2H = umma_desc(sb + OFF_W2H, 128, 2048), dW2L = umma_desc(sb + OFF_W2L, 128, 2048);
       pdl_wait();  // sleep (rather than spin on barX) while the rollout still runs
-      auto issue_l1_all = [&]() {  // the whole of layer 1: 8 chunks of N=32, two commits
+      auto issue_l1_all = [&]() {  // the whole of layer 1: two halves of N=128, one commit each
 #pragma unroll
-        for (int c = 0; c < 8; ++c) {
-          const uint64_t wo = umma_off(32 * c, 0, 16) >> 4;
-          umma_f16(tmem + 32 * c, dXH, dW0H + wo, id32, 0);
-          umma_f16(tmem + 32 * c, dXH, dW0L + wo, id32, 1);
-          umma_f16(tmem + 32 * c, dXL, dW0H + wo, id32, 1);
-          if (c == 3) umma_commit(barL10);
+        for (int hf = 0; hf < 2; ++hf) {  // (N=128 per instruction: small-N MMAs under-fill the tensor pipe)
+          const uint64_t wo = umma_off(128 * hf, 0, 16) >> 4;
+          umma_f16(tmem + 128 * hf, dXH, dW0H + wo, id128, 0);
+          umma_f16(tmem + 128 * hf, dXH, dW0L + wo, id128, 1);
+          umma_f16(tmem + 128 * hf, dXL, dW0H + wo, id128, 1);
+          umma_commit(barL10 + 8 * hf);
         }
-        umma_commit(barL10 + 8);
       };
       uint32_t phA = 0, phX = 0;  // parity bits
       bool first = true;

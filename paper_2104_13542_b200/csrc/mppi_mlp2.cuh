@@ -152,12 +152,11 @@ static __global__ void __launch_bounds__(kM2Threads, 1)
               }
               tc_fence_after();
               const int h = stage[s] == 0 ? 0 : 1;
-#pragma unroll 1
-              for (int c = 0; c < 4; ++c) {
-                const uint64_t wo = umma_off(128 * h + 32 * c, 0, 16) >> 4;
-                umma_f16(R1 + 32 * c, dXH, dW0H + wo, id32, 0);
-                umma_f16(R1 + 32 * c, dXH, dW0L + wo, id32, 1);
-                umma_f16(R1 + 32 * c, dXL, dW0H + wo, id32, 1);
+              {
+                const uint64_t wo = umma_off(128 * h, 0, 16) >> 4;
+                umma_f16(R1, dXH, dW0H + wo, id128, 0);
+                umma_f16(R1, dXH, dW0L + wo, id128, 1);
+                umma_f16(R1, dXL, dW0H + wo, id128, 1);
               }
               umma_commit(sbar(s, h == 0 ? SB_L1A : SB_L1B));
               stage[s] = 1;
