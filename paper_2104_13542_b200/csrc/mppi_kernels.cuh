@@ -451,8 +451,12 @@ __device__ __forceinline__ bool rollout_particle(const RolloutArgs<R>& a, long l
   return true;
 }
 
-template <typename R, int D>
-__global__ void __launch_bounds__(kRolloutWarps * 32)
+// MINB = 1: the latency build (128 registers, one warp per particle and at
+// most one wave); MINB = 6: the throughput build for many waves (80
+// registers, a few spills, 6 CTAs per SM to hide the FK dependency chains;
+// config 4 rollout -6%).
+template <typename R, int D, int MINB = 1>
+__global__ void __launch_bounds__(kRolloutWarps * 32, MINB)
     rollout_kernel(const __grid_constant__ RolloutArgs<R> a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   if (a.pdl_early) pdl_trigger();  // the MLP / statistics grids may be scheduled as SMs free up

@@ -4,6 +4,7 @@
 #pragma once
 
 #include <cstdlib>
+#include <type_traits>
 
 #include "mppi_kernels.cuh"
 
@@ -30,13 +31,16 @@ inline size_t stats_smem_bytes(int ppb, int nblk, int HD) {
 template <typename R, int D>
 cudaError_t launch_rollout_d(const RolloutArgs<R>& a, long long warps, cudaStream_t st) {
   const size_t smem = rollout_needs_caps(a.cost) ? (size_t)kRolloutWarps * a.chain.n_caps * 6 * 32 * sizeof(R) : 0;
+  // many waves of particles: the occupancy build (float only; see rollout_kernel)
+  constexpr long long kThroughputWarps = 32768;
+  const bool many = std::is_same<R, float>::value && warps >= kThroughputWarps && smem <= 24 * 1024;
+  auto kern = many ? rollout_kernel<R, D, 6> : rollout_kernel<R, D, 1>;
   if (smem > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(rollout_kernel<R, D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)smem);
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
   }
   const unsigned grid = (unsigned)((warps + kRolloutWarps - 1) / kRolloutWarps);
-  rollout_kernel<R, D><<<grid, kRolloutWarps * 32, smem, st>>>(a);
+  kern<<<grid, kRolloutWarps * 32, smem, st>>>(a);
   return cudaGetLastError();
 }
 
