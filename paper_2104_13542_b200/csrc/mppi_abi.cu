@@ -300,11 +300,18 @@ void stats_static(mppi_plan* p, int H, double gamma, double tw, StatsArgs<R>& s)
   s.learned = p->learned() ? 1 : 0;
 }
 
-void choose_blocks(int N, int& ppb, int& nblk) {
-  // 32 particles per block (latency: more blocks pull eps/step costs in
+void choose_blocks(int N, int B, int& ppb, int& nblk) {
+  // Many instances (config 4) already fill the GPU: one block per instance,
+  // no record combine (4096 x 500: statistics 2.22 -> 1.59 ms). Otherwise 32
+  // particles per block (latency: more blocks pull eps/step costs in
   // parallel); up to 1024 particles grow the block to keep one <= 16-CTA
   // cluster per instance (stats_cluster_kernel); beyond that at most 296
   // blocks per instance (the record combine is linear in it)
+  if (B >= 64 && N <= 2048) {
+    ppb = N;
+    nblk = 1;
+    return;
+  }
   ppb = 32;
   if (N > 16 * 32 && N <= 16 * 64) ppb = (N + 15) / 16;
   nblk = (N + ppb - 1) / ppb;
@@ -692,7 +699,7 @@ int mppi_plan_create(const mppi_chain_desc* chain, const mppi_cost_desc* costs,
     for (auto& e : p->stage_ev) CK(cudaEventCreate(&e));
     const int B = p->B, D = p->D, H = p->H, N = p->N;
     const size_t HD = (size_t)H * D;
-    choose_blocks(N, p->ppb, p->nblk);
+    choose_blocks(N, B, p->ppb, p->nblk);
     const size_t rsz = p->precision == MPPI_FP64 ? sizeof(double) : sizeof(float);
     const int reclen = kRecHead + 2 * (int)HD;
     CKR(p->eps.alloc((size_t)N * HD));
@@ -1148,7 +1155,7 @@ int mppi_evaluate(mppi_plan* p, int32_t mode, int32_t n, int32_t H, const double
   CKR(p->e_stepbuf.alloc(nh * sizeof(double)));
   CKR(p->e_status.alloc(2));
   int ppb, nblk;
-  choose_blocks(n, ppb, nblk);
+  choose_blocks(n, 1, ppb, nblk);
   CKR(p->e_records.alloc((size_t)nblk * (kRecHead + 2 * H * D)));
   CKR(p->e_counters.alloc(1));
   if (p->learned()) {

@@ -100,3 +100,30 @@ def test_emulated_particle_shards_match_unsharded():
             np.testing.assert_allclose(c, cmd_ref, atol=1e-9)
         np.testing.assert_array_equal(outs[0], outs[1])
         np.testing.assert_allclose(plans[0].get_policy(0)[1], ref.plan.get_policy(0)[1], atol=1e-9)
+
+
+@pytest.mark.parametrize("B", [12, 70])  # multi-block statistics with a record combine / one block per instance
+def test_batched_statistics_layouts_match_oracle(B):
+    """Batches between 9 and 63 instances use 32-particle statistics blocks and
+    the last-block record combine; from 64 instances on, one block per
+    instance (choose_blocks). Both must match independent oracles."""
+    from paper_2104_13542_b200 import configs
+    from paper_2104_13542_b200.batched import BatchedController
+    from paper_2104_13542_b200.kinematics import load_chain
+    from paper_2104_13542_b200.surrogate import load_arm7_surrogate
+
+    n = 128
+    goals, th0 = configs.batched_problem(B)
+    kw = dict(configs.CONTROLLER_KW)
+    kw.pop("seed")
+    kw["particles"] = n
+    bc = BatchedController(load_chain("arm7.chain"), goals, weights=configs.make_weights(2),
+                           self_collision=load_arm7_surrogate(), precision="fp64", **kw)
+    picks = [0, B // 2, B - 1]
+    oracles = {b: _oracle_for(goals[b], th0[b], particles=n) for b in picks}
+    cmds, diag = bc.control_step(th0, np.zeros_like(th0))
+    assert (diag.status == 0).all()
+    for b in picks:
+        ref = oracles[b].step(th0[b], np.zeros(7))
+        np.testing.assert_allclose(cmds[b], ref, atol=1e-4, err_msg=f"instance {b}")
+        np.testing.assert_allclose(bc.policy(b).means, oracles[b].means, atol=1e-4)
