@@ -196,8 +196,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
 #pragma unroll
         for (int j = 0; j < 2; ++j) {
           const uint64_t aj = ao + (uint64_t)(j * 256 >> 4), wj = (uint64_t)((4 * c + 2 * j) * 128 >> 4);
-          umma_f16(acc3, dAH + aj, dW2H + wj, id64, (c | j) ? 1u : 0u);
-          umma_f16(acc3, dAH + aj, dW2L + wj, id64, 1);
+          umma_f16(acc3, dAH + aj, dW2H + wj, id128, (c | j) ? 1u : 0u);  // [W2 hi | W2 lo]
           umma_f16(acc3, dAL + aj, dW2H + wj, id64, 1);
         }
         umma_commit(barL30 + 8 * bf);
@@ -268,10 +267,12 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
     float part = 0.f;
     {
       constexpr int C3 = kMlpH2 / kFusedCG;  // layer-3 columns per warp
-      float y[C3];
+      float y[C3], z[C3];
       tmem_ld_cols<C3>(acc3 + lane_base + C3 * cg, y);
+      tmem_ld_cols<C3>(acc3 + lane_base + 64 + C3 * cg, z);
 #pragma unroll
-      for (int i = 0; i < C3; ++i) part = fmaf(fmaxf(fmaf(y[i], s2, b2[C3 * cg + i]), 0.f), w3[C3 * cg + i], part);
+      for (int i = 0; i < C3; ++i)
+        part = fmaf(fmaxf(fmaf(y[i] + z[i], s2, b2[C3 * cg + i]), 0.f), w3[C3 * cg + i], part);
     }
     float* red = reinterpret_cast<float*>(sm + OFF_A);
     red[cg * 128 + row_in_tile] = part;

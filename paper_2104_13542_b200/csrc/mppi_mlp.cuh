@@ -73,6 +73,7 @@ constexpr uint32_t OFF_BAR = OFF_A + 2 * kABuf;     // 16 mbarriers
 constexpr uint32_t OFF_TMEMPTR = OFF_BAR + 16 * 8;  // 12 used
 constexpr uint32_t kMlpSmem = OFF_TMEMPTR + 16;
 
+static_assert(OFF_W2L == OFF_W2H + 64 * kMlpH1 * 2, "layer-3 N=128 MMA reads W2 hi and lo as one operand");
 static_assert(kMlpSmem <= 232448, "MLP tile does not fit the 227 KiB of shared memory");
 static_assert(kSeg0 % 16 == 0 && kSeg1 % 16 == 0 && kSeg2 % 16 == 0, "bulk copy sizes");
 
@@ -296,7 +297,7 @@ static __global__ void __maxnreg__(88)
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     fence_async_smem();
   }
-  if (warp == 0) {  // TMEM: acc1 8 x 32 (all of layer 1) | acc2 (128) | acc3 (64) -> 448 of 512 columns
+  if (warp == 0) {  // TMEM: acc1 8 x 32 (all of layer 1) | acc2 (128) | acc3 (2 x 64) -> all 512 columns
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
                  "r"(512));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
@@ -382,8 +383,9 @@ static __global__ void __maxnreg__(88)
 #pragma unroll
           for (int j = 0; j < 2; ++j) {
             const uint64_t aj = ao + (uint64_t)(j * 256 >> 4), wj = (uint64_t)((4 * c + 2 * j) * 128 >> 4);
-            umma_f16(acc3, dAH + aj, dW2H + wj, id64, (c | j) ? 1u : 0u);
-            umma_f16(acc3, dAH + aj, dW2L + wj, id64, 1);
+            // W2 hi and lo are adjacent 64-row operands: one N=128 MMA gives
+            // A_hi W_hi (cols 0-63) and A_hi W_lo (cols 64-127); A_lo W_hi adds to 0-63
+            umma_f16(acc3, dAH + aj, dW2H + wj, id128, (c | j) ? 1u : 0u);
             umma_f16(acc3, dAL + aj, dW2H + wj, id64, 1);
           }
           umma_commit(barL30 + 8 * bf);
@@ -499,11 +501,12 @@ static __global__ void __maxnreg__(88)
       tc_fence_after();
       float part = 0.f;
       {
-        float y[16];
-        tmem_ld16(acc3 + lane_base + 16 * cg, y);
+        float y[16], z[16];
+        tmem_ld16(acc3 + lane_base + 16 * cg, y);       // A_hi W_hi + A_lo W_hi
+        tmem_ld16(acc3 + lane_base + 64 + 16 * cg, z);  // A_hi W_lo
 #pragma unroll
         for (int i = 0; i < 16; ++i)
-          part = fmaf(fmaxf(fmaf(y[i], s2, b2[16 * cg + i]), 0.f), w3[16 * cg + i], part);
+          part = fmaf(fmaxf(fmaf(y[i] + z[i], s2, b2[16 * cg + i]), 0.f), w3[16 * cg + i], part);
       }
       red[cg * 128 + row_in_tile] = part;  // A buffer 0 is free: every L3 MMA has completed
       epi_barrier();

@@ -206,8 +206,7 @@ static __global__ void __launch_bounds__(kM2Threads, 1)
               for (int g = 0; g < 2; ++g) {
                 const uint32_t ah = R2 + 32 * c + 16 * g, al = ah + 8;
                 const uint64_t wj = (uint64_t)((4 * c + 2 * g) * 128 >> 4);
-                umma_f16_ts(R1, ah, dW2H + wj, id64, (c | g) ? 1u : 0u);
-                umma_f16_ts(R1, ah, dW2L + wj, id64, 1);
+                umma_f16_ts(R1, ah, dW2H + wj, id128, (c | g) ? 1u : 0u);  // [W2 hi | W2 lo]
                 umma_f16_ts(R1, al, dW2H + wj, id64, 1);
               }
               if (c == 3) {
@@ -312,15 +311,17 @@ static __global__ void __launch_bounds__(kM2Threads, 1)
       // ---- layer-3 epilogue and the 64 -> 1 output layer
       mbar_wait(sbar(s, SB_L3), par_t);
       tc_fence_after();
-      // four 16-column partial sums, combined in the one-tile kernel's order
+      // four 16-column partial sums (A_hi W_hi + A_lo W_hi in cols 0-63, A_hi W_lo
+      // in 64-127), combined in the one-tile kernel's order
 #pragma unroll
       for (int q = 0; q < 2; ++q) {
-        float y[16], part = 0.f;
+        float y[16], z[16], part = 0.f;
         tmem_ld16(R1 + 32 * cg + 16 * q, y);
+        tmem_ld16(R1 + 64 + 32 * cg + 16 * q, z);
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
           const int j = 32 * cg + 16 * q + i;
-          part = fmaf(fmaxf(fmaf(y[i], s2, b2[j]), 0.f), w3[j], part);
+          part = fmaf(fmaxf(fmaf(y[i] + z[i], s2, b2[j]), 0.f), w3[j], part);
         }
         red[(2 * cg + q) * 128 + row_in_tile] = part;
       }
