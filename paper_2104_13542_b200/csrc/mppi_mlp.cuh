@@ -71,7 +71,8 @@ constexpr uint32_t kABuf = 2 * kAHalf;              // hi + lo = 16 KiB
 constexpr uint32_t OFF_A = OFF_XL + 128 * 16 * 2;
 constexpr uint32_t OFF_BAR = OFF_A + 2 * kABuf;     // 16 mbarriers
 constexpr uint32_t OFF_TMEMPTR = OFF_BAR + 16 * 8;  // 12 used
-constexpr uint32_t kMlpSmem = OFF_TMEMPTR + 16;
+constexpr uint32_t OFF_RED = OFF_TMEMPTR + 16;      // output-layer partial sums, 4 x 128 fp32
+constexpr uint32_t kMlpSmem = OFF_RED + 4 * 128 * 4;
 
 static_assert(OFF_W2L == OFF_W2H + 64 * kMlpH1 * 2, "layer-3 N=128 MMA reads W2 hi and lo as one operand");
 static_assert(kMlpSmem <= 232448, "MLP tile does not fit the 227 KiB of shared memory");
@@ -403,7 +404,7 @@ static __global__ void __maxnreg__(88)
     const int quad = warp & 3, cg = warp >> 2;
     const int row_in_tile = quad * 32 + lane;
     const uint32_t lane_base = (uint32_t)(quad * 32) << 16;
-    float* red = reinterpret_cast<float*>(sm + OFF_A);  // final partials reuse A buffer 0
+    float* red = reinterpret_cast<float*>(sm + OFF_RED);
     const float* par = reinterpret_cast<const float*>(sm + OFF_PAR);
     const float* b0 = par;
     const float* b1 = par + kMlpH0;
@@ -445,9 +446,12 @@ static __global__ void __maxnreg__(88)
     const float s0 = par[kMlpH0 + kMlpH1 + 2 * kMlpH2 + 1];
     const float s1 = par[kMlpH0 + kMlpH1 + 2 * kMlpH2 + 2];
     const float s2 = par[kMlpH0 + kMlpH1 + 2 * kMlpH2 + 3];
-    for (; tile < ntiles; tile += gridDim.x) {
-      const bool has_next = tile + gridDim.x < ntiles;
-      if (has_next) load_x(tile + gridDim.x, xnext);  // in flight during layer 1
+    // Layer-1 epilogue of tile t (8 chunks into the two A buffers). `after_l3`:
+    // the previous tile's layer 3 last read buffers 0/1 (its chunks 2/3), so
+    // chunks 0/1 wait for those MMAs; also stages the X of tile t + G.
+    auto epilogue_l1 = [&](long long t, bool after_l3) {
+      const bool nxt = t + gridDim.x < ntiles;
+      if (nxt) load_x(t + gridDim.x, xnext);  // in flight during layer 1
 #pragma unroll
       for (int c = 0; c < 8; ++c) {
         const int bf = c & 1;
@@ -464,15 +468,26 @@ static __global__ void __maxnreg__(88)
         if (c >= 2) {  // A[bf] was last read by the layer-2 MMAs of chunk c-2
           mbar_wait(barL20 + 8 * bf, (phL2 >> bf) & 1u);
           phL2 ^= 1u << bf;
+        } else if (after_l3) {  // ... or by the previous tile's layer-3 chunk 2 + c
+          mbar_wait(barL30 + 8 * bf, (phL3 >> bf) & 1u);
+          phL3 ^= 1u << bf;
         }
         store_split8(sm, OFF_A + bf * kABuf, OFF_A + bf * kABuf + kAHalf,
                      umma_off(row_in_tile, 8 * cg, kAChunkK), y);
         publish(barA0 + 8 * bf);
-        if (c == 7 && has_next) {  // every layer-1 MMA of this tile is complete: reuse X
+        if (c == 7 && nxt) {  // every layer-1 MMA of this tile is complete: reuse X
           if (tid < 256) store_split8(sm, OFF_XH, OFF_XL, umma_off(tid & 127, (tid >> 7) * 8, 16), xnext);
           publish(barX);
         }
       }
+    };
+    // Per tile: layer-2 epilogue, then the NEXT tile's layer-1 epilogue, then
+    // this tile's output layer. The next tile's layer 2 can start as soon as
+    // this tile's layer 3 is done, instead of after the output layer too (the
+    // output layer reads acc3, which only the next tile's layer 3 rewrites).
+    if (tile < ntiles) epilogue_l1(tile, false);
+    for (; tile < ntiles; tile += gridDim.x) {
+      const bool has_next = tile + gridDim.x < ntiles;
       MPPI_TSTAMP(dbg, 3);
       mbar_wait(barL20, phL2 & 1u);  // chunk 6's and chunk 7's layer-2 MMAs: all of layer 2
       mbar_wait(barL20 + 8, (phL2 >> 1) & 1u);
@@ -494,9 +509,13 @@ static __global__ void __maxnreg__(88)
         publish(barA0 + 8 * bf);
       }
       MPPI_TSTAMP(dbg, 4);
-      mbar_wait(barL30, phL3 & 1u);
-      mbar_wait(barL30 + 8, (phL3 >> 1) & 1u);
-      phL3 ^= 3u;
+      if (has_next) {
+        epilogue_l1(tile + gridDim.x, true);  // also waits for this tile's layer-3 chunks 2, 3
+      } else {
+        mbar_wait(barL30, phL3 & 1u);
+        mbar_wait(barL30 + 8, (phL3 >> 1) & 1u);
+        phL3 ^= 3u;
+      }
       MPPI_TSTAMP(dbg, 5);
       tc_fence_after();
       float part = 0.f;
@@ -508,7 +527,7 @@ static __global__ void __maxnreg__(88)
         for (int i = 0; i < 16; ++i)
           part = fmaf(fmaxf(fmaf(y[i] + z[i], s2, b2[16 * cg + i]), 0.f), w3[16 * cg + i], part);
       }
-      red[cg * 128 + row_in_tile] = part;  // A buffer 0 is free: every L3 MMA has completed
+      red[cg * 128 + row_in_tile] = part;
       epi_barrier();
       if (cg == 0) {
         const long long row = tile * 128 + row_in_tile;
@@ -517,7 +536,7 @@ static __global__ void __maxnreg__(88)
         if (row < M) out[row] = o;
       }
       tc_fence_before();
-      epi_barrier();  // red (A buffer 0) is rewritten by the next tile's first epilogue
+      epi_barrier();  // red is rewritten by the next tile's output layer
       MPPI_TSTAMP(dbg, 6);
     }
   }
