@@ -301,13 +301,14 @@ void stats_static(mppi_plan* p, int H, double gamma, double tw, StatsArgs<R>& s)
 }
 
 void choose_blocks(int N, int B, int& ppb, int& nblk) {
-  // Many instances (config 4) already fill the GPU: one block per instance,
-  // no record combine (4096 x 500: statistics 2.22 -> 1.59 ms). Otherwise 32
+  // Enough instances to fill the GPU on their own (>= one per SM; config 4):
+  // one block per instance, no record combine (4096 x 500: statistics 2.22
+  // -> 1.59 ms; at 64 instances it would halve the parallelism). Otherwise 32
   // particles per block (latency: more blocks pull eps/step costs in
   // parallel); up to 1024 particles grow the block to keep one <= 16-CTA
   // cluster per instance (stats_cluster_kernel); beyond that at most 296
   // blocks per instance (the record combine is linear in it)
-  if (B >= 64 && N <= 2048) {
+  if (B >= 148 && N <= 2048) {
     ppb = N;
     nblk = 1;
     return;

@@ -102,10 +102,10 @@ def test_emulated_particle_shards_match_unsharded():
         np.testing.assert_allclose(plans[0].get_policy(0)[1], ref.plan.get_policy(0)[1], atol=1e-9)
 
 
-@pytest.mark.parametrize("B", [12, 70])  # multi-block statistics with a record combine / one block per instance
+@pytest.mark.parametrize("B", [12, 150])  # multi-block statistics with a record combine / one block per instance
 def test_batched_statistics_layouts_match_oracle(B):
-    """Batches between 9 and 63 instances use 32-particle statistics blocks and
-    the last-block record combine; from 64 instances on, one block per
+    """Batches between 9 and 147 instances use 32-particle statistics blocks
+    and the last-block record combine; from 148 instances on, one block per
     instance (choose_blocks). Both must match independent oracles."""
     from paper_2104_13542_b200 import configs
     from paper_2104_13542_b200.batched import BatchedController
