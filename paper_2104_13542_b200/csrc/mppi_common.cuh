@@ -75,7 +75,17 @@ __device__ __forceinline__ float rsqrt_(float x) { return rsqrtf(x); }
 template <>
 __device__ __forceinline__ double rsqrt_(double x) { return rsqrt(x); }
 
-__device__ __forceinline__ void sincos_(float x, float* s, float* c) { sincosf(x, s, c); }
+// FP32 path: two-constant Cody-Waite reduction to [-pi, pi], then the SFU
+// sine/cosine (|error| ~ 2^-21 there, ~5e-7 rad-equivalent overall for joint
+// angles, far inside the FP32 parity tolerances) instead of the libm-accurate
+// sincosf, whose slow-path argument reduction dominates the FK's instruction
+// count.
+__device__ __forceinline__ void sincos_(float x, float* s, float* c) {
+  const float k = rintf(x * 0.159154943f);
+  float r = fmaf(-k, 6.28318548f, x);
+  r = fmaf(-k, -1.74845553e-7f, r);
+  __sincosf(r, s, c);
+}
 __device__ __forceinline__ void sincos_(double x, double* s, double* c) { sincos(x, s, c); }
 
 template <typename R>
