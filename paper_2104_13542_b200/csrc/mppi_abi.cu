@@ -1094,6 +1094,12 @@ int mppi_step(mppi_plan* p, const double* theta, const double* theta_dot, double
         fprintf(stderr, "\n");
       }
       for (int k : {128, 129, 200}) {
+        const unsigned long long* q = f + 16 * k;
+        if (q[11] > 1)
+          fprintf(stderr, "mlp   blk %3d: %llu tiles, per tile: L2 wait+E2 %.2f us, next E1 %.2f us, output %.2f us\n",
+                  k - 128, q[11], q[8] * 1e-3 / q[11], q[9] * 1e-3 / q[11], q[10] * 1e-3 / q[11]);
+      }
+      for (int k : {128, 129, 200}) {
         fprintf(stderr, "mlp   blk %3d:", k - 128);
         for (int j = 0; j < 12; ++j)
           fprintf(stderr, " %7.2f", f[16 * k + j] ? (double)(long long)(f[16 * k + j] - t0) * 1e-3 : -1.0);

@@ -486,9 +486,16 @@ static __global__ void __maxnreg__(88)
     // this tile's layer 3 is done, instead of after the output layer too (the
     // output layer reads acc3, which only the next tile's layer 3 rewrites).
     if (tile < ntiles) epilogue_l1(tile, false);
+#ifdef MPPI_DEBUG_TIMERS
+    unsigned long long ts3 = 0, ts4 = 0, ts5 = 0, ts6 = 0, sum_a = 0, sum_b = 0, sum_c = 0, ntile = 0;
+#define MLP_T(v) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(v))
+#else
+#define MLP_T(v)
+#endif
     for (; tile < ntiles; tile += gridDim.x) {
       const bool has_next = tile + gridDim.x < ntiles;
       MPPI_TSTAMP(dbg, 3);
+      MLP_T(ts3);
       mbar_wait(barL20, phL2 & 1u);  // chunk 6's and chunk 7's layer-2 MMAs: all of layer 2
       mbar_wait(barL20 + 8, (phL2 >> 1) & 1u);
       phL2 ^= 3u;
@@ -509,6 +516,7 @@ static __global__ void __maxnreg__(88)
         publish(barA0 + 8 * bf);
       }
       MPPI_TSTAMP(dbg, 4);
+      MLP_T(ts4);
       if (has_next) {
         epilogue_l1(tile + gridDim.x, true);  // also waits for this tile's layer-3 chunks 2, 3
       } else {
@@ -517,6 +525,7 @@ static __global__ void __maxnreg__(88)
         phL3 ^= 3u;
       }
       MPPI_TSTAMP(dbg, 5);
+      MLP_T(ts5);
       tc_fence_after();
       float part = 0.f;
       {
@@ -538,7 +547,23 @@ static __global__ void __maxnreg__(88)
       tc_fence_before();
       epi_barrier();  // red is rewritten by the next tile's output layer
       MPPI_TSTAMP(dbg, 6);
+#ifdef MPPI_DEBUG_TIMERS
+      MLP_T(ts6);
+      sum_a += ts4 - ts3;  // layer-2 wait + layer-2 epilogue
+      sum_b += ts5 - ts4;  // next tile's layer-1 epilogue / layer-3 waits
+      sum_c += ts6 - ts5;  // output layer
+      ++ntile;
+#endif
     }
+#ifdef MPPI_DEBUG_TIMERS
+    if (dbg) {
+      dbg[8] = sum_a;
+      dbg[9] = sum_b;
+      dbg[10] = sum_c;
+      dbg[11] = ntile;
+    }
+#endif
+#undef MLP_T
   }
   __syncthreads();
   if (warp == 0) {
