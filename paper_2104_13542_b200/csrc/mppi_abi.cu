@@ -18,7 +18,6 @@
 #include "mppi_aux_kernels.cuh"
 #include "mppi_launch.cuh"
 #include "mppi_mlp.cuh"
-#include "mppi_mlp2.cuh"
 #include "mppi_episode.cuh"
 
 using namespace mppi;
@@ -375,7 +374,7 @@ int enqueue_iteration(mppi_plan* p, int it, bool inline_final, double* out_recor
   if (!fused) {
     if (stages & 1u) CK(launch_rollout_any<R>(a, p->D, (long long)p->B * p->N, st));
     if ((stages & 2u) && p->learned())
-      CK(mlp_forward_auto(p->mlp, p->mlp_x.p, (long long)p->B * p->N * p->H, p->mlp_d.p, st,
+      CK(mlp_forward(p->mlp, p->mlp_x.p, (long long)p->B * p->N * p->H, p->mlp_d.p, st,
                      p->dbg.p ? p->dbg.p + 16 * p->nblk + 16 * 128 : nullptr));
   }
   StatsArgs<R> s;
@@ -551,7 +550,7 @@ int enqueue_instant_costs(mppi_plan* p, cudaStream_t st) {
   a.bad = p->ev_status.p + 1;
   a.out_terms = p->ev_out.p + 1;
   CK(launch_rollout_any<R>(a, D, 1, st));
-  if (p->learned()) CK(mlp_forward_auto(p->mlp, p->ev_x.p, 1, p->ev_d.p, st));
+  if (p->learned()) CK(mlp_forward(p->mlp, p->ev_x.p, 1, p->ev_d.p, st));
   StatsArgs<R> s;
   stats_static<R>(p, 1, p->gamma, 1.0, s);
   s.N = 1;
@@ -1201,7 +1200,7 @@ int mppi_evaluate(mppi_plan* p, int32_t mode, int32_t n, int32_t H, const double
     a.out_acc = p->e_acc.p;
     a.out_terms = p->e_terms.p;
     CK(launch_rollout_any<R>(a, D, n, st));
-    if (p->learned()) CK(mlp_forward_auto(p->mlp, p->e_x.p, (long long)nh, p->e_d.p, st));
+    if (p->learned()) CK(mlp_forward(p->mlp, p->e_x.p, (long long)nh, p->e_d.p, st));
     StatsArgs<R> s;
     stats_static<R>(p, H, gamma, tw, s);
     s.N = n;
@@ -1741,7 +1740,7 @@ int mppi_mlp_forward(mppi_plan* p, const double* q, int64_t m, double* out) {
   DEVPTR(S, double, dout, m, (const double*)nullptr);
   CK(cudaMemsetAsync(dx, 0, sizeof(float) * rows * 16, S.st));
   posenc_kernel<<<grid_for(m, 256), 256, 0, S.st>>>(dq, m, p->D, dx);
-  CK(mlp_forward_auto(p->mlp, dx, m, dd, S.st));
+  CK(mlp_forward(p->mlp, dx, m, dd, S.st));
   float_to_double_kernel<<<grid_for(m, 256), 256, 0, S.st>>>(dd, m, dout);
   CK(cudaGetLastError());
   CK(cudaMemcpyAsync(out, dout, sizeof(double) * m, cudaMemcpyDeviceToHost, S.st));

@@ -535,17 +535,3 @@ def test_top_rollouts_match_bundle_argsort(arm7):
     _, trans = fk_batch(arm7, b.positions[order].reshape(-1, 7))
     np.testing.assert_allclose(ee, trans[:, -1].reshape(8, 30, 3), atol=1e-12)
 
-
-@pytest.mark.gpu
-def test_two_slot_mlp_is_bit_identical(monkeypatch):
-    """mlp2_tcgen05_kernel (A operand from TMEM, two tiles in flight, opt-in)
-    computes exactly what mlp_tcgen05_kernel computes, ragged last tile included."""
-    from paper_2104_13542_b200.surrogate import load_arm7_surrogate
-
-    m = load_arm7_surrogate()
-    q = np.random.default_rng(5).uniform(-3, 3, size=(300_017, 7))
-    outs = []
-    for v in ("0", "1"):
-        monkeypatch.setenv("MPPI_MLP2", v)
-        outs.append(m.distance(q))
-    np.testing.assert_array_equal(outs[0], outs[1])
