@@ -191,29 +191,54 @@ def _have_reference() -> bool:
     return (ROOT / "oracle" / "_ref" / "jointmpc" / "controller.py").exists()
 
 
+def _port_controller(particles=500):
+    """The oracle port (oracle/mppi_oracle.py) of the same config-2 step: the
+    CPU baseline when the reference itself is not installed (bench-only)."""
+    from oracle import mppi_oracle as O
+    from paper_2104_13542_b200 import configs
+    from paper_2104_13542_b200.kinematics import load_chain
+    from paper_2104_13542_b200.surrogate import ARM7_SURROGATE
+
+    with np.load(ARM7_SURROGATE) as z:
+        mlp = {k: z[k] for k in z.files if k.startswith(("W", "b"))}
+    kw = dict(configs.CONTROLLER_KW)
+    kw.pop("seed")
+    kw["particles"] = particles
+    oc = O.OracleController(load_chain("arm7.chain"), configs.make_weights(2), configs.reach_goal_rotation(),
+                            configs.REACH_GOAL_POS, True, provider="learned", mlp_state=mlp, **kw)
+    return oc
+
+
 def _time_reference(steps: int, warmup: int, budget_s: float | None = None):
-    c, st = _reference_controller()
+    """(latencies in ms, workers, kind): the installed reference (oracle/_ref,
+    numba, all host threads) or, without it, the oracle port."""
+    if _have_reference():
+        c, st = _reference_controller()
+        step, workers, kind = (lambda: c.control_step(st)), c.workers, "reference"
+    else:
+        from paper_2104_13542_b200 import configs
+
+        oc = _port_controller()
+        th = configs.REACH_START.copy()
+        step, workers, kind = (lambda: oc.step(th, np.zeros(7))), os.cpu_count() or 1, "port"
     for _ in range(max(1, warmup)):
-        c.control_step(st)
+        step()
     lat = []
     t_end = time.perf_counter() + budget_s if budget_s else None
     for _ in range(steps):
         t0 = time.perf_counter()
-        c.control_step(st)
+        step()
         lat.append((time.perf_counter() - t0) * 1e3)
         if t_end and time.perf_counter() > t_end and len(lat) >= 5:
             break
-    return lat, c.workers
+    return lat, workers, kind
 
 
 def run_reference(args):
     ws, rank, _ = _dist_env()
     if rank != 0:
         return 0
-    if not _have_reference():
-        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref missing (run oracle/build_ref.py)"}))
-        return 0
-    lat, workers = _time_reference(args.steps, args.warmup)
+    lat, workers, kind = _time_reference(args.steps, args.warmup)
     v = float(np.mean(lat))
     cores = os.cpu_count() or 1
     line = {
@@ -223,9 +248,10 @@ def run_reference(args):
         "config": {"workload": "config2: arm7 reach, full cost stack + learned MLP, 500 particles x H30",
                    "particles": 500, "horizon": 30},
         "impl": "reference",
-        "cpu_baseline": {"value": v, "unit": "ms", "cores": cores, "kind": "reference",
+        "cpu_baseline": {"value": v, "unit": "ms", "cores": cores, "kind": kind,
                          "sample": f"{len(lat)} control_steps of config 2 after {args.warmup} warm-up, "
-                                   f"numba backend, workers={workers}"},
+                                   + (f"numba backend, workers={workers}" if kind == "reference"
+                                      else "oracle port (numpy float64; oracle/_ref not installed)")},
         "e2e": {"value": v, "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "median_ms": float(np.median(lat)),
     }
@@ -649,13 +675,11 @@ def _scale_roofline(args, local, peaks, peaks_kind, instances=256, steps=5):
 
 
 def _cpu_baseline(args):
-    if not _have_reference():
-        return {"value": None, "unit": "ms", "cores": os.cpu_count(), "kind": "reference",
-                "sample": "unavailable: oracle/_ref missing"}
-    lat, workers = _time_reference(steps=30, warmup=2, budget_s=20.0)
-    return {"value": float(np.median(lat)), "unit": "ms", "cores": os.cpu_count() or 1, "kind": "reference",
-            "sample": f"median of {len(lat)} reference control_steps (config 2, 500x30, numba, "
-                      f"workers={workers}) after 2 warm-up steps"}
+    lat, workers, kind = _time_reference(steps=30, warmup=2, budget_s=20.0)
+    what = (f"reference control_steps (config 2, 500x30, numba, workers={workers})" if kind == "reference"
+            else "oracle-port control steps (config 2, 500x30, numpy float64; oracle/_ref not installed)")
+    return {"value": float(np.median(lat)), "unit": "ms", "cores": os.cpu_count() or 1, "kind": kind,
+            "sample": f"median of {len(lat)} {what} after 2 warm-up steps"}
 
 
 def main():
