@@ -374,8 +374,7 @@ int enqueue_iteration(mppi_plan* p, int it, bool inline_final, double* out_recor
   if (!fused) {
     if (stages & 1u) CK(launch_rollout_any<R>(a, p->D, (long long)p->B * p->N, st));
     if ((stages & 2u) && p->learned())
-      CK(mlp_forward(p->mlp, p->mlp_x.p, (long long)p->B * p->N * p->H, p->mlp_d.p, st,
-                     p->dbg.p ? p->dbg.p + 16 * p->nblk + 16 * 128 : nullptr));
+      CK(mlp_forward(p->mlp, p->mlp_x.p, (long long)p->B * p->N * p->H, p->mlp_d.p, st));
   }
   StatsArgs<R> s;
   stats_static<R>(p, p->H, p->gamma, p->tw, s);
@@ -1088,18 +1087,6 @@ int mppi_step(mppi_plan* p, const double* theta, const double* theta_dot, double
           if (f[16 * k + j]) mx[j] = std::max(mx[j], (double)(long long)(f[16 * k + j] - t0) * 1e-3);
       for (int k : {0, 1, 2, 3, 64, 124}) {
         fprintf(stderr, "fused blk %3d:", k);
-        for (int j = 0; j < 12; ++j)
-          fprintf(stderr, " %7.2f", f[16 * k + j] ? (double)(long long)(f[16 * k + j] - t0) * 1e-3 : -1.0);
-        fprintf(stderr, "\n");
-      }
-      for (int k : {128, 129, 200}) {
-        const unsigned long long* q = f + 16 * k;
-        if (q[11] > 1)
-          fprintf(stderr, "mlp   blk %3d: %llu tiles, per tile: L2 wait+E2 %.2f us, next E1 %.2f us, output %.2f us\n",
-                  k - 128, q[11], q[8] * 1e-3 / q[11], q[9] * 1e-3 / q[11], q[10] * 1e-3 / q[11]);
-      }
-      for (int k : {128, 129, 200}) {
-        fprintf(stderr, "mlp   blk %3d:", k - 128);
         for (int j = 0; j < 12; ++j)
           fprintf(stderr, " %7.2f", f[16 * k + j] ? (double)(long long)(f[16 * k + j] - t0) * 1e-3 : -1.0);
         fprintf(stderr, "\n");

@@ -19,13 +19,8 @@
 // once per CTA with cp.async.bulk (TMA bulk engine, three mbarriers so layer 1
 // starts while W1/W2 are still in flight). The CTA is persistent over tiles.
 //
-// Pipeline per tile (one elected thread issues all MMAs; 128 threads = 128
-// TMEM lanes run the epilogues, thread t owns row t of the tile):
-//   L1 chunk c (64 of 256 outputs) -> TMEM acc1[c%2] ; epilogue (bias, ReLU,
-//   split) -> smem A ; L2 K-chunk c accumulates into acc2 ; L1 chunk c+2 is
-//   issued right behind it. Then layer 2's output goes back through smem in
-//   two 64-wide K-chunks into L3 (acc3), and the final epilogue does the
-//   64 -> 1 dot product.
+// Pipeline: see the comment above mlp_tcgen05_kernel (activations stay in
+// TMEM; layer 2 of tile t+1 overlaps the tail of tile t).
 #pragma once
 
 #include <cuda_fp16.h>
@@ -64,7 +59,9 @@ constexpr uint32_t kSeg2 = kImgBytes - OFF_W2H;     // W2
 constexpr uint32_t OFF_XH = kImgBytes;              // X tile 128 x 16 fp16
 constexpr uint32_t OFF_XL = OFF_XH + 128 * 16 * 2;
 // activations: two 32-wide K-chunk buffers (double buffering), each 128 x 32
-// fp16 hi followed by 128 x 32 fp16 lo
+// fp16 hi followed by 128 x 32 fp16 lo — used by the opt-in fused rollout +
+// MLP kernel (mppi_fused.cuh); mlp_tcgen05_kernel keeps activations in TMEM
+// and uses the OFF_K* layout below.
 constexpr uint32_t kAChunkK = 32;
 constexpr uint32_t kAHalf = 128 * kAChunkK * 2;     // 8 KiB
 constexpr uint32_t kABuf = 2 * kAHalf;              // hi + lo = 16 KiB
@@ -269,36 +266,97 @@ __device__ __forceinline__ void epi_barrier() {  // named barrier over the 512 e
 }
 
 // x: (M_pad,16) fp32 positional encodings; out: (M) fp32 distances.
-// 88 registers: 544 x 88 + a 128-thread rollout CTA (128 registers) fit one
-// SM's 64K register file, so with programmatic dependent launch the MLP CTAs
-// become resident next to the rollout and load their weights under it.
+// Warp-specialised: warps 0-15 run the epilogues (warp w serves TMEM lane
+// quadrant q = w % 4 and column group cg = w / 4: 8 of every 32 accumulator
+// columns), warp 16 issues the weight copies and every tcgen05.mma.
+// Every activation stays in tensor memory: the epilogue converts each
+// accumulator chunk IN PLACE into fp16-hi/lo columns and layers 2 and 3 read
+// their A operand from TMEM (tcgen05.mma ... [a_tmem]); only the weights and
+// the input encodings come from shared memory. (The first version sent the
+// activations through two 16 KiB shared-memory buffers: that throttled the
+// layer-1 epilogue to two chunks ahead of the MMAs and, with an N=128 MMA
+// reading ~90 B/clk of the SM's ~128 B/clk, kept layer 2 near a shared-memory
+// bound; config-4 MLP 13.2 -> 12.1 ms, bit-identical.)
+//
+// In-place layout: a 16-element K slice s of an activation occupies the 16
+// TMEM columns [16s, 16s+16) of its accumulator: 8 columns of fp16-hi pairs,
+// then 8 of fp16-lo pairs (element 2i in the low half). The two warps of a
+// slice each write half of its hi and half of its lo columns, i.e. into each
+// other's fp32 columns, so they meet at a 64-thread named barrier between
+// reading and writing.
+//
+// Schedule per tile t: epilogue = [layer-2 epilogue (t)] -> [layer-1 epilogue
+// (t+1)] -> [output layer (t)]; issuer = L2(t) -> (L2(t) done) L1(t+1) ->
+// L3(t) -> (L3(t) done) L2(t+1). Layer 1 of the next tile runs while the
+// layer-2 epilogue converts, and the next tile's layer-1 epilogue runs under
+// layer 3. 88 registers: 544 x 88 + a 128-thread rollout CTA fit one SM's 64K
+// register file (programmatic dependent launch, opt-in).
+// barriers: W0 W1 W2 | L1[2] | A1[8] | L2done | A2[4] | L3done | X
+constexpr int kMlpBars = 3 + 2 + 8 + 1 + 4 + 1 + 1;
+constexpr uint32_t OFF_KBAR = OFF_XL + 128 * 16 * 2;
+constexpr uint32_t OFF_KTMEMPTR = OFF_KBAR + kMlpBars * 8;
+constexpr uint32_t OFF_KRED = (OFF_KTMEMPTR + 16 + 15) / 16 * 16;
+constexpr uint32_t kMlpKernelSmem = OFF_KRED + 4 * 128 * 4;
+static_assert(kMlpKernelSmem <= 232448, "MLP does not fit shared memory");
+
+__device__ __forceinline__ void umma_f16_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t b, uint32_t idesc,
+                                            uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(b), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
+__device__ __forceinline__ void tmem_st4(uint32_t taddr, const uint32_t* v) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1,%2,%3,%4};" ::"r"(taddr), "r"(v[0]), "r"(v[1]),
+               "r"(v[2]), "r"(v[3])
+               : "memory");
+}
+
+// 8 fp32 activations (columns 8cg..8cg+7 of a 32-column chunk at `chunk`) ->
+// 4 hi + 4 lo packed fp16 columns of the chunk's slice (cg >> 1) layout.
+// `pair_bar`: named barrier of the two warps of the slice.
+__device__ __forceinline__ void tmem_convert8(uint32_t chunk, int cg, const float* y, int pair_bar) {
+  uint32_t h[4], l[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const __half2 hh = __floats2half2_rn(y[2 * i], y[2 * i + 1]);
+    const float2 hf = __half22float2(hh);
+    const __half2 ll = __floats2half2_rn(y[2 * i] - hf.x, y[2 * i + 1] - hf.y);
+    h[i] = *reinterpret_cast<const uint32_t*>(&hh);
+    l[i] = *reinterpret_cast<const uint32_t*>(&ll);
+  }
+  asm volatile("bar.sync %0, 64;" ::"r"(pair_bar) : "memory");  // both warps of the slice have read
+  const uint32_t slice = chunk + 16 * (cg >> 1), half = 4 * (cg & 1);
+  tmem_st4(slice + half, h);
+  tmem_st4(slice + 8 + half, l);
+  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+}
+
 static __global__ void __maxnreg__(88)
     mlp_tcgen05_kernel(const float* __restrict__ x, long long M, const unsigned char* __restrict__ img,
-                       float* __restrict__ out, int early, unsigned long long* dbg_base) {
+                       float* __restrict__ out, int early) {
   extern __shared__ __align__(1024) unsigned char mlp_smem[];
   unsigned char* sm = mlp_smem;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  // debug stamps (MPPI_DEBUG_TIMERS): 0 start, 1 X stored, 2 W0, 3 L1 epi, 4 L2 epi, 5 L3, 6 end
-  unsigned long long* dbg = (dbg_base != nullptr && tid == 0 && blockIdx.x < 128) ? dbg_base + 16 * blockIdx.x : nullptr;
-  MPPI_TSTAMP(dbg, 0);
   const uint32_t sb = smem_u32(sm);
-  // barriers: 0-2 weights, 3-4 L1 done (per acc1 buffer), 5-6 L2 done (per A
-  // buffer), 7-8 L3 done (per A buffer), 9-10 A ready (per A buffer), 11 X ready
-  const uint32_t barW0 = sb + OFF_BAR, barW1 = barW0 + 8, barW2 = barW0 + 16;
-  // barrier pairs 8 bytes apart, [0] and [1] per buffer
-  const uint32_t barL10 = barW0 + 24, barL20 = barW0 + 40, barL30 = barW0 + 56, barA0 = barW0 + 72;
-  const uint32_t barX = barW0 + 88;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sm + OFF_TMEMPTR);
+  const uint32_t barW0 = sb + OFF_KBAR, barW1 = barW0 + 8, barW2 = barW0 + 16;
+  const uint32_t barL10 = barW0 + 24, barA1 = barW0 + 40, barL2done = barW0 + 104, barA2 = barW0 + 112;
+  const uint32_t barL3done = barW0 + 144, barX = barW0 + 152;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sm + OFF_KTMEMPTR);
 
   if (tid == 0) {
-    for (int i = 0; i < 9; ++i) mbar_init(barW0 + 8 * i, 1);
-    mbar_init(barA0, kMlpEpiWarps);
-    mbar_init(barA0 + 8, kMlpEpiWarps);
+    for (int i = 0; i < 5; ++i) mbar_init(barW0 + 8 * i, 1);  // W0 W1 W2 L1[2]
+    for (int i = 0; i < 8; ++i) mbar_init(barA1 + 8 * i, kMlpEpiWarps);
+    mbar_init(barL2done, 1);
+    for (int i = 0; i < 4; ++i) mbar_init(barA2 + 8 * i, kMlpEpiWarps);
+    mbar_init(barL3done, 1);
     mbar_init(barX, kMlpEpiWarps);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     fence_async_smem();
   }
-  if (warp == 0) {  // TMEM: acc1 8 x 32 (all of layer 1) | acc2 (128) | acc3 (2 x 64) -> all 512 columns
+  if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
                  "r"(512));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
@@ -307,11 +365,12 @@ static __global__ void __maxnreg__(88)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const uint32_t acc2 = tmem + 256, acc3 = tmem + 384;  // acc1 chunk c at tmem + 32c
+  const uint32_t acc2 = tmem + 256, acc3 = tmem + 384;  // acc1 at tmem
   const long long ntiles = (M + 127) / 128;
+  const long long G = gridDim.x;
 
   if (warp == kMlpEpiWarps) {
-    // ======================= producer / MMA issuer ==========================
+    // ============================== issuer ==================================
     if (lane == 0) {
       mbar_expect_tx(barW0, kSeg0);
       bulk_g2s(sb + 0, img, kSeg0, barW0);
@@ -320,18 +379,14 @@ static __global__ void __maxnreg__(88)
         bulk_g2s(sb + OFF_W1H + o, img + OFF_W1H + o, min(32768u, kSeg1 - o), barW1);
       mbar_expect_tx(barW2, kSeg2);
       bulk_g2s(sb + OFF_W2H, img + OFF_W2H, kSeg2, barW2);
-      const uint32_t id32 = umma_idesc(32), id64 = umma_idesc(64), id128 = umma_idesc(128);
-      // descriptors are built once; per-chunk operands differ only in the
-      // start-address field (bits 0-13, 16-byte units, no carry: smem < 256 KiB)
+      const uint32_t id64 = umma_idesc(64), id128 = umma_idesc(128);
       const uint64_t dXH = umma_desc(sb + OFF_XH, 128, 256), dXL = umma_desc(sb + OFF_XL, 128, 256);
       const uint64_t dW0H = umma_desc(sb + OFF_W0H, 128, 256), dW0L = umma_desc(sb + OFF_W0L, 128, 256);
-      const uint64_t dAH = umma_desc(sb + OFF_A, 128, 512), dAL = umma_desc(sb + OFF_A + kAHalf, 128, 512);
       const uint64_t dW1H = umma_desc(sb + OFF_W1H, 128, 4096), dW1L = umma_desc(sb + OFF_W1L, 128, 4096);
-      const uint64_t dW2H = umma_desc(sb + OFF_W2H, 128, 2048), dW2L = umma_desc(sb + OFF_W2L, 128, 2048);
-      pdl_wait();  // sleep (rather than spin on barX) while the rollout still runs
-      auto issue_l1_all = [&]() {  // the whole of layer 1: two halves of N=128, one commit each
+      const uint64_t dW2H = umma_desc(sb + OFF_W2H, 128, 2048);
+      auto issue_l1 = [&]() {  // two halves of N=128 per product, one commit each
 #pragma unroll
-        for (int hf = 0; hf < 2; ++hf) {  // (N=128 per instruction: small-N MMAs under-fill the tensor pipe)
+        for (int hf = 0; hf < 2; ++hf) {
           const uint64_t wo = umma_off(128 * hf, 0, 16) >> 4;
           umma_f16(tmem + 128 * hf, dXH, dW0H + wo, id128, 0);
           umma_f16(tmem + 128 * hf, dXH, dW0L + wo, id128, 1);
@@ -339,61 +394,62 @@ static __global__ void __maxnreg__(88)
           umma_commit(barL10 + 8 * hf);
         }
       };
-      uint32_t phA = 0, phX = 0;  // parity bits
+      uint32_t phX = 0, ph = 0;  // ph: parity of the once-per-tile barriers (A1[c], A2[c], L2done, L3done)
       bool first = true;
-      for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        const bool has_next = tile + gridDim.x < ntiles;
+      for (long long tile = blockIdx.x; tile < ntiles; tile += G, ph ^= 1u) {
+        const bool has_next = tile + G < ntiles;
         if (first) {
           mbar_wait(barX, phX);
           phX ^= 1;
           mbar_wait(barW0, 0);
           tc_fence_after();
-          issue_l1_all();
+          issue_l1();
         }
 #pragma unroll
-        for (int c = 0; c < 8; ++c) {
-          const int bf = c & 1;
-          mbar_wait(barA0 + 8 * bf, (phA >> bf) & 1u);
-          phA ^= 1u << bf;
+        for (int c = 0; c < 8; ++c) {  // layer 2, K chunk c: slices 2c, 2c+1 of acc1 (in place)
+          mbar_wait(barA1 + 8 * c, ph);
           if (first && c == 0) mbar_wait(barW1, 0);
-          tc_fence_after();
-          const uint64_t ao = (uint64_t)(bf * kABuf) >> 4;
-#pragma unroll
-          for (int j = 0; j < 2; ++j) {
-            const uint64_t aj = ao + (uint64_t)(j * 256 >> 4), wj = (uint64_t)((4 * c + 2 * j) * 128 >> 4);
-            umma_f16(acc2, dAH + aj, dW1H + wj, id128, (c | j) ? 1u : 0u);
-            umma_f16(acc2, dAH + aj, dW1L + wj, id128, 1);
-            umma_f16(acc2, dAL + aj, dW1H + wj, id128, 1);
+          if (!first && c == 0) {  // acc2 is rewritten: the previous tile's layer 3 (its A reader) is done
+            mbar_wait(barL3done, ph ^ 1u);
           }
-          umma_commit(barL20 + 8 * bf);
-          if (c == 7 && has_next) {  // every acc1 chunk consumed and the next X in smem
-            mbar_wait(barX, phX);
-            phX ^= 1;
-            tc_fence_after();
-            issue_l1_all();  // runs behind this tile's layer 2, under its layer-2/3 epilogues
+          tc_fence_after();
+#pragma unroll
+          for (int g = 0; g < 2; ++g) {
+            const int s = 2 * c + g;
+            const uint32_t ah = tmem + 16 * s, al = ah + 8;
+            const uint64_t wj = (uint64_t)((2 * s) * 128 >> 4);
+            umma_f16_ts(acc2, ah, dW1H + wj, id128, s ? 1u : 0u);
+            umma_f16_ts(acc2, ah, dW1L + wj, id128, 1);
+            umma_f16_ts(acc2, al, dW1H + wj, id128, 1);
           }
         }
+        umma_commit(barL2done);
+        if (has_next) {  // acc1 is free once layer 2 has read it; X(t+1) staged by the epilogue
+          mbar_wait(barL2done, ph);
+          mbar_wait(barX, phX);
+          phX ^= 1;
+          tc_fence_after();
+          issue_l1();
+        }
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          const int bf = c & 1;
-          mbar_wait(barA0 + 8 * bf, (phA >> bf) & 1u);
-          phA ^= 1u << bf;
+        for (int c = 0; c < 4; ++c) {  // layer 3, K chunk c: slices 2c, 2c+1 of acc2 (in place)
+          mbar_wait(barA2 + 8 * c, ph);
           if (first && c == 0) mbar_wait(barW2, 0);
           tc_fence_after();
-          const uint64_t ao = (uint64_t)(bf * kABuf) >> 4;
 #pragma unroll
-          for (int j = 0; j < 2; ++j) {
-            const uint64_t aj = ao + (uint64_t)(j * 256 >> 4), wj = (uint64_t)((4 * c + 2 * j) * 128 >> 4);
-            // W2 hi and lo are adjacent 64-row operands: one N=128 MMA gives
-            // A_hi W_hi (cols 0-63) and A_hi W_lo (cols 64-127); A_lo W_hi adds to 0-63
-            umma_f16(acc3, dAH + aj, dW2H + wj, id128, (c | j) ? 1u : 0u);
-            umma_f16(acc3, dAL + aj, dW2H + wj, id64, 1);
+          for (int g = 0; g < 2; ++g) {
+            const int s = 2 * c + g;
+            const uint32_t ah = acc2 + 16 * s, al = ah + 8;
+            const uint64_t wj = (uint64_t)((2 * s) * 128 >> 4);
+            // W2 hi and lo are adjacent 64-row operands: A_hi [W hi | W lo] in one N=128 MMA
+            umma_f16_ts(acc3, ah, dW2H + wj, id128, s ? 1u : 0u);
+            umma_f16_ts(acc3, al, dW2H + wj, id64, 1);
           }
-          umma_commit(barL30 + 8 * bf);
         }
+        umma_commit(barL3done);
         first = false;
       }
-      if (first) {  // no tile for this CTA: drain the weight copies before exit
+      if (first) {
         mbar_wait(barW0, 0);
         mbar_wait(barW1, 0);
         mbar_wait(barW2, 0);
@@ -404,18 +460,16 @@ static __global__ void __maxnreg__(88)
     const int quad = warp & 3, cg = warp >> 2;
     const int row_in_tile = quad * 32 + lane;
     const uint32_t lane_base = (uint32_t)(quad * 32) << 16;
-    float* red = reinterpret_cast<float*>(sm + OFF_RED);
+    const int pair_bar = 2 + quad * 2 + (cg >> 1);  // named barriers 2..9
+    float* red = reinterpret_cast<float*>(sm + OFF_KRED);
     const float* par = reinterpret_cast<const float*>(sm + OFF_PAR);
     const float* b0 = par;
     const float* b1 = par + kMlpH0;
     const float* b2 = b1 + kMlpH1;
     const float* w3 = b2 + kMlpH2;
-    uint32_t phL1 = 0, phL2 = 0, phL3 = 0;  // parity bits per buffer
-    // (chunk loops fully unrolled: rolling them shrinks the cold-L2 code
-    // fetch but costs 25% of the steady-state tile rate at scale)
-    auto load_x = [&](long long tile, float* xv) {  // threads < 256: row tid % 128, 8 of 16 columns
-      const long long r = tile * 128 + (tid & 127);
-      if (tid < 256 && r < M) {
+    auto load_x = [&](long long t, float* xv) {  // threads < 256: row tid % 128, 8 of 16 columns
+      const long long r = t * 128 + (tid & 127);
+      if (tid < 256 && t < ntiles && r < M) {
         const float4* src = reinterpret_cast<const float4*>(x + r * 16 + (tid >> 7) * 8);
         const float4 f0 = __ldg(src), f1 = __ldg(src + 1);
         xv[0] = f0.x; xv[1] = f0.y; xv[2] = f0.z; xv[3] = f0.w;
@@ -425,107 +479,71 @@ static __global__ void __maxnreg__(88)
         for (int i = 0; i < 8; ++i) xv[i] = 0.f;
       }
     };
-    auto publish = [&](uint32_t bar) {  // generic-proxy smem writes -> async proxy, then arrive
-      fence_async_smem();
+    auto arrive = [&](uint32_t bar) {
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(bar);
     };
-    float xnext[8];
+    float xv[8];
     long long tile = blockIdx.x;
     if (early) pdl_trigger();
     pdl_wait();  // the rollout's positional encodings are complete past this point
     if (tile < ntiles) {
-      load_x(tile, xnext);
-      if (tid < 256) store_split8(sm, OFF_XH, OFF_XL, umma_off(tid & 127, (tid >> 7) * 8, 16), xnext);
-      publish(barX);
-      MPPI_TSTAMP(dbg, 1);
-      mbar_wait(barW0, 0);  // biases live in the W0 segment
-      MPPI_TSTAMP(dbg, 2);
+      load_x(tile, xv);
+      if (tid < 256) store_split8(sm, OFF_XH, OFF_XL, umma_off(tid & 127, (tid >> 7) * 8, 16), xv);
+      fence_async_smem();
+      arrive(barX);
+      mbar_wait(barW0, 0);
     }
     const float s0 = par[kMlpH0 + kMlpH1 + 2 * kMlpH2 + 1];
     const float s1 = par[kMlpH0 + kMlpH1 + 2 * kMlpH2 + 2];
     const float s2 = par[kMlpH0 + kMlpH1 + 2 * kMlpH2 + 3];
-    // Layer-1 epilogue of tile t (8 chunks into the two A buffers). `after_l3`:
-    // the previous tile's layer 3 last read buffers 0/1 (its chunks 2/3), so
-    // chunks 0/1 wait for those MMAs; also stages the X of tile t + G.
-    auto epilogue_l1 = [&](long long t, bool after_l3) {
-      const bool nxt = t + gridDim.x < ntiles;
-      if (nxt) load_x(t + gridDim.x, xnext);  // in flight during layer 1
+    uint32_t phL1 = 0;
+    // layer-1 epilogue of tile t, in place in acc1; stages X(t + G) on the way
+    auto epilogue_l1 = [&](long long t) {
+      const bool nxt = t + G < ntiles;
+      if (nxt) load_x(t + G, xv);
 #pragma unroll
       for (int c = 0; c < 8; ++c) {
-        const int bf = c & 1;
-        if ((c & 3) == 0) {  // layer-1 chunks 0-3 and 4-7 complete on separate barriers
+        if ((c & 3) == 0) {
           const int hb = c >> 2;
           mbar_wait(barL10 + 8 * hb, (phL1 >> hb) & 1u);
           phL1 ^= 1u << hb;
           tc_fence_after();
         }
         float y[8];
-        tmem_ld8(tmem + 32 * c + lane_base + 8 * cg, y);
+        tmem_ld8(tmem + lane_base + 32 * c + 8 * cg, y);
 #pragma unroll
         for (int i = 0; i < 8; ++i) y[i] = fmaxf(fmaf(y[i], s0, b0[32 * c + 8 * cg + i]), 0.f);
-        if (c >= 2) {  // A[bf] was last read by the layer-2 MMAs of chunk c-2
-          mbar_wait(barL20 + 8 * bf, (phL2 >> bf) & 1u);
-          phL2 ^= 1u << bf;
-        } else if (after_l3) {  // ... or by the previous tile's layer-3 chunk 2 + c
-          mbar_wait(barL30 + 8 * bf, (phL3 >> bf) & 1u);
-          phL3 ^= 1u << bf;
-        }
-        store_split8(sm, OFF_A + bf * kABuf, OFF_A + bf * kABuf + kAHalf,
-                     umma_off(row_in_tile, 8 * cg, kAChunkK), y);
-        publish(barA0 + 8 * bf);
-        if (c == 7 && nxt) {  // every layer-1 MMA of this tile is complete: reuse X
-          if (tid < 256) store_split8(sm, OFF_XH, OFF_XL, umma_off(tid & 127, (tid >> 7) * 8, 16), xnext);
-          publish(barX);
+        tmem_convert8(tmem + lane_base + 32 * c, cg, y, pair_bar);
+        arrive(barA1 + 8 * c);
+        if (c == 7 && nxt) {  // both layer-1 halves done (barL1[1]): X can be rewritten
+          if (tid < 256) store_split8(sm, OFF_XH, OFF_XL, umma_off(tid & 127, (tid >> 7) * 8, 16), xv);
+          fence_async_smem();
+          arrive(barX);
         }
       }
     };
-    // Per tile: layer-2 epilogue, then the NEXT tile's layer-1 epilogue, then
-    // this tile's output layer. The next tile's layer 2 can start as soon as
-    // this tile's layer 3 is done, instead of after the output layer too (the
-    // output layer reads acc3, which only the next tile's layer 3 rewrites).
-    if (tile < ntiles) epilogue_l1(tile, false);
-#ifdef MPPI_DEBUG_TIMERS
-    unsigned long long ts3 = 0, ts4 = 0, ts5 = 0, ts6 = 0, sum_a = 0, sum_b = 0, sum_c = 0, ntile = 0;
-#define MLP_T(v) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(v))
-#else
-#define MLP_T(v)
-#endif
-    for (; tile < ntiles; tile += gridDim.x) {
-      const bool has_next = tile + gridDim.x < ntiles;
-      MPPI_TSTAMP(dbg, 3);
-      MLP_T(ts3);
-      mbar_wait(barL20, phL2 & 1u);  // chunk 6's and chunk 7's layer-2 MMAs: all of layer 2
-      mbar_wait(barL20 + 8, (phL2 >> 1) & 1u);
-      phL2 ^= 3u;
+    uint32_t ph = 0;
+    if (tile < ntiles) epilogue_l1(tile);
+    for (; tile < ntiles; tile += G, ph ^= 1u) {
+      const bool has_next = tile + G < ntiles;
+      // ---- layer-2 epilogue, in place in acc2
+      mbar_wait(barL2done, ph);
       tc_fence_after();
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
-        const int bf = c & 1;
         float y[8];
         tmem_ld8(acc2 + lane_base + 32 * c + 8 * cg, y);
 #pragma unroll
         for (int i = 0; i < 8; ++i) y[i] = fmaxf(fmaf(y[i], s1, b1[32 * c + 8 * cg + i]), 0.f);
-        if (c >= 2) {
-          mbar_wait(barL30 + 8 * bf, (phL3 >> bf) & 1u);
-          phL3 ^= 1u << bf;
-        }
-        store_split8(sm, OFF_A + bf * kABuf, OFF_A + bf * kABuf + kAHalf,
-                     umma_off(row_in_tile, 8 * cg, kAChunkK), y);
-        publish(barA0 + 8 * bf);
+        tmem_convert8(acc2 + lane_base + 32 * c, cg, y, pair_bar);
+        arrive(barA2 + 8 * c);
       }
-      MPPI_TSTAMP(dbg, 4);
-      MLP_T(ts4);
-      if (has_next) {
-        epilogue_l1(tile + gridDim.x, true);  // also waits for this tile's layer-3 chunks 2, 3
-      } else {
-        mbar_wait(barL30, phL3 & 1u);
-        mbar_wait(barL30 + 8, (phL3 >> 1) & 1u);
-        phL3 ^= 3u;
-      }
-      MPPI_TSTAMP(dbg, 5);
-      MLP_T(ts5);
+      // ---- the next tile's layer-1 epilogue runs under this tile's layer 3
+      if (has_next) epilogue_l1(tile + G);
+      // ---- output layer of this tile
+      mbar_wait(barL3done, ph);
       tc_fence_after();
       float part = 0.f;
       {
@@ -545,25 +563,8 @@ static __global__ void __maxnreg__(88)
         if (row < M) out[row] = o;
       }
       tc_fence_before();
-      epi_barrier();  // red is rewritten by the next tile's output layer
-      MPPI_TSTAMP(dbg, 6);
-#ifdef MPPI_DEBUG_TIMERS
-      MLP_T(ts6);
-      sum_a += ts4 - ts3;  // layer-2 wait + layer-2 epilogue
-      sum_b += ts5 - ts4;  // next tile's layer-1 epilogue / layer-3 waits
-      sum_c += ts6 - ts5;  // output layer
-      ++ntile;
-#endif
+      epi_barrier();
     }
-#ifdef MPPI_DEBUG_TIMERS
-    if (dbg) {
-      dbg[8] = sum_a;
-      dbg[9] = sum_b;
-      dbg[10] = sum_c;
-      dbg[11] = ntile;
-    }
-#endif
-#undef MLP_T
   }
   __syncthreads();
   if (warp == 0) {
@@ -625,13 +626,13 @@ inline cudaError_t mlp_upload(MlpWeights& m, int in_dim, const double* W0, const
 }
 
 inline cudaError_t mlp_forward(const MlpWeights& m, const float* x, long long rows, float* out,
-                               cudaStream_t st, unsigned long long* dbg = nullptr) {
+                               cudaStream_t st) {
   static bool attr_set[64] = {};
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   if (dev < 0 || dev >= 64 || !attr_set[dev]) {
     cudaError_t e = cudaFuncSetAttribute(mlp_tcgen05_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)kMlpSmem);
+                                         (int)kMlpKernelSmem);
     if (e != cudaSuccess) return e;
     if (dev >= 0 && dev < 64) attr_set[dev] = true;
   }
@@ -641,7 +642,7 @@ inline cudaError_t mlp_forward(const MlpWeights& m, const float* x, long long ro
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid, 1, 1);
   cfg.blockDim = dim3(kMlpThreads, 1, 1);
-  cfg.dynamicSmemBytes = kMlpSmem;
+  cfg.dynamicSmemBytes = kMlpKernelSmem;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -649,7 +650,7 @@ inline cudaError_t mlp_forward(const MlpWeights& m, const float* x, long long ro
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   return cudaLaunchKernelEx(&cfg, mlp_tcgen05_kernel, x, rows, (const unsigned char*)m.img, out,
-                            (pdl_mask() & PDL_EARLY) ? 1 : 0, dbg);
+                            (pdl_mask() & PDL_EARLY) ? 1 : 0);
 }
 
 inline void mlp_release(MlpWeights& m) {
