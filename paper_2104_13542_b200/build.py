@@ -19,8 +19,11 @@ from pathlib import Path
 PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
-OUT = PKG / "_mppi_b200.so"
-OBJ = ROOT / "build" / "obj"
+# MPPI_BUILD_TAG=<tag>: a variant build (e.g. with MPPI_NVCC_FLAGS=-DMPPI_DEBUG_TIMERS)
+# next to the production library, loaded with MPPI_LIB for A/B runs
+TAG = os.environ.get("MPPI_BUILD_TAG", "")
+OUT = PKG / (f"_mppi_b200_{TAG}.so" if TAG else "_mppi_b200.so")
+OBJ = ROOT / "build" / (f"obj-{TAG}" if TAG else "obj")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",

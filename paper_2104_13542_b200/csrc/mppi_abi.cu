@@ -185,6 +185,20 @@ struct mppi_plan {
   // graph
   cudaGraphExec_t graph = nullptr;       // lean step graph (production)
   cudaGraphExec_t graph_prof = nullptr;  // same step + event-record nodes between the stages
+  // Single-instance plans pass the joint state as a rollout kernel PARAMETER:
+  // each step rewrites the captured rollout nodes' arguments
+  // (cudaGraphExecKernelNodeSetParams) instead of replaying an H2D copy node,
+  // whose copy-engine hand-off cost ~4 us of device time per step.
+  struct InlineNode {
+    cudaGraphNode_t node;
+    cudaKernelNodeParams kp;
+    std::vector<unsigned char> args;  // RolloutArgs<R> image
+    size_t st_off;                    // offsetof(RolloutArgs<R>, st0)
+    void* argv[1];
+  };
+  std::vector<InlineNode> inl, inl_prof;
+  std::vector<InlineNode>* capture_inl = nullptr;  // set while capturing a graph with inline state
+  cudaGraph_t graph_tmpl = nullptr, graph_tmpl_prof = nullptr;  // kept alive: node handles index them
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   std::vector<cudaEvent_t> stage_ev;
   int profile_level = 0;  // 0 none, 1 device time of the lean graph, 2 instrumented graph (stage times)
@@ -230,6 +244,11 @@ int set_device(mppi_plan* p) {
 void invalidate_graph(mppi_plan* p) {
   if (p->graph) cudaGraphExecDestroy(p->graph);
   if (p->graph_prof) cudaGraphExecDestroy(p->graph_prof);
+  if (p->graph_tmpl) cudaGraphDestroy(p->graph_tmpl);
+  if (p->graph_tmpl_prof) cudaGraphDestroy(p->graph_tmpl_prof);
+  p->graph_tmpl = p->graph_tmpl_prof = nullptr;
+  p->inl.clear();
+  p->inl_prof.clear();
   if (p->ep_graph) cudaGraphExecDestroy(p->ep_graph);
   p->ep_graph = nullptr;
   p->graph = nullptr;
@@ -314,6 +333,10 @@ void choose_blocks(int N, int B, int& ppb, int& nblk) {
   }
   ppb = 32;
   if (N > 16 * 32 && N <= 16 * 64) ppb = (N + 15) / 16;
+  if (const char* env = getenv("MPPI_STATS_PPB")) {  // A/B experiments on the cluster size
+    const int v = atoi(env);
+    if (v >= (N + 15) / 16 && v <= 64) ppb = v;
+  }
   nblk = (N + ppb - 1) / ppb;
   if (nblk > 296) {
     nblk = 296;
@@ -372,7 +395,24 @@ int enqueue_iteration(mppi_plan* p, int it, bool inline_final, double* out_recor
     }
   }
   if (!fused) {
+    if (p->capture_inl && (stages & 1u)) {
+      a.state_inline = 1;
+      for (int j = 0; j < 2 * p->D; ++j) a.st0[j] = p->h_state[j];
+    }
     if (stages & 1u) CK(launch_rollout_any<R>(a, p->D, (long long)p->B * p->N, st));
+    if (p->capture_inl && (stages & 1u)) {  // remember the node and its argument image
+      cudaStreamCaptureStatus cs;
+      const cudaGraphNode_t* deps = nullptr;
+      size_t ndeps = 0;
+      CK(cudaStreamGetCaptureInfo(st, &cs, nullptr, nullptr, &deps, &ndeps));
+      if (cs != cudaStreamCaptureStatusActive || ndeps != 1) return fail(MPPI_E_CUDA, "rollout node not found");
+      mppi_plan::InlineNode n;
+      n.node = deps[0];
+      CK(cudaGraphKernelNodeGetParams(n.node, &n.kp));
+      n.args.assign(reinterpret_cast<const unsigned char*>(&a), reinterpret_cast<const unsigned char*>(&a) + sizeof(a));
+      n.st_off = offsetof(RolloutArgs<R>, st0);
+      p->capture_inl->push_back(std::move(n));
+    }
     if ((stages & 2u) && p->learned())
       CK(mlp_forward(p->mlp, p->mlp_x.p, (long long)p->B * p->N * p->H, p->mlp_d.p, st));
   }
@@ -409,6 +449,9 @@ int enqueue_iteration(mppi_plan* p, int it, bool inline_final, double* out_recor
     s.dump_terms = p->d_terms.p;
     s.dump_weights = inline_final ? p->d_w.p : nullptr;
   }
+#ifdef MPPI_DEBUG_TIMERS
+  if ((stages & 4u) && getenv("MPPI_DEBUG_TWICE")) CK(launch_stats_any<R>(s, p->D, st));  // warm re-run (timing only)
+#endif
   if (stages & 4u) CK(launch_stats_any<R>(s, p->D, st));
   return MPPI_OK;
 }
@@ -438,7 +481,10 @@ int enqueue_step_body(mppi_plan* p, cudaStream_t st, bool stage_events, bool h2d
   // one H2D node: the (B,2d) state followed by the step counter (pseudorandom
   // generator). Status words were re-armed by the previous step's finalize.
   // (The episode graph writes the state on the device instead.)
-  if (h2d)
+#ifdef MPPI_DEBUG_TIMERS
+  if (getenv("MPPI_DEBUG_NO_H2D")) h2d = false;  // timing experiment only: the state goes stale
+#endif
+  if (h2d && !p->capture_inl)
     CK(cudaMemcpyAsync(p->state.p, p->h_state, sizeof(double) * (B * 2 * D + 1), cudaMemcpyHostToDevice, st));
   // event-record nodes between the stages give per-kernel device times of
   // every replayed step (mppi_step_info.*_ms)
@@ -469,16 +515,35 @@ int ensure_graph(mppi_plan* p, bool prof = false) {
   if (p->learned() && !p->mlp_ready)
     return fail(MPPI_E_CONFIG, "learned self-collision selected but mppi_set_mlp was not called");
   cudaGraph_t g = nullptr;
+  // the state as a kernel parameter: one instance, no device-side step counter
+  // (Philox), the two-kernel path (MPPI_INLINE_STATE=0 restores the H2D node)
+  const char* env = getenv("MPPI_INLINE_STATE");
+  std::vector<mppi_plan::InlineNode>& nodes = prof ? p->inl_prof : p->inl;
+  nodes.clear();
+  const bool inl = p->B == 1 && p->generator != MPPI_GEN_PSEUDORANDOM && !(env && env[0] == '0') &&
+                   getenv("MPPI_FUSE") == nullptr;
+  p->capture_inl = inl ? &nodes : nullptr;
   CK(cudaStreamBeginCapture(p->stream, cudaStreamCaptureModeThreadLocal));
   int rc = enqueue_step_body(p, p->stream, prof);
+  p->capture_inl = nullptr;
   cudaError_t e = cudaStreamEndCapture(p->stream, &g);
   if (rc != MPPI_OK) {
     if (g) cudaGraphDestroy(g);
+    nodes.clear();
     return rc;
   }
   if (e != cudaSuccess) return fail(MPPI_E_CUDA, std::string("graph capture: ") + cudaGetErrorString(e));
   e = cudaGraphInstantiate(slot, g, 0);
-  cudaGraphDestroy(g);
+  if (nodes.empty()) {
+    cudaGraphDestroy(g);
+  } else {
+    (prof ? p->graph_tmpl_prof : p->graph_tmpl) = g;
+    for (auto& n : nodes) {
+      n.argv[0] = n.args.data();
+      n.kp.kernelParams = n.argv;
+      n.kp.extra = nullptr;
+    }
+  }
   if (e != cudaSuccess) return fail(MPPI_E_CUDA, std::string("graph instantiate: ") + cudaGetErrorString(e));
   return MPPI_OK;
 }
@@ -1066,6 +1131,10 @@ int mppi_step(mppi_plan* p, const double* theta, const double* theta_dot, double
   // extra runtime call is host time between the state and the command
   const bool prof = p->profile_level >= 2;
   if (prof) CKR(ensure_graph(p, true));
+  for (auto& n : prof ? p->inl_prof : p->inl) {
+    memcpy(n.args.data() + n.st_off, p->h_state, sizeof(double) * 2 * D);
+    CK(cudaGraphExecKernelNodeSetParams(prof ? p->graph_prof : p->graph, n.node, &n.kp));
+  }
   if (p->profile_level) CK(cudaEventRecord(p->ev0, p->stream));
   CK(cudaGraphLaunch(prof ? p->graph_prof : p->graph, p->stream));
   if (p->profile_level) CK(cudaEventRecord(p->ev1, p->stream));

@@ -244,6 +244,45 @@ __device__ __forceinline__ bool capsule_hits_sphere(const R* P0, const R* P1, R 
 // dependent grid may start (and run its prologue) while its predecessor
 // drains, and blocks in pdl_wait() until the predecessor has completed and its
 // writes are visible. pdl_trigger() lets the dependent grid be scheduled early.
+// ---------------------------------------------------------------- cluster push
+// Distributed-shared-memory pushes that complete on the RECEIVER's mbarrier
+// (st.async ... complete_tx): no cluster-wide fence, no L1 invalidation.
+__device__ __forceinline__ uint32_t smem_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ uint32_t mapa_rank(uint32_t addr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void push_f64(uint32_t raddr, double v, uint32_t rbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];" ::"r"(raddr),
+               "l"(__double_as_longlong(v)), "r"(rbar)
+               : "memory");
+}
+__device__ __forceinline__ void push_f64x2(uint32_t raddr, double a, double b, uint32_t rbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.b64 [%0], {%1, %2}, [%3];" ::"r"(raddr),
+               "l"(__double_as_longlong(a)), "l"(__double_as_longlong(b)), "r"(rbar)
+               : "memory");
+}
+__device__ __forceinline__ void cbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void cbar_arrive_expect(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void cbar_wait(uint32_t bar, uint32_t phase) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra WAIT_%=;\n}" ::"r"(bar),
+      "r"(phase)
+      : "memory");
+}
+__device__ __forceinline__ void cluster_init_fence_arrive() {
+  asm volatile("fence.mbarrier_init.release.cluster;\n\tbarrier.cluster.arrive.relaxed.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void cluster_wait() { asm volatile("barrier.cluster.wait.aligned;" ::: "memory"); }
+
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 // host side: which PDL features are on (MPPI_PDL bit mask, A/B switch):

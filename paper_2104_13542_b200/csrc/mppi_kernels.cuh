@@ -38,6 +38,8 @@ struct RolloutArgs {
   int check_var;  // PolicyStateError check of build_control_batch (sampling.py:282)
   int skip_on_status;
   int pdl_early;  // trigger the dependent grid at entry
+  int state_inline;  // single instance: theta, theta_dot travel in st0 (kernel parameter), not `state`
+  double st0[2 * MAXD];
   double tail_mean, tail_sd;
   const double* eps;     // (N,H,d)
   const double* means;   // (B,H,d)
@@ -137,7 +139,7 @@ __device__ __forceinline__ bool rollout_particle(const RolloutArgs<R>& a, long l
   const int h = act ? lane : H - 1;
   const ChainT<R>& ch = a.chain;
   const CostT<R>& cs = a.cost;
-  const double* st = a.state + (size_t)b * 2 * D;
+  const double* st = a.state_inline ? a.st0 : a.state + (size_t)b * 2 * D;
   R st_p[D], st_v[D];
 #pragma unroll
   for (int j = 0; j < D; ++j) {
@@ -910,14 +912,28 @@ __global__ void __launch_bounds__(kStatsThreads) stats_kernel(const __grid_const
 }
 
 // Cluster statistics (latency path, N <= 16 * kClusterMaxPPB): the nblk <= 16
-// CTAs of one instance form one thread-block cluster. They agree on the global
-// best finite total through distributed shared memory BEFORE computing
-// weights (so weights are exactly exp(-(c - min)/beta), policy.py:113-114, with
-// no rescaling), and the rank-0 CTA reduces the per-CTA statistics straight out
-// of its peers' shared memory: no global records, fences, atomics or last-block
-// hand-off. Cluster barriers replace the grid-level round trips.
+// CTAs of one instance form one thread-block cluster. Every exchange is a
+// PUSH into the receiver's shared memory (st.async) completing on the
+// receiver's mbarrier, so no CTA ever waits on a cluster-wide fence:
+//   1. each CTA's best finite total -> slot [blk] of every peer's `mins`;
+//      after the barrier all CTAs hold the instance minimum, so weights are
+//      exactly exp(-(c - min)/beta) (policy.py:113-114) with no rescaling;
+//   2. each CTA's S0/count/sum and S1|S2 rows -> slot [blk] of rank 0;
+//      after the barrier rank 0 reduces them in rank order from its own
+//      shared memory and applies the update in registers (policy.py:124-177).
+// The perturbation rows of the CTA's particles do not depend on this step's
+// costs: they are loaded into registers before the totals, so the weighted
+// sums are pure FMA chains once the weights exist. No global records,
+// fences, atomics or last-block hand-off; the only cluster barrier publishes
+// the mbarrier initialisation and is waited on after the totals.
 constexpr int kClusterMax = 16;
 constexpr int kClusterMaxPPB = 64;
+constexpr int kClusterEpsRegs = 32;  // perturbation rows held in registers per thread
+
+inline size_t stats_cluster_smem_bytes(int ppb, int HD) {
+  return sizeof(double) * (2 * (size_t)ppb + 32 + kClusterMax + kClusterMax * 4 + (size_t)kClusterMax * 2 * HD + HD) +
+         2 * sizeof(unsigned long long);
+}
 
 template <typename R, int D>
 __global__ void __launch_bounds__(kStatsThreads) stats_cluster_kernel(const __grid_constant__ StatsArgs<R> a) {
@@ -930,34 +946,45 @@ __global__ void __launch_bounds__(kStatsThreads) stats_cluster_kernel(const __gr
   const int H = a.H, HD = H * D, N = a.N;
   const int n0 = blk * a.ppb;
   const int cnt = max(0, min(N, n0 + a.ppb) - n0);
-  double* tot = sm;                 // [ppb]
-  double* wt = tot + a.ppb;         // [ppb]
-  double* red = wt + a.ppb;         // [32]
-  double* part = red + 32;          // [2*HD] this CTA's S1 | S2
-  double* head = part + 2 * HD;     // [8]: local min, S0, count, sumfinite
-  double* rec = head + 8;           // [kRecHead + 2*HD] (rank 0: the combined record)
-  double* emp = rec + kRecHead + 2 * HD;  // [HD]
-  int* nz = reinterpret_cast<int*>(emp + HD);  // [ppb]
+  double* tot = sm;                      // [ppb]
+  double* wt = tot + a.ppb;              // [ppb]
+  double* red = wt + a.ppb;              // [32]
+  double* mins = red + 32;               // [kClusterMax] per-CTA best finite totals (pushed by peers)
+  double* heads = mins + kClusterMax;    // [kClusterMax][4] S0, count, sum finite (rank 0)
+  double* parts = heads + kClusterMax * 4;  // [kClusterMax][HD][2] S1, S2 pairs (rank 0)
+  double* emp = parts + (size_t)kClusterMax * 2 * HD;  // [HD]
+  unsigned long long* bars = reinterpret_cast<unsigned long long*>(emp + HD);  // [0] mins, [1] rank-0 sums
+  const uint32_t bar_min = smem_addr(&bars[0]), bar_sum = smem_addr(&bars[1]);
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  // prologue under the predecessor's tail: the policy was written by the
-  // previous step, not by the kernels this one depends on
-  double mo_pre = 0.0, so_pre = 0.0;
-  if (threadIdx.x < HD) {
-    const int h = threadIdx.x / D, j = threadIdx.x - h * D;
-    const int hs = a.shift ? h + 1 : h;
-    mo_pre = hs < H ? a.means[(size_t)b * HD + hs * D + j] : a.tail_mean;
-    so_pre = hs < H ? a.sd[(size_t)b * HD + hs * D + j] : a.tail_sd;
+  const int o = threadIdx.x;
+  const bool owner = o < HD;  // H*d <= 256 = blockDim: one policy entry per thread
+  if (threadIdx.x == 0) {  // each receive barrier completes on bytes alone
+    cbar_init(bar_min, 1);
+    cbar_init(bar_sum, 1);
+    cbar_arrive_expect(bar_min, 8u * nblk);
+    if (blk == 0) cbar_arrive_expect(bar_sum, (16u * HD + 32u) * nblk);
   }
-  const double disc_pre = lane < H - 1 ? a.disc[lane] : a.dlast;
+  cluster_init_fence_arrive();  // waited on before the first push
+  // ---- requests that do not depend on this step's costs ----------------------
+  double mo = 0.0, so = 0.0, vo = 0.0;
+  double e[kClusterEpsRegs];
+  const double* ep = a.eps + (size_t)n0 * HD + o;
+  if (owner) {
+    const int h = o / D, j = o - h * D;
+    const int hs = a.shift ? h + 1 : h;
+    mo = hs < H ? a.means[(size_t)b * HD + hs * D + j] : a.tail_mean;
+    so = hs < H ? a.sd[(size_t)b * HD + hs * D + j] : a.tail_sd;
+    vo = hs < H ? a.var[(size_t)b * HD + hs * D + j] : a.tail_var;
+#pragma unroll
+    for (int i = 0; i < kClusterEpsRegs; ++i) e[i] = i < cnt ? __ldg(ep + (size_t)i * HD) : 0.0;
+  }
+  const double disc_l = lane < H - 1 ? a.disc[lane] : a.dlast;
   pdl_wait();
   const int status0 = a.status[b];
   const bool failed = status0 != 0;
   MPPI_STAMP(0);
 
   // ---- totals (rollout.py:111-171), 4 particles per warp, loads batched -----
-  // the discount row is read per lane: take it from a register, not from the
-  // (address-serialising) constant bank inside the loop
-  const double disc_l = disc_pre;
   {
     constexpr int PA = 4;
     for (int i0 = wid * PA; i0 < cnt; i0 += nw * PA) {
@@ -1005,132 +1032,175 @@ __global__ void __launch_bounds__(kStatsThreads) stats_cluster_kernel(const __gr
   }
   __syncthreads();
   MPPI_STAMP(1);
-  // ---- cluster-wide best finite total ---------------------------------------
-  double mloc = CUDART_INF;
-  for (int i = threadIdx.x; i < cnt; i += blockDim.x)
-    if (isfinite(tot[i])) mloc = fmin(mloc, tot[i]);
-  mloc = block_min_d(mloc, red);
-  if (threadIdx.x == 0) head[0] = mloc;
-  cluster.sync();
-  double m = CUDART_INF;
+  // ---- instance-wide best finite total: pushed to every peer -----------------
+  cluster_wait();  // every peer's receive barriers are initialised
   if (wid == 0) {
-    double v = lane < nblk ? *cluster.map_shared_rank(&head[0], lane) : CUDART_INF;
+    double v = CUDART_INF;
+    for (int i = lane; i < cnt; i += 32)
+      if (isfinite(tot[i])) v = fmin(v, tot[i]);
     for (int off = 16; off > 0; off >>= 1) v = fmin(v, __shfl_xor_sync(0xffffffffu, v, off));
-    if (lane == 0) red[0] = v;
+    if (lane < nblk) push_f64(mapa_rank(smem_addr(&mins[blk]), lane), v, mapa_rank(bar_min, lane));
   }
-  __syncthreads();
-  m = red[0];
+  cbar_wait(bar_min, 0);
+  double m = CUDART_INF;
+  for (int k = 0; k < nblk; ++k) m = fmin(m, mins[k]);
   MPPI_STAMP(2);
-  // ---- weights (policy.py:103-121), compaction, local sums ------------------
+  // ---- weights (policy.py:103-121) ------------------------------------------
   for (int i = threadIdx.x; i < cnt; i += blockDim.x)
     wt[i] = (!failed && isfinite(tot[i])) ? exp(-(tot[i] - m) / a.beta) : 0.0;
+  if (b == 0 && a.dump_weights && !failed)
+    for (int i = threadIdx.x; i < cnt; i += blockDim.x) a.dump_weights[n0 + i] = wt[i];
   __syncthreads();
-  __shared__ int s_nnz;
-  if (wid == 0) {
-    int base = 0;
-    for (int c0 = 0; c0 < cnt; c0 += 32) {
-      const int i = c0 + lane;
-      const bool keep = i < cnt && wt[i] > 0.0;
-      const unsigned bal = __ballot_sync(0xffffffffu, keep);
-      if (keep) nz[base + __popc(bal & ((1u << lane) - 1u))] = i;
-      base += __popc(bal);
+  MPPI_STAMP(3);
+  // ---- weighted sufficient statistics around the old mean, pushed to rank 0 --
+  // Zero weights add exact zeros, so the sums equal the reference's sums over
+  // the particles with nonzero weight in ascending order.
+  if (owner) {
+    double s1 = 0.0, s2 = 0.0;
+    if (!failed) {
+      auto acc = [&](int i, double ev) {
+        const int ng = n0 + i + a.particle_offset;
+        const double dv = ng < a.null_count ? 0.0 - mo : (ng == a.null_count ? 0.0 : (mo + so * ev) - mo);
+        const double w = wt[i];
+        s1 += w * dv;
+        s2 += w * dv * dv;
+      };
+#pragma unroll
+      for (int i = 0; i < kClusterEpsRegs; ++i)
+        if (i < cnt) acc(i, e[i]);
+      for (int i = kClusterEpsRegs; i < cnt; ++i) acc(i, __ldg(ep + (size_t)i * HD));
     }
-    if (lane == 0) s_nnz = base;
-  } else if (wid == 1) {
+    push_f64x2(mapa_rank(smem_addr(parts + ((size_t)blk * HD + o) * 2), 0), s1, s2, mapa_rank(bar_sum, 0));
+  }
+  if (wid == nw - 1) {
     double s0 = 0.0, c = 0.0, sf = 0.0;
-    for (int i = lane; i < cnt; i += 32) {
-      s0 += wt[i];
-      if (isfinite(tot[i])) {
-        c += 1.0;
-        sf += tot[i];
+    if (!failed)
+      for (int i = lane; i < cnt; i += 32) {
+        s0 += wt[i];
+        if (isfinite(tot[i])) {
+          c += 1.0;
+          sf += tot[i];
+        }
       }
-    }
     s0 = warp_sum(s0);
     c = warp_sum(c);
     sf = warp_sum(sf);
-    if (lane == 0) {
-      head[1] = s0;
-      head[2] = c;
-      head[3] = sf;
-    }
+    if (lane == 0) push_f64x2(mapa_rank(smem_addr(heads + blk * 4), 0), s0, c, mapa_rank(bar_sum, 0));
+    if (lane == 1) push_f64x2(mapa_rank(smem_addr(heads + blk * 4 + 2), 0), sf, 0.0, mapa_rank(bar_sum, 0));
   }
-  __syncthreads();
-  const int nnz = s_nnz;
-  MPPI_STAMP(3);
-  // ---- weighted sufficient statistics around the old mean -------------------
-  if (threadIdx.x < HD) {
-    const int o = threadIdx.x;
-    double s1 = 0.0, s2 = 0.0;
-    if (!failed) {
-      const double* ep = a.eps + (size_t)n0 * HD + o;
-      constexpr int PD = 32;
-      for (int k0 = 0; k0 < nnz; k0 += PD) {
-        double e[PD];
-        int ii[PD];
-#pragma unroll
-        for (int u = 0; u < PD; ++u) {
-          ii[u] = k0 + u < nnz ? nz[k0 + u] : -1;
-          e[u] = ii[u] >= 0 ? __ldg(ep + (size_t)ii[u] * HD) : 0.0;
-        }
-#pragma unroll
-        for (int u = 0; u < PD; ++u) {
-          if (ii[u] < 0) break;
-          const int ng = n0 + ii[u] + a.particle_offset;
-          const double dv = ng < a.null_count ? 0.0 - mo_pre
-                                              : (ng == a.null_count ? 0.0 : (mo_pre + so_pre * e[u]) - mo_pre);
-          const double w = wt[ii[u]];
-          s1 += w * dv;
-          s2 += w * dv * dv;
-        }
-      }
-    }
-    part[o] = s1;
-    part[HD + o] = s2;
-  }
-  if (b == 0 && a.dump_weights && !failed)
-    for (int i = threadIdx.x; i < cnt; i += blockDim.x) a.dump_weights[n0 + i] = wt[i];
   MPPI_STAMP(4);
-  cluster.sync();
+  if (blk != 0) return;  // peers are done: every push into them has landed
+  cbar_wait(bar_sum, 0);
   MPPI_STAMP(5);
-  // ---- rank 0 reduces the cluster's statistics in rank order ----------------
-  if (blk == 0) {
-    double* out = a.finalize_inline ? rec : a.out_record + (size_t)b * (kRecHead + 2 * HD);
-    for (int o = threadIdx.x; o < 2 * HD; o += blockDim.x) {
-      double v[kClusterMax];
-#pragma unroll
-      for (int k = 0; k < kClusterMax; ++k) v[k] = k < nblk ? *cluster.map_shared_rank(&part[o], k) : 0.0;
-      double s = 0.0;
-#pragma unroll
-      for (int k = 0; k < kClusterMax; ++k)
-        if (k < nblk) s += v[k];
-      out[kRecHead + o] = s;
+  // ---- rank 0: reduce in rank order, update in registers ---------------------
+  double S0, cntf, sumf;
+  {
+    double x0 = 0.0, x1 = 0.0, x2 = 0.0;  // one lane per peer CTA, fixed-order warp tree
+    if (lane < nblk) {
+      x0 = heads[lane * 4 + 0];
+      x1 = heads[lane * 4 + 1];
+      x2 = heads[lane * 4 + 2];
     }
-    if (wid == 7) {  // one lane per peer CTA, then a fixed-order warp tree
-      double s0 = 0.0, c = 0.0, sf = 0.0;
-      if (lane < nblk) {
-        const double* hk = cluster.map_shared_rank(head, lane);
-        s0 = hk[1];
-        c = hk[2];
-        sf = hk[3];
+    S0 = warp_sum(x0);
+    cntf = warp_sum(x1);
+    sumf = warp_sum(x2);
+  }
+  double S1 = 0.0, S2 = 0.0;
+  if (owner)
+    for (int k = 0; k < nblk; ++k) {
+      S1 += parts[((size_t)k * HD + o) * 2];
+      S2 += parts[((size_t)k * HD + o) * 2 + 1];
+    }
+  if (!a.finalize_inline) {  // rank record for the particle-sharded exchange
+    double* out = a.out_record + (size_t)b * (kRecHead + 2 * HD);
+    if (owner) {
+      out[kRecHead + o] = S1;
+      out[kRecHead + HD + o] = S2;
+    }
+    if (o == 0) {
+      out[0] = cntf > 0.0 ? m : CUDART_INF;
+      out[1] = S0;
+      out[2] = cntf;
+      out[3] = sumf;
+      out[4] = (double)status0;
+      out[5] = (double)a.bad[b];
+    }
+    return;
+  }
+  int stt = status0;
+  if (stt == 0 && cntf <= 0.0) stt = MPPI_E_ALL_QUARANTINED;
+  if (stt == 0 && !(S0 > 0.0)) stt = MPPI_E_WEIGHT_UNDERFLOW;
+  double mu_new = mo, var_new = vo;
+  int varbad = 0;
+  if (stt == 0 && owner) {
+    const double avg = mo + S1 / S0;
+    mu_new = (1.0 - a.alpha_mu) * mo + a.alpha_mu * avg;
+    const double dl = mu_new - mo;
+    double em = S2 / S0 - 2.0 * dl * (S1 / S0) + dl * dl;
+    if (a.isotropic) emp[o] = em;
+    var_new = em;
+  }
+  if (a.isotropic) __syncthreads();
+  if (stt == 0 && owner) {
+    double em = var_new;
+    if (a.isotropic) {
+      const int h = o / D;
+      double sacc = 0.0;
+      for (int jj = 0; jj < D; ++jj) sacc += emp[h * D + jj];
+      em = sacc / D;
+    }
+    double vn = (1.0 - a.alpha_sigma) * vo + a.alpha_sigma * em;
+    vn = vn < a.smin ? a.smin : (vn > a.smax ? a.smax : vn);  // np.clip keeps NaN
+    var_new = vn;
+    varbad = (!(vn > 0.0) && !isnan(vn)) ? 1 : 0;
+  }
+  varbad = __syncthreads_or(varbad);
+  double* means = a.means + (size_t)b * HD;
+  double* var = a.var + (size_t)b * HD;
+  double* sd = a.sd + (size_t)b * HD;
+  if (owner) {
+    if (a.prev_means) {
+      a.prev_means[(size_t)b * HD + o] = mo;
+      a.prev_sd[(size_t)b * HD + o] = so;
+    }
+    if (stt == 0) {
+      means[o] = mu_new;
+      if (!varbad) {
+        var[o] = var_new;
+        sd[o] = sqrt(var_new);
+      } else {
+        var[o] = vo;
+        sd[o] = so;
       }
-      s0 = warp_sum(s0);
-      c = warp_sum(c);
-      sf = warp_sum(sf);
-      if (lane == 0) {
-        out[0] = c > 0.0 ? m : CUDART_INF;
-        out[1] = s0;
-        out[2] = c;
-        out[3] = sf;
-        out[4] = (double)status0;
-        out[5] = (double)a.bad[b];
-      }
+    } else if (a.shift && stt != MPPI_E_SKIPPED) {  // failure: the shift of controller.py:200 still stands
+      means[o] = mo;
+      var[o] = vo;
+      sd[o] = so;
     }
   }
-  cluster.sync();  // peers' shared memory stays alive until rank 0 has read it
-  MPPI_STAMP(6);
-  if (blk != 0 || !a.finalize_inline) return;
-  finalize_policy(a, b, rec, emp);
-  __syncthreads();
+  if (stt == 0 && o < D && a.cmd) a.cmd[(size_t)b * D + o] = mu_new;  // next_command "mean"
+  if (threadIdx.x == 0) {
+    const int stt2 = (stt == 0 && varbad) ? MPPI_E_NONPOSITIVE_VARIANCE : stt;
+    const int bad = a.bad[b];
+    if (a.info) {
+      mppi_step_info inf;
+      inf.status = stt2;
+      inf.bad_particle = bad >= 0x7f000000 ? -1 : bad;
+      inf.finite_count = (int)cntf;
+      inf._pad = 0;
+      inf.best_cost = cntf > 0.0 ? m : CUDART_NAN;
+      inf.mean_cost = cntf > 0.0 ? sumf / cntf : CUDART_NAN;
+      inf.device_ms = 0.0;
+      inf.sample_ms = inf.rollout_ms = inf.mlp_ms = inf.update_ms = 0.0;
+      a.info[b] = inf;
+    }
+    if (a.reset_status) {
+      a.status[b] = 0;
+      a.bad[b] = 0x7f7f7f7f;
+    } else {
+      a.status[b] = stt2;
+    }
+  }
   MPPI_STAMP(7);
 }
 

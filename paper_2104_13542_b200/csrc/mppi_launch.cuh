@@ -46,12 +46,14 @@ cudaError_t launch_rollout_d(const RolloutArgs<R>& a, long long warps, cudaStrea
 
 template <typename R, int D>
 cudaError_t launch_stats_cluster_d(const StatsArgs<R>& s, cudaStream_t st) {
-  const int HD = s.H * D;
-  const size_t smem = sizeof(double) * (2 * (size_t)s.ppb + 32 + 2 * HD + 8 + kRecHead + 2 * HD + HD) +
-                      sizeof(int) * (size_t)s.ppb;
+  const size_t smem = stats_cluster_smem_bytes(s.ppb, s.H * D);
   auto kern = stats_cluster_kernel<R, D>;
   if (s.nblk > 8) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (e != cudaSuccess) return e;
+  }
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
   }
   cudaLaunchConfig_t cfg = {};
