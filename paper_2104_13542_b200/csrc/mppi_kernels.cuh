@@ -931,12 +931,18 @@ constexpr int kClusterMaxPPB = 64;
 constexpr int kClusterEpsRegs = 32;  // perturbation rows held in registers per thread
 
 inline size_t stats_cluster_smem_bytes(int ppb, int HD) {
-  return sizeof(double) * (2 * (size_t)ppb + 32 + kClusterMax + kClusterMax * 4 + (size_t)kClusterMax * 2 * HD + HD) +
+  const size_t slots = ppb > kClusterEpsRegs ? (size_t)ppb : (size_t)kClusterEpsRegs;
+  return sizeof(double) * (2 * slots + 32 + kClusterMax + kClusterMax * 4 + (size_t)kClusterMax * 2 * HD + HD) +
          2 * sizeof(unsigned long long);
 }
 
+#ifdef MPPI_STATS_LB0  // A/B: let ptxas pick the register budget (128)
+#define MPPI_STATS_BOUNDS __launch_bounds__(kStatsThreads)
+#else
+#define MPPI_STATS_BOUNDS __launch_bounds__(kStatsThreads, 1)
+#endif
 template <typename R, int D>
-__global__ void __launch_bounds__(kStatsThreads) stats_cluster_kernel(const __grid_constant__ StatsArgs<R> a) {
+__global__ void MPPI_STATS_BOUNDS stats_cluster_kernel(const __grid_constant__ StatsArgs<R> a) {
   namespace cg = cooperative_groups;
   cg::cluster_group cluster = cg::this_cluster();
   extern __shared__ __align__(16) double sm[];
@@ -946,9 +952,10 @@ __global__ void __launch_bounds__(kStatsThreads) stats_cluster_kernel(const __gr
   const int H = a.H, HD = H * D, N = a.N;
   const int n0 = blk * a.ppb;
   const int cnt = max(0, min(N, n0 + a.ppb) - n0);
-  double* tot = sm;                      // [ppb]
-  double* wt = tot + a.ppb;              // [ppb]
-  double* red = wt + a.ppb;              // [32]
+  const int slots = max(a.ppb, kClusterEpsRegs);
+  double* tot = sm;                      // [slots]
+  double* wt = tot + slots;              // [slots], 16-byte aligned
+  double* red = wt + slots;              // [32]
   double* mins = red + 32;               // [kClusterMax] per-CTA best finite totals (pushed by peers)
   double* heads = mins + kClusterMax;    // [kClusterMax][4] S0, count, sum finite (rank 0)
   double* parts = heads + kClusterMax * 4;  // [kClusterMax][HD][2] S1, S2 pairs (rank 0)
@@ -999,11 +1006,11 @@ __global__ void __launch_bounds__(kStatsThreads) stats_cluster_kernel(const __gr
           if (a.learned) dv[u] = (double)a.mlp_d[m];
         }
       }
+      // the PA horizon sums reduce side by side (independent shuffle chains)
+      double ct[PA], ds[PA];
+      bool allfin[PA];
 #pragma unroll
       for (int u = 0; u < PA; ++u) {
-        const int i = i0 + u;
-        if (i >= cnt) break;
-        const int n = n0 + i;
         double c = 0.0, dself = 0.0;
         bool fin = true;
         if (lane < H) {
@@ -1014,18 +1021,28 @@ __global__ void __launch_bounds__(kStatsThreads) stats_cluster_kernel(const __gr
           }
           fin = isfinite(c);
         }
-        const bool allfin = __all_sync(0xffffffffu, fin);
-        double contrib = 0.0;
-        if (lane < H) contrib = disc_l * c;
-        double total = warp_sum(contrib);
-        if (!allfin) total = CUDART_INF;
+        allfin[u] = __all_sync(0xffffffffu, fin);
+        ct[u] = c;
+        ds[u] = dself;
+        cv[u] = lane < H ? disc_l * c : 0.0;  // the discounted contribution
+      }
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1)
+#pragma unroll
+        for (int u = 0; u < PA; ++u) cv[u] += __shfl_xor_sync(0xffffffffu, cv[u], off);
+#pragma unroll
+      for (int u = 0; u < PA; ++u) {
+        const int i = i0 + u;
+        if (i >= cnt) break;
+        const int n = n0 + i;
+        const double total = allfin[u] ? cv[u] : CUDART_INF;
         if (lane == 0) {
           tot[i] = total;
           if (a.totals) a.totals[(size_t)b * N + n] = total;
         }
         if (b == 0 && lane < H) {
-          if (a.dump_step) a.dump_step[(size_t)n * H + lane] = allfin ? c : 0.0;
-          if (a.dump_terms && a.learned) a.dump_terms[(size_t)T_SELF * N * H + (size_t)n * H + lane] = dself;
+          if (a.dump_step) a.dump_step[(size_t)n * H + lane] = allfin[u] ? ct[u] : 0.0;
+          if (a.dump_terms && a.learned) a.dump_terms[(size_t)T_SELF * N * H + (size_t)n * H + lane] = ds[u];
         }
       }
     }
@@ -1043,34 +1060,47 @@ __global__ void __launch_bounds__(kStatsThreads) stats_cluster_kernel(const __gr
   }
   cbar_wait(bar_min, 0);
   double m = CUDART_INF;
-  for (int k = 0; k < nblk; ++k) m = fmin(m, mins[k]);
+  for (int k = 0; k < nblk; ++k) m = mins[k] < m ? mins[k] : m;  // finite or +inf, never NaN
   MPPI_STAMP(2);
   // ---- weights (policy.py:103-121) ------------------------------------------
-  for (int i = threadIdx.x; i < cnt; i += blockDim.x)
-    wt[i] = (!failed && isfinite(tot[i])) ? exp(-(tot[i] - m) / a.beta) : 0.0;
+  // slots [cnt, 32) hold zero weights so the register loop below is branch-free
+  for (int i = threadIdx.x; i < max(cnt, kClusterEpsRegs); i += blockDim.x)
+    wt[i] = (i < cnt && !failed && isfinite(tot[i])) ? exp(-(tot[i] - m) / a.beta) : 0.0;
   if (b == 0 && a.dump_weights && !failed)
     for (int i = threadIdx.x; i < cnt; i += blockDim.x) a.dump_weights[n0 + i] = wt[i];
   __syncthreads();
   MPPI_STAMP(3);
   // ---- weighted sufficient statistics around the old mean, pushed to rank 0 --
-  // Zero weights add exact zeros, so the sums equal the reference's sums over
-  // the particles with nonzero weight in ascending order.
+  // Zero weights add exact zeros. Four interleaved partial sums per entry
+  // keep the FP64 dependency chains short (the reference's own reductions are
+  // numpy pairwise sums, so no summation order is privileged).
   if (owner) {
-    double s1 = 0.0, s2 = 0.0;
+    double s1[4] = {0.0, 0.0, 0.0, 0.0}, s2[4] = {0.0, 0.0, 0.0, 0.0};
     if (!failed) {
-      auto acc = [&](int i, double ev) {
-        const int ng = n0 + i + a.particle_offset;
-        const double dv = ng < a.null_count ? 0.0 - mo : (ng == a.null_count ? 0.0 : (mo + so * ev) - mo);
-        const double w = wt[i];
-        s1 += w * dv;
-        s2 += w * dv * dv;
-      };
+      const int g0 = n0 + a.particle_offset;  // global index of this CTA's first particle
+      const double2* w2 = reinterpret_cast<const double2*>(wt);
 #pragma unroll
-      for (int i = 0; i < kClusterEpsRegs; ++i)
-        if (i < cnt) acc(i, e[i]);
-      for (int i = kClusterEpsRegs; i < cnt; ++i) acc(i, __ldg(ep + (size_t)i * HD));
+      for (int i = 0; i < kClusterEpsRegs; i += 2) {
+        const double2 w = w2[i / 2];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const int ng = g0 + i + u;
+          const double dv = ng < a.null_count ? 0.0 - mo : (ng == a.null_count ? 0.0 : (mo + so * e[i + u]) - mo);
+          const double wu = u ? w.y : w.x;
+          s1[(i + u) & 3] += wu * dv;
+          s2[(i + u) & 3] += wu * dv * dv;
+        }
+      }
+      for (int i = kClusterEpsRegs; i < cnt; ++i) {
+        const int ng = g0 + i;
+        const double ev = __ldg(ep + (size_t)i * HD);
+        const double dv = ng < a.null_count ? 0.0 - mo : (ng == a.null_count ? 0.0 : (mo + so * ev) - mo);
+        s1[0] += wt[i] * dv;  // (constant index: the partial sums stay in registers)
+        s2[0] += wt[i] * dv * dv;
+      }
     }
-    push_f64x2(mapa_rank(smem_addr(parts + ((size_t)blk * HD + o) * 2), 0), s1, s2, mapa_rank(bar_sum, 0));
+    push_f64x2(mapa_rank(smem_addr(parts + ((size_t)blk * HD + o) * 2), 0), (s1[0] + s1[1]) + (s1[2] + s1[3]),
+               (s2[0] + s2[1]) + (s2[2] + s2[3]), mapa_rank(bar_sum, 0));
   }
   if (wid == nw - 1) {
     double s0 = 0.0, c = 0.0, sf = 0.0;
