@@ -449,9 +449,6 @@ int enqueue_iteration(mppi_plan* p, int it, bool inline_final, double* out_recor
     s.dump_terms = p->d_terms.p;
     s.dump_weights = inline_final ? p->d_w.p : nullptr;
   }
-#ifdef MPPI_DEBUG_TIMERS
-  if ((stages & 4u) && getenv("MPPI_DEBUG_TWICE")) CK(launch_stats_any<R>(s, p->D, st));  // warm re-run (timing only)
-#endif
   if (stages & 4u) CK(launch_stats_any<R>(s, p->D, st));
   return MPPI_OK;
 }
@@ -481,9 +478,6 @@ int enqueue_step_body(mppi_plan* p, cudaStream_t st, bool stage_events, bool h2d
   // one H2D node: the (B,2d) state followed by the step counter (pseudorandom
   // generator). Status words were re-armed by the previous step's finalize.
   // (The episode graph writes the state on the device instead.)
-#ifdef MPPI_DEBUG_TIMERS
-  if (getenv("MPPI_DEBUG_NO_H2D")) h2d = false;  // timing experiment only: the state goes stale
-#endif
   if (h2d && !p->capture_inl)
     CK(cudaMemcpyAsync(p->state.p, p->h_state, sizeof(double) * (B * 2 * D + 1), cudaMemcpyHostToDevice, st));
   // event-record nodes between the stages give per-kernel device times of
@@ -789,8 +783,12 @@ int mppi_plan_create(const mppi_chain_desc* chain, const mppi_cost_desc* costs,
     CKR(p->info.alloc(B));
     if (getenv("MPPI_DEBUG_TIMERS")) {
       // stats phases (16 per stats block) + fused rollout/MLP phases (8 per CTA, <= 256 CTAs)
-      CKR(p->dbg.alloc((size_t)16 * p->nblk + 16 * 256));
-      CK(cudaMemset(p->dbg.p, 0, sizeof(unsigned long long) * (16 * p->nblk + 16 * 256)));
+      CKR(p->dbg.alloc((size_t)16 * p->nblk + 2 * 16 * 256));
+      CK(cudaMemset(p->dbg.p, 0, sizeof(unsigned long long) * (16 * p->nblk + 2 * 16 * 256)));
+#ifdef MPPI_DEBUG_TIMERS
+      unsigned long long* mdbg = p->dbg.p + 16 * p->nblk + 16 * 256;
+      CK(cudaMemcpyToSymbol(mlp_dbg, &mdbg, sizeof(mdbg)));
+#endif
     }
     if (p->dump) {
       CKR(p->d_pos.alloc((size_t)N * HD));
@@ -1143,7 +1141,7 @@ int mppi_step(mppi_plan* p, const double* theta, const double* theta_dot, double
   if (p->profile_level) CK(cudaEventElapsedTime(&ms, p->ev0, p->ev1));
   memcpy(command_out, p->h_cmd, sizeof(double) * B * D);
   if (p->dbg.p) {  // debug: stats-kernel phase timeline of instance 0, relative to block 0 start
-    std::vector<unsigned long long> t((size_t)16 * p->nblk + 16 * 256);
+    std::vector<unsigned long long> t((size_t)16 * p->nblk + 2 * 16 * 256);
     CK(cudaMemcpy(t.data(), p->dbg.p, sizeof(unsigned long long) * t.size(), cudaMemcpyDeviceToHost));
     const unsigned long long* f = t.data() + 16 * p->nblk;
     unsigned long long t0 = t[0];
@@ -1162,6 +1160,26 @@ int mppi_step(mppi_plan* p, const double* theta, const double* theta_dot, double
       }
       fprintf(stderr, "fused max    :");
       for (int j = 0; j < 12; ++j) fprintf(stderr, " %7.2f", mx[j]);
+      fprintf(stderr, "\n");
+    }
+    {  // MLP phase stamps: min / max over CTAs, relative to the same origin
+      const unsigned long long* g = t.data() + 16 * p->nblk + 16 * 256;
+      double lo[16], hi[16];
+      for (int j = 0; j < 16; ++j) lo[j] = 1e30, hi[j] = -1e30;
+      for (int k = 0; k < 255; ++k)
+        for (int j = 0; j < 16; ++j)
+          if (g[16 * k + j]) {
+            const double v = (double)(long long)(g[16 * k + j] - t0) * 1e-3;
+            lo[j] = std::min(lo[j], v);
+            hi[j] = std::max(hi[j], v);
+          }
+      const unsigned long long re = t[16 * p->nblk + 16 * 255 + 15], me = g[16 * 255 + 15];
+      fprintf(stderr, "rollout last warp end %.2f, mlp last CTA end %.2f\n",
+              re ? (double)(long long)(re - t0) * 1e-3 : -1.0, me ? (double)(long long)(me - t0) * 1e-3 : -1.0);
+      fprintf(stderr, "mlp min     :");
+      for (int j = 0; j < 13; ++j) fprintf(stderr, " %7.2f", lo[j] < 1e29 ? lo[j] : -1.0);
+      fprintf(stderr, "\nmlp max     :");
+      for (int j = 0; j < 13; ++j) fprintf(stderr, " %7.2f", hi[j] > -1e29 ? hi[j] : -1.0);
       fprintf(stderr, "\n");
     }
     for (int k = 0; k < p->nblk; ++k) {

@@ -239,11 +239,6 @@ __device__ __forceinline__ bool capsule_hits_sphere(const R* P0, const R* P1, R 
   return sqrt(ex * ex + ey * ey + ez * ez) < rcap + sph[3];
 }
 
-// ---------------------------------------------------------------- programmatic dependent launch
-// The step's kernels are chained with programmatic stream serialisation: a
-// dependent grid may start (and run its prologue) while its predecessor
-// drains, and blocks in pdl_wait() until the predecessor has completed and its
-// writes are visible. pdl_trigger() lets the dependent grid be scheduled early.
 // ---------------------------------------------------------------- cluster push
 // Distributed-shared-memory pushes that complete on the RECEIVER's mbarrier
 // (st.async ... complete_tx): no cluster-wide fence, no L1 invalidation.
@@ -283,6 +278,11 @@ __device__ __forceinline__ void cluster_init_fence_arrive() {
 }
 __device__ __forceinline__ void cluster_wait() { asm volatile("barrier.cluster.wait.aligned;" ::: "memory"); }
 
+// ---------------------------------------------------------------- programmatic dependent launch
+// The step's kernels are chained with programmatic stream serialisation: a
+// dependent grid may start (and run its prologue) while its predecessor
+// drains, and blocks in pdl_wait() until the predecessor has completed and its
+// writes are visible. pdl_trigger() lets the dependent grid be scheduled early.
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 // host side: which PDL features are on (MPPI_PDL bit mask, A/B switch):

@@ -471,6 +471,13 @@ __global__ void __launch_bounds__(kRolloutWarps * 32, MINB)
   R* cap = reinterpret_cast<R*>(smem_raw) + (size_t)wib * a.chain.n_caps * 6 * 32;
   rollout_particle<R, D>(a, g, lane, cap, nullptr);
   MPPI_TSTAMP(dbg, 1);
+#ifdef MPPI_DEBUG_TIMERS
+  if (a.dbg != nullptr && lane == 0) {  // latest warp end over the grid
+    unsigned long long t_;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));
+    atomicMax(&a.dbg[16 * 255 + 15], t_);
+  }
+#endif
 }
 
 // ============================================================== statistics
@@ -965,6 +972,7 @@ __global__ void MPPI_STATS_BOUNDS stats_cluster_kernel(const __grid_constant__ S
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const int o = threadIdx.x;
   const bool owner = o < HD;  // H*d <= 256 = blockDim: one policy entry per thread
+  MPPI_STAMP(6);  // (debug) CTA entry
   if (threadIdx.x == 0) {  // each receive barrier completes on bytes alone
     cbar_init(bar_min, 1);
     cbar_init(bar_sum, 1);

@@ -67,9 +67,9 @@ cudaError_t launch_stats_cluster_d(const StatsArgs<R>& s, cudaStream_t st) {
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
   attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[1].val.programmaticStreamSerializationAllowed = (pdl_mask() & PDL_STATS) != 0;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 2;
+  cfg.numAttrs = (pdl_mask() & PDL_STATS) ? 2 : 1;  // no programmatic edge unless asked for
   return cudaLaunchKernelEx(&cfg, kern, s);
 }
 

@@ -334,6 +334,23 @@ __device__ __forceinline__ void tmem_convert8(uint32_t chunk, int cg, const floa
   asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
 }
 
+#ifdef MPPI_DEBUG_TIMERS
+// phase stamps (globaltimer) of CTAs < 256, 16 slots each: set by the host
+static __device__ unsigned long long* mlp_dbg = nullptr;
+#define MLP_STAMP(k)                                                         \
+  do {                                                                       \
+    if (mlp_dbg != nullptr && blockIdx.x < 256) {                            \
+      unsigned long long t_;                                                 \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                 \
+      mlp_dbg[16 * blockIdx.x + (k)] = t_;                                   \
+    }                                                                        \
+  } while (0)
+#else
+#define MLP_STAMP(k) \
+  do {               \
+  } while (0)
+#endif
+
 static __global__ void __maxnreg__(88)
     mlp_tcgen05_kernel(const float* __restrict__ x, long long M, const unsigned char* __restrict__ img,
                        float* __restrict__ out, int early) {
@@ -347,6 +364,7 @@ static __global__ void __maxnreg__(88)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sm + OFF_KTMEMPTR);
 
   if (tid == 0) {
+    MLP_STAMP(12);
     for (int i = 0; i < 5; ++i) mbar_init(barW0 + 8 * i, 1);  // W0 W1 W2 L1[2]
     for (int i = 0; i < 8; ++i) mbar_init(barA1 + 8 * i, kMlpEpiWarps);
     mbar_init(barL2done, 1);
@@ -372,6 +390,7 @@ static __global__ void __maxnreg__(88)
   if (warp == kMlpEpiWarps) {
     // ============================== issuer ==================================
     if (lane == 0) {
+      MLP_STAMP(11);
       mbar_expect_tx(barW0, kSeg0);
       bulk_g2s(sb + 0, img, kSeg0, barW0);
       mbar_expect_tx(barW1, kSeg1);
@@ -408,7 +427,10 @@ static __global__ void __maxnreg__(88)
 #pragma unroll
         for (int c = 0; c < 8; ++c) {  // layer 2, K chunk c: slices 2c, 2c+1 of acc1 (in place)
           mbar_wait(barA1 + 8 * c, ph);
-          if (first && c == 0) mbar_wait(barW1, 0);
+          if (first && c == 0) {
+            mbar_wait(barW1, 0);
+            MLP_STAMP(9);
+          }
           if (!first && c == 0) {  // acc2 is rewritten: the previous tile's layer 3 (its A reader) is done
             mbar_wait(barL3done, ph ^ 1u);
           }
@@ -434,7 +456,10 @@ static __global__ void __maxnreg__(88)
 #pragma unroll
         for (int c = 0; c < 4; ++c) {  // layer 3, K chunk c: slices 2c, 2c+1 of acc2 (in place)
           mbar_wait(barA2 + 8 * c, ph);
-          if (first && c == 0) mbar_wait(barW2, 0);
+          if (first && c == 0) {
+            mbar_wait(barW2, 0);
+            MLP_STAMP(10);
+          }
           tc_fence_after();
 #pragma unroll
           for (int g = 0; g < 2; ++g) {
@@ -486,6 +511,7 @@ static __global__ void __maxnreg__(88)
     };
     float xv[8];
     long long tile = blockIdx.x;
+    if (tid == 0) MLP_STAMP(0);
     if (early) pdl_trigger();
     pdl_wait();  // the rollout's positional encodings are complete past this point
     if (tile < ntiles) {
@@ -493,7 +519,9 @@ static __global__ void __maxnreg__(88)
       if (tid < 256) store_split8(sm, OFF_XH, OFF_XL, umma_off(tid & 127, (tid >> 7) * 8, 16), xv);
       fence_async_smem();
       arrive(barX);
+      if (tid == 0) MLP_STAMP(1);
       mbar_wait(barW0, 0);
+      if (tid == 0) MLP_STAMP(2);
     }
     const float s0 = par[kMlpH0 + kMlpH1 + 2 * kMlpH2 + 1];
     const float s1 = par[kMlpH0 + kMlpH1 + 2 * kMlpH2 + 2];
@@ -508,6 +536,7 @@ static __global__ void __maxnreg__(88)
         if ((c & 3) == 0) {
           const int hb = c >> 2;
           mbar_wait(barL10 + 8 * hb, (phL1 >> hb) & 1u);
+          if (tid == 0 && hb == 0 && t == blockIdx.x) MLP_STAMP(3);
           phL1 ^= 1u << hb;
           tc_fence_after();
         }
@@ -526,10 +555,12 @@ static __global__ void __maxnreg__(88)
     };
     uint32_t ph = 0;
     if (tile < ntiles) epilogue_l1(tile);
+    if (tid == 0) MLP_STAMP(4);
     for (; tile < ntiles; tile += G, ph ^= 1u) {
       const bool has_next = tile + G < ntiles;
       // ---- layer-2 epilogue, in place in acc2
       mbar_wait(barL2done, ph);
+      if (tid == 0 && tile == blockIdx.x) MLP_STAMP(5);
       tc_fence_after();
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
@@ -540,10 +571,12 @@ static __global__ void __maxnreg__(88)
         tmem_convert8(acc2 + lane_base + 32 * c, cg, y, pair_bar);
         arrive(barA2 + 8 * c);
       }
+      if (tid == 0 && tile == blockIdx.x) MLP_STAMP(6);
       // ---- the next tile's layer-1 epilogue runs under this tile's layer 3
       if (has_next) epilogue_l1(tile + G);
       // ---- output layer of this tile
       mbar_wait(barL3done, ph);
+      if (tid == 0 && tile == blockIdx.x) MLP_STAMP(7);
       tc_fence_after();
       float part = 0.f;
       {
@@ -564,6 +597,7 @@ static __global__ void __maxnreg__(88)
       }
       tc_fence_before();
       epi_barrier();
+      if (tid == 0 && tile == blockIdx.x) MLP_STAMP(8);
     }
   }
   __syncthreads();
@@ -571,6 +605,13 @@ static __global__ void __maxnreg__(88)
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
   }
+#ifdef MPPI_DEBUG_TIMERS
+  if (mlp_dbg != nullptr && tid == 0) {  // latest CTA end over the grid
+    unsigned long long t_;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));
+    atomicMax(&mlp_dbg[16 * 255 + 15], t_);
+  }
+#endif
 }
 
 // ------------------------------------------------------------------ host side
@@ -639,6 +680,10 @@ inline cudaError_t mlp_forward(const MlpWeights& m, const float* x, long long ro
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const long long tiles = (rows + 127) / 128;
   const unsigned grid = (unsigned)(tiles < sms ? tiles : sms);
+  if (!(pdl_mask() & (PDL_MLP | PDL_EARLY))) {  // plain launch: no programmatic edge in a captured graph
+    mlp_tcgen05_kernel<<<grid, kMlpThreads, kMlpKernelSmem, st>>>(x, rows, (const unsigned char*)m.img, out, 0);
+    return cudaGetLastError();
+  }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid, 1, 1);
   cfg.blockDim = dim3(kMlpThreads, 1, 1);
