@@ -38,11 +38,36 @@ def update_bytes_per_unit(dof: int = 7) -> int:
     return dof * 8 + 4 + 4  # eps row re-read, step cost + learned distance read
 
 
+# kernel-name fragments of each stage in an ncu summary (scripts/ncu_summary.py)
+NCU_KERNEL = {"rollout": "rollout_kernel", "mlp": "mlp_tcgen05", "update": "stats_"}
+
+
+def ncu_traffic(summary: list | None, stage: str):
+    """DRAM bytes (read + write) per launch of the stage's kernel in a committed
+    ``ncu --set full`` summary (one step's capture), or None."""
+    for k in summary or []:
+        if NCU_KERNEL[stage] in k.get("kernel", "") and k.get("dram_read_B") is not None:
+            return float(k["dram_read_B"]) + float(k.get("dram_write_B") or 0.0)
+    return None
+
+
 def step_roofline(stage_ms: dict, rows: int, particles: int, horizon: int, dof: int, config: int,
-                  peaks: dict, peaks_kind: str) -> dict:
+                  peaks: dict, peaks_kind: str, ncu_summary: list | None = None,
+                  ncu_source: str | None = None) -> dict:
     """Roofline entry for the dominant kernel of the step (stage_ms from the
-    event-record nodes of the timed graph replays)."""
+    event-record nodes of the timed graph replays); `traffic` from the
+    committed ncu summary of the same workload when one is given."""
     stage = max(("rollout", "mlp", "update"), key=lambda k: stage_ms.get(k, 0.0))
+    out = _stage_roofline(stage, stage_ms, rows, dof, config, peaks, peaks_kind)
+    tr = ncu_traffic(ncu_summary, stage)
+    if tr is not None and out.get("kernel"):
+        out["traffic"] = tr
+        out["traffic_source"] = f"{ncu_source}: dram__bytes_read.sum + dram__bytes_write.sum (ncu replay, cold L2)"
+    return out
+
+
+def _stage_roofline(stage: str, stage_ms: dict, rows: int, dof: int, config: int, peaks: dict,
+                    peaks_kind: str) -> dict:
     t = stage_ms[stage] * 1e-3
     if not t > 0.0:  # stage events disabled (MPPI_STAGE_EVENTS=0): no per-kernel time
         return {"kernel": None, "bound": None, "achieved": None, "peak": None, "unit": None, "frac": None,

@@ -6,6 +6,9 @@ set -x
 python bench.py --steps 300 --warmup 10 > $O/${R}_bench_c2.json 2> $O/${R}_bench_c2.err
 python bench.py --workload c4 --steps 20 --warmup 3 --no-cpu-baseline > $O/${R}_bench_c4.json 2> $O/${R}_bench_c4.err
 python bench.py --workload c3 --steps 100 --warmup 10 --no-cpu-baseline --no-scale-roofline > $O/${R}_bench_c3.json 2> $O/${R}_bench_c3.err
+for n in 4096 32768 262144; do
+  python bench.py --workload c5 --particles $n --steps 20 --warmup 3 --no-cpu-baseline > $O/${R}_bench_c5_$n.json 2> $O/${R}_bench_c5_$n.err
+done
 B="python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-scale-roofline"
 $B > /dev/null 2>&1 && ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
   --log-file $O/${R}_bench_launches.csv $B > /dev/null 2>&1
