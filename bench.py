@@ -591,12 +591,15 @@ def run_sweep(args):
         ctrl = configs.make_controller(2, particles=Np, precision=args.precision, device=local)
         step = lambda: ctrl.control_step(st)  # noqa: E731
     else:
-        from paper_2104_13542_b200.sharded import RecordExchange, ShardedController
+        from paper_2104_13542_b200.sharded import PeerExchange, RecordExchange, ShardedController
 
         kw = dict(configs.CONTROLLER_KW)
         kw.pop("particles")
+        # the record exchange fused into the statistics kernel over NVLink peer
+        # memory; MPPI_EXCHANGE=nccl: one NCCL all-gather between two kernels
+        nccl = os.environ.get("MPPI_EXCHANGE", "peer") == "nccl"
         ctrl = ShardedController(load_chain("arm7.chain"), configs.make_goal(2), particles=Np, world_size=ws,
-                                 rank=rank, device=local, exchange=RecordExchange(),
+                                 rank=rank, device=local, exchange=RecordExchange() if nccl else PeerExchange(),
                                  weights=configs.make_weights(2), self_collision=load_arm7_surrogate(),
                                  precision=args.precision, **kw)
         step = lambda: ctrl.control_step(st)  # noqa: E731
@@ -626,7 +629,9 @@ def run_sweep(args):
         "scaling": "strong", "vs_baseline": None, "dtype": args.precision.replace("fp", "f"), "data": "synthetic",
         "config": {"workload": f"config5: one controller, {Np} particles x H30, config-2 costs, "
                                + ("particle-sharded, 1 all-gather/iteration" if ws > 1 else "single GPU"),
-                   "particles": Np, "horizon": 30, "l2": "flushed before every timed step"},
+                   "particles": Np, "horizon": 30, "l2": "flushed before every timed step",
+                   **({"exchange": "nccl all-gather" if nccl else "fused peer-memory push (NVLink P2P)"}
+                      if ws > 1 else {})},
         "e2e": {"value": Np * 30 / (wall_ms * 1e-3), "unit": "particle-steps/s", "h2d_bytes_per_step": 112,
                 "d2h_bytes_per_step": 136, "wall_ms_per_step": wall_ms,
                 "api": "Controller / ShardedController.control_step (host wall clock)"},

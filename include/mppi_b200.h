@@ -34,6 +34,8 @@
  *   mppi_stats_dev /        (new: particle-sharded update, §8(e) config 5 —
  *   mppi_finalize_dev         per-rank weighted sufficient statistics, one
  *                             all-gather, fixed-order combine)
+ *   mppi_step_exchange      (new: the same with the exchange fused into the
+ *                             statistics kernel over NVLink peer memory)
  *
  *   The reference's fine-grained operator seam (kernels/__init__.py:50-66),
  *   float64 in / float64 out, caller-owned outputs:
@@ -83,6 +85,7 @@ extern "C" {
 #define MPPI_MAX_HORIZON  32  /* one warp per particle, one lane per step   */
 #define MPPI_MAX_CAPSULES 16
 #define MPPI_MAX_PAIRS    64
+#define MPPI_MAX_PEERS    8   /* ranks of one node in the peer-memory exchange */
 #define MPPI_MLP_IN_MAX   16  /* 2*dof positional encoding, padded          */
 
 enum mppi_status {
@@ -424,6 +427,29 @@ int mppi_stats_dev(mppi_plan* plan, const double* theta, const double* theta_dot
  * update; command/info as in mppi_step (instance 0). */
 int mppi_finalize_dev(mppi_plan* plan, const void* records_dev, int32_t n_records,
                       double* command_out, mppi_step_info* info, void* stream);
+
+/* ---- particle-sharded update over peer memory (config 5) ---------------
+ * The same algebra as mppi_stats_dev + all-gather + mppi_finalize_dev, with
+ * the collective fused into the statistics kernel: the kernel pushes the
+ * rank record into slot [rank] of every rank's receive buffer with NVLink
+ * P2P stores, publishes it with a release store of a sequence number into
+ * every rank's flag [rank], waits for all ranks' flags and applies the update
+ * (replaces sharded.py's NCCL all-gather; reference: controller.py:198-260
+ * run on one controller's particles split over the ranks).
+ * Setup, once per rank: mppi_peer_buffers -> mppi_ipc_get_handle on both
+ * buffers -> exchange handles (any host collective) -> mppi_ipc_open_handle
+ * for the peers' -> mppi_set_peers (slot [rank] = this plan's own buffers). */
+int mppi_peer_buffers(mppi_plan* plan, int32_t world, void** recv_dev, void** flags_dev);
+int mppi_set_peers(mppi_plan* plan, int32_t world, int32_t rank, void* const* recv_ptrs,
+                   void* const* flag_ptrs);
+/* One control step (all iterations) of this rank's particle shard; every rank
+ * calls it with the same state and receives the same command. */
+int mppi_step_exchange(mppi_plan* plan, const double* theta, const double* theta_dot,
+                       double* command_out, mppi_step_info* info);
+/* CUDA IPC of device buffers (handle: 64 bytes). */
+int mppi_ipc_get_handle(void* dev_ptr, void* handle_out);
+int mppi_ipc_open_handle(const void* handle, void** dev_ptr_out);
+int mppi_ipc_close(void* dev_ptr);
 
 /* ---- stateless free functions (host in, host out) ---------------------- */
 int mppi_halton_points(int64_t count, int32_t dims, double* out /* (count,dims) */);

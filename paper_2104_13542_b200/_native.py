@@ -177,6 +177,12 @@ _SIGS = {
     "mppi_stats_record_len":(C.c_int, [_vp, C.POINTER(C.c_int32)]),
     "mppi_stats_dev": (C.c_int, [_vp, _dp, _dp, _vp, _vp]),
     "mppi_finalize_dev": (C.c_int, [_vp, _vp, C.c_int32, _dp, C.POINTER(StepInfo), _vp]),
+    "mppi_peer_buffers": (C.c_int, [_vp, C.c_int32, C.POINTER(_vp), C.POINTER(_vp)]),
+    "mppi_set_peers": (C.c_int, [_vp, C.c_int32, C.c_int32, C.POINTER(_vp), C.POINTER(_vp)]),
+    "mppi_step_exchange": (C.c_int, [_vp, _dp, _dp, _dp, C.POINTER(StepInfo)]),
+    "mppi_ipc_get_handle": (C.c_int, [_vp, C.c_char_p]),
+    "mppi_ipc_open_handle": (C.c_int, [C.c_char_p, C.POINTER(_vp)]),
+    "mppi_ipc_close": (C.c_int, [_vp]),
     "mppi_halton_points": (C.c_int, [C.c_int64, C.c_int32, _dp]),
     "mppi_gaussianize": (C.c_int, [_dp, C.c_int64, _dp]),
     "mppi_bspline_basis": (C.c_int, [C.c_int32, C.c_int32, C.c_int32, _dp]),

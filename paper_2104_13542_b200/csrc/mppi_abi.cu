@@ -204,6 +204,14 @@ struct mppi_plan {
   int profile_level = 0;  // 0 none, 1 device time of the lean graph, 2 instrumented graph (stage times)
   unsigned long long step_counter = 0;
   int sharded_iter = 0;
+  // particle-sharded exchange over peer memory (mppi_step_exchange)
+  DevBuf<double> peer_recv_buf;             // [2][world][reclen] this rank's receive slots
+  DevBuf<unsigned long long> peer_flag_buf;  // [world]
+  DevBuf<double*> peer_recv_tab;            // [world] pointers (peer mappings), device
+  DevBuf<unsigned long long*> peer_flag_tab;
+  int peer_world = 0, peer_rank = 0;
+  bool peer_active = false;                 // set while enqueuing an exchange step
+  unsigned long long peer_seq = 0;
   // eval scratch
   DevBuf<double> e_in0, e_in1, e_pos, e_vel, e_acc, e_terms, e_step, e_tot, e_state, e_dts;
   DevBuf<unsigned char> e_stepbuf;
@@ -442,6 +450,16 @@ int enqueue_iteration(mppi_plan* p, int it, bool inline_final, double* out_recor
   s.status = p->status.p;
   s.bad = p->bad.p;
   s.dbg = p->dbg.p;
+  if (p->peer_active && !inline_final) {
+    s.peer_recv = p->peer_recv_tab.p;
+    s.peer_flags = p->peer_flag_tab.p;
+    s.my_recv = p->peer_recv_buf.p;
+    s.my_flags = p->peer_flag_buf.p;
+    s.world = p->peer_world;
+    s.rank = p->peer_rank;
+    s.seq = p->peer_seq;
+    s.reset_status = it == p->iters - 1;
+  }
   s.cmd = p->cmd_dst ? p->cmd_dst : p->m_cmd;  // mapped host memory: no D2H copy node
   s.info = p->info_dst ? p->info_dst : p->m_info;
   if (p->dump) {
@@ -887,6 +905,10 @@ int mppi_plan_destroy(mppi_plan* p) {
   if (p->ev1) cudaEventDestroy(p->ev1);
   for (auto e : p->stage_ev) cudaEventDestroy(e);
   if (p->stream) cudaStreamDestroy(p->stream);
+  p->peer_recv_buf.release();
+  p->peer_flag_buf.release();
+  p->peer_recv_tab.release();
+  p->peer_flag_tab.release();
   if (p->stream2) cudaStreamDestroy(p->stream2);
   if (p->ev_fork) cudaEventDestroy(p->ev_fork);
   if (p->ev_join) cudaEventDestroy(p->ev_join);
@@ -1640,6 +1662,96 @@ int mppi_finalize_dev(mppi_plan* p, const void* records_dev, int32_t n_records, 
     if (command_out) memcpy(command_out, p->h_cmd, sizeof(double) * p->D);
     if (info) memcpy(info, p->h_info, sizeof(mppi_step_info));
   }
+  return MPPI_OK;
+}
+
+// ---------------------------------------------------------------- exchange over peer memory
+int mppi_peer_buffers(mppi_plan* p, int32_t world, void** recv_dev, void** flags_dev) {
+  if (!p || !recv_dev || !flags_dev || world < 1 || world > MPPI_MAX_PEERS)
+    return fail(MPPI_E_BAD_ARGUMENT, "world size out of range");
+  if (p->B != 1) return fail(MPPI_E_CONFIG, "particle sharding is for single-instance plans");
+  CKR(set_device(p));
+  const size_t reclen = kRecHead + 2 * (size_t)p->H * p->D;
+  if (p->peer_world != world) {
+    p->peer_recv_buf.release();
+    p->peer_flag_buf.release();
+    CKR(p->peer_recv_buf.alloc(2 * (size_t)world * reclen));
+    CKR(p->peer_flag_buf.alloc(world));
+    CK(cudaMemset(p->peer_flag_buf.p, 0, sizeof(unsigned long long) * world));
+    p->peer_world = world;
+    p->peer_seq = 0;
+  }
+  *recv_dev = p->peer_recv_buf.p;
+  *flags_dev = p->peer_flag_buf.p;
+  return MPPI_OK;
+}
+
+int mppi_set_peers(mppi_plan* p, int32_t world, int32_t rank, void* const* recv_ptrs, void* const* flag_ptrs) {
+  if (!p || !recv_ptrs || !flag_ptrs) return fail(MPPI_E_BAD_ARGUMENT, "null argument");
+  if (world != p->peer_world || rank < 0 || rank >= world)
+    return fail(MPPI_E_BAD_ARGUMENT, "mppi_peer_buffers(world) first; rank out of range");
+  if (recv_ptrs[rank] != p->peer_recv_buf.p || flag_ptrs[rank] != p->peer_flag_buf.p)
+    return fail(MPPI_E_BAD_ARGUMENT, "slot [rank] must hold this plan's own buffers");
+  CKR(set_device(p));
+  p->peer_recv_tab.release();
+  p->peer_flag_tab.release();
+  CKR(p->peer_recv_tab.alloc(world));
+  CKR(p->peer_flag_tab.alloc(world));
+  CK(cudaMemcpy(p->peer_recv_tab.p, recv_ptrs, sizeof(double*) * world, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(p->peer_flag_tab.p, flag_ptrs, sizeof(unsigned long long*) * world, cudaMemcpyHostToDevice));
+  p->peer_rank = rank;
+  return MPPI_OK;
+}
+
+int mppi_step_exchange(mppi_plan* p, const double* theta, const double* theta_dot, double* command_out,
+                       mppi_step_info* info) {
+  if (!p || !theta || !theta_dot || !command_out) return fail(MPPI_E_BAD_ARGUMENT, "null argument");
+  if (!p->peer_recv_tab.p) return fail(MPPI_E_CONFIG, "mppi_set_peers first");
+  if (p->learned() && !p->mlp_ready) return fail(MPPI_E_CONFIG, "learned provider without weights");
+  CKR(set_device(p));
+  cudaStream_t st = p->stream;
+  const int D = p->D;
+  memcpy(p->h_state, theta, sizeof(double) * D);
+  memcpy(p->h_state + D, theta_dot, sizeof(double) * D);
+  const unsigned long long ctr = p->step_counter++;
+  memcpy(p->h_state + 2 * D, &ctr, sizeof(ctr));
+  CK(cudaMemcpyAsync(p->state.p, p->h_state, sizeof(double) * (2 * D + 1), cudaMemcpyHostToDevice, st));
+  p->peer_active = true;
+  int rc = MPPI_OK;
+  for (int it = 0; it < p->iters && rc == MPPI_OK; ++it) {
+    ++p->peer_seq;  // one exchange per iteration, the same count on every rank
+    rc = enqueue_sampling(p, it, st);
+    if (rc == MPPI_OK)
+      rc = p->precision == MPPI_FP64 ? enqueue_iteration<double>(p, it, false, nullptr, st)
+                                     : enqueue_iteration<float>(p, it, false, nullptr, st);
+  }
+  p->peer_active = false;
+  CKR(rc);
+  CK(cudaStreamSynchronize(st));
+  memcpy(command_out, p->h_cmd, sizeof(double) * D);
+  if (info) memcpy(info, p->h_info, sizeof(mppi_step_info));
+  return MPPI_OK;
+}
+
+int mppi_ipc_get_handle(void* dev_ptr, void* handle_out) {
+  if (!dev_ptr || !handle_out) return fail(MPPI_E_BAD_ARGUMENT, "null argument");
+  cudaIpcMemHandle_t h;
+  CK(cudaIpcGetMemHandle(&h, dev_ptr));
+  memcpy(handle_out, &h, sizeof(h));
+  return MPPI_OK;
+}
+
+int mppi_ipc_open_handle(const void* handle, void** dev_ptr_out) {
+  if (!handle || !dev_ptr_out) return fail(MPPI_E_BAD_ARGUMENT, "null argument");
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle, sizeof(h));
+  CK(cudaIpcOpenMemHandle(dev_ptr_out, h, cudaIpcMemLazyEnablePeerAccess));
+  return MPPI_OK;
+}
+
+int mppi_ipc_close(void* dev_ptr) {
+  if (!dev_ptr) return fail(MPPI_E_BAD_ARGUMENT, "null argument");
+  CK(cudaIpcCloseMemHandle(dev_ptr));
   return MPPI_OK;
 }
 

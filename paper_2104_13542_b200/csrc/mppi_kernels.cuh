@@ -510,6 +510,19 @@ struct StatsArgs {
   double* dump_terms;  // (6,N,H) instance 0 (selfcoll row written for learned)
   double* dump_weights;  // (N) instance 0
   unsigned long long* dbg;  // debug phase timers (globaltimer ns), NULL in production
+  // Particle-sharded exchange over peer memory (config 5, mppi_step_exchange):
+  // when peer_recv is set the rank record is not written to out_record but
+  // pushed into slot [rank] of every rank's receive buffer (NVLink P2P
+  // stores), published by a release store of `seq` into every rank's flag
+  // [rank]; the block then waits for all `world` flags and applies the update
+  // itself (exchange_and_finalize). Receive buffers are [2][world][reclen]
+  // (parity of seq), flags [world] u64, monotonically increasing.
+  double* const* peer_recv;               // [world] device pointers (peer mappings)
+  unsigned long long* const* peer_flags;  // [world]
+  const double* my_recv;
+  const unsigned long long* my_flags;
+  int world, rank;
+  unsigned long long seq;
 };
 
 __device__ __forceinline__ double block_min_d(double v, double* red) {
@@ -712,6 +725,44 @@ static __device__ void finalize_policy(const StatsArgs<R>& a, int b, const doubl
   }
 }
 
+// The rank record `rec` (reclen doubles, shared memory) -> every rank's
+// receive slot [rank], release flag, wait for all ranks, fixed-order combine,
+// update. One block, all threads. scratch: >= reclen + HD + 8 * (1 + kRecHead)
+// + 32 doubles of shared memory not aliasing `rec`.
+template <typename R>
+static __device__ void exchange_and_finalize(const StatsArgs<R>& a, const double* rec, int HD, double* scratch) {
+  const int reclen = kRecHead + 2 * HD;
+  const int par = (int)(a.seq & 1ull);
+  for (int k = 0; k < a.world; ++k) {  // NVLink P2P stores (local for k == rank)
+    double* dst = a.peer_recv[k] + ((size_t)par * a.world + a.rank) * reclen;
+    for (int i = threadIdx.x; i < reclen; i += blockDim.x) dst[i] = rec[i];
+  }
+  __threadfence_system();
+  __syncthreads();
+  if ((int)threadIdx.x < a.world) {
+    unsigned long long* f = a.peer_flags[threadIdx.x] + a.rank;
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(f), "l"(a.seq) : "memory");
+    const unsigned long long* mine = a.my_flags + threadIdx.x;
+    unsigned long long v = 0;
+#ifdef MPPI_WATCHDOG
+    long long spins = 0;
+#endif
+    do {
+      asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(mine) : "memory");
+#ifdef MPPI_WATCHDOG
+      if (++spins > (1ll << 26)) __trap();
+#endif
+    } while (v < a.seq);
+  }
+  __syncthreads();
+  double* comb = scratch;
+  double* emp = comb + reclen;
+  double* red = emp + HD;
+  double* scale = red + 32;
+  combine_records(a.my_recv + (size_t)par * a.world * reclen, a.world, reclen, HD, a.beta, comb, scale, red);
+  finalize_policy(a, 0, comb, emp);
+}
+
 template <typename R, int D>
 __global__ void __launch_bounds__(kStatsThreads) stats_kernel(const __grid_constant__ StatsArgs<R> a) {
   extern __shared__ __align__(16) double sm[];
@@ -898,11 +949,17 @@ __global__ void __launch_bounds__(kStatsThreads) stats_kernel(const __grid_const
   MPPI_STAMP(4);
   __threadfence();
   if (threadIdx.x == 0) a.counters[b] = 0u;
-  double* comb = a.finalize_inline ? (sm + 2 * a.ppb + 32 + max(a.nblk, 8) * (1 + kRecHead))
-                                   : a.out_record + (size_t)b * reclen;
+  const bool peer = a.peer_recv != nullptr;
+  double* comb = (a.finalize_inline || peer) ? (sm + 2 * a.ppb + 32 + max(a.nblk, 8) * (1 + kRecHead))
+                                             : a.out_record + (size_t)b * reclen;
   combine_records(a.records + (size_t)b * a.nblk * reclen, a.nblk, reclen, HD, a.beta, comb, scale,
                   red);
   MPPI_STAMP(5);
+  if (peer) {  // the rank record goes to every rank over peer memory; the update happens here
+    __syncthreads();
+    exchange_and_finalize(a, comb, HD, comb + reclen + HD);
+    return;
+  }
   if (!a.finalize_inline) return;
   double* emp = comb + reclen;
   finalize_policy(a, b, comb, emp);
@@ -1150,7 +1207,9 @@ __global__ void MPPI_STATS_BOUNDS stats_cluster_kernel(const __grid_constant__ S
       S2 += parts[((size_t)k * HD + o) * 2 + 1];
     }
   if (!a.finalize_inline) {  // rank record for the particle-sharded exchange
-    double* out = a.out_record + (size_t)b * (kRecHead + 2 * HD);
+    const bool peer = a.peer_recv != nullptr;
+    double* out = peer ? parts : a.out_record + (size_t)b * (kRecHead + 2 * HD);
+    if (peer) __syncthreads();  // every thread has read its partial sums out of `parts`
     if (owner) {
       out[kRecHead + o] = S1;
       out[kRecHead + HD + o] = S2;
@@ -1162,6 +1221,10 @@ __global__ void MPPI_STATS_BOUNDS stats_cluster_kernel(const __grid_constant__ S
       out[3] = sumf;
       out[4] = (double)status0;
       out[5] = (double)a.bad[b];
+    }
+    if (peer) {
+      __syncthreads();
+      exchange_and_finalize(a, parts, HD, parts + kRecHead + 2 * HD);
     }
     return;
   }

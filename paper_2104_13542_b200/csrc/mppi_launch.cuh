@@ -23,7 +23,8 @@ size_t fused_cap_bytes_f32(const RolloutArgs<float>& a);
 
 inline size_t stats_smem_bytes(int ppb, int nblk, int HD) {
   return sizeof(double) * (2 * (size_t)ppb + 32 + (size_t)(nblk > 8 ? nblk : 8) * (1 + kRecHead) +
-                           (kRecHead + 2 * HD) + HD) +
+                           (kRecHead + 2 * HD) + HD +
+                           (kRecHead + 2 * HD) + HD + 8 * (1 + kRecHead) + 32) +  // peer-exchange scratch
          sizeof(int) * ((size_t)ppb + 2);
 }
 

@@ -387,6 +387,39 @@ class Plan:
         N.check(self.lib.mppi_stats_dev(self.handle, N.dptr(th), N.dptr(thd), C.c_void_p(record_ptr),
                                         C.c_void_p(stream_ptr or None)))
 
+    # ---- exchange over peer memory (mppi_step_exchange)
+    def peer_buffers(self, world: int) -> tuple[int, int]:
+        """(receive buffer, flags) device pointers of this rank for `world` ranks."""
+        r, f = C.c_void_p(), C.c_void_p()
+        N.check(self.lib.mppi_peer_buffers(self.handle, int(world), C.byref(r), C.byref(f)))
+        return int(r.value), int(f.value)
+
+    def set_peers(self, rank: int, recv_ptrs, flag_ptrs):
+        world = len(recv_ptrs)
+        rv = (C.c_void_p * world)(*[C.c_void_p(int(x)) for x in recv_ptrs])
+        fv = (C.c_void_p * world)(*[C.c_void_p(int(x)) for x in flag_ptrs])
+        N.check(self.lib.mppi_set_peers(self.handle, world, int(rank), rv, fv))
+
+    def step_exchange(self, theta, theta_dot):
+        cmd = np.empty(self.dof)
+        info = N.StepInfo()
+        N.check(self.lib.mppi_step_exchange(self.handle, N.dptr(N.f64(theta, (self.dof,))),
+                                            N.dptr(N.f64(theta_dot, (self.dof,))), N.dptr(cmd), C.byref(info)))
+        return cmd, info
+
+    def ipc_handle(self, ptr: int) -> bytes:
+        buf = C.create_string_buffer(64)
+        N.check(self.lib.mppi_ipc_get_handle(C.c_void_p(int(ptr)), buf))
+        return buf.raw
+
+    def ipc_open(self, handle: bytes) -> int:
+        out = C.c_void_p()
+        N.check(self.lib.mppi_ipc_open_handle(bytes(handle), C.byref(out)))
+        return int(out.value)
+
+    def ipc_close(self, ptr: int):
+        N.check(self.lib.mppi_ipc_close(C.c_void_p(int(ptr))))
+
     def finalize_dev(self, records_ptr: int, n_records: int, stream_ptr: int = 0):
         cmd = np.empty(self.dof)
         info = N.StepInfo()

@@ -7,8 +7,10 @@ and mean rows live on rank 0) and the full, replicated policy. One iteration is
   rank-local: rollout + costs + MLP + weights relative to the LOCAL best cost
               -> record = [m_k, S0_k, count_k, sumfinite_k, status, bad,
                            S1_k (H*d), S2_k (H*d)]         (mppi_stats_dev)
-  exchange:   ONE all-gather of G records (426 doubles each for arm7 H=30:
-              3.4 KB per rank) over NCCL / NVLink
+  exchange:   every rank's record to every rank (426 doubles each for arm7
+              H=30: 3.4 KB per rank): fused into the statistics kernel as
+              NVLink P2P stores + a release flag (PeerExchange), or ONE NCCL
+              all-gather between two kernels (RecordExchange)
   replicated: fixed-order combine, rescaling record k by exp(-(m_k - m)/beta),
               then the mean/covariance update, shift and command on every
               rank identically (mppi_finalize_dev)
@@ -51,6 +53,56 @@ class RecordExchange:
         out = torch.empty(self.world * record.numel(), dtype=record.dtype, device=record.device)
         self.dist.all_gather_into_tensor(out, record.contiguous(), group=self.group)
         return out
+
+
+class PeerExchange:
+    """The exchange fused into the statistics kernel over NVLink peer memory
+    (mppi_step_exchange): every rank's kernel pushes its record straight into
+    slot [rank] of every rank's receive buffer and publishes it with a flag;
+    no NCCL call, no separate finalize launch. This object only wires the
+    buffers: it exports CUDA IPC handles of this rank's receive buffer and
+    flags, gathers every rank's handles with one host-side collective (any
+    torch.distributed backend) and hands the kernel a pointer table whose
+    slot k addresses rank k's buffers (slot [rank] = the plan's own).
+
+    `ops` defaults to the plan; tests pass a stand-in with the same four
+    methods (peer_buffers, ipc_handle, ipc_open, set_peers).
+    """
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+
+        self.dist = dist
+        self.group = group
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        self.opened: list[int] = []
+        self.tables = None
+
+    def attach(self, ops):
+        """Allocate, export, gather, open; returns (recv pointers, flag pointers) in rank order."""
+        recv, flags = ops.peer_buffers(self.world)
+        mine = (ops.ipc_handle(recv), ops.ipc_handle(flags))
+        gathered = [None] * self.world
+        self.dist.all_gather_object(gathered, mine, group=self.group)
+        recv_ptrs, flag_ptrs = [], []
+        for k, (hr, hf) in enumerate(gathered):
+            if k == self.rank:
+                recv_ptrs.append(recv)
+                flag_ptrs.append(flags)
+            else:
+                pr, pf = ops.ipc_open(hr), ops.ipc_open(hf)
+                self.opened += [pr, pf]
+                recv_ptrs.append(pr)
+                flag_ptrs.append(pf)
+        ops.set_peers(self.rank, recv_ptrs, flag_ptrs)
+        self.tables = (recv_ptrs, flag_ptrs)
+        return self.tables
+
+    def close(self, ops):
+        for ptr in self.opened:
+            ops.ipc_close(ptr)
+        self.opened = []
 
 
 class ShardedController:
@@ -111,8 +163,14 @@ class ShardedController:
         self.plan.set_goal(g.target_pose.rotation, g.target_pose.translation, g.mode_code, 0)
         self.dev = torch.device("cuda", device)
         self.record = torch.empty(self.plan.record_len(), dtype=torch.float64, device=self.dev)
+        if isinstance(exchange, PeerExchange):
+            torch.cuda.set_device(device)
+            exchange.attach(self.plan)
 
     def control_step(self, state):
+        if isinstance(self.exchange, PeerExchange):  # exchange fused into the statistics kernel
+            cmd, info = self.plan.step_exchange(state.theta, state.theta_dot)
+            return cmd, info
         torch = self.torch
         stream = torch.cuda.current_stream(self.dev).cuda_stream
         cmd = info = None

@@ -127,3 +127,51 @@ def test_batched_statistics_layouts_match_oracle(B):
         ref = oracles[b].step(th0[b], np.zeros(7))
         np.testing.assert_allclose(cmds[b], ref, atol=1e-4, err_msg=f"instance {b}")
         np.testing.assert_allclose(bc.policy(b).means, oracles[b].means, atol=1e-4)
+
+
+def test_peer_exchange_step_matches_allgather_path():
+    """mppi_step_exchange (the record pushed over peer memory and the update
+    applied inside the statistics kernel) against mppi_stats_dev + all-gather
+    + mppi_finalize_dev on a one-rank world: identical commands and policies,
+    both within tolerance of the unsharded controller. (Ranks whose kernels
+    wait on one another need one GPU each; the multi-rank wiring is covered by
+    tests/test_sharding_gloo.py.)"""
+    import torch
+
+    from paper_2104_13542_b200 import configs
+    from paper_2104_13542_b200 import _native as N
+    from paper_2104_13542_b200.engine import Plan, PlanSpec
+    from paper_2104_13542_b200.kinematics import load_chain
+
+    total = 600  # > 512 particles: the multi-block statistics kernel with its record combine
+    for n, precision in ((total, N.FP64), (300, N.FP32)):
+        ref = configs.make_controller(1, particles=n, precision="fp64" if precision == N.FP64 else "fp32")
+        chain = load_chain("arm7.chain")
+        goal = configs.make_goal(1)
+        plans = []
+        for _ in range(2):
+            spec = PlanSpec(horizon=30, particles=n, dts=ref.sched.dts, null_count=2, precision=precision,
+                            particle_offset=0, particles_total=n, gamma=0.99, beta=1.0, alpha_mu=0.9,
+                            alpha_sigma=0.5, sigma0_sq=0.5, sigma_sq_min=0.01, sigma_sq_max=0.5, knots=5)
+            p = Plan(chain, configs.make_weights(1), spec)
+            p.init_noise()
+            p.set_goal(goal.target_pose.rotation, goal.target_pose.translation, goal.mode_code, 0)
+            plans.append(p)
+        peer, gather = plans
+        recv, flags = peer.peer_buffers(1)
+        peer.set_peers(0, [recv], [flags])
+        rec = torch.zeros(gather.record_len(), dtype=torch.float64, device="cuda:0")
+        st = configs.start_state()
+        for step in range(4):
+            st.theta[:] = configs.start_state().theta + 0.01 * step
+            cmd_ref, _ = ref.control_step(st)
+            cmd_p, info_p = peer.step_exchange(st.theta, st.theta_dot)
+            gather.stats_dev(st.theta, st.theta_dot, rec.data_ptr())
+            torch.cuda.synchronize()
+            cmd_g, info_g = gather.finalize_dev(rec.data_ptr(), 1)
+            assert info_p.status == 0 and info_g.status == 0
+            np.testing.assert_array_equal(cmd_p, cmd_g)
+            np.testing.assert_array_equal(peer.get_policy(0)[0], gather.get_policy(0)[0])
+            np.testing.assert_array_equal(peer.get_policy(0)[1], gather.get_policy(0)[1])
+            assert info_p.best_cost == info_g.best_cost
+            np.testing.assert_allclose(cmd_p, cmd_ref, atol=1e-9 if precision == N.FP64 else 1e-3)

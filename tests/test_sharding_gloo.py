@@ -108,3 +108,71 @@ def test_shard_arithmetic():
                 off, cnt = particle_shard(total, world, r)
                 assert (off, off + cnt) == (a, b)
             assert seen == list(range(total))
+
+
+class _FakePeerOps:
+    """Stand-in for the plan's IPC surface: rank r's buffers are the integers
+    r*100 + {1, 2}; a handle is the pointer's text; opening maps it into this
+    process as 10**6 + pointer."""
+
+    def __init__(self, rank):
+        self.rank = rank
+        self.calls = []
+
+    def peer_buffers(self, world):
+        self.calls.append(("peer_buffers", world))
+        return self.rank * 100 + 1, self.rank * 100 + 2
+
+    def ipc_handle(self, ptr):
+        return str(ptr).encode().ljust(64, b"\0")
+
+    def ipc_open(self, handle):
+        return 10 ** 6 + int(handle.rstrip(b"\0"))
+
+    def ipc_close(self, ptr):
+        self.calls.append(("close", ptr))
+
+    def set_peers(self, rank, recv, flags):
+        self.calls.append(("set_peers", rank, list(recv), list(flags)))
+
+
+def _peer_worker(rank, world, port, out_q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        sys.path.insert(0, str(ROOT))
+        from paper_2104_13542_b200.sharded import PeerExchange
+
+        ops = _FakePeerOps(rank)
+        ex = PeerExchange()
+        tables = ex.attach(ops)
+        ex.close(ops)
+        out_q.put((rank, tables, ops.calls))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_peer_exchange_tables(world):
+    """PeerExchange wiring over gloo: slot k of every rank's table addresses
+    rank k's buffers — its own raw pointers in slot [rank], the opened IPC
+    mappings elsewhere — and every opened mapping is closed again."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_peer_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    results = sorted([q.get(timeout=300) for _ in range(world)], key=lambda r: r[0])
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank, (recv, flags), calls in results:
+        assert calls[0] == ("peer_buffers", world)
+        for k in range(world):
+            base = 0 if k == rank else 10 ** 6
+            assert recv[k] == base + k * 100 + 1 and flags[k] == base + k * 100 + 2
+        sp = [c for c in calls if c[0] == "set_peers"]
+        assert sp == [("set_peers", rank, recv, flags)]
+        closed = sorted(c[1] for c in calls if c[0] == "close")
+        assert closed == sorted(x for k in range(world) if k != rank for x in (recv[k], flags[k]))
