@@ -123,7 +123,8 @@ class BatchedController:
         if not (np.isfinite(theta).all() and np.isfinite(theta_dot).all()):
             raise ContractError("joint state is not finite")
         cmds, infos = self.plan.step(theta, theta_dot)
-        status = np.array([i.status for i in infos], dtype=np.int32)
+        cols = self.plan.info_columns  # (B,) record view of infos
+        status = cols["status"].astype(np.int32)
         fallback = [""] * self.B
         bad = np.flatnonzero(status != N.OK)
         if bad.size:
@@ -144,7 +145,7 @@ class BatchedController:
         i0 = infos[0]
         diag = BatchDiagnostics(
             status=status, fallback=fallback,
-            best_cost=np.array([i.best_cost for i in infos]), mean_cost=np.array([i.mean_cost for i in infos]),
+            best_cost=cols["best_cost"].copy(), mean_cost=cols["mean_cost"].copy(),
             device_ms=float(i0.device_ms),
             stage_ms={"sample": i0.sample_ms, "rollout": i0.rollout_ms, "mlp": i0.mlp_ms,
                       "update": i0.update_ms})

@@ -261,8 +261,11 @@ class Controller:
         else:  # host rng, as next_command(policy, "sample", rng) (policy.py:174-176)
             pol = self.policy
             command = self.rng.normal(pol.means[0], pol.stddev()[0])
-        self._prev_command = command.copy()
-        self.filter.last_command = command.copy()
+        # one private copy shared by the fallback ladder and the filter (both
+        # only ever rebind it); the caller owns `command`
+        kept = command.copy()
+        self._prev_command = kept
+        self.filter.last_command = kept
         latency = (time.perf_counter() - t_start) * 1e3
         if latency > self.latency_budget * 1e3:
             log.debug("control step overran budget: %.2f ms", latency)

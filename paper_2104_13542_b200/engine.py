@@ -142,6 +142,9 @@ class Plan:
         proto = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p)
         self._step_raw = proto(C.cast(self.lib.mppi_step, C.c_void_p).value)
         self._a_cmd, self._a_info = self._cmd.ctypes.data, C.addressof(self._info)
+        # the same memory as a numpy record array: batched callers read whole
+        # columns (status, costs) without touching B ctypes structs
+        self.info_columns = np.ctypeslib.as_array(self._info)
         if provider is not None and self.kind == N.SELFCOLL_LEARNED:
             self.set_mlp(provider)
         if world is not None:
