@@ -1196,6 +1196,12 @@ int mppi_step(mppi_plan* p, const double* theta, const double* theta_dot, double
             hi[j] = std::max(hi[j], v);
           }
       const unsigned long long re = t[16 * p->nblk + 16 * 255 + 15], me = g[16 * 255 + 15];
+      const unsigned long long* ec = t.data() + 16 * p->nblk + 16 * 253;
+      if (ec[15] || ec[0] || ec[1]) {
+        fprintf(stderr, "world exact tests (cumulative) per capsule:");
+        for (int c = 0; c < 8; ++c) fprintf(stderr, " %llu", ec[c]);
+        fprintf(stderr, " | ternary searches %llu\n", ec[15]);
+      }
       fprintf(stderr, "rollout last warp end %.2f, mlp last CTA end %.2f\n",
               re ? (double)(long long)(re - t0) * 1e-3 : -1.0, me ? (double)(long long)(me - t0) * 1e-3 : -1.0);
       fprintf(stderr, "mlp min     :");

@@ -63,7 +63,7 @@ struct RolloutArgs {
 // Capsule endpoints live in shared memory, [cap][6][32 lanes].
 template <typename R>
 __device__ __forceinline__ bool env_any_hit(const WorldT<R>& w, const ChainT<R>& ch, const R* cap,
-                                            int lane) {
+                                            int lane, unsigned long long* dbg_counts = nullptr) {
   const int nc = ch.n_caps;
   for (int c = 0; c < nc; ++c) {
     R P0[3], P1[3];
@@ -90,22 +90,58 @@ __device__ __forceinline__ bool env_any_hit(const WorldT<R>& w, const ChainT<R>&
       const R len = sqrt(dx * dx + dy * dy + dz * dz);
       const int ns = 1 + (int)ceil(len / (R(0.5) * w.voxel));
       const R half = R(0.5) * len / R(ns > 1 ? ns - 1 : 1);
+      // sample s sits at grid coordinate g0 + s * gs (voxel units): one FMA
+      // per axis per sample instead of three divisions. Rounding moves a
+      // sample by ~1e-7 voxel; a point on a voxel face may take either
+      // neighbour, and both clearances bound it — the 1e-5 margin covers it.
+      const R iv = R(1) / w.voxel, is = ns > 1 ? R(1) / R(ns - 1) : R(0);
+      const R gx0 = (P0[0] - w.ox) * iv, gy0 = (P0[1] - w.oy) * iv, gz0 = (P0[2] - w.oz) * iv;
+      const R gsx = dx * iv * is, gsy = dy * iv * is, gsz = dz * iv * is;
+      // samples in batches of SB independent gathers
+      constexpr int SB = 8;
       R lb = R(1e30);
-      for (int s = 0; s < ns; ++s) {
-        const R t = ns > 1 ? R(s) / R(ns - 1) : R(0);
-        int ix = (int)floor((P0[0] + t * dx - w.ox) / w.voxel);
-        int iy = (int)floor((P0[1] + t * dy - w.oy) / w.voxel);
-        int iz = (int)floor((P0[2] + t * dz - w.oz) / w.voxel);
-        ix = ix < 0 ? 0 : (ix >= w.nx ? w.nx - 1 : ix);
-        iy = iy < 0 ? 0 : (iy >= w.ny ? w.ny - 1 : iy);
-        iz = iz < 0 ? 0 : (iz >= w.nz ? w.nz - 1 : iz);
-        const R f = R(__ldg(w.sdf + ((size_t)ix * w.ny + iy) * w.nz + iz));
-        lb = f < lb ? f : lb;
+      for (int s0 = 0; s0 < ns; s0 += SB) {
+        float f[SB];
+#pragma unroll
+        for (int u = 0; u < SB; ++u) {
+          const int s = s0 + u;
+          f[u] = 1e30f;
+          if (s < ns) {
+            int ix = (int)floor(gx0 + R(s) * gsx);
+            int iy = (int)floor(gy0 + R(s) * gsy);
+            int iz = (int)floor(gz0 + R(s) * gsz);
+            ix = ix < 0 ? 0 : (ix >= w.nx ? w.nx - 1 : ix);
+            iy = iy < 0 ? 0 : (iy >= w.ny ? w.ny - 1 : iy);
+            iz = iz < 0 ? 0 : (iz >= w.nz ? w.nz - 1 : iz);
+            f[u] = __ldg(w.sdf + (ix * w.ny + iy) * w.nz + iz);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < SB; ++u) lb = R(f[u]) < lb ? R(f[u]) : lb;
       }
       if (lb - half >= rc + R(1e-5)) continue;
     }
+#ifdef MPPI_DEBUG_TIMERS
+    if (dbg_counts) atomicAdd(dbg_counts + c, 1ull);  // (configuration, capsule) pairs reaching the exact test
+#endif
+    // Exact narrow phase (60 ternary steps per box), skipped for boxes whose
+    // gap to the segment's bounding box already exceeds the radius: every
+    // point the ternary search evaluates lies in that bounding box, so its
+    // distance cannot fall below the gap (margin as in the broad phase).
+    const R rlim = rc + R(1e-5);
     for (int ob = 0; ob < w.nb; ++ob) {
       const R* bx = w.boxes + 6 * ob;
+      R g2 = R(0);
+#pragma unroll
+      for (int i = 0; i < 3; ++i) {
+        const R smin = P0[i] < P1[i] ? P0[i] : P1[i], smax = P0[i] < P1[i] ? P1[i] : P0[i];
+        const R gi = fmax(bx[i] - smax, R(0)) + fmax(smin - bx[3 + i], R(0));
+        g2 += gi * gi;
+      }
+      if (g2 >= rlim * rlim) continue;
+#ifdef MPPI_DEBUG_TIMERS
+      if (dbg_counts) atomicAdd(dbg_counts + 15, 1ull);  // ternary searches run
+#endif
       if (seg_box_dist(P0, P1, bx, bx + 3) < rc) return true;
     }
   }
@@ -402,7 +438,11 @@ __device__ __forceinline__ bool rollout_particle(const RolloutArgs<R>& a, long l
   }
   // world collision, binary (jit.py:289-332, costs.py:235-240)
   R envc = R(0);
+#ifdef MPPI_DEBUG_TIMERS
+  if (cs.use_env) envc = env_any_hit(a.world, ch, cap, lane, a.dbg ? a.dbg + 16 * 253 : nullptr) ? R(1) : R(0);
+#else
   if (cs.use_env) envc = env_any_hit(a.world, ch, cap, lane) ? R(1) : R(0);
+#endif
 
   MPPI_TSTAMP(pdbg, 4);  // cost terms
   // total_cost (costs.py:176-187) minus the learned self-collision term
