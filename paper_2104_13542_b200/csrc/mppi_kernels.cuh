@@ -65,6 +65,41 @@ template <typename R>
 __device__ __forceinline__ bool env_any_hit(const WorldT<R>& w, const ChainT<R>& ch, const R* cap,
                                             int lane, unsigned long long* dbg_counts = nullptr) {
   const int nc = ch.n_caps;
+  // Capsule-level screen, one gather per capsule, all in flight together:
+  // every point of a segment lies within len/2 of its midpoint, and the
+  // midpoint's voxel clearance bounds the midpoint's distance to the boxes
+  // (see the sampled broad phase below), so clearance - len/2 >= r + margin
+  // clears the capsule of every box without sampling it.
+  unsigned clear = 0;
+  if (w.sdf != nullptr && w.nb > 0) {
+    const R iv = R(1) / w.voxel;
+    float f[MAXC];
+    R hl[MAXC];
+#pragma unroll
+    for (int c = 0; c < MAXC; ++c) {
+      f[c] = 0.f;
+      hl[c] = R(0);
+      if (c < nc) {
+        R m[3], d2 = R(0);
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+          const R a0 = cap[(c * 6 + i) * 32 + lane], a1 = cap[(c * 6 + 3 + i) * 32 + lane];
+          m[i] = R(0.5) * (a0 + a1);
+          d2 += (a1 - a0) * (a1 - a0);
+        }
+        hl[c] = R(0.5) * sqrt(d2);
+        int ix = (int)floor((m[0] - w.ox) * iv), iy = (int)floor((m[1] - w.oy) * iv),
+            iz = (int)floor((m[2] - w.oz) * iv);
+        ix = ix < 0 ? 0 : (ix >= w.nx ? w.nx - 1 : ix);
+        iy = iy < 0 ? 0 : (iy >= w.ny ? w.ny - 1 : iy);
+        iz = iz < 0 ? 0 : (iz >= w.nz ? w.nz - 1 : iz);
+        f[c] = __ldg(w.sdf + (ix * w.ny + iy) * w.nz + iz);
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < MAXC; ++c)
+      if (c < nc && R(f[c]) - hl[c] >= ch.cap_r[c] + R(1e-5)) clear |= 1u << c;
+  }
   for (int c = 0; c < nc; ++c) {
     R P0[3], P1[3];
 #pragma unroll
@@ -75,7 +110,7 @@ __device__ __forceinline__ bool env_any_hit(const WorldT<R>& w, const ChainT<R>&
     const R rc = ch.cap_r[c];
     for (int o = 0; o < w.ns; ++o)
       if (capsule_hits_sphere(P0, P1, rc, w.spheres + 4 * o)) return true;
-    if (w.nb == 0) continue;
+    if (w.nb == 0 || ((clear >> c) & 1u)) continue;
     if (w.sdf != nullptr) {
       // Conservative voxel broad phase. w.sdf holds, per voxel, the exact
       // distance from the voxel CUBE to the obstacle set (the union of the
