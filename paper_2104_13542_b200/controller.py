@@ -68,7 +68,7 @@ def filter_state(raw: JointState, filt: FilterState, dt: float) -> JointState:
     return est
 
 
-@dataclass
+@dataclass(slots=True)  # built once per control step: slots make that ~2x cheaper
 class StepDiagnostics:
     latency_ms: float
     sample_ms: float
@@ -272,10 +272,9 @@ class Controller:
         bundle = LazyBundle(self, self._step_serial) if self.keep_bundle else None
         # without profile_stages() the whole fused step is reported as rollout time
         roll = info.rollout_ms + info.mlp_ms
-        return command, StepDiagnostics(latency_ms=latency, sample_ms=info.sample_ms,
-                                        rollout_ms=roll if roll > 0.0 else latency,
-                                        update_ms=info.update_ms, best_cost=info.best_cost,
-                                        mean_cost=info.mean_cost, bundle=bundle)
+        # positional: latency, sample, rollout, update, best, mean, fallback, bundle
+        return command, StepDiagnostics(latency, info.sample_ms, roll if roll > 0.0 else latency, info.update_ms,
+                                        info.best_cost, info.mean_cost, "", bundle)
 
     def top_rollouts(self, k: int):
         """The k best rollouts of the last step for telemetry (bridge.py:196-203):

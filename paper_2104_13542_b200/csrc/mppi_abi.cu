@@ -10,6 +10,7 @@
 #include <cstdlib>
 #include <cmath>
 #include <cstdio>
+#include <chrono>
 #include <cstring>
 #include <string>
 #include <type_traits>
@@ -1151,14 +1152,38 @@ int mppi_step(mppi_plan* p, const double* theta, const double* theta_dot, double
   // extra runtime call is host time between the state and the command
   const bool prof = p->profile_level >= 2;
   if (prof) CKR(ensure_graph(p, true));
+#ifdef MPPI_DEBUG_TIMERS
+  using clk = std::chrono::steady_clock;
+  const auto h0 = clk::now();
+#endif
   for (auto& n : prof ? p->inl_prof : p->inl) {
     memcpy(n.args.data() + n.st_off, p->h_state, sizeof(double) * 2 * D);
     CK(cudaGraphExecKernelNodeSetParams(prof ? p->graph_prof : p->graph, n.node, &n.kp));
   }
+#ifdef MPPI_DEBUG_TIMERS
+  const auto h1 = clk::now();
+#endif
   if (p->profile_level) CK(cudaEventRecord(p->ev0, p->stream));
   CK(cudaGraphLaunch(prof ? p->graph_prof : p->graph, p->stream));
   if (p->profile_level) CK(cudaEventRecord(p->ev1, p->stream));
+#ifdef MPPI_DEBUG_TIMERS
+  const auto h2 = clk::now();
+#endif
   CK(cudaStreamSynchronize(p->stream));
+#ifdef MPPI_DEBUG_TIMERS
+  if (getenv("MPPI_HOST_TIMING")) {  // host-side split of one step: set params | launch | wait
+    static double acc[3] = {0, 0, 0};
+    static long cnt = 0;
+    const auto h3 = clk::now();
+    acc[0] += std::chrono::duration<double, std::micro>(h1 - h0).count();
+    acc[1] += std::chrono::duration<double, std::micro>(h2 - h1).count();
+    acc[2] += std::chrono::duration<double, std::micro>(h3 - h2).count();
+    if (++cnt % 1000 == 0) {
+      fprintf(stderr, "host us/step: set params %.2f  graph launch %.2f  wait %.2f\n", acc[0] / cnt, acc[1] / cnt,
+              acc[2] / cnt);
+    }
+  }
+#endif
   float ms = 0.f;
   if (p->profile_level) CK(cudaEventElapsedTime(&ms, p->ev0, p->ev1));
   memcpy(command_out, p->h_cmd, sizeof(double) * B * D);
