@@ -342,10 +342,6 @@ void choose_blocks(int N, int B, int& ppb, int& nblk) {
   }
   ppb = 32;
   if (N > 16 * 32 && N <= 16 * 64) ppb = (N + 15) / 16;
-  if (const char* env = getenv("MPPI_STATS_PPB")) {  // A/B experiments on the cluster size
-    const int v = atoi(env);
-    if (v >= (N + 15) / 16 && v <= 64) ppb = v;
-  }
   nblk = (N + ppb - 1) / ppb;
   if (nblk > 296) {
     nblk = 296;
