@@ -343,8 +343,8 @@ void choose_blocks(int N, int B, int& ppb, int& nblk) {
   ppb = 32;
   if (N > 16 * 32 && N <= 16 * 64) ppb = (N + 15) / 16;
   nblk = (N + ppb - 1) / ppb;
-  if (nblk > 296) {
-    nblk = 296;
+  if (nblk > kStatsMaxBlocks) {
+    nblk = kStatsMaxBlocks;
     ppb = (N + nblk - 1) / nblk;
     nblk = (N + ppb - 1) / ppb;
   }
@@ -786,11 +786,11 @@ int mppi_plan_create(const mppi_chain_desc* chain, const mppi_cost_desc* costs,
     CKR(p->state.alloc((size_t)B * 2 * D + 1));  // + step counter slot
     CKR(p->stepbuf.alloc((size_t)B * N * H * rsz));
     CKR(p->totals.alloc((size_t)B * N));
-    CKR(p->records.alloc((size_t)B * p->nblk * reclen));
+    CKR(p->records.alloc((size_t)B * stats_rec_stride(p->nblk) * reclen));
     CKR(p->out_record.alloc(reclen));
     CKR(p->cmd.alloc((size_t)B * D));
-    CKR(p->counters.alloc(B));
-    CK(cudaMemset(p->counters.p, 0, sizeof(unsigned) * B));
+    CKR(p->counters.alloc((size_t)B * kStatsCounterStride));
+    CK(cudaMemset(p->counters.p, 0, sizeof(unsigned) * B * kStatsCounterStride));
     CKR(p->status.alloc(B));
     CKR(p->bad.alloc(B));
     CK(cudaMemset(p->status.p, 0, sizeof(int) * B));

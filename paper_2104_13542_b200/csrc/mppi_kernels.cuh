@@ -24,6 +24,19 @@ namespace mppi {
 constexpr int kRolloutWarps = 4;  // 128-thread blocks, one warp per particle
 constexpr int kStatsThreads = 256;
 constexpr int kRecHead = 6;       // m, S0, count, sum_finite, status, first bad row
+// Statistics blocks of one instance combine their records in two levels when
+// there are more than kStatsGroup of them: the last block of each group of
+// kStatsGroup combines the group's records, the last group the group
+// records (a single block combining ~300 records took 14-31 us). Records per
+// instance: nblk block records + one per group; counters per instance: one
+// for the instance + one per group.
+constexpr int kStatsGroup = 16;
+constexpr int kStatsMaxBlocks = 296;
+constexpr int kStatsCounterStride = 1 + (kStatsMaxBlocks + kStatsGroup - 1) / kStatsGroup;
+__host__ __device__ inline int stats_groups(int nblk) {
+  return nblk > kStatsGroup ? (nblk + kStatsGroup - 1) / kStatsGroup : 0;
+}
+__host__ __device__ inline int stats_rec_stride(int nblk) { return nblk + stats_groups(nblk); }
 
 template <typename R>
 struct RolloutArgs {
@@ -941,7 +954,8 @@ __global__ void __launch_bounds__(kStatsThreads) stats_kernel(const __grid_const
   // Particles whose weight underflowed to exactly 0 contribute nothing; warp 0
   // compacts the others (ascending, so the summation order is fixed) and every
   // output then runs a branch-free loop with PD independent eps loads in flight.
-  double* rec = a.records + ((size_t)b * a.nblk + blk) * reclen;
+  const int rstride = stats_rec_stride(a.nblk);
+  double* rec = a.records + ((size_t)b * rstride + blk) * reclen;
   int* nz = reinterpret_cast<int*>(sm + 2 * a.ppb + 32 + max(a.nblk, 8) * (1 + kRecHead) + reclen + HD);
   __shared__ int s_nnz;
   if (wid == 0) {
@@ -1013,22 +1027,37 @@ __global__ void __launch_bounds__(kStatsThreads) stats_kernel(const __grid_const
   // ---- last block of this instance combines + finalizes --------------------
   __shared__ bool s_last;
   MPPI_STAMP(3);
+  unsigned* ctr = a.counters + (size_t)b * kStatsCounterStride;
+  const int ngroups = stats_groups(a.nblk);
+  const double* level = a.records + (size_t)b * rstride * reclen;  // records the final combine reads
+  int nlevel = a.nblk;
+  if (ngroups > 0) {  // first level: the last block of this group combines the group
+    const int grp = blk / kStatsGroup, g0 = grp * kStatsGroup, gs = min(kStatsGroup, a.nblk - g0);
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) s_last = atomicAdd(&ctr[1 + grp], 1u) == (unsigned)(gs - 1);
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    if (threadIdx.x == 0) ctr[1 + grp] = 0u;
+    double* grec = a.records + ((size_t)b * rstride + a.nblk + grp) * reclen;
+    combine_records(a.records + ((size_t)b * rstride + g0) * reclen, gs, reclen, HD, a.beta, grec, scale, red);
+    level = a.records + ((size_t)b * rstride + a.nblk) * reclen;
+    nlevel = ngroups;
+  }
   __threadfence();
   __syncthreads();
-  if (threadIdx.x == 0) {
-    const unsigned prev = atomicAdd(&a.counters[b], 1u);
-    s_last = (prev == (unsigned)(a.nblk - 1));
-  }
+  if (threadIdx.x == 0) s_last = atomicAdd(&ctr[0], 1u) == (unsigned)((ngroups > 0 ? ngroups : a.nblk) - 1);
   __syncthreads();
   if (!s_last) return;
   MPPI_STAMP(4);
   __threadfence();
-  if (threadIdx.x == 0) a.counters[b] = 0u;
+  if (threadIdx.x == 0) ctr[0] = 0u;
+  MPPI_STAMP(7);
   const bool peer = a.peer_recv != nullptr;
   double* comb = (a.finalize_inline || peer) ? (sm + 2 * a.ppb + 32 + max(a.nblk, 8) * (1 + kRecHead))
                                              : a.out_record + (size_t)b * reclen;
-  combine_records(a.records + (size_t)b * a.nblk * reclen, a.nblk, reclen, HD, a.beta, comb, scale,
-                  red);
+  combine_records(level, nlevel, reclen, HD, a.beta, comb, scale, red);
   MPPI_STAMP(5);
   if (peer) {  // the rank record goes to every rank over peer memory; the update happens here
     __syncthreads();
