@@ -74,8 +74,13 @@ struct RolloutArgs {
 
 // Any capsule of this lane's configuration penetrates the world (costs.py:235-240).
 // Capsule endpoints live in shared memory, [cap][6][32 lanes].
+#ifdef MPPI_ENV_INLINE
+#define MPPI_ENV_LINKAGE __forceinline__
+#else  // out of line: config 1/2 rollouts never fetch the world code
+#define MPPI_ENV_LINKAGE __noinline__
+#endif
 template <typename R>
-__device__ __forceinline__ bool env_any_hit(const WorldT<R>& w, const ChainT<R>& ch, const R* cap,
+__device__ MPPI_ENV_LINKAGE bool env_any_hit(const WorldT<R>& w, const ChainT<R>& ch, const R* cap,
                                             int lane, unsigned long long* dbg_counts = nullptr) {
   const int nc = ch.n_caps;
   // Capsule-level screen, one gather per capsule, all in flight together:
