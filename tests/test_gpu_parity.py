@@ -323,6 +323,29 @@ def test_pseudorandom_injected_noise_vs_oracle(arm7, rng):
         np.testing.assert_allclose(cmd, ocmd, atol=1e-7)
 
 
+@pytest.mark.parametrize("particles", [1500, 9000])
+def test_many_statistics_blocks_vs_oracle(arm7, rng, particles):
+    """More than 1024 particles leave the one-cluster statistics kernel: 32
+    particles per block with a record combine, in two levels once there are
+    more than 16 blocks (47 and 282 blocks here: 3 and 18 groups)."""
+    from paper_2104_13542_b200 import configs
+
+    c = configs.make_controller(1, particles=particles, precision="fp64")
+    eps = rng.standard_normal((particles, 30, 7))
+    c.set_perturbations(eps)
+    kw = dict(configs.CONTROLLER_KW)
+    kw.pop("seed")
+    kw["particles"] = particles
+    oc = O.OracleController(arm7, configs.make_weights(1), configs.reach_goal_rotation(), configs.REACH_GOAL_POS,
+                            True, eps_source=lambda: eps, **kw)
+    st = configs.start_state()
+    for _ in range(2):
+        cmd, diag = c.control_step(st)
+        ocmd = oc.step(st.theta, st.theta_dot)
+        np.testing.assert_allclose(cmd, ocmd, atol=1e-7)
+        np.testing.assert_allclose(c.policy.variances, oc.variances, atol=1e-7)
+
+
 def test_pseudorandom_generator_runs_and_is_seeded():
     from paper_2104_13542_b200 import configs
 
