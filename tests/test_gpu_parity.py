@@ -558,3 +558,22 @@ def test_top_rollouts_match_bundle_argsort(arm7):
     _, trans = fk_batch(arm7, b.positions[order].reshape(-1, 7))
     np.testing.assert_allclose(ee, trans[:, -1].reshape(8, 30, 3), atol=1e-12)
 
+
+
+def test_state_parameter_reaches_both_step_graphs():
+    """The joint state travels as a rollout kernel parameter of the captured
+    step graph; the instrumented copy (profile_stages(2)) is a second graph
+    with its own nodes. Alternating between them over a moving state must give
+    the commands of a controller that only ever used the lean graph."""
+    from paper_2104_13542_b200 import configs
+
+    a = configs.make_controller(2, particles=256)
+    b = configs.make_controller(2, particles=256)
+    st = configs.start_state()
+    for i in range(6):
+        st.theta = configs.start_state().theta + 0.02 * i
+        st.theta_dot = np.full(7, 0.01 * i)
+        a.profile_stages(2 if i % 2 else 0)
+        ca, _ = a.control_step(st)
+        cb, _ = b.control_step(st)
+        np.testing.assert_array_equal(ca, cb)
