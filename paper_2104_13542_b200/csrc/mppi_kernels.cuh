@@ -213,7 +213,11 @@ __host__ __device__ __forceinline__ bool rollout_needs_caps(const CostT<R>& cs) 
 // warp's [cap][6][32] staging area; `enc` (16 floats, may be NULL) receives the
 // lane's positional encoding [sin q, cos q, 0...] (surrogate.py:24-28).
 // Returns false when the instance already failed (nothing written).
-template <typename R, int D>
+// LEAN: the control-step specialisation — sampled controls (mode 0), no
+// capsule staging, no capsule self-collision oracle, no world — so the
+// kernel's code holds only what a config-1/2 step executes (the latency
+// build fetches its instructions cold after an L2 flush).
+template <typename R, int D, bool LEAN = false>
 __device__ __forceinline__ bool rollout_particle(const RolloutArgs<R>& a, long long g, int lane, R* cap,
                                                  float* enc) {
   const int b = (int)(g / a.N);
@@ -246,7 +250,7 @@ __device__ __forceinline__ bool rollout_particle(const RolloutArgs<R>& a, long l
   // ---- controls -> positions / velocities --------------------------------
   R p[D], v[D], u[D];
   const size_t row = ((size_t)n * H + h) * D;
-  if (a.mode == 2) {
+  if (!LEAN && a.mode == 2) {
 #pragma unroll
     for (int j = 0; j < D; ++j) {
       p[j] = (R)a.in0[row + j];
@@ -257,7 +261,7 @@ __device__ __forceinline__ bool rollout_particle(const RolloutArgs<R>& a, long l
   } else {
     bool bad = false, varbad = false;
     const int ng = n + a.particle_offset;
-    if (a.mode == 0) {
+    if (LEAN || a.mode == 0) {
       const int hs = a.shift ? h + 1 : h;
       const double* mu = a.means + (size_t)b * H * D;
       const double* sdv = a.sd + (size_t)b * H * D;
@@ -312,7 +316,7 @@ __device__ __forceinline__ bool rollout_particle(const RolloutArgs<R>& a, long l
   R tw[3] = {R(0), R(0), R(0)};
   R ja[D][3], jp[D][3];  // Jacobian column data: world axis, joint origin
   R sq[D], cq[D];
-  const int nc = rollout_needs_caps(cs) ? ch.n_caps : 0;
+  const int nc = (!LEAN && rollout_needs_caps(cs)) ? ch.n_caps : 0;
 #pragma unroll
   for (int j = 0; j < 3; ++j) {
     ja[0][j] = ch.axes[0][j];
@@ -472,7 +476,7 @@ __device__ __forceinline__ bool rollout_particle(const RolloutArgs<R>& a, long l
   }
   // capsule self collision oracle (jit.py:241-260, costs.py:234)
   R selfc = R(0);
-  if (cs.selfcoll == MPPI_SELFCOLL_ORACLE) {
+  if (!LEAN && cs.selfcoll == MPPI_SELFCOLL_ORACLE) {
     R best = R(NO_CONTACT);
     for (int pi = 0; pi < ch.n_pairs; ++pi) {
       const int i = ch.pair_a[pi], j = ch.pair_b[pi];
@@ -492,9 +496,10 @@ __device__ __forceinline__ bool rollout_particle(const RolloutArgs<R>& a, long l
   // world collision, binary (jit.py:289-332, costs.py:235-240)
   R envc = R(0);
 #ifdef MPPI_DEBUG_TIMERS
-  if (cs.use_env) envc = env_any_hit(a.world, ch, cap, lane, a.dbg ? a.dbg + 16 * 253 : nullptr) ? R(1) : R(0);
+  if (!LEAN && cs.use_env)
+    envc = env_any_hit(a.world, ch, cap, lane, a.dbg ? a.dbg + 16 * 253 : nullptr) ? R(1) : R(0);
 #else
-  if (cs.use_env) envc = env_any_hit(a.world, ch, cap, lane) ? R(1) : R(0);
+  if (!LEAN && cs.use_env) envc = env_any_hit(a.world, ch, cap, lane) ? R(1) : R(0);
 #endif
 
   MPPI_TSTAMP(pdbg, 4);  // cost terms
@@ -550,7 +555,7 @@ __device__ __forceinline__ bool rollout_particle(const RolloutArgs<R>& a, long l
 // most one wave); MINB = 6: the throughput build for many waves (80
 // registers, a few spills, 6 CTAs per SM to hide the FK dependency chains;
 // config 4 rollout -6%).
-template <typename R, int D, int MINB = 1>
+template <typename R, int D, int MINB = 1, bool LEAN = false>
 __global__ void __launch_bounds__(kRolloutWarps * 32, MINB)
     rollout_kernel(const __grid_constant__ RolloutArgs<R> a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -562,7 +567,7 @@ __global__ void __launch_bounds__(kRolloutWarps * 32, MINB)
       (a.dbg != nullptr && threadIdx.x == 0 && blockIdx.x < 256) ? a.dbg + 16 * blockIdx.x : nullptr;
   MPPI_TSTAMP(dbg, 0);
   R* cap = reinterpret_cast<R*>(smem_raw) + (size_t)wib * a.chain.n_caps * 6 * 32;
-  rollout_particle<R, D>(a, g, lane, cap, nullptr);
+  rollout_particle<R, D, LEAN>(a, g, lane, cap, nullptr);
   MPPI_TSTAMP(dbg, 1);
 #ifdef MPPI_DEBUG_TIMERS
   if (a.dbg != nullptr && lane == 0) {  // latest warp end over the grid

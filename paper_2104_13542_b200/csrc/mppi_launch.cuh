@@ -35,7 +35,12 @@ cudaError_t launch_rollout_d(const RolloutArgs<R>& a, long long warps, cudaStrea
   // many waves of particles: the occupancy build (float only; see rollout_kernel)
   constexpr long long kThroughputWarps = 32768;
   const bool many = std::is_same<R, float>::value && warps >= kThroughputWarps && smem <= 24 * 1024;
-  auto kern = many ? rollout_kernel<R, D, 6> : rollout_kernel<R, D, 1>;
+  // the lean specialisation for control steps of configs 1/2 (float; the
+  // float64 exact path and the evaluation modes keep the general kernel)
+  const bool lean = std::is_same<R, float>::value && a.mode == 0 && !rollout_needs_caps(a.cost) &&
+                    getenv("MPPI_ROLLOUT_GENERAL") == nullptr;
+  auto kern = many ? (lean ? rollout_kernel<R, D, 6, std::is_same<R, float>::value> : rollout_kernel<R, D, 6>)
+                   : (lean ? rollout_kernel<R, D, 1, std::is_same<R, float>::value> : rollout_kernel<R, D, 1>);
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
