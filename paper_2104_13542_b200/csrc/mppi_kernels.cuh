@@ -1116,7 +1116,9 @@ inline size_t stats_cluster_smem_bytes(int ppb, int HD) {
 
 // (kStatsThreads, 1): the full register budget — without the minimum-blocks
 // hint ptxas caps this kernel at 128 registers and the step is 1.3 us slower
-template <typename R, int D>
+// LEAN: the control-step specialisation (update applied here, no bundle
+// dumps, no rank record / peer exchange) — only the code a step executes.
+template <typename R, int D, bool LEAN = false>
 __global__ void __launch_bounds__(kStatsThreads, 1) stats_cluster_kernel(const __grid_constant__ StatsArgs<R> a) {
   namespace cg = cooperative_groups;
   cg::cluster_group cluster = cg::this_cluster();
@@ -1217,8 +1219,9 @@ __global__ void __launch_bounds__(kStatsThreads, 1) stats_cluster_kernel(const _
           if (a.totals) a.totals[(size_t)b * N + n] = total;
         }
         if (b == 0 && lane < H) {
-          if (a.dump_step) a.dump_step[(size_t)n * H + lane] = allfin[u] ? ct[u] : 0.0;
-          if (a.dump_terms && a.learned) a.dump_terms[(size_t)T_SELF * N * H + (size_t)n * H + lane] = ds[u];
+          if (!LEAN && a.dump_step) a.dump_step[(size_t)n * H + lane] = allfin[u] ? ct[u] : 0.0;
+          if (!LEAN && a.dump_terms && a.learned)
+            a.dump_terms[(size_t)T_SELF * N * H + (size_t)n * H + lane] = ds[u];
         }
       }
     }
@@ -1242,7 +1245,7 @@ __global__ void __launch_bounds__(kStatsThreads, 1) stats_cluster_kernel(const _
   // slots [cnt, 32) hold zero weights so the register loop below is branch-free
   for (int i = threadIdx.x; i < max(cnt, kClusterEpsRegs); i += blockDim.x)
     wt[i] = (i < cnt && !failed && isfinite(tot[i])) ? exp(-(tot[i] - m) / a.beta) : 0.0;
-  if (b == 0 && a.dump_weights && !failed)
+  if (!LEAN && b == 0 && a.dump_weights && !failed)
     for (int i = threadIdx.x; i < cnt; i += blockDim.x) a.dump_weights[n0 + i] = wt[i];
   __syncthreads();
   MPPI_STAMP(3);
@@ -1317,7 +1320,7 @@ __global__ void __launch_bounds__(kStatsThreads, 1) stats_cluster_kernel(const _
       S1 += parts[((size_t)k * HD + o) * 2];
       S2 += parts[((size_t)k * HD + o) * 2 + 1];
     }
-  if (!a.finalize_inline) {  // rank record for the particle-sharded exchange
+  if (!LEAN && !a.finalize_inline) {  // rank record for the particle-sharded exchange
     const bool peer = a.peer_recv != nullptr;
     double* out = peer ? parts : a.out_record + (size_t)b * (kRecHead + 2 * HD);
     if (peer) __syncthreads();  // every thread has read its partial sums out of `parts`

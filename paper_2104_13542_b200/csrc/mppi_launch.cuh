@@ -53,7 +53,9 @@ cudaError_t launch_rollout_d(const RolloutArgs<R>& a, long long warps, cudaStrea
 template <typename R, int D>
 cudaError_t launch_stats_cluster_d(const StatsArgs<R>& s, cudaStream_t st) {
   const size_t smem = stats_cluster_smem_bytes(s.ppb, s.H * D);
-  auto kern = stats_cluster_kernel<R, D>;
+  const bool lean = s.finalize_inline && !s.dump_step && !s.dump_terms && !s.dump_weights && !s.peer_recv &&
+                    getenv("MPPI_STATS_GENERAL") == nullptr;
+  auto kern = lean ? stats_cluster_kernel<R, D, true> : stats_cluster_kernel<R, D, false>;
   if (s.nblk > 8) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     if (e != cudaSuccess) return e;
