@@ -351,6 +351,10 @@ static __device__ unsigned long long* mlp_dbg = nullptr;
   } while (0)
 #endif
 
+// ONE_TILE: every CTA owns at most one tile (the latency path: rows <= 128 x
+// SMs); the next-tile pipelining is compiled out, so the kernel's code holds
+// only what such a launch executes (its instructions are fetched cold).
+template <bool ONE_TILE>
 static __global__ void __maxnreg__(88)
     mlp_tcgen05_kernel(const float* __restrict__ x, long long M, const unsigned char* __restrict__ img,
                        float* __restrict__ out, int early) {
@@ -416,7 +420,7 @@ static __global__ void __maxnreg__(88)
       uint32_t phX = 0, ph = 0;  // ph: parity of the once-per-tile barriers (A1[c], A2[c], L2done, L3done)
       bool first = true;
       for (long long tile = blockIdx.x; tile < ntiles; tile += G, ph ^= 1u) {
-        const bool has_next = tile + G < ntiles;
+        const bool has_next = !ONE_TILE && tile + G < ntiles;
         if (first) {
           mbar_wait(barX, phX);
           phX ^= 1;
@@ -529,7 +533,7 @@ static __global__ void __maxnreg__(88)
     uint32_t phL1 = 0;
     // layer-1 epilogue of tile t, in place in acc1; stages X(t + G) on the way
     auto epilogue_l1 = [&](long long t) {
-      const bool nxt = t + G < ntiles;
+      const bool nxt = !ONE_TILE && t + G < ntiles;
       if (nxt) load_x(t + G, xv);
 #pragma unroll
       for (int c = 0; c < 8; ++c) {
@@ -557,7 +561,7 @@ static __global__ void __maxnreg__(88)
     if (tile < ntiles) epilogue_l1(tile);
     if (tid == 0) MLP_STAMP(4);
     for (; tile < ntiles; tile += G, ph ^= 1u) {
-      const bool has_next = tile + G < ntiles;
+      const bool has_next = !ONE_TILE && tile + G < ntiles;
       // ---- layer-2 epilogue, in place in acc2
       mbar_wait(barL2done, ph);
       if (tid == 0 && tile == blockIdx.x) MLP_STAMP(5);
@@ -672,16 +676,19 @@ inline cudaError_t mlp_forward(const MlpWeights& m, const float* x, long long ro
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   if (dev < 0 || dev >= 64 || !attr_set[dev]) {
-    cudaError_t e = cudaFuncSetAttribute(mlp_tcgen05_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)kMlpKernelSmem);
-    if (e != cudaSuccess) return e;
+    for (auto k : {mlp_tcgen05_kernel<false>, mlp_tcgen05_kernel<true>}) {
+      cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMlpKernelSmem);
+      if (e != cudaSuccess) return e;
+    }
     if (dev >= 0 && dev < 64) attr_set[dev] = true;
   }
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const long long tiles = (rows + 127) / 128;
   const unsigned grid = (unsigned)(tiles < sms ? tiles : sms);
+  auto kern = (tiles <= sms && getenv("MPPI_MLP_GENERAL") == nullptr) ? mlp_tcgen05_kernel<true>
+                                                                       : mlp_tcgen05_kernel<false>;
   if (!(pdl_mask() & (PDL_MLP | PDL_EARLY))) {  // plain launch: no programmatic edge in a captured graph
-    mlp_tcgen05_kernel<<<grid, kMlpThreads, kMlpKernelSmem, st>>>(x, rows, (const unsigned char*)m.img, out, 0);
+    kern<<<grid, kMlpThreads, kMlpKernelSmem, st>>>(x, rows, (const unsigned char*)m.img, out, 0);
     return cudaGetLastError();
   }
   cudaLaunchConfig_t cfg = {};
@@ -694,7 +701,7 @@ inline cudaError_t mlp_forward(const MlpWeights& m, const float* x, long long ro
   attr[0].val.programmaticStreamSerializationAllowed = (pdl_mask() & PDL_MLP) != 0;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, mlp_tcgen05_kernel, x, rows, (const unsigned char*)m.img, out,
+  return cudaLaunchKernelEx(&cfg, kern, x, rows, (const unsigned char*)m.img, out,
                             (pdl_mask() & PDL_EARLY) ? 1 : 0);
 }
 
