@@ -53,16 +53,22 @@ def ncu_traffic(summary: list | None, stage: str):
 
 def step_roofline(stage_ms: dict, rows: int, particles: int, horizon: int, dof: int, config: int,
                   peaks: dict, peaks_kind: str, ncu_summary: list | None = None,
-                  ncu_source: str | None = None) -> dict:
+                  ncu_source: str | None = None, ncu_rows: int | None = None) -> dict:
     """Roofline entry for the dominant kernel of the step (stage_ms from the
     event-record nodes of the timed graph replays); `traffic` from the
-    committed ncu summary of the same workload when one is given."""
+    committed ncu summary of the same kernel when one is given. `ncu_rows`:
+    the rows of the captured launch when it was a smaller batch than this
+    step's — its bytes per row are then scaled to this launch and labelled so."""
     stage = max(("rollout", "mlp", "update"), key=lambda k: stage_ms.get(k, 0.0))
     out = _stage_roofline(stage, stage_ms, rows, dof, config, peaks, peaks_kind)
     tr = ncu_traffic(ncu_summary, stage)
     if tr is not None and out.get("kernel"):
+        src = f"{ncu_source}: dram__bytes_read.sum + dram__bytes_write.sum (ncu replay, cold L2)"
+        if ncu_rows and ncu_rows != rows:
+            src += f"; captured at {ncu_rows} rows ({tr / ncu_rows:.1f} B/row), scaled to this launch's {rows}"
+            tr = tr / ncu_rows * rows
         out["traffic"] = tr
-        out["traffic_source"] = f"{ncu_source}: dram__bytes_read.sum + dram__bytes_write.sum (ncu replay, cold L2)"
+        out["traffic_source"] = src
     return out
 
 
