@@ -161,3 +161,27 @@ def test_roofline_counts():
     assert RL.MLP_TENSOR_FLOPS_PER_ROW == 89216
     assert 1400 < RL.rollout_flops_per_unit(1) < 1600
     assert 1700 < RL.rollout_flops_per_unit(2) < 2000
+
+
+def test_reference_arm_bench_line():
+    """`bench.py --impl reference` (the reference's own CPU control_step from
+    oracle/_ref on the host cores) prints one JSON line with the contract's
+    keys and the reference arm's e2e / cpu_baseline blocks."""
+    import json
+    import subprocess
+    import sys
+
+    root = Path(__file__).resolve().parents[1]
+    if not (root / "oracle" / "_ref" / "jointmpc").exists():
+        pytest.skip("reference not installed (oracle/build_ref.py)")
+    out = subprocess.run([sys.executable, str(root / "bench.py"), "--impl", "reference", "--steps", "1",
+                          "--warmup", "1"], capture_output=True, text=True, timeout=600, cwd=root)
+    assert out.returncode == 0, out.stderr[-2000:]
+    line = json.loads(out.stdout.strip().splitlines()[-1])
+    for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
+              "scaling", "vs_baseline", "dtype", "data", "config", "e2e", "cpu_baseline"):
+        assert k in line, k
+    assert line["impl"] == "reference" and line["unit"] == "ms" and line["higher_is_better"] is False
+    assert line["e2e"]["value"] == line["value"] and line["e2e"]["h2d_bytes_per_step"] == 0
+    assert line["cpu_baseline"]["kind"] == "reference" and line["cpu_baseline"]["cores"] >= 1
+    assert line["value"] > 0.0
