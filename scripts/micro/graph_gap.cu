@@ -84,11 +84,43 @@ __global__ void k_tmem(int slot) {
   if (threadIdx.x == 0 && blockIdx.x == 0) g_t[2 * slot + 1] = t + sm[5];
 }
 
+// MLP-shaped launch: 544 threads, 88 registers in use, ~190 KB of dynamic
+// shared memory, a TMEM allocation and a large body
+__global__ void __launch_bounds__(544, 1) k_mlp_like(int slot, float* out) {
+  extern __shared__ unsigned char sm[];
+  __shared__ unsigned slot_addr;
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  if (threadIdx.x == 0 && blockIdx.x == 0) g_t[2 * slot] = t;
+  if (threadIdx.x < 32) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+        (unsigned)__cvta_generic_to_shared(&slot_addr)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  float r[60];
+#pragma unroll
+  for (int i = 0; i < 60; ++i) r[i] = threadIdx.x * (i + 1) * 0.5f;
+#pragma unroll
+  for (int k = 0; k < 40; ++k)
+#pragma unroll
+    for (int i = 0; i < 60; ++i) r[i] = __sinf(r[i]) * r[(i + 7) % 60] + 0.25f;
+  float acc = 0.f;
+#pragma unroll
+  for (int i = 0; i < 60; ++i) acc += r[i];
+  sm[threadIdx.x] = (unsigned char)acc;
+  __syncthreads();
+  if (threadIdx.x < 32) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(slot_addr));
+  if (acc == 1234.5f) out[0] = acc;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  if (threadIdx.x == 0 && blockIdx.x == 0) g_t[2 * slot + 1] = t + sm[5];
+}
+
 int main(int argc, char**) {
   cudaStream_t st;
   cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
   cudaFuncSetAttribute(k_big, cudaFuncAttributeMaxDynamicSharedMemorySize, 190 * 1024);
   cudaFuncSetAttribute(k_tmem, cudaFuncAttributeMaxDynamicSharedMemorySize, 190 * 1024);
+  cudaFuncSetAttribute(k_mlp_like, cudaFuncAttributeMaxDynamicSharedMemorySize, 193840);
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
@@ -99,7 +131,7 @@ int main(int argc, char**) {
   unsigned char* flush;
   cudaMalloc(&flush, 256u << 20);
   const bool do_flush = argc > 1;
-  for (int variant = 0; variant < 12; ++variant) {
+  for (int variant = 0; variant < 14; ++variant) {
     cudaGraph_t g;
     cudaGraphExec_t ge;
     cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal);
@@ -118,6 +150,13 @@ int main(int argc, char**) {
       k_params<<<125, 128, 0, st>>>(bp0, nullptr);
       k_big<<<118, 544, 190 * 1024, st>>>(1);
       nk = 2;
+    } else if (variant == 12) {  // small kernel, then the MLP-shaped one, then small
+      k_small<<<125, 128, 0, st>>>(nk++, 100);
+      k_mlp_like<<<118, 544, 193840, st>>>(nk++, buf);
+      k_small<<<16, 256, 0, st>>>(nk++, 100);
+    } else if (variant == 13) {  // large-code 128-thread kernel (rollout-like), then the MLP-shaped one
+      k_code<600><<<125, 128, 0, st>>>(nk++, buf);
+      k_mlp_like<<<118, 544, 193840, st>>>(nk++, buf);
     } else if (variant == 10) {  // small kernel, then a TMEM-allocating 190 KB kernel, then small
       k_small<<<125, 128, 0, st>>>(nk++, 100);
       k_tmem<<<118, 544, 190 * 1024, st>>>(nk++);
