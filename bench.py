@@ -527,8 +527,10 @@ def run_tracking(args):
     # the lean graph (value, e2e), then the instrumented graph (stage attribution)
     with ClockSampler(local) as clk:
         rec = loop(1, args.steps, lambda wall, inf: (wall, inf.device_ms))
-    e2e = [w for w, _ in rec]
     dev_ms = [d for _, d in rec]
+    # end to end on the lean graph without device events (level 0), as the
+    # config-2 line does: the events of level 1 are host calls inside control_step
+    e2e = loop(0, args.steps, lambda wall, inf: wall)
     srec = loop(2, min(args.steps, 50), lambda wall, inf: (inf.sample_ms, inf.rollout_ms, inf.mlp_ms,
                                                           inf.update_ms))
     st_mean = {k: float(np.mean([r[j] for r in srec])) for j, k in enumerate(("sample", "rollout", "mlp",

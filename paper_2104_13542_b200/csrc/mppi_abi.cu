@@ -183,6 +183,7 @@ struct mppi_plan {
   double* m_cmd = nullptr;
   mppi_step_info* m_info = nullptr;
   std::vector<double> goal_host;
+  bool goal_dirty = false;  // goal_host newer than the device copy (uploaded lazily: flush_goal)
   // graph
   cudaGraphExec_t graph = nullptr;       // lean step graph (production)
   cudaGraphExec_t graph_prof = nullptr;  // same step + event-record nodes between the stages
@@ -195,6 +196,7 @@ struct mppi_plan {
     cudaKernelNodeParams kp;
     std::vector<unsigned char> args;  // RolloutArgs<R> image
     size_t st_off;                    // offsetof(RolloutArgs<R>, st0)
+    size_t g_off;                     // offsetof(RolloutArgs<R>, g0)
     void* argv[1];
   };
   std::vector<InlineNode> inl, inl_prof;
@@ -247,6 +249,18 @@ namespace {
 
 int set_device(mppi_plan* p) {
   CK(cudaSetDevice(p->device));
+  return MPPI_OK;
+}
+
+// The device copy of the goals, brought up to date before any work that
+// reads it (the inline-state step graph carries the goal in its parameters
+// and does not need it). From pageable memory: the copy has read goal_host
+// when cudaMemcpyAsync returns, so the host may edit it right away.
+int flush_goal(mppi_plan* p) {
+  if (!p->goal_dirty) return MPPI_OK;
+  CK(cudaMemcpyAsync(p->goal.p, p->goal_host.data(), sizeof(double) * 16 * p->B, cudaMemcpyHostToDevice,
+                     p->stream));
+  p->goal_dirty = false;
   return MPPI_OK;
 }
 
@@ -403,6 +417,7 @@ int enqueue_iteration(mppi_plan* p, int it, bool inline_final, double* out_recor
     if (p->capture_inl && (stages & 1u)) {
       a.state_inline = 1;
       for (int j = 0; j < 2 * p->D; ++j) a.st0[j] = p->h_state[j];
+      for (int j = 0; j < 16; ++j) a.g0[j] = p->goal_host[j];
     }
     if (stages & 1u) CK(launch_rollout_any<R>(a, p->D, (long long)p->B * p->N, st));
     if (p->capture_inl && (stages & 1u)) {  // remember the node and its argument image
@@ -416,6 +431,7 @@ int enqueue_iteration(mppi_plan* p, int it, bool inline_final, double* out_recor
       CK(cudaGraphKernelNodeGetParams(n.node, &n.kp));
       n.args.assign(reinterpret_cast<const unsigned char*>(&a), reinterpret_cast<const unsigned char*>(&a) + sizeof(a));
       n.st_off = offsetof(RolloutArgs<R>, st0);
+      n.g_off = offsetof(RolloutArgs<R>, g0);
       p->capture_inl->push_back(std::move(n));
     }
     if ((stages & 2u) && p->learned())
@@ -984,9 +1000,7 @@ int mppi_set_goal(mppi_plan* p, int32_t inst, const double* R, const double* t, 
     for (int i = 0; i < 3; ++i) g[9 + i] = t[i];
     g[12] = (double)mode;
   }
-  CK(cudaMemcpyAsync(p->goal.p + (size_t)b0 * 16, &p->goal_host[(size_t)b0 * 16],
-                     sizeof(double) * 16 * (b1 - b0), cudaMemcpyHostToDevice, p->stream));
-  CK(cudaStreamSynchronize(p->stream));
+  p->goal_dirty = true;  // uploaded with the next step (flush_goal / the step graph's parameters)
   return MPPI_OK;
 }
 
@@ -1001,9 +1015,7 @@ int mppi_set_goals(mppi_plan* p, int32_t first, int32_t count, const double* R, 
     for (int k = 0; k < 3; ++k) g[9 + k] = t[(size_t)i * 3 + k];
     g[12] = (double)modes[i];
   }
-  CK(cudaMemcpyAsync(p->goal.p + (size_t)first * 16, &p->goal_host[(size_t)first * 16],
-                     sizeof(double) * 16 * count, cudaMemcpyHostToDevice, p->stream));
-  CK(cudaStreamSynchronize(p->stream));
+  p->goal_dirty = true;
   return MPPI_OK;
 }
 
@@ -1152,8 +1164,11 @@ int mppi_step(mppi_plan* p, const double* theta, const double* theta_dot, double
   using clk = std::chrono::steady_clock;
   const auto h0 = clk::now();
 #endif
-  for (auto& n : prof ? p->inl_prof : p->inl) {
+  auto& inl_nodes = prof ? p->inl_prof : p->inl;
+  if (inl_nodes.empty()) CKR(flush_goal(p));  // the graph reads the device goals
+  for (auto& n : inl_nodes) {
     memcpy(n.args.data() + n.st_off, p->h_state, sizeof(double) * 2 * D);
+    memcpy(n.args.data() + n.g_off, p->goal_host.data(), sizeof(double) * 16);
     CK(cudaGraphExecKernelNodeSetParams(prof ? p->graph_prof : p->graph, n.node, &n.kp));
   }
 #ifdef MPPI_DEBUG_TIMERS
@@ -1269,6 +1284,7 @@ int mppi_evaluate(mppi_plan* p, int32_t mode, int32_t n, int32_t H, const double
   if (n < 1) return fail(MPPI_E_BAD_ARGUMENT, "empty batch");
   if (p->learned() && !p->mlp_ready) return fail(MPPI_E_CONFIG, "learned provider without weights");
   CKR(set_device(p));
+  CKR(flush_goal(p));
   cudaStream_t st = p->stream;
   const int D = p->D;
   const size_t nhd = (size_t)n * H * D, nh = (size_t)n * H;
@@ -1413,6 +1429,7 @@ int mppi_episode(mppi_plan* p, const mppi_episode_desc* d, const double* theta0,
   const int S = d->steps, D = p->D;
   if (S == 0) return MPPI_OK;
   CKR(set_device(p));
+  CKR(flush_goal(p));
   cudaStream_t st = p->stream;
   // ---- buffers
   const size_t flog = (size_t)S * (1 + 3 * D + 3 + 9 + 3 + 9 + 1 + N_TERMS);
@@ -1599,6 +1616,7 @@ int mppi_profile_stages(mppi_plan* p, int32_t enable) {
 int mppi_time_stage(mppi_plan* p, int32_t stage, int32_t reps, double* ms_per_launch) {
   if (!p || !ms_per_launch || reps < 1 || stage < 0 || stage > 3) return fail(MPPI_E_BAD_ARGUMENT, "bad arguments");
   CKR(set_device(p));
+  CKR(flush_goal(p));
   CKR(ensure_graph(p));
   cudaStream_t st = p->stream;
   const unsigned mask = stage == 3 ? 7u : (1u << stage);
@@ -1634,6 +1652,7 @@ int mppi_stats_dev(mppi_plan* p, const double* theta, const double* theta_dot, v
   if (p->B != 1) return fail(MPPI_E_CONFIG, "particle sharding is for single-instance plans");
   if (p->learned() && !p->mlp_ready) return fail(MPPI_E_CONFIG, "learned provider without weights");
   CKR(set_device(p));
+  CKR(flush_goal(p));
   cudaStream_t st = stream ? (cudaStream_t)stream : p->stream;
   const int D = p->D, it = p->sharded_iter;
   if (it == 0) {
@@ -1736,6 +1755,7 @@ int mppi_step_exchange(mppi_plan* p, const double* theta, const double* theta_do
   if (!p->peer_recv_tab.p) return fail(MPPI_E_CONFIG, "mppi_set_peers first");
   if (p->learned() && !p->mlp_ready) return fail(MPPI_E_CONFIG, "learned provider without weights");
   CKR(set_device(p));
+  CKR(flush_goal(p));
   cudaStream_t st = p->stream;
   const int D = p->D;
   memcpy(p->h_state, theta, sizeof(double) * D);

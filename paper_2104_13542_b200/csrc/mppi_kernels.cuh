@@ -51,8 +51,9 @@ struct RolloutArgs {
   int check_var;  // PolicyStateError check of build_control_batch (sampling.py:282)
   int skip_on_status;
   int pdl_early;  // trigger the dependent grid at entry
-  int state_inline;  // single instance: theta, theta_dot travel in st0 (kernel parameter), not `state`
-  double st0[2 * MAXD];
+  int state_inline;  // single instance: theta, theta_dot travel in st0 (kernel parameter), not `state`,
+  double st0[2 * MAXD];  // and the goal in g0, not `goal`
+  double g0[16];
   double tail_mean, tail_sd;
   const double* eps;     // (N,H,d)
   const double* means;   // (B,H,d)
@@ -239,7 +240,7 @@ __device__ __forceinline__ bool rollout_particle(const RolloutArgs<R>& a, long l
     st_p[j] = (R)st[j];
     st_v[j] = (R)st[D + j];
   }
-  const double* gl = a.goal + (size_t)b * 16;
+  const double* gl = a.state_inline ? a.g0 : a.goal + (size_t)b * 16;
   R Rg[9], tg[3];
 #pragma unroll
   for (int i = 0; i < 9; ++i) Rg[i] = (R)gl[i];
