@@ -204,5 +204,24 @@ int main(int argc, char**) {
     cudaGraphExecDestroy(ge);
     cudaGraphDestroy(g);
   }
+  // the same chains launched directly into the stream (no graph), events around them
+  for (int nk = 1; nk <= 3; ++nk) {
+    float best = 1e9, sum = 0;
+    const int reps = 200;
+    for (int r = 0; r < reps + 10; ++r) {
+      if (do_flush) cudaMemsetAsync(flush, r & 255, 256u << 20, st);
+      cudaEventRecord(e0, st);
+      for (int i = 0; i < nk; ++i) k_small<<<125, 128, 0, st>>>(i, 100);
+      cudaEventRecord(e1, st);
+      cudaStreamSynchronize(st);
+      float ms;
+      cudaEventElapsedTime(&ms, e0, e1);
+      if (r >= 10) {
+        sum += ms;
+        if (ms < best) best = ms;
+      }
+    }
+    printf("direct launches (%d kernels): event mean %.2f us, min %.2f us\n", nk, 1e3 * sum / reps, 1e3 * best);
+  }
   return 0;
 }
