@@ -875,7 +875,7 @@ __global__ void __launch_bounds__(kStatsThreads) stats_kernel(const __grid_const
   double* red = wt + a.ppb;     // [32]
   double* scale = red + 32;     // [max(nblk, 8)] scales + [max(nblk, 8) * kRecHead] heads
   const int reclen = kRecHead + 2 * HD;
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = kStatsThreads / 32;  // launched with kStatsThreads
   pdl_wait();  // rollout / MLP outputs and the status word are ready past this point
   const bool failed = (a.status[b] != 0);
 #ifdef MPPI_DEBUG_TIMERS
@@ -1140,7 +1140,7 @@ __global__ void __launch_bounds__(kStatsThreads, 1) stats_cluster_kernel(const _
   double* emp = parts + (size_t)kClusterMax * 2 * HD;  // [HD]
   unsigned long long* bars = reinterpret_cast<unsigned long long*>(emp + HD);  // [0] mins, [1] rank-0 sums
   const uint32_t bar_min = smem_addr(&bars[0]), bar_sum = smem_addr(&bars[1]);
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = kStatsThreads / 32;  // launched with kStatsThreads
   const int o = threadIdx.x;
   const bool owner = o < HD;  // H*d <= 256 = blockDim: one policy entry per thread
   MPPI_STAMP(6);  // (debug) CTA entry
