@@ -896,6 +896,9 @@ __global__ void __launch_bounds__(kStatsThreads) stats_kernel(const __grid_const
   // the first reduction, so the HBM/L2 latency is paid once per batch.
   {  // runs even when the step already failed: cheap, and the status load overlaps it
     constexpr int PA = 4;
+    // the lane's discount, read once: a lane-indexed parameter read inside the
+    // loop is a serialised constant-cache load per row
+    const double disc_l = lane < H ? (lane < H - 1 ? a.disc[lane] : a.dlast) : 0.0;
     for (int i0 = wid * PA; i0 < cnt; i0 += nw * PA) {
       double cv[PA], dv[PA];
 #pragma unroll
@@ -925,7 +928,7 @@ __global__ void __launch_bounds__(kStatsThreads) stats_kernel(const __grid_const
         }
         const bool allfin = __all_sync(0xffffffffu, fin);
         double contrib = 0.0;
-        if (lane < H) contrib = (lane < H - 1 ? a.disc[lane] : a.dlast) * c;
+        if (lane < H) contrib = disc_l * c;
         double total = warp_sum(contrib);
         if (!allfin) total = CUDART_INF;
         if (lane == 0) {
@@ -1418,6 +1421,193 @@ __global__ void __launch_bounds__(kStatsThreads, 1) stats_cluster_kernel(const _
     }
   }
   MPPI_STAMP(7);
+}
+
+// Batched statistics, G instances per block (config 4: B >= 148, one block's
+// worth of particles per instance, no bundle dumps, update applied here).
+// stats_kernel with nblk == 1 re-reads the shared perturbation block
+// (N*H*d doubles, 840 KB at 500 x 30 x 7) once per instance; here one load of
+// eps[n][o] feeds the weighted sums of all G instances. Same arithmetic as
+// stats_kernel + combine_records(count = 1) + finalize_policy, term by term:
+//   totals      rollout.py:111-171 (rows of the G instances are contiguous)
+//   weights     policy.py:103-121 (warp g reduces instance g in lane order)
+//   S0/S1/S2    policy.py:124-155 around the pre-update mean; a particle in
+//               the union of nonzero weights adds w*dv with w = 0 for the
+//               instances where it underflowed, which leaves the sum unchanged
+//   record      combine_records with one record: scale exp(-0/beta) = 1
+template <typename R, int D, int G>
+__global__ void __launch_bounds__(kStatsThreads) stats_multi_kernel(const __grid_constant__ StatsArgs<R> a) {
+  extern __shared__ __align__(16) double sm[];
+  const int H = a.H, HD = H * D, N = a.N, cnt = N;
+  const int b0 = blockIdx.x * G;
+  const int gn = min(G, a.B - b0);
+  const int reclen = kRecHead + 2 * HD;
+  double* tot = sm;                  // [G][N]
+  double* wt = tot + G * N;          // [G][N]
+  double* recs = wt + G * N;         // [G][reclen]
+  double* emp = recs + G * reclen;   // [HD]
+  int* nz = reinterpret_cast<int*>(emp + HD);  // [N]
+  __shared__ int s_failed[G];
+  __shared__ int s_nnz;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = kStatsThreads / 32;
+  pdl_wait();
+  if (threadIdx.x < G) s_failed[threadIdx.x] = threadIdx.x < gn ? (a.status[b0 + threadIdx.x] != 0) : 1;
+
+  // ---- totals of the G*N contiguous rows -----------------------------------
+  {
+    constexpr int PA = 4;
+    const int rows = gn * N;
+    const double disc_l = lane < H ? (lane < H - 1 ? a.disc[lane] : a.dlast) : 0.0;
+    for (int r0 = wid * PA; r0 < rows; r0 += nw * PA) {
+      double cv[PA], dv[PA];
+#pragma unroll
+      for (int u = 0; u < PA; ++u) {
+        cv[u] = 0.0;
+        dv[u] = 0.0;
+        if (r0 + u < rows && lane < H) {
+          const size_t m = ((size_t)b0 * N + r0 + u) * H + lane;
+          cv[u] = (double)a.step[m];
+          if (a.learned) dv[u] = (double)a.mlp_d[m];
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < PA; ++u) {
+        const int r = r0 + u;
+        if (r >= rows) break;  // warp-uniform
+        double c = 0.0;
+        bool fin = true;
+        if (lane < H) {
+          c = cv[u];
+          if (a.learned) c = c + a.a_coll * (dv[u] > 0.0 ? dv[u] : 0.0);
+          fin = isfinite(c);
+        }
+        const bool allfin = __all_sync(0xffffffffu, fin);
+        double contrib = 0.0;
+        if (lane < H) contrib = disc_l * c;
+        double total = warp_sum(contrib);
+        if (!allfin) total = CUDART_INF;
+        if (lane == 0) {
+          tot[r] = total;
+          if (a.totals) a.totals[(size_t)b0 * N + r] = total;
+        }
+      }
+    }
+  }
+  __syncthreads();
+
+  // ---- per instance: minimum, weights, record head (warp g) ----------------
+  if (wid < gn) {
+    const int g = wid;
+    const double* tg = tot + g * N;
+    double* wg = wt + g * N;
+    const bool failed = s_failed[g] != 0;
+    double mloc = CUDART_INF;
+    if (!failed)
+      for (int i = lane; i < cnt; i += 32)
+        if (isfinite(tg[i])) mloc = fmin(mloc, tg[i]);
+    for (int off = 16; off > 0; off >>= 1) mloc = fmin(mloc, __shfl_xor_sync(0xffffffffu, mloc, off));
+    const double mb = mloc;
+    double s0 = 0.0, c = 0.0, sf = 0.0;
+    for (int i = lane; i < cnt; i += 32) {
+      const double w = (!failed && isfinite(tg[i])) ? exp(-(tg[i] - mb) / a.beta) : 0.0;
+      wg[i] = w;
+      if (!failed) {
+        s0 += w;
+        if (isfinite(tg[i])) {
+          c += 1.0;
+          sf += tg[i];
+        }
+      }
+    }
+    s0 = warp_sum(s0);
+    c = warp_sum(c);
+    sf = warp_sum(sf);
+    if (lane == 0) {  // == combine_records over this single record
+      const double sc = c > 0.0 ? 1.0 : 0.0;
+      double* rec = recs + g * reclen;
+      rec[0] = c > 0.0 ? mb : CUDART_INF;
+      rec[1] = sc * s0 + 0.0;
+      rec[2] = c + 0.0;
+      rec[3] = sf + 0.0;
+      rec[4] = fmax(0.0, (double)a.status[b0 + g]);
+      rec[5] = fmin(2147483647.0, (double)a.bad[b0 + g]);
+    }
+  }
+  __syncthreads();
+  // union of the nonzero weights, ascending (the summation order of stats_kernel)
+  if (wid == 0) {
+    int base = 0;
+    for (int c0 = 0; c0 < cnt; c0 += 32) {
+      const int i = c0 + lane;
+      bool keep = false;
+      if (i < cnt)
+#pragma unroll
+        for (int g = 0; g < G; ++g)
+          if (g < gn) keep |= wt[g * N + i] > 0.0;
+      const unsigned bal = __ballot_sync(0xffffffffu, keep);
+      if (keep) nz[base + __popc(bal & ((1u << lane) - 1u))] = i;
+      base += __popc(bal);
+    }
+    if (lane == 0) s_nnz = base;
+  }
+  double mo[G], so[G];
+  if (threadIdx.x < HD) {
+    const int h = threadIdx.x / D, j = threadIdx.x - h * D;
+    const int hs = a.shift ? h + 1 : h;
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      const int b = b0 + (g < gn ? g : 0);
+      mo[g] = hs < H ? a.means[(size_t)b * HD + hs * D + j] : a.tail_mean;
+      so[g] = hs < H ? a.sd[(size_t)b * HD + hs * D + j] : a.tail_sd;
+    }
+  }
+  __syncthreads();
+  const int nnz = s_nnz;
+
+  // ---- weighted sums: one eps load feeds G instances ------------------------
+  if (threadIdx.x < HD) {
+    const int o = threadIdx.x;
+    double s1[G], s2[G];
+#pragma unroll
+    for (int g = 0; g < G; ++g) s1[g] = s2[g] = 0.0;
+    const double* ep = a.eps + o;
+    constexpr int PD = 8;
+    for (int k0 = 0; k0 < nnz; k0 += PD) {
+      double e[PD];
+      int ii[PD];
+#pragma unroll
+      for (int u = 0; u < PD; ++u) {
+        ii[u] = k0 + u < nnz ? nz[k0 + u] : -1;
+        e[u] = ii[u] >= 0 ? __ldg(ep + (size_t)ii[u] * HD) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < PD; ++u) {
+        if (ii[u] < 0) break;
+        const int ng = ii[u] + a.particle_offset;
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+          const double dv = ng < a.null_count ? 0.0 - mo[g]
+                                              : (ng == a.null_count ? 0.0 : (mo[g] + so[g] * e[u]) - mo[g]);
+          const double w = wt[g * N + ii[u]];
+          s1[g] += w * dv;
+          s2[g] += w * dv * dv;
+        }
+      }
+    }
+#pragma unroll
+    for (int g = 0; g < G; ++g)
+      if (g < gn) {
+        double* rec = recs + g * reclen;
+        const double sc = rec[2] > 0.0 ? 1.0 : 0.0;
+        rec[kRecHead + o] = sc * s1[g] + 0.0;
+        rec[kRecHead + HD + o] = sc * s2[g] + 0.0;
+      }
+  }
+  __syncthreads();
+  for (int g = 0; g < gn; ++g) {
+    finalize_policy(a, b0 + g, recs + g * reclen, emp);
+    __syncthreads();
+  }
 }
 
 // Finalize from R rank records (config 5, after the all-gather).

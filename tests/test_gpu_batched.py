@@ -175,3 +175,39 @@ def test_peer_exchange_step_matches_allgather_path():
             np.testing.assert_array_equal(peer.get_policy(0)[1], gather.get_policy(0)[1])
             assert info_p.best_cost == info_g.best_cost
             np.testing.assert_allclose(cmd_p, cmd_ref, atol=1e-9 if precision == N.FP64 else 1e-3)
+
+
+@pytest.mark.parametrize("precision", ["fp64", "fp32"])
+def test_multi_instance_statistics_bit_identical(precision, monkeypatch):
+    """stats_multi_kernel (G instances per block sharing the perturbation
+    loads; mppi_kernels.cuh) against stats_kernel with one block per instance
+    (MPPI_STATS_G=1): identical commands, policies, best and mean costs over
+    several steps, with a ragged last block (150 = 37 x 4 + 2, 75 x 2)."""
+    from paper_2104_13542_b200 import configs
+    from paper_2104_13542_b200.batched import BatchedController
+    from paper_2104_13542_b200.kinematics import load_chain
+    from paper_2104_13542_b200.surrogate import load_arm7_surrogate
+
+    B, n = 150, 128
+    goals, th0 = configs.batched_problem(B)
+    kw = dict(configs.CONTROLLER_KW)
+    kw.pop("seed")
+    kw["particles"] = n
+    runs = {}
+    for g in ("1", "2", "4"):
+        monkeypatch.setenv("MPPI_STATS_G", g)  # read when the step is launched / captured
+        bc = BatchedController(load_chain("arm7.chain"), goals, weights=configs.make_weights(2),
+                               self_collision=load_arm7_surrogate(), precision=precision, **kw)
+        th, thd = th0.copy(), np.zeros_like(th0)
+        out = []
+        for step in range(3):
+            cmds, diag = bc.control_step(th + 0.01 * step, thd)
+            assert (diag.status == 0).all()
+            out.append((cmds.copy(), diag.best_cost.copy(), diag.mean_cost.copy()))
+        out.append(tuple(np.stack([getattr(bc.policy(b), f) for b in range(B)])
+                         for f in ("means", "variances")))
+        runs[g] = out
+    for g in ("2", "4"):
+        for a, b in zip(runs["1"], runs[g]):
+            for x, y in zip(a, b):
+                np.testing.assert_array_equal(x, y, err_msg=f"G={g}")
