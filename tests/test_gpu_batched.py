@@ -56,7 +56,8 @@ def test_batched_instances_match_independent_controllers(precision, tol):
         theta = theta + 0.05 * thetad
 
 
-def test_emulated_particle_shards_match_unsharded():
+@pytest.mark.parametrize("total,R", [(600, 3), (262144, 2)])  # config 5's largest N at full size
+def test_emulated_particle_shards_match_unsharded(total, R):
     """R plans holding disjoint particle shards on one GPU; their records are
     concatenated on the device exactly as the all-gather would, and every
     shard's finalize must reproduce the unsharded controller."""
@@ -68,7 +69,6 @@ def test_emulated_particle_shards_match_unsharded():
     from paper_2104_13542_b200.sharded import particle_shard
     from paper_2104_13542_b200 import _native as N
 
-    total, R = 600, 3
     ref = configs.make_controller(1, particles=total, precision="fp64")
     chain = load_chain("arm7.chain")
     goal = configs.make_goal(1)
