@@ -1435,8 +1435,8 @@ __global__ void __launch_bounds__(kStatsThreads, 1) stats_cluster_kernel(const _
 //               the union of nonzero weights adds w*dv with w = 0 for the
 //               instances where it underflowed, which leaves the sum unchanged
 //   record      combine_records with one record: scale exp(-0/beta) = 1
-template <typename R, int D, int G>
-__global__ void __launch_bounds__(kStatsThreads) stats_multi_kernel(const __grid_constant__ StatsArgs<R> a) {
+template <typename R, int D, int G, int PD = 8, int MINB = 1>
+__global__ void __launch_bounds__(kStatsThreads, MINB) stats_multi_kernel(const __grid_constant__ StatsArgs<R> a) {
   extern __shared__ __align__(16) double sm[];
   const int H = a.H, HD = H * D, N = a.N, cnt = N;
   const int b0 = blockIdx.x * G;
@@ -1571,7 +1571,6 @@ __global__ void __launch_bounds__(kStatsThreads) stats_multi_kernel(const __grid
 #pragma unroll
     for (int g = 0; g < G; ++g) s1[g] = s2[g] = 0.0;
     const double* ep = a.eps + o;
-    constexpr int PD = 8;
     for (int k0 = 0; k0 < nnz; k0 += PD) {
       double e[PD];
       int ii[PD];

@@ -29,7 +29,10 @@ inline size_t stats_smem_bytes(int ppb, int nblk, int HD) {
 }
 
 // stats_multi_kernel: G instances per block (MPPI_STATS_G=1 selects stats_kernel)
-constexpr int kStatsMultiG = 2;  // A/B at 4096 x 500: update 1.66 (G=1) -> 0.89 (2) / 0.98 ms (4)
+// A/B at 4096 x 500 (update stage): 1.66 ms (G=1) -> 0.89 (G=2) / 0.98 (G=4);
+// with the discount hoisted, same box: 0.79 (G=2, 72 registers, 3 blocks/SM)
+// -> 0.70 (G=2 at 5 blocks/SM, code 22) / 0.96 (16 loads in flight) / 0.88 (G=4)
+constexpr int kStatsMultiG = 22;
 inline size_t stats_multi_smem_bytes(int G, int N, int HD) {
   return sizeof(double) * (2 * (size_t)G * N + (size_t)G * (kRecHead + 2 * HD) + HD) + sizeof(int) * (size_t)N;
 }
@@ -99,16 +102,19 @@ cudaError_t launch_stats_d(const StatsArgs<R>& s, cudaStream_t st) {
       !s.dump_step && !s.dump_terms && !s.dump_weights && !s.dbg && s.H * D <= kStatsThreads) {
     const char* ev = getenv("MPPI_STATS_G");
     const int g = ev ? atoi(ev) : kStatsMultiG;
-    if (g == 2 || g == 4) {
-      const size_t smem = stats_multi_smem_bytes(g, s.N, s.H * D);
+    // 22 = G 2 at >= 5 blocks per SM (48 registers), 2 = G 2 at the compiler's 72
+    if (g == 2 || g == 4 || g == 22) {
+      const size_t smem = stats_multi_smem_bytes(g == 4 ? 4 : 2, s.N, s.H * D);
       if (smem <= 200 * 1024) {
-        auto kern = g == 2 ? stats_multi_kernel<R, D, 2> : stats_multi_kernel<R, D, 4>;
+        auto kern = g == 2 ? stats_multi_kernel<R, D, 2>
+                    : g == 4 ? stats_multi_kernel<R, D, 4>
+                    : stats_multi_kernel<R, D, 2, 8, 5>;
         if (smem > 48 * 1024) {
           cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
           if (e != cudaSuccess) return e;
         }
         cudaLaunchConfig_t cfg = {};
-        cfg.gridDim = dim3((s.B + g - 1) / g, 1, 1);
+        cfg.gridDim = dim3((s.B + (g == 4 ? 4 : 2) - 1) / (g == 4 ? 4 : 2), 1, 1);
         cfg.blockDim = dim3(kStatsThreads, 1, 1);
         cfg.dynamicSmemBytes = smem;
         cfg.stream = st;

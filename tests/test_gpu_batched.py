@@ -194,7 +194,7 @@ def test_multi_instance_statistics_bit_identical(precision, monkeypatch):
     kw.pop("seed")
     kw["particles"] = n
     runs = {}
-    for g in ("1", "2", "4"):
+    for g in ("1", "2", "4", "22"):  # 22: the default, two instances at 5 blocks per SM
         monkeypatch.setenv("MPPI_STATS_G", g)  # read when the step is launched / captured
         bc = BatchedController(load_chain("arm7.chain"), goals, weights=configs.make_weights(2),
                                self_collision=load_arm7_surrogate(), precision=precision, **kw)
@@ -207,7 +207,7 @@ def test_multi_instance_statistics_bit_identical(precision, monkeypatch):
         out.append(tuple(np.stack([getattr(bc.policy(b), f) for b in range(B)])
                          for f in ("means", "variances")))
         runs[g] = out
-    for g in ("2", "4"):
+    for g in ("2", "4", "22"):
         for a, b in zip(runs["1"], runs[g]):
             for x, y in zip(a, b):
                 np.testing.assert_array_equal(x, y, err_msg=f"G={g}")
