@@ -356,7 +356,7 @@ void choose_blocks(int N, int B, int& ppb, int& nblk) {
   }
   ppb = 32;
   if (N > 16 * 32 && N <= 16 * 64) ppb = (N + 15) / 16;
-  if (const char* ev = getenv("MPPI_STATS_PPB")) ppb = std::max(ppb, atoi(ev));  // A/B
+  if (const char* ev = getenv("MPPI_STATS_PPB")) ppb = std::max(1, atoi(ev));  // A/B
   nblk = (N + ppb - 1) / ppb;
   if (nblk > kStatsMaxBlocks) {
     nblk = kStatsMaxBlocks;
