@@ -123,6 +123,10 @@ class BatchedController:
         if not (np.isfinite(theta).all() and np.isfinite(theta_dot).all()):
             raise ContractError("joint state is not finite")
         cmds, infos = self.plan.step(theta, theta_dot)
+        return self._apply_ladder(cmds, infos)
+
+    def _apply_ladder(self, cmds, infos):
+        """Per-instance statuses of the last plan step -> fallback ladder and diagnostics."""
         cols = self.plan.info_columns  # (B,) record view of infos
         status = cols["status"].astype(np.int32)
         fallback = [""] * self.B

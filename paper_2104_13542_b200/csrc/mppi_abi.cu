@@ -256,10 +256,12 @@ int set_device(mppi_plan* p) {
 // reads it (the inline-state step graph carries the goal in its parameters
 // and does not need it). From pageable memory: the copy has read goal_host
 // when cudaMemcpyAsync returns, so the host may edit it right away.
-int flush_goal(mppi_plan* p) {
+// The copy is queued on the stream the reading work is queued on (`st`, the
+// plan's stream unless the caller passed its own), so it is ordered before it.
+int flush_goal(mppi_plan* p, cudaStream_t st = nullptr) {
   if (!p->goal_dirty) return MPPI_OK;
   CK(cudaMemcpyAsync(p->goal.p, p->goal_host.data(), sizeof(double) * 16 * p->B, cudaMemcpyHostToDevice,
-                     p->stream));
+                     st ? st : p->stream));
   p->goal_dirty = false;
   return MPPI_OK;
 }
@@ -356,7 +358,9 @@ void choose_blocks(int N, int B, int& ppb, int& nblk) {
   }
   ppb = 32;
   if (N > 16 * 32 && N <= 16 * 64) ppb = (N + 15) / 16;
-  if (const char* ev = getenv("MPPI_STATS_PPB")) ppb = std::max(1, atoi(ev));  // A/B
+  // A/B knob, clamped to a layout the plan can launch: [1, min(N, 1024)]
+  // particles per block (statistics shared memory stays < 64 KB at H*D <= 512)
+  if (const char* ev = getenv("MPPI_STATS_PPB")) ppb = std::min(std::max(1, atoi(ev)), std::min(N, 1024));
   nblk = (N + ppb - 1) / ppb;
   if (nblk > kStatsMaxBlocks) {
     nblk = kStatsMaxBlocks;
@@ -1653,8 +1657,8 @@ int mppi_stats_dev(mppi_plan* p, const double* theta, const double* theta_dot, v
   if (p->B != 1) return fail(MPPI_E_CONFIG, "particle sharding is for single-instance plans");
   if (p->learned() && !p->mlp_ready) return fail(MPPI_E_CONFIG, "learned provider without weights");
   CKR(set_device(p));
-  CKR(flush_goal(p));
   cudaStream_t st = stream ? (cudaStream_t)stream : p->stream;
+  CKR(flush_goal(p, st));
   const int D = p->D, it = p->sharded_iter;
   if (it == 0) {
     if (!theta || !theta_dot) return fail(MPPI_E_BAD_ARGUMENT, "state missing");

@@ -28,11 +28,27 @@ inline size_t stats_smem_bytes(int ppb, int nblk, int HD) {
          sizeof(int) * ((size_t)ppb + 2);
 }
 
-// stats_multi_kernel: G instances per block (MPPI_STATS_G=1 selects stats_kernel)
+// stats_multi_kernel: G instances per block. MPPI_STATS_G in {1, 2, 4}
+// (1 selects stats_kernel) and MPPI_STATS_MINBLOCKS in {0, 5} (0: the
+// compiler's register count) override the default variant below.
 // A/B at 4096 x 500 (update stage): 1.66 ms (G=1) -> 0.89 (G=2) / 0.98 (G=4);
 // with the discount hoisted, same box: 0.79 (G=2, 72 registers, 3 blocks/SM)
-// -> 0.70 (G=2 at 5 blocks/SM, code 22) / 0.96 (16 loads in flight) / 0.88 (G=4)
-constexpr int kStatsMultiG = 22;
+// -> 0.70 (G=2 at >= 5 blocks/SM, 48 registers) / 0.96 (16 loads in flight) / 0.88 (G=4)
+struct StatsMultiVariant {
+  int g;           // instances per block: 1 (stats_kernel), 2 or 4
+  int min_blocks;  // __launch_bounds__ minimum blocks per SM: 0 (none) or 5
+};
+constexpr StatsMultiVariant kStatsMultiDefault = {2, 5};
+inline StatsMultiVariant stats_multi_variant() {
+  StatsMultiVariant v = kStatsMultiDefault;
+  if (const char* ev = getenv("MPPI_STATS_G")) {
+    const int g = atoi(ev);
+    if (g == 1 || g == 2 || g == 4) v.g = g;
+  }
+  if (const char* ev = getenv("MPPI_STATS_MINBLOCKS")) v.min_blocks = atoi(ev) == 5 ? 5 : 0;
+  if (v.g == 4) v.min_blocks = 0;  // only G=2 has the occupancy build
+  return v;
+}
 inline size_t stats_multi_smem_bytes(int G, int N, int HD) {
   return sizeof(double) * (2 * (size_t)G * N + (size_t)G * (kRecHead + 2 * HD) + HD) + sizeof(int) * (size_t)N;
 }
@@ -100,21 +116,19 @@ cudaError_t launch_stats_d(const StatsArgs<R>& s, cudaStream_t st) {
   // in-kernel, nothing dumped -> several instances per block share eps reads
   if (s.nblk == 1 && s.ppb == s.N && s.B >= 148 && !s.totals_only && s.finalize_inline && !s.peer_recv &&
       !s.dump_step && !s.dump_terms && !s.dump_weights && !s.dbg && s.H * D <= kStatsThreads) {
-    const char* ev = getenv("MPPI_STATS_G");
-    const int g = ev ? atoi(ev) : kStatsMultiG;
-    // 22 = G 2 at >= 5 blocks per SM (48 registers), 2 = G 2 at the compiler's 72
-    if (g == 2 || g == 4 || g == 22) {
-      const size_t smem = stats_multi_smem_bytes(g == 4 ? 4 : 2, s.N, s.H * D);
+    const StatsMultiVariant v = stats_multi_variant();
+    if (v.g != 1) {
+      const size_t smem = stats_multi_smem_bytes(v.g, s.N, s.H * D);
       if (smem <= 200 * 1024) {
-        auto kern = g == 2 ? stats_multi_kernel<R, D, 2>
-                    : g == 4 ? stats_multi_kernel<R, D, 4>
-                    : stats_multi_kernel<R, D, 2, 8, 5>;
+        auto kern = v.g == 4            ? stats_multi_kernel<R, D, 4>
+                    : v.min_blocks == 5 ? stats_multi_kernel<R, D, 2, 8, 5>
+                                        : stats_multi_kernel<R, D, 2>;
         if (smem > 48 * 1024) {
           cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
           if (e != cudaSuccess) return e;
         }
         cudaLaunchConfig_t cfg = {};
-        cfg.gridDim = dim3((s.B + (g == 4 ? 4 : 2) - 1) / (g == 4 ? 4 : 2), 1, 1);
+        cfg.gridDim = dim3((s.B + v.g - 1) / v.g, 1, 1);
         cfg.blockDim = dim3(kStatsThreads, 1, 1);
         cfg.dynamicSmemBytes = smem;
         cfg.stream = st;

@@ -177,27 +177,37 @@ def test_peer_exchange_step_matches_allgather_path():
             np.testing.assert_allclose(cmd_p, cmd_ref, atol=1e-9 if precision == N.FP64 else 1e-3)
 
 
+# statistics variants: (MPPI_STATS_G, MPPI_STATS_MINBLOCKS); ("2", "5") is the default
+_STATS_VARIANTS = (("1", "0"), ("2", "0"), ("4", "0"), ("2", "5"))
+
+
+def _batched_c2(B, n, precision):
+    from paper_2104_13542_b200 import configs
+    from paper_2104_13542_b200.batched import BatchedController
+    from paper_2104_13542_b200.kinematics import load_chain
+    from paper_2104_13542_b200.surrogate import load_arm7_surrogate
+
+    goals, th0 = configs.batched_problem(B)
+    kw = dict(configs.CONTROLLER_KW)
+    kw.pop("seed")
+    kw["particles"] = n
+    bc = BatchedController(load_chain("arm7.chain"), goals, weights=configs.make_weights(2),
+                           self_collision=load_arm7_surrogate(), precision=precision, **kw)
+    return bc, th0
+
+
 @pytest.mark.parametrize("precision", ["fp64", "fp32"])
 def test_multi_instance_statistics_bit_identical(precision, monkeypatch):
     """stats_multi_kernel (G instances per block sharing the perturbation
     loads; mppi_kernels.cuh) against stats_kernel with one block per instance
     (MPPI_STATS_G=1): identical commands, policies, best and mean costs over
     several steps, with a ragged last block (150 = 37 x 4 + 2, 75 x 2)."""
-    from paper_2104_13542_b200 import configs
-    from paper_2104_13542_b200.batched import BatchedController
-    from paper_2104_13542_b200.kinematics import load_chain
-    from paper_2104_13542_b200.surrogate import load_arm7_surrogate
-
     B, n = 150, 128
-    goals, th0 = configs.batched_problem(B)
-    kw = dict(configs.CONTROLLER_KW)
-    kw.pop("seed")
-    kw["particles"] = n
     runs = {}
-    for g in ("1", "2", "4", "22"):  # 22: the default, two instances at 5 blocks per SM
+    for g, mb in _STATS_VARIANTS:
         monkeypatch.setenv("MPPI_STATS_G", g)  # read when the step is launched / captured
-        bc = BatchedController(load_chain("arm7.chain"), goals, weights=configs.make_weights(2),
-                               self_collision=load_arm7_surrogate(), precision=precision, **kw)
+        monkeypatch.setenv("MPPI_STATS_MINBLOCKS", mb)
+        bc, th0 = _batched_c2(B, n, precision)
         th, thd = th0.copy(), np.zeros_like(th0)
         out = []
         for step in range(3):
@@ -206,8 +216,109 @@ def test_multi_instance_statistics_bit_identical(precision, monkeypatch):
             out.append((cmds.copy(), diag.best_cost.copy(), diag.mean_cost.copy()))
         out.append(tuple(np.stack([getattr(bc.policy(b), f) for b in range(B)])
                          for f in ("means", "variances")))
-        runs[g] = out
-    for g in ("2", "4", "22"):
-        for a, b in zip(runs["1"], runs[g]):
+        runs[(g, mb)] = out
+    for v in _STATS_VARIANTS[1:]:
+        for a, b in zip(runs[_STATS_VARIANTS[0]], runs[v]):
             for x, y in zip(a, b):
-                np.testing.assert_array_equal(x, y, err_msg=f"G={g}")
+                np.testing.assert_array_equal(x, y, err_msg=f"variant {v}")
+
+
+@pytest.mark.parametrize("precision", ["fp64", "fp32"])
+def test_multi_instance_statistics_failing_instances(precision, monkeypatch):
+    """Failure paths of the multi-instance statistics: instances
+    whose every rollout is non-finite (state poisoned below the host check)
+    must report PolicyStateError's status, keep their policy, and leave their
+    block neighbours untouched. Failing instances sit in the first and the
+    second half of a G=2 pair (10, 13), in a G=4 block's middle (41) and in
+    the ragged last block (149 of 150 = 37 x 4 + 2). Every variant must agree
+    with one block per instance bit for bit, over a failing and a healthy step,
+    and the BatchedController fallback ladder must reissue then brake."""
+    from paper_2104_13542_b200 import _native as N
+
+    B, n = 150, 128
+    bad = [10, 13, 41, 149]
+    runs = {}
+    for g, mb in _STATS_VARIANTS:
+        monkeypatch.setenv("MPPI_STATS_G", g)
+        monkeypatch.setenv("MPPI_STATS_MINBLOCKS", mb)
+        bc, th0 = _batched_c2(B, n, precision)
+        thd = np.zeros_like(th0)
+        cmds0, d0 = bc.control_step(th0, thd)  # healthy: arms the reissue command
+        m_before = np.stack([bc.policy(b).means for b in range(B)])
+        poisoned = th0.copy()
+        poisoned[bad, 2] = np.nan
+        cmds, infos = bc.plan.step(poisoned, thd)  # below the host finiteness check
+        status = bc.plan.info_columns["status"].astype(np.int32).copy()
+        m_after = np.stack([bc.policy(b).means for b in range(B)])
+        cmds2, d2 = bc.control_step(th0 + 0.01, thd)  # all healthy again
+        runs[(g, mb)] = (status, cmds, m_after, cmds2, d2.best_cost.copy(), d2.mean_cost.copy())
+        expect = np.zeros(B, np.int32)
+        expect[bad] = N.E_ALL_QUARANTINED
+        np.testing.assert_array_equal(status, expect, err_msg=f"variant {(g, mb)}")
+        ok = np.setdiff1d(np.arange(B), bad)
+        assert np.isfinite(cmds[ok]).all()
+        # a failed instance's policy is the shifted warm start, not an update
+        # from non-finite rollouts: finite and equal to the pre-step policy moved one step
+        assert np.isfinite(m_after[bad]).all()
+        np.testing.assert_array_equal(m_after[bad][:, :-1], m_before[bad][:, 1:])
+        assert (d2.status == 0).all()
+    for v in _STATS_VARIANTS[1:]:
+        for x, y in zip(runs[_STATS_VARIANTS[0]], runs[v]):
+            np.testing.assert_array_equal(x, y, err_msg=f"variant {v}")
+
+    # the host ladder on top of per-instance statuses (controller.py:224-241)
+    bc, th0 = _batched_c2(B, n, precision)
+    thd = np.zeros_like(th0)
+    c0, _ = bc.control_step(th0, thd)
+    for expect_fb in ("reissue", "brake"):
+        poisoned = th0.copy()
+        poisoned[bad, 2] = np.nan
+        # the host check in control_step raises for the whole batch before the
+        # device sees the state: step the plan directly, then apply the ladder
+        cmds, diag = bc._apply_ladder(*bc.plan.step(poisoned, thd))
+        for b in bad:
+            assert diag.fallback[b] == expect_fb, (b, diag.fallback[b])
+            if expect_fb == "reissue":
+                np.testing.assert_array_equal(cmds[b], c0[b])
+            else:
+                assert (cmds[b] == 0).all()
+        assert all(diag.fallback[b] == "" for b in range(B) if b not in bad)
+
+
+def test_sharded_goal_change_on_caller_stream():
+    """the lazily uploaded goal must be ordered before the
+    statistics work queued on the CALLER's stream (ShardedController passes
+    torch's current stream, not the plan's). A one-rank shard stepped on a
+    side stream, with the goal changed before every step, must track the
+    unsharded controller that sees the same goals."""
+    import torch
+
+    from paper_2104_13542_b200 import configs
+    from paper_2104_13542_b200 import _native as N
+    from paper_2104_13542_b200.costs import FULL_POSE, GoalSpec
+    from paper_2104_13542_b200.engine import Plan, PlanSpec
+    from paper_2104_13542_b200.kinematics import Pose, load_chain
+
+    n = 600
+    ref = configs.make_controller(1, particles=n, precision="fp64")
+    chain = load_chain("arm7.chain")
+    spec = PlanSpec(horizon=30, particles=n, dts=ref.sched.dts, null_count=2, precision=N.FP64,
+                    particle_offset=0, particles_total=n, gamma=0.99, beta=1.0, alpha_mu=0.9,
+                    alpha_sigma=0.5, sigma0_sq=0.5, sigma_sq_min=0.01, sigma_sq_max=0.5, knots=5)
+    p = Plan(chain, configs.make_weights(1), spec)
+    p.init_noise()
+    rec = torch.zeros(p.record_len(), dtype=torch.float64, device="cuda:0")
+    side = torch.cuda.Stream(device="cuda:0")
+    st = configs.start_state()
+    goals, _ = configs.batched_problem(4)
+    for step, g in enumerate(goals):
+        goal = GoalSpec(target_pose=Pose(rotation=g.target_pose.rotation, translation=g.target_pose.translation),
+                        mode=FULL_POSE)
+        ref.set_goal(goal)
+        p.set_goal(goal.target_pose.rotation, goal.target_pose.translation, goal.mode_code, 0)
+        cmd_ref, _ = ref.control_step(st)
+        with torch.cuda.stream(side):
+            p.stats_dev(st.theta, st.theta_dot, rec.data_ptr(), side.cuda_stream)
+            cmd, info = p.finalize_dev(rec.data_ptr(), 1, side.cuda_stream)
+        assert info.status == 0
+        np.testing.assert_allclose(cmd, cmd_ref, atol=1e-9, err_msg=f"step {step}")
