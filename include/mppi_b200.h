@@ -287,6 +287,16 @@ int mppi_evaluate(mppi_plan* plan, int32_t mode, int32_t n, int32_t horizon,
                   const double* theta0, const double* theta_dot0,
                   const double* controls, const double* controls2, mppi_eval_out* out);
 
+/* The inputs of the last iteration of the last mppi_step for one instance:
+ * the joint state it started from and the (shifted) policy view its controls
+ * were built from, u = means + stddev * eps (sampling.py:268-290). Replaying
+ * them through mppi_evaluate (mode 0) reproduces that iteration's
+ * RolloutBundle on a lean plan (dump = 0): Controller's lazily built
+ * StepDiagnostics.bundle (controller.py:250-259).                            */
+int mppi_get_step_inputs(mppi_plan* plan, int32_t instance, double* theta /* (d,) */,
+                         double* theta_dot /* (d,) */, double* means /* (H,d) */,
+                         double* stddev /* (H,d) */);
+
 /* Instance 0's RolloutBundle of the last iteration of the last mppi_step
  * (plan created with dump = 1), plus the particle weights (N,). */
 int mppi_get_bundle(mppi_plan* plan, mppi_eval_out* out, double* weights);
@@ -494,6 +504,27 @@ int mppi_env_collision_batch(const double* rot, const double* trans, int64_t m, 
 int mppi_integrate_batch(const double* u, int64_t n, int32_t h, int32_t d, const double* dts,
                          const double* th0, const double* thd0, double* pos_out,
                          double* vel_out);
+
+/* ---- cost-term free functions (costs.py:76-133) ---------------------------
+ * float64, stateless, caller-owned outputs, like the seam above. They replace
+ * the reference's numpy bodies of the same names; the fused rollout computes
+ * the same terms in-register and does not call these.                       */
+/* pose_cost (costs.py:76-95): ||alpha_trans . R_g^T (t_ee - t_g)||_2, plus
+ * ||diag(alpha_rot) (I - R_g^T R_ee)||_F unless mode = MPPI_GOAL_POSITION_ONLY */
+int mppi_pose_cost(const double* rot_ee /* (m,3,3) */, const double* trans_ee /* (m,3) */, int64_t m,
+                   const double* goal_rot /* (3,3) */, const double* goal_trans /* (3,) */, int32_t mode,
+                   const double* alpha_rot /* (3,) */, const double* alpha_trans /* (3,) */,
+                   double* out /* (m,) */);
+/* stop_cost (costs.py:104-108): ||max(|v| - limits[h], 0)||_2 over joints;
+ * limits = braking_limits (costs.py:98-101), (h,d)                          */
+int mppi_stop_cost(const double* vel /* (n,h,d) */, int64_t n, int32_t h, int32_t d,
+                   const double* limits /* (h,d) */, double* out /* (n,h) */);
+/* joint_limit_cost (costs.py:118-123) against shrunken limits lo/hi (d,)   */
+int mppi_joint_limit_cost(const double* pos /* (m,d) */, int64_t m, int32_t d, const double* lo,
+                          const double* hi, double* out /* (m,) */);
+/* manipulability_cost_from_values (costs.py:126-127): 1 - m if m < k_m else 0 */
+int mppi_manipulability_cost(const double* manip /* (m,) */, int64_t m, double k_m,
+                             double* out /* (m,) */);
 
 #ifdef __cplusplus
 }

@@ -324,6 +324,32 @@ def first_obstacle_hit(rot, trans, chain, spheres, boxes) -> np.ndarray:
     return hit
 
 
+def obstacle_margin(rot, trans, chain, spheres, boxes) -> np.ndarray:
+    """Signed clearance behind first_obstacle_hit's decision (jit.py:289-332):
+    min over capsules and obstacles of (segment distance - contact radius);
+    the reference reports a hit exactly when this is < 0 (strict). +inf with
+    no capsules or no obstacles. Test infrastructure for the SURVEY §8(c)
+    decision band: entries with |margin| < band may take either branch."""
+    M = rot.shape[0]
+    out = np.full(M, np.inf)
+    if len(chain.cap_r) == 0 or (len(spheres) == 0 and len(boxes) == 0):
+        return out
+    P0, P1 = _capsules_world(rot, trans, chain)
+    d = P1 - P0
+    dd = (d * d).sum(-1)
+    for sph in spheres:
+        with np.errstate(divide="ignore", invalid="ignore"):
+            t = np.where(dd <= SEG_EPS, 0.0,
+                         np.minimum(np.maximum(((sph[:3] - P0) * d).sum(-1) / dd, 0.0), 1.0))
+        close = P0 + t[..., None] * d - sph[:3]
+        gap = np.sqrt((close * close).sum(-1)) - (chain.cap_r[None] + sph[3])
+        out = np.minimum(out, gap.min(axis=1))
+    for box in boxes:
+        gap = segment_box_distance(P0, P1, box[:3], box[3:]) - chain.cap_r[None]
+        out = np.minimum(out, gap.min(axis=1))
+    return out
+
+
 # ============================================================== costs
 TERMS = ("pose", "stop", "joint", "manip", "selfcoll", "envcoll")
 
@@ -351,10 +377,14 @@ def mlp_distance(q, state: dict) -> np.ndarray:
 
 
 def cost_terms(pos, vel, dts, chain, weights, goal_R, goal_t, full_pose: bool, provider=None,
-               mlp_state=None, spheres=None, boxes=None):
+               mlp_state=None, spheres=None, boxes=None, decisions=None):
     """CostStack.evaluate (costs.py:209-242): returns (step (n,H), terms dict).
 
     provider: None | "oracle" | "learned" (mlp_state holds W0..W3, b0..b3).
+    decisions: optional dict, filled with the margins of the two discontinuous
+    branches (SURVEY §8(c) decision bands): "manip" = m - k_m (the cost jumps
+    where it crosses 0, costs.py:126-127) and "env" = obstacle_margin (hit iff
+    < 0), both (n,H); +inf where the term is off.
     """
     n, H, d = pos.shape
     flat = pos.reshape(-1, d)
@@ -376,6 +406,8 @@ def cost_terms(pos, vel, dts, chain, weights, goal_R, goal_t, full_pose: bool, p
     if weights.alpha_manip > 0.0:
         m = manipulability(geometric_jacobian(rot, trans, chain), chain.task_dim).reshape(n, H)
         terms["manip"] = np.where(m < weights.k_m, 1.0 - m, 0.0)
+        if decisions is not None:
+            decisions["manip"] = m - weights.k_m
     if weights.alpha_coll > 0.0 and provider == "oracle":
         terms["selfcoll"] = np.maximum(capsule_self_collision(rot, trans, chain), 0.0).reshape(n, H)
     elif weights.alpha_coll > 0.0 and provider == "learned":
@@ -385,6 +417,11 @@ def cost_terms(pos, vel, dts, chain, weights, goal_R, goal_t, full_pose: bool, p
         sp = np.zeros((0, 4)) if spheres is None else spheres
         bx = np.zeros((0, 6)) if boxes is None else boxes
         terms["envcoll"] = (first_obstacle_hit(rot, trans, chain, sp, bx) >= 0).astype(float).reshape(n, H)
+        if decisions is not None:
+            decisions["env"] = obstacle_margin(rot, trans, chain, sp, bx).reshape(n, H)
+    if decisions is not None:
+        for k in ("manip", "env"):
+            decisions.setdefault(k, np.full((n, H), np.inf))
     step = (terms["pose"] + weights.alpha_stop * terms["stop"] + weights.alpha_joint * terms["joint"]
             + weights.alpha_manip * terms["manip"]
             + weights.alpha_coll * (terms["selfcoll"] + terms["envcoll"]))
@@ -399,19 +436,43 @@ def discounted(step, gamma: float, terminal_weight: float) -> np.ndarray:
 
 
 def rollout_scores(th0, thd0, u, dts, chain, weights, goal_R, goal_t, full_pose, gamma, terminal_weight,
-                   **kw):
-    """evaluate_rollouts (rollout.py:124-180) incl. quarantine of non-finite rows."""
+                   chunk=None, keep=None, **kw):
+    """evaluate_rollouts (rollout.py:124-180) incl. quarantine of non-finite rows.
+
+    chunk: evaluate `chunk` particles at a time (the reference's own per-slice
+    evaluation, rollout.py:149-162, is what makes this exact: rows are
+    independent) so N >= 65k fits in memory (SURVEY §8(c) "Scale limits").
+    keep: names of the per-row outputs to keep (default all); with "decisions"
+    the branch margins of cost_terms are returned as well.
+    """
     if not np.isfinite(u).all():
         bad = int(np.flatnonzero(~np.isfinite(u).all(axis=(1, 2)))[0])
         raise ValueError(f"non-finite control in particle {bad}")
-    pos, vel = euler(u, dts, th0, thd0)
-    step, terms = cost_terms(pos, vel, dts, chain, weights, goal_R, goal_t, full_pose, **kw)
-    ok = np.isfinite(step).all(axis=1)
-    step = np.where(ok[:, None], step, 0.0)
-    totals = discounted(step, gamma, terminal_weight)
-    totals[~ok] = np.inf
-    return dict(positions=pos, velocities=vel, accelerations=u, step_costs=step, terms=terms,
-                totals=totals)
+    keep = set(keep or ("positions", "velocities", "accelerations", "step_costs", "terms"))
+    n = u.shape[0]
+    chunk = n if not chunk else int(chunk)
+    parts = []
+    for a in range(0, n, chunk):
+        uc = u[a:a + chunk]
+        pos, vel = euler(uc, dts, th0, thd0)
+        dec = {} if "decisions" in keep else None
+        step, terms = cost_terms(pos, vel, dts, chain, weights, goal_R, goal_t, full_pose, decisions=dec, **kw)
+        ok = np.isfinite(step).all(axis=1)
+        step = np.where(ok[:, None], step, 0.0)
+        totals = discounted(step, gamma, terminal_weight)
+        totals[~ok] = np.inf
+        rec = dict(positions=pos, velocities=vel, accelerations=uc, step_costs=step, terms=terms,
+                   totals=totals, decisions=dec)
+        parts.append({k: v for k, v in rec.items() if k in keep or k == "totals"})
+    if len(parts) == 1:
+        return parts[0]
+    out = {}
+    for k in parts[0]:
+        if isinstance(parts[0][k], dict):
+            out[k] = {t: np.concatenate([p[k][t] for p in parts]) for t in parts[0][k]}
+        else:
+            out[k] = np.concatenate([p[k] for p in parts])
+    return out
 
 
 # ============================================================== policy update
@@ -495,7 +556,8 @@ class OracleController:
                  dt_base=0.05, dt_ramp="two_phase", gamma=0.99, terminal_weight=1.0, null_count=2,
                  beta=0.5, alpha_mu=0.9, alpha_sigma=0.5, sigma0_sq=1.0, sigma_sq_min=1e-4,
                  sigma_sq_max=0.0, isotropic=False, iterations=1, provider=None, mlp_state=None,
-                 spheres=None, boxes=None, smoothing="bspline", degree=3, knots=0, eps_source=None):
+                 spheres=None, boxes=None, smoothing="bspline", degree=3, knots=0, eps_source=None,
+                 chunk=None, keep=None):
         self.chain, self.weights = chain, weights
         self.goal_R, self.goal_t, self.full_pose = np.asarray(goal_R, float), np.asarray(goal_t, float), full_pose
         self.H, self.N, self.null = horizon, particles, null_count
@@ -515,6 +577,7 @@ class OracleController:
             block = fixed_halton_block(particles, horizon, d, smoothing, degree, knots)
             eps_source = lambda: block  # noqa: E731
         self.eps_source = eps_source
+        self.chunk, self.keep = chunk, keep  # chunked evaluation for N >= 65k (rollout_scores)
         self.last = None
 
     def step(self, theta, theta_dot):
@@ -523,7 +586,9 @@ class OracleController:
             eps = self.eps_source()
             u = shape_controls(eps, self.means, self.variances, self.null)
             res = rollout_scores(theta, theta_dot, u, self.dts, self.chain, self.weights, self.goal_R,
-                                 self.goal_t, self.full_pose, self.gamma, self.tw, **self.kw)
+                                 self.goal_t, self.full_pose, self.gamma, self.tw, chunk=self.chunk,
+                                 keep=self.keep, **self.kw)
+            res["controls"] = u
             w = weights_from_totals(res["totals"], self.beta)
             self.means, self.variances = blend_policy(self.means, self.variances, u, w, self.alpha_mu,
                                                       self.alpha_sigma, self.smin, self.smax, self.iso)

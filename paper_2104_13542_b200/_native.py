@@ -168,6 +168,7 @@ _SIGS = {
     "mppi_evaluate": (C.c_int, [_vp, C.c_int32, C.c_int32, C.c_int32, _dp, C.c_double, C.c_double,
                                 _dp, _dp, _dp, _dp, C.POINTER(EvalOut)]),
     "mppi_get_bundle": (C.c_int, [_vp, C.POINTER(EvalOut), _dp]),
+    "mppi_get_step_inputs": (C.c_int, [_vp, C.c_int32, _dp, _dp, _dp, _dp]),
     "mppi_episode": (C.c_int, [_vp, C.POINTER(EpisodeDesc), _dp, _dp, C.POINTER(EpisodeState),
                                C.POINTER(EpisodeLogC), _ip, _dp]),
     "mppi_top_rollouts": (C.c_int, [_vp, C.c_int32, _ip, _dp, _dp]),
@@ -203,6 +204,10 @@ _SIGS = {
                                            C.c_int32, _dp, C.c_int32, _dp, C.c_int32, _lp]),
     "mppi_integrate_batch": (C.c_int, [_dp, C.c_int64, C.c_int32, C.c_int32, _dp, _dp, _dp, _dp,
                                        _dp]),
+    "mppi_pose_cost": (C.c_int, [_dp, _dp, C.c_int64, _dp, _dp, C.c_int32, _dp, _dp, _dp]),
+    "mppi_stop_cost": (C.c_int, [_dp, C.c_int64, C.c_int32, C.c_int32, _dp, _dp]),
+    "mppi_joint_limit_cost": (C.c_int, [_dp, C.c_int64, C.c_int32, _dp, _dp, _dp]),
+    "mppi_manipulability_cost": (C.c_int, [_dp, C.c_int64, C.c_double, _dp]),
 }
 
 EXPORTED = tuple(_SIGS)

@@ -28,7 +28,7 @@ OBJ = ROOT / "build" / (f"obj-{TAG}" if TAG else "obj")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
          f"-I{ROOT / 'include'}"] + os.environ.get("MPPI_NVCC_FLAGS", "").split()
-SOURCES = ["mppi_abi.cu", "mppi_launch_f32.cu", "mppi_launch_f64.cu", "mppi_train.cu"]
+SOURCES = ["mppi_abi.cu", "mppi_seam.cu", "mppi_launch_f32.cu", "mppi_launch_f64.cu", "mppi_train.cu"]
 
 
 def nvcc() -> str:

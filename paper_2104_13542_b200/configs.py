@@ -87,13 +87,18 @@ def batched_problem(instances: int, first: int = 0, chain=None):
     return goals, th0
 
 
-def tracking_problem(seed: int = 0, n_boxes: int = 8, dims: int = 64):
+def tracking_problem(seed: int = 0, n_boxes: int = 8, dims: int = 64, fk=None):
     """Config 3: moving target (TargetScript, linear, 5 waypoints = FK of seeded
     in-limit q, one every 3 s, position_only) and a 64^3 grid over [-1,1]^3
     built from 8 seeded voxel-aligned boxes that do not touch the start pose's
-    capsules."""
-    from .kinematics import fk_batch, load_chain
+    capsules (SURVEY §8(d)). ``fk(chain, q)`` defaults to the device seam;
+    tests/golden/make_golden.py passes the reference's own FK."""
+    from .kinematics import load_chain
     from .simworld import TargetScript, seeded_box_grid
+
+    if fk is None:
+        from .kinematics import fk_batch as fk
+    fk_batch = fk
 
     chain = load_chain("arm7.chain")
     rng = np.random.default_rng(seed)

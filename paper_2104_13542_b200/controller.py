@@ -13,8 +13,12 @@ allows it.
 
 Differences from the reference, by design:
   * ``workers`` is accepted and ignored (particles map to warps, not threads);
-  * ``diag.bundle`` is a lazily fetched view of the last iteration's device
-    dump (pass ``keep_bundle=True`` to have the graph write it);
+  * ``diag.bundle`` is always set, as in the reference (controller.py:250-259),
+    but lazily: with ``keep_bundle=True`` the step graph dumps the last
+    iteration and the bundle reads that dump back; by default (the lean
+    latency graph) first access replays the last iteration on the device from
+    its recorded inputs (state, policy view, perturbations) — one evaluation
+    pass, paid only by callers that read the bundle;
   * per-stage times are device event times (event-record nodes in the step graph).
 """
 
@@ -208,6 +212,7 @@ class Controller:
     def set_goal(self, goal: GoalSpec):
         self.cost_stack.goal = goal
         self._sync_goal()
+        self._step_serial += 1  # a replayed bundle would see the new goal: expire it
 
     def set_perturbations(self, eps):
         """Overwrite the device perturbation block (the parity hook for
@@ -269,7 +274,7 @@ class Controller:
         latency = (time.perf_counter() - t_start) * 1e3
         if latency > self.latency_budget * 1e3:
             log.debug("control step overran budget: %.2f ms", latency)
-        bundle = LazyBundle(self, self._step_serial) if self.keep_bundle else None
+        bundle = LazyBundle(self, self._step_serial)
         # without profile_stages() the whole fused step is reported as rollout time
         roll = info.rollout_ms + info.mlp_ms
         # positional: latency, sample, rollout, update, best, mean, fallback, bundle
@@ -302,7 +307,9 @@ class Controller:
 
 class LazyBundle:
     """RolloutBundle of the last iteration of one step, fetched from the device
-    on first attribute access. Valid until the controller's next step."""
+    on first attribute access (the graph's dump with keep_bundle=True, else a
+    device replay of that iteration). Valid until the controller's next step
+    or goal change."""
 
     _FIELDS = ("positions", "velocities", "accelerations", "step_costs", "term_breakdown",
                "total_per_particle", "weights")
@@ -316,7 +323,13 @@ class LazyBundle:
         if self._data is None:
             if self._ctrl._step_serial != self._serial:
                 raise ContractError("bundle expired: the controller has stepped since")
-            self._data = self._ctrl._plan.get_bundle()
+            c = self._ctrl
+            if c.keep_bundle:
+                self._data = c._plan.get_bundle()
+            else:
+                cfg = c.update_cfg
+                self._data = c._plan.replay_bundle(c.sched.dts, cfg.gamma, c.terminal_weight, cfg.beta,
+                                                   c.null_count)
         return self._data
 
     def __getattr__(self, name):

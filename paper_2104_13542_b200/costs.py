@@ -76,6 +76,103 @@ def goal_at_position(position, mode: str = POSITION_ONLY) -> GoalSpec:
     return GoalSpec(target_pose=Pose(rotation=np.eye(3), translation=p), mode=mode)
 
 
+# ---------------------------------------------------------------- cost-term free functions
+# The reference's per-term functions (costs.py:76-173), same signatures and
+# broadcasting; the per-state arithmetic runs in the float64 cost-term kernels
+# of the native library (csrc/mppi_seam.cu). braking_limits and
+# shrunken_limits are O(H*d) configuration constants and stay on the host, as
+# the plan builder computes them.
+
+def pose_cost(rot_ee, trans_ee, goal: GoalSpec, alpha_rot, alpha_trans) -> np.ndarray:
+    """Weighted pose distance for (..., 3, 3)/(..., 3) end-effector poses
+    (costs.py:76-95): translation residual in the goal frame, plus the
+    row-weighted Frobenius norm of I - R_g^T R_ee unless position_only."""
+    trans_ee = N.f64(trans_ee)
+    lead = trans_ee.shape[:-1]
+    if trans_ee.shape[-1:] != (3,):
+        raise ContractError("end-effector translations must be (..., 3)")
+    m = int(np.prod(lead, dtype=np.int64))
+    full = goal.mode != POSITION_ONLY
+    rot = N.f64(rot_ee).reshape(m, 3, 3) if full else None
+    out = np.empty(m)
+    N.check(kernels._lib().mppi_pose_cost(
+        N.dptr(rot), N.dptr(trans_ee.reshape(m, 3)), m, N.dptr(N.f64(goal.target_pose.rotation, (3, 3))),
+        N.dptr(N.f64(goal.target_pose.translation, (3,))), N.GOAL_FULL_POSE if full else N.GOAL_POSITION_ONLY,
+        N.dptr(np.broadcast_to(N.f64(alpha_rot), (3,)).copy()),
+        N.dptr(np.broadcast_to(N.f64(alpha_trans), (3,)).copy()), N.dptr(out)))
+    return out.reshape(lead)
+
+
+def braking_limits(accel_max: np.ndarray, sched) -> np.ndarray:
+    """(H, d) speeds still stoppable at maximum deceleration over the rest of
+    the horizon (costs.py:98-101): suffix sums of dt times accel_max."""
+    remaining = np.cumsum(np.asarray(sched.dts, dtype=np.float64)[::-1])[::-1]
+    return np.multiply.outer(remaining, np.asarray(accel_max, dtype=np.float64))
+
+
+def stop_cost(velocities: np.ndarray, accel_max: np.ndarray, sched) -> np.ndarray:
+    """||max(|v| - braking limit, 0)||_2 per state (costs.py:104-108);
+    velocities (..., H, d) -> (..., H)."""
+    limits = N.f64(braking_limits(accel_max, sched))
+    vel = N.f64(velocities)
+    H, d = limits.shape
+    if vel.shape[-2:] != (H, d):
+        raise ContractError(f"velocities must be (..., {H}, {d}), got {vel.shape}")
+    lead = vel.shape[:-2] if vel.ndim > 2 else (1,)  # (H, d) broadcasts to one batch row
+    n = int(np.prod(lead, dtype=np.int64))
+    out = np.empty((n, H))
+    N.check(kernels._lib().mppi_stop_cost(N.dptr(vel.reshape(n, H, d)), n, H, d, N.dptr(limits), N.dptr(out)))
+    return out.reshape(*lead, H)
+
+
+def shrunken_limits(chain: KinematicChain, k_jl: float):
+    """Joint range pulled in by k_jl of its span at both ends (costs.py:111-115)."""
+    lo, hi = chain.joint_limits[:, 0], chain.joint_limits[:, 1]
+    margin = k_jl * (hi - lo)
+    return lo + margin, hi - margin
+
+
+def joint_limit_cost(positions: np.ndarray, chain: KinematicChain, k_jl: float) -> np.ndarray:
+    """Euclidean depth outside the shrunken limits (costs.py:118-123); (..., d) -> (...)."""
+    lo, hi = shrunken_limits(chain, k_jl)
+    pos = N.f64(positions)
+    d = chain.dof
+    if pos.shape[-1] != d:
+        raise ContractError(f"expected {d} joint values, got shape {pos.shape}")
+    lead = pos.shape[:-1]
+    m = int(np.prod(lead, dtype=np.int64))
+    out = np.empty(m)
+    N.check(kernels._lib().mppi_joint_limit_cost(N.dptr(pos.reshape(m, d)), m, d, N.dptr(N.f64(lo)),
+                                                 N.dptr(N.f64(hi)), N.dptr(out)))
+    return out.reshape(lead)
+
+
+def manipulability_cost_from_values(manip: np.ndarray, k_m: float) -> np.ndarray:
+    """1 - m below the threshold k_m, else 0 (costs.py:126-127; discontinuous at k_m)."""
+    mv = N.f64(manip)
+    out = np.empty(mv.size)
+    N.check(kernels._lib().mppi_manipulability_cost(N.dptr(mv.reshape(-1)), mv.size, float(k_m), N.dptr(out)))
+    return out.reshape(mv.shape)
+
+
+def manipulability_cost(chain: KinematicChain, q: np.ndarray, k_m: float) -> np.ndarray:
+    """manipulability_cost_from_values of the chain's manipulability at q (costs.py:130-133)."""
+    from .kinematics import manipulability_batch
+
+    return manipulability_cost_from_values(manipulability_batch(chain, q), k_m)
+
+
+def env_collision_cost(rot, trans, chain: KinematicChain, world) -> np.ndarray:
+    """1.0 where any capsule hits an obstacle, else 0.0, for (..., d, 3, 3)/(..., d, 3)
+    link poses (costs.py:164-173; deliberately discrete)."""
+    trans = N.f64(trans)
+    lead = trans.shape[:-2]
+    hit = kernels.env_collision_batch(N.f64(rot).reshape(-1, chain.dof, 3, 3), trans.reshape(-1, chain.dof, 3),
+                                      chain.cap_p0, chain.cap_p1, chain.cap_r, chain.cap_link,
+                                      world.spheres, world.boxes)
+    return (hit >= 0).astype(np.float64).reshape(lead)
+
+
 class OracleSelfCollision:
     """Exact capsule-pair penetration (costs.py:136-156), on the GPU seam."""
 

@@ -16,6 +16,7 @@
 #include <type_traits>
 #include <vector>
 
+#include "mppi_abi_util.cuh"
 #include "mppi_aux_kernels.cuh"
 #include "mppi_launch.cuh"
 #include "mppi_mlp.cuh"
@@ -26,33 +27,7 @@ using namespace mppi;
 // ------------------------------------------------------------------ errors
 static thread_local std::string g_last_error;
 
-static int fail(int code, const std::string& msg) {
-  g_last_error = msg;
-  return code;
-}
-
-#define CK(call)                                                                              \
-  do {                                                                                        \
-    cudaError_t _e = (call);                                                                  \
-    if (_e != cudaSuccess)                                                                    \
-      return fail(MPPI_E_CUDA, std::string(#call " failed: ") + cudaGetErrorString(_e) +       \
-                                   " (" __FILE__ ":" + std::to_string(__LINE__) + ")");       \
-  } while (0)
-
-#define CKR(expr)              \
-  do {                         \
-    int _rc = (expr);          \
-    if (_rc != MPPI_OK) return _rc; \
-  } while (0)
-
 namespace {
-
-inline unsigned grid_for(long long n, int threads, int cap = 148 * 16) {
-  long long g = (n + threads - 1) / threads;
-  if (g < 1) g = 1;
-  if (g > cap) g = cap;
-  return (unsigned)g;
-}
 
 template <typename T>
 struct DevBuf {
@@ -725,7 +700,10 @@ int32_t mppi_abi_version(void) { return MPPI_ABI_VERSION; }
 const char* mppi_last_error(void) { return g_last_error.c_str(); }
 
 // error hand-off from the other translation units (mppi_train.cu); not part of the public header
-int mppi_internal_fail(int code, const char* msg) { return fail(code, msg); }
+int mppi_internal_fail(int code, const char* msg) {
+  g_last_error = msg;
+  return code;
+}
 
 const char* mppi_build_info(void) {
 #define MPPI_STR2(x) #x
@@ -982,6 +960,24 @@ int mppi_set_noise(mppi_plan* p, const double* eps) {
   if (!p || !eps) return fail(MPPI_E_BAD_ARGUMENT, "null argument");
   CKR(set_device(p));
   CK(cudaMemcpyAsync(p->eps.p, eps, sizeof(double) * p->N * p->H * p->D, cudaMemcpyHostToDevice, p->stream));
+  CK(cudaStreamSynchronize(p->stream));
+  return MPPI_OK;
+}
+
+int mppi_get_step_inputs(mppi_plan* p, int32_t inst, double* theta, double* theta_dot, double* means,
+                         double* stddev) {
+  if (!p || !theta || !theta_dot || !means || !stddev) return fail(MPPI_E_BAD_ARGUMENT, "null argument");
+  if (inst < 0 || inst >= p->B) return fail(MPPI_E_BAD_ARGUMENT, "instance out of range");
+  if (p->step_counter == 0) return fail(MPPI_E_CONFIG, "no step has run on this plan");
+  CKR(set_device(p));
+  const int D = p->D, HD = p->H * p->D;
+  CK(cudaStreamSynchronize(p->stream));
+  memcpy(theta, p->h_state + (size_t)inst * 2 * D, sizeof(double) * D);
+  memcpy(theta_dot, p->h_state + (size_t)inst * 2 * D + D, sizeof(double) * D);
+  CK(cudaMemcpyAsync(means, p->prev_means.p + (size_t)inst * HD, sizeof(double) * HD, cudaMemcpyDeviceToHost,
+                     p->stream));
+  CK(cudaMemcpyAsync(stddev, p->prev_sd.p + (size_t)inst * HD, sizeof(double) * HD, cudaMemcpyDeviceToHost,
+                     p->stream));
   CK(cudaStreamSynchronize(p->stream));
   return MPPI_OK;
 }
@@ -1807,164 +1803,7 @@ int mppi_ipc_close(void* dev_ptr) {
   return MPPI_OK;
 }
 
-// ---------------------------------------------------------------- stateless functions
-}  // extern "C"
-namespace {
-struct Scratch {
-  std::vector<void*> ptrs;
-  cudaStream_t st = nullptr;
-  ~Scratch() {
-    for (void* q : ptrs) cudaFree(q);
-    if (st) cudaStreamDestroy(st);
-  }
-  template <typename T>
-  T* dev(size_t n, const T* host = nullptr) {
-    void* q = nullptr;
-    if (cudaMalloc(&q, std::max<size_t>(1, n) * sizeof(T)) != cudaSuccess) return nullptr;
-    ptrs.push_back(q);
-    if (host && n) cudaMemcpyAsync(q, host, n * sizeof(T), cudaMemcpyHostToDevice, st);
-    return (T*)q;
-  }
-  int init() {
-    CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
-    return MPPI_OK;
-  }
-};
-#define SCRATCH_OR_FAIL(S) \
-  Scratch S;               \
-  CKR(S.init())
-#define DEVPTR(S, T, name, n, host)                                 \
-  T* name = S.dev<T>((n), (host));                                  \
-  if (!name) return fail(MPPI_E_CUDA, "cudaMalloc failed (" #name ")")
-}  // namespace
-extern "C" {
-
-int mppi_halton_points(int64_t count, int32_t dims, double* out) {
-  if (count < 1) return fail(MPPI_E_BAD_ARGUMENT, "count must be >= 1");
-  if (dims > 40) return fail(MPPI_E_CONFIG, "halton supports at most 40 dims, got " + std::to_string(dims));
-  SCRATCH_OR_FAIL(S);
-  DEVPTR(S, double, d, (size_t)count * dims, (const double*)nullptr);
-  halton_points_kernel<<<grid_for(count * dims, 256), 256, 0, S.st>>>(d, count, dims);
-  CK(cudaGetLastError());
-  CK(cudaMemcpyAsync(out, d, sizeof(double) * count * dims, cudaMemcpyDeviceToHost, S.st));
-  CK(cudaStreamSynchronize(S.st));
-  return MPPI_OK;
-}
-
-int mppi_gaussianize(const double* p, int64_t n, double* out) {
-  if (n < 0) return fail(MPPI_E_BAD_ARGUMENT, "negative size");
-  if (n == 0) return MPPI_OK;
-  SCRATCH_OR_FAIL(S);
-  DEVPTR(S, double, dp, n, p);
-  DEVPTR(S, double, dout, n, (const double*)nullptr);
-  DEVPTR(S, int, err, 1, (const int*)nullptr);
-  CK(cudaMemsetAsync(err, 0, sizeof(int), S.st));
-  gaussianize_kernel<<<grid_for(n, 256), 256, 0, S.st>>>(dp, n, dout, err);
-  CK(cudaGetLastError());
-  int herr = 0;
-  CK(cudaMemcpyAsync(&herr, err, sizeof(int), cudaMemcpyDeviceToHost, S.st));
-  CK(cudaMemcpyAsync(out, dout, sizeof(double) * n, cudaMemcpyDeviceToHost, S.st));
-  CK(cudaStreamSynchronize(S.st));
-  if (herr) return fail(MPPI_E_BAD_ARGUMENT, "unit samples must lie in [0, 1)");
-  return MPPI_OK;
-}
-
-int mppi_smooth_sequences(const double* knots, int64_t n, int32_t k, int32_t d, int32_t mode,
-                          const double* basis, const double* comb, int32_t horizon, double* out) {
-  if (n < 0 || k < 1 || d < 1 || horizon < 1) return fail(MPPI_E_BAD_ARGUMENT, "bad shape");
-  if (n == 0) return MPPI_OK;
-  if (mode == MPPI_SMOOTH_BSPLINE && !basis) return fail(MPPI_E_BAD_ARGUMENT, "basis missing");
-  if (mode != MPPI_SMOOTH_BSPLINE && k != horizon) return fail(MPPI_E_BAD_ARGUMENT, "K != H");
-  SCRATCH_OR_FAIL(S);
-  DEVPTR(S, double, dz, (size_t)n * k * d, knots);
-  DEVPTR(S, double, db, (size_t)horizon * k, mode == MPPI_SMOOTH_BSPLINE ? basis : nullptr);
-  DEVPTR(S, double, dout, (size_t)n * horizon * d, (const double*)nullptr);
-  const double c1 = comb ? comb[0] : 0.3, c2 = comb ? comb[1] : 0.4, c3 = comb ? comb[2] : 0.3;
-  smooth_kernel<<<grid_for(n * horizon * d, 256), 256, 0, S.st>>>(dz, dout, n, k, horizon, d, mode, db, c1, c2, c3);
-  CK(cudaGetLastError());
-  CK(cudaMemcpyAsync(out, dout, sizeof(double) * n * horizon * d, cudaMemcpyDeviceToHost, S.st));
-  CK(cudaStreamSynchronize(S.st));
-  return MPPI_OK;
-}
-
-int mppi_bspline_basis(int32_t horizon, int32_t k, int32_t degree, double* out) {
-  if (k < degree + 1) return fail(MPPI_E_CONFIG, "bspline of degree " + std::to_string(degree) +
-                                                     " needs at least " + std::to_string(degree + 1) +
-                                                     " control points");
-  if (horizon < 1 || k + degree + 1 > 64 || degree > 15) return fail(MPPI_E_BAD_ARGUMENT, "bad basis shape");
-  SCRATCH_OR_FAIL(S);
-  DEVPTR(S, double, db, (size_t)horizon * k, (const double*)nullptr);
-  bspline_basis_kernel<<<(horizon + 63) / 64, 64, 0, S.st>>>(horizon, k, degree, db);
-  CK(cudaGetLastError());
-  CK(cudaMemcpyAsync(out, db, sizeof(double) * horizon * k, cudaMemcpyDeviceToHost, S.st));
-  CK(cudaStreamSynchronize(S.st));
-  return MPPI_OK;
-}
-
-int mppi_build_controls(const double* eps, const double* means, const double* stddev, int64_t n,
-                        int32_t h, int32_t d, int32_t null_count, double* out) {
-  if (n < 1 || h < 1 || d < 1) return fail(MPPI_E_BAD_ARGUMENT, "bad shape");
-  SCRATCH_OR_FAIL(S);
-  const size_t nhd = (size_t)n * h * d;
-  DEVPTR(S, double, de, nhd, eps);
-  DEVPTR(S, double, dm, (size_t)h * d, means);
-  DEVPTR(S, double, ds, (size_t)h * d, stddev);
-  DEVPTR(S, double, dout, nhd, (const double*)nullptr);
-  DEVPTR(S, int, bad, 1, (const int*)nullptr);
-  CK(cudaMemsetAsync(bad, 0, sizeof(int), S.st));
-  build_controls_kernel<<<grid_for(nhd, 256), 256, 0, S.st>>>(de, dm, ds, n, h, d, null_count, dout, bad);
-  CK(cudaGetLastError());
-  int hb = 0;
-  CK(cudaMemcpyAsync(&hb, bad, sizeof(int), cudaMemcpyDeviceToHost, S.st));
-  CK(cudaMemcpyAsync(out, dout, sizeof(double) * nhd, cudaMemcpyDeviceToHost, S.st));
-  CK(cudaStreamSynchronize(S.st));
-  if (hb) return fail(MPPI_E_NONFINITE_CONTROL, "control batch contains non-finite entries");
-  return MPPI_OK;
-}
-
-int mppi_particle_weights(const double* totals, int64_t n, double beta, double* weights) {
-  if (n < 1) return fail(MPPI_E_ALL_QUARANTINED, "all particles quarantined; no finite costs");
-  SCRATCH_OR_FAIL(S);
-  DEVPTR(S, double, dt, n, totals);
-  DEVPTR(S, double, dw, n, (const double*)nullptr);
-  DEVPTR(S, int, stt, 1, (const int*)nullptr);
-  CK(cudaMemsetAsync(stt, 0, sizeof(int), S.st));
-  weights_kernel<<<1, 1024, 0, S.st>>>(dt, n, beta, dw, stt);
-  CK(cudaGetLastError());
-  int hs = 0;
-  CK(cudaMemcpyAsync(&hs, stt, sizeof(int), cudaMemcpyDeviceToHost, S.st));
-  CK(cudaMemcpyAsync(weights, dw, sizeof(double) * n, cudaMemcpyDeviceToHost, S.st));
-  CK(cudaStreamSynchronize(S.st));
-  if (hs == MPPI_E_ALL_QUARANTINED) return fail(hs, "all particles quarantined; no finite costs");
-  if (hs == MPPI_E_WEIGHT_UNDERFLOW) return fail(hs, "all particle weights underflowed to zero; increase beta");
-  return MPPI_OK;
-}
-
-int mppi_update_policy(const double* controls, const double* weights, int64_t n, int32_t h, int32_t d,
-                       int32_t policy_mode, double alpha_mu, double alpha_sigma, double smin, double smax,
-                       int32_t do_mean, int32_t do_cov, double* means, double* variances) {
-  if (n < 1 || h < 1 || d < 1 || h * d > 1024) return fail(MPPI_E_BAD_ARGUMENT, "bad shape");
-  SCRATCH_OR_FAIL(S);
-  const size_t nhd = (size_t)n * h * d;
-  const size_t nv = policy_mode == MPPI_POLICY_ISOTROPIC ? (size_t)h : (size_t)h * d;
-  DEVPTR(S, double, du, nhd, controls);
-  DEVPTR(S, double, dw, n, weights);
-  DEVPTR(S, double, dm, (size_t)h * d, means);
-  DEVPTR(S, double, dv, nv, variances);
-  DEVPTR(S, int, stt, 1, (const int*)nullptr);
-  CK(cudaMemsetAsync(stt, 0, sizeof(int), S.st));
-  update_policy_kernel<<<1, 1024, 0, S.st>>>(du, dw, n, h, d, policy_mode == MPPI_POLICY_ISOTROPIC,
-                                             alpha_mu, alpha_sigma, smin, smax, do_mean, do_cov, dm, dv, stt);
-  CK(cudaGetLastError());
-  int hs = 0;
-  CK(cudaMemcpyAsync(&hs, stt, sizeof(int), cudaMemcpyDeviceToHost, S.st));
-  CK(cudaMemcpyAsync(means, dm, sizeof(double) * h * d, cudaMemcpyDeviceToHost, S.st));
-  CK(cudaMemcpyAsync(variances, dv, sizeof(double) * nv, cudaMemcpyDeviceToHost, S.st));
-  CK(cudaStreamSynchronize(S.st));
-  if (hs) return fail(hs, "weight sum must be positive");
-  return MPPI_OK;
-}
-
+// ---------------------------------------------------------------- parity: the plan's MLP
 int mppi_mlp_forward(mppi_plan* p, const double* q, int64_t m, double* out) {
   if (!p || !q || !out) return fail(MPPI_E_BAD_ARGUMENT, "null argument");
   if (!p->mlp_ready) return fail(MPPI_E_CONFIG, "mppi_set_mlp was not called");
@@ -1982,128 +1821,6 @@ int mppi_mlp_forward(mppi_plan* p, const double* q, int64_t m, double* out) {
   float_to_double_kernel<<<grid_for(m, 256), 256, 0, S.st>>>(dd, m, dout);
   CK(cudaGetLastError());
   CK(cudaMemcpyAsync(out, dout, sizeof(double) * m, cudaMemcpyDeviceToHost, S.st));
-  CK(cudaStreamSynchronize(S.st));
-  return MPPI_OK;
-}
-
-// ---------------------------------------------------------------- operator seam
-int mppi_fk_batch(const double* q, int64_t m, int32_t d, const double* axes, const double* orot,
-                  const double* otrans, const int64_t* jtype, double* rot_out, double* trans_out) {
-  if (m < 0 || d < 1) return fail(MPPI_E_BAD_ARGUMENT, "bad shape");
-  if (m == 0) return MPPI_OK;
-  SCRATCH_OR_FAIL(S);
-  DEVPTR(S, double, dq, (size_t)m * d, q);
-  DEVPTR(S, double, da, (size_t)3 * d, axes);
-  DEVPTR(S, double, dr, (size_t)9 * d, orot);
-  DEVPTR(S, double, dt, (size_t)3 * d, otrans);
-  DEVPTR(S, long long, dj, (size_t)d, (const long long*)jtype);
-  DEVPTR(S, double, rot, (size_t)m * d * 9, (const double*)nullptr);
-  DEVPTR(S, double, tr, (size_t)m * d * 3, (const double*)nullptr);
-  SeamChain ch{da, dr, dt, dj};
-  fk_seam_kernel<<<(unsigned)((m + 127) / 128), 128, 0, S.st>>>(dq, m, d, ch, rot, tr);
-  CK(cudaGetLastError());
-  CK(cudaMemcpyAsync(rot_out, rot, sizeof(double) * m * d * 9, cudaMemcpyDeviceToHost, S.st));
-  CK(cudaMemcpyAsync(trans_out, tr, sizeof(double) * m * d * 3, cudaMemcpyDeviceToHost, S.st));
-  CK(cudaStreamSynchronize(S.st));
-  return MPPI_OK;
-}
-
-int mppi_jacobian_batch(const double* q, int64_t m, int32_t d, const double* rot, const double* trans,
-                        const double* axes, const int64_t* jtype, double* jac_out) {
-  (void)q;
-  if (m < 0 || d < 1) return fail(MPPI_E_BAD_ARGUMENT, "bad shape");
-  if (m == 0) return MPPI_OK;
-  SCRATCH_OR_FAIL(S);
-  DEVPTR(S, double, drot, (size_t)m * d * 9, rot);
-  DEVPTR(S, double, dtr, (size_t)m * d * 3, trans);
-  DEVPTR(S, double, da, (size_t)3 * d, axes);
-  DEVPTR(S, long long, dj, (size_t)d, (const long long*)jtype);
-  DEVPTR(S, double, J, (size_t)m * 6 * d, (const double*)nullptr);
-  jacobian_seam_kernel<<<(unsigned)((m + 127) / 128), 128, 0, S.st>>>(m, d, drot, dtr, da, dj, J);
-  CK(cudaGetLastError());
-  CK(cudaMemcpyAsync(jac_out, J, sizeof(double) * m * 6 * d, cudaMemcpyDeviceToHost, S.st));
-  CK(cudaStreamSynchronize(S.st));
-  return MPPI_OK;
-}
-
-int mppi_manip_batch(const double* jac, int64_t m, int32_t d, int32_t task_dim, double* out) {
-  if (m < 0 || d < 1 || (task_dim != 2 && task_dim != 3)) return fail(MPPI_E_BAD_ARGUMENT, "bad shape");
-  if (m == 0) return MPPI_OK;
-  SCRATCH_OR_FAIL(S);
-  DEVPTR(S, double, dj, (size_t)m * 6 * d, jac);
-  DEVPTR(S, double, dout, (size_t)m, (const double*)nullptr);
-  manip_seam_kernel<<<(unsigned)((m + 127) / 128), 128, 0, S.st>>>(dj, m, d, task_dim, dout);
-  CK(cudaGetLastError());
-  CK(cudaMemcpyAsync(out, dout, sizeof(double) * m, cudaMemcpyDeviceToHost, S.st));
-  CK(cudaStreamSynchronize(S.st));
-  return MPPI_OK;
-}
-
-int mppi_self_collision_batch(const double* rot, const double* trans, int64_t m, int32_t d,
-                              const double* cap_p0, const double* cap_p1, const double* cap_r,
-                              const int64_t* cap_link, int32_t n_caps, const int64_t* pair_a,
-                              const int64_t* pair_b, int32_t n_pairs, double* out) {
-  if (m < 0 || d < 1) return fail(MPPI_E_BAD_ARGUMENT, "bad shape");
-  if (m == 0) return MPPI_OK;
-  SCRATCH_OR_FAIL(S);
-  DEVPTR(S, double, drot, (size_t)m * d * 9, rot);
-  DEVPTR(S, double, dtr, (size_t)m * d * 3, trans);
-  DEVPTR(S, double, p0, (size_t)3 * n_caps, cap_p0);
-  DEVPTR(S, double, p1, (size_t)3 * n_caps, cap_p1);
-  DEVPTR(S, double, r, (size_t)n_caps, cap_r);
-  DEVPTR(S, long long, lk, (size_t)n_caps, (const long long*)cap_link);
-  DEVPTR(S, long long, pa, (size_t)n_pairs, (const long long*)pair_a);
-  DEVPTR(S, long long, pb, (size_t)n_pairs, (const long long*)pair_b);
-  DEVPTR(S, double, dout, (size_t)m, (const double*)nullptr);
-  SeamCaps caps{p0, p1, r, lk, n_caps};
-  selfcoll_seam_kernel<<<(unsigned)((m + 127) / 128), 128, 0, S.st>>>(drot, dtr, m, d, caps, pa, pb, n_pairs, dout);
-  CK(cudaGetLastError());
-  CK(cudaMemcpyAsync(out, dout, sizeof(double) * m, cudaMemcpyDeviceToHost, S.st));
-  CK(cudaStreamSynchronize(S.st));
-  return MPPI_OK;
-}
-
-int mppi_env_collision_batch(const double* rot, const double* trans, int64_t m, int32_t d,
-                             const double* cap_p0, const double* cap_p1, const double* cap_r,
-                             const int64_t* cap_link, int32_t n_caps, const double* spheres,
-                             int32_t n_spheres, const double* boxes, int32_t n_boxes, int64_t* hit_out) {
-  if (m < 0 || d < 1) return fail(MPPI_E_BAD_ARGUMENT, "bad shape");
-  if (m == 0) return MPPI_OK;
-  SCRATCH_OR_FAIL(S);
-  DEVPTR(S, double, drot, (size_t)m * d * 9, rot);
-  DEVPTR(S, double, dtr, (size_t)m * d * 3, trans);
-  DEVPTR(S, double, p0, (size_t)3 * n_caps, cap_p0);
-  DEVPTR(S, double, p1, (size_t)3 * n_caps, cap_p1);
-  DEVPTR(S, double, r, (size_t)n_caps, cap_r);
-  DEVPTR(S, long long, lk, (size_t)n_caps, (const long long*)cap_link);
-  DEVPTR(S, double, sp, (size_t)4 * n_spheres, spheres);
-  DEVPTR(S, double, bx, (size_t)6 * n_boxes, boxes);
-  DEVPTR(S, long long, hit, (size_t)m, (const long long*)nullptr);
-  SeamCaps caps{p0, p1, r, lk, n_caps};
-  envcoll_seam_kernel<<<(unsigned)((m + 127) / 128), 128, 0, S.st>>>(drot, dtr, m, d, caps, sp, n_spheres, bx,
-                                                                      n_boxes, hit);
-  CK(cudaGetLastError());
-  CK(cudaMemcpyAsync(hit_out, hit, sizeof(long long) * m, cudaMemcpyDeviceToHost, S.st));
-  CK(cudaStreamSynchronize(S.st));
-  return MPPI_OK;
-}
-
-int mppi_integrate_batch(const double* u, int64_t n, int32_t h, int32_t d, const double* dts,
-                         const double* th0, const double* thd0, double* pos_out, double* vel_out) {
-  if (n < 0 || h < 1 || d < 1) return fail(MPPI_E_BAD_ARGUMENT, "bad shape");
-  if (n == 0) return MPPI_OK;
-  SCRATCH_OR_FAIL(S);
-  const size_t nhd = (size_t)n * h * d;
-  DEVPTR(S, double, du, nhd, u);
-  DEVPTR(S, double, ddt, (size_t)h, dts);
-  DEVPTR(S, double, t0, (size_t)d, th0);
-  DEVPTR(S, double, v0, (size_t)d, thd0);
-  DEVPTR(S, double, pos, nhd, (const double*)nullptr);
-  DEVPTR(S, double, vel, nhd, (const double*)nullptr);
-  integrate_seam_kernel<<<(unsigned)((n * d + 127) / 128), 128, 0, S.st>>>(du, n, h, d, ddt, t0, v0, pos, vel);
-  CK(cudaGetLastError());
-  CK(cudaMemcpyAsync(pos_out, pos, sizeof(double) * nhd, cudaMemcpyDeviceToHost, S.st));
-  CK(cudaMemcpyAsync(vel_out, vel, sizeof(double) * nhd, cudaMemcpyDeviceToHost, S.st));
   CK(cudaStreamSynchronize(S.st));
   return MPPI_OK;
 }

@@ -15,7 +15,7 @@ namespace mppi {
 // ------------------------------------------------------------------ noise
 // z[(n*K + k)*d + j] for global particle rows [0, rows): Halton (gen 0) or
 // Philox (gen 1; counter = (row*K+k, j, step, 0), key = seed).
-__global__ void knots_kernel(double* z, long long rows, int K, int d, int gen, uint64_t seed,
+static __global__ void knots_kernel(double* z, long long rows, int K, int d, int gen, uint64_t seed,
                              unsigned long long step, int* err) {
   const long long total = rows * K * d;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
@@ -38,7 +38,7 @@ __global__ void knots_kernel(double* z, long long rows, int K, int d, int gen, u
 
 // eps[n][h][j] from knot values (smooth_sequences, sampling.py:240-265).
 // mode 0: sum_k basis[h][k] z[n][k][j]; 1: comb c1 x_h + c2 x_{h-1} + c3 x_{h-2}; 2: identity.
-__global__ void smooth_kernel(const double* z, double* eps, long long rows, int K, int H, int d,
+static __global__ void smooth_kernel(const double* z, double* eps, long long rows, int K, int H, int d,
                               int mode, const double* basis, double c1, double c2, double c3) {
   const long long total = rows * H * d;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
@@ -64,7 +64,7 @@ __global__ void smooth_kernel(const double* z, double* eps, long long rows, int 
 
 // Column means over `rows` particles of an (rows, cols) matrix, fixed-order
 // tree per column (one block per column). controller.py:174.
-__global__ void column_mean_kernel(const double* x, long long rows, int cols, double* mean) {
+static __global__ void column_mean_kernel(const double* x, long long rows, int cols, double* mean) {
   __shared__ double red[256];
   const int c = blockIdx.x;
   double s = 0.0;
@@ -79,7 +79,7 @@ __global__ void column_mean_kernel(const double* x, long long rows, int cols, do
 }
 
 // dst[r][c] = src[(r + row0)][c] - mean[c] for r < rows.
-__global__ void center_slice_kernel(const double* src, const double* mean, double* dst,
+static __global__ void center_slice_kernel(const double* src, const double* mean, double* dst,
                                     long long row0, long long rows, int cols) {
   const long long total = rows * cols;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
@@ -91,7 +91,7 @@ __global__ void center_slice_kernel(const double* src, const double* mean, doubl
 
 // Clamped uniform B-spline design matrix (bspline_basis, sampling.py:205-237),
 // one thread per horizon step, numpy linspace arithmetic reproduced exactly.
-__global__ void bspline_basis_kernel(int H, int K, int deg, double* basis) {
+static __global__ void bspline_basis_kernel(int H, int K, int deg, double* basis) {
   const int hi = blockIdx.x * blockDim.x + threadIdx.x;
   if (hi >= H) return;
   double kv[64];
@@ -136,7 +136,7 @@ struct SeamChain {
   const long long* jtype;
 };
 
-__global__ void fk_seam_kernel(const double* q, long long M, int d, SeamChain ch, double* rot,
+static __global__ void fk_seam_kernel(const double* q, long long M, int d, SeamChain ch, double* rot,
                                double* trans) {
   const long long m = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (m >= M) return;
@@ -165,7 +165,7 @@ __global__ void fk_seam_kernel(const double* q, long long M, int d, SeamChain ch
   }
 }
 
-__global__ void jacobian_seam_kernel(long long M, int d, const double* rot, const double* trans,
+static __global__ void jacobian_seam_kernel(long long M, int d, const double* rot, const double* trans,
                                      const double* axes, const long long* jtype, double* J) {
   const long long m = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (m >= M) return;
@@ -199,7 +199,7 @@ __global__ void jacobian_seam_kernel(long long M, int d, const double* rot, cons
   }
 }
 
-__global__ void manip_seam_kernel(const double* J, long long M, int d, int td, double* out) {
+static __global__ void manip_seam_kernel(const double* J, long long M, int d, int td, double* out) {
   const long long m = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (m >= M) return;
   const double* Jm = J + m * 6 * d;
@@ -255,7 +255,7 @@ __device__ __forceinline__ void seam_capsule(const double* rot, const double* tr
   }
 }
 
-__global__ void selfcoll_seam_kernel(const double* rot, const double* trans, long long M, int d,
+static __global__ void selfcoll_seam_kernel(const double* rot, const double* trans, long long M, int d,
                                      SeamCaps caps, const long long* pa, const long long* pb, int np,
                                      double* out) {
   const long long m = blockIdx.x * (long long)blockDim.x + threadIdx.x;
@@ -272,7 +272,7 @@ __global__ void selfcoll_seam_kernel(const double* rot, const double* trans, lon
 }
 
 // First colliding obstacle index, spheres first, -1 when clear (jit.py:289-332).
-__global__ void envcoll_seam_kernel(const double* rot, const double* trans, long long M, int d,
+static __global__ void envcoll_seam_kernel(const double* rot, const double* trans, long long M, int d,
                                     SeamCaps caps, const double* spheres, int ns,
                                     const double* boxes, int nb, long long* hit) {
   const long long m = blockIdx.x * (long long)blockDim.x + threadIdx.x;
@@ -303,7 +303,7 @@ __global__ void envcoll_seam_kernel(const double* rot, const double* trans, long
 
 // Sequential semi-implicit Euler per (n, j) (jit.py:335-349) — the seam keeps
 // the reference's summation order exactly.
-__global__ void integrate_seam_kernel(const double* u, long long N, int H, int d, const double* dts,
+static __global__ void integrate_seam_kernel(const double* u, long long N, int H, int d, const double* dts,
                                       const double* th0, const double* thd0, double* pos,
                                       double* vel) {
   const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
@@ -322,7 +322,7 @@ __global__ void integrate_seam_kernel(const double* u, long long N, int H, int d
 
 // ------------------------------------------------------------------ policy (stateless)
 // particle_weights (policy.py:103-121); single block; status 2 = none finite, 3 = sum <= 0.
-__global__ void weights_kernel(const double* totals, long long n, double beta, double* w,
+static __global__ void weights_kernel(const double* totals, long long n, double beta, double* w,
                                int* status) {
   __shared__ double red[32];
   double m = CUDART_INF;
@@ -355,7 +355,7 @@ __global__ void weights_kernel(const double* totals, long long n, double beta, d
 
 // update_mean then update_covariance (policy.py:124-155) with the reference's
 // two-pass formulas; one thread per (h, j), single block (H*d <= 1024).
-__global__ void update_policy_kernel(const double* u, const double* w, long long n, int H, int d,
+static __global__ void update_policy_kernel(const double* u, const double* w, long long n, int H, int d,
                                      int iso, double alpha_mu, double alpha_sigma, double smin,
                                      double smax, int do_mean, int do_cov, double* means,
                                      double* var, int* status) {
@@ -405,7 +405,7 @@ __global__ void update_policy_kernel(const double* u, const double* w, long long
 }
 
 // build_control_batch (sampling.py:268-290).
-__global__ void build_controls_kernel(const double* eps, const double* means, const double* sd,
+static __global__ void build_controls_kernel(const double* eps, const double* means, const double* sd,
                                       long long n, int H, int d, int null_count, double* out,
                                       int* bad) {
   const long long total = n * H * d;
@@ -429,7 +429,7 @@ __global__ void build_controls_kernel(const double* eps, const double* means, co
 // Pseudorandom knots for a captured graph: the step number is read from the
 // device copy of the host input block. Row index is global (row + offset) so a
 // particle-sharded plan draws exactly the rows an unsharded plan would.
-__global__ void knots_ptr_kernel(double* z, long long rows, int K, int d, uint64_t seed,
+static __global__ void knots_ptr_kernel(double* z, long long rows, int K, int d, uint64_t seed,
                                  const unsigned long long* stepctr, unsigned long long iters, int it,
                                  int offset, int* err) {
   const unsigned long long step = stepctr[0] * iters + (unsigned long long)it;
@@ -446,7 +446,7 @@ __global__ void knots_ptr_kernel(double* z, long long rows, int K, int d, uint64
   (void)err;
 }
 
-__global__ void halton_points_kernel(double* out, long long count, int dims) {
+static __global__ void halton_points_kernel(double* out, long long count, int dims) {
   const long long total = count * dims;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
        i += (long long)gridDim.x * blockDim.x) {
@@ -455,7 +455,7 @@ __global__ void halton_points_kernel(double* out, long long count, int dims) {
   }
 }
 
-__global__ void gaussianize_kernel(const double* p, long long n, double* out, int* err) {
+static __global__ void gaussianize_kernel(const double* p, long long n, double* out, int* err) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
        i += (long long)gridDim.x * blockDim.x) {
     const double x = p[i];
@@ -470,7 +470,7 @@ __global__ void gaussianize_kernel(const double* p, long long n, double* out, in
 
 // Exact distance from every voxel cube to the union of boxes (the broad-phase
 // clearance field of env_any_hit).
-__global__ void clearance_kernel(const double* boxes, int nb, int nx, int ny, int nz, double ox,
+static __global__ void clearance_kernel(const double* boxes, int nb, int nx, int ny, int nz, double ox,
                                  double oy, double oz, double vox, float* clr) {
   const long long total = (long long)nx * ny * nz;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
@@ -495,7 +495,7 @@ __global__ void clearance_kernel(const double* boxes, int nb, int nx, int ny, in
   }
 }
 
-__global__ void posenc_kernel(const double* q, long long m, int d, float* x) {
+static __global__ void posenc_kernel(const double* q, long long m, int d, float* x) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < m;
        i += (long long)gridDim.x * blockDim.x) {
     for (int k = 0; k < d; ++k) {
@@ -507,7 +507,7 @@ __global__ void posenc_kernel(const double* q, long long m, int d, float* x) {
   }
 }
 
-__global__ void float_to_double_kernel(const float* a, long long n, double* b) {
+static __global__ void float_to_double_kernel(const float* a, long long n, double* b) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
        i += (long long)gridDim.x * blockDim.x)
     b[i] = (double)a[i];

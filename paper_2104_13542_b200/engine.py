@@ -286,6 +286,38 @@ class Plan:
         res["quarantined"] = int(out.quarantined)
         return res
 
+    def get_step_inputs(self, instance: int = 0):
+        """(theta, theta_dot, means, stddev) the last step's last iteration ran from."""
+        th, thd = np.empty(self.dof), np.empty(self.dof)
+        m, sd = np.empty((self.H, self.dof)), np.empty((self.H, self.dof))
+        N.check(self.lib.mppi_get_step_inputs(self.handle, int(instance), N.dptr(th), N.dptr(thd), N.dptr(m),
+                                              N.dptr(sd)))
+        return th, thd, m, sd
+
+    def replay_bundle(self, dts, gamma: float, terminal_weight: float, beta: float, null_count: int,
+                      instance: int = 0) -> dict:
+        """The last step's last-iteration RolloutBundle of a lean plan (dump=0),
+        recomputed on the device from its inputs: controls from the perturbation
+        block and the policy view of that iteration, then one evaluation pass
+        (rollout, cost stack, MLP, discounted totals) and the particle weights.
+        Equal to the step's own rollouts up to the plan precision's rounding."""
+        from .costs import TERM_NAMES
+
+        th, thd, m, sd = self.get_step_inputs(instance)
+        eps = self.get_noise()
+        u = np.empty_like(eps)
+        N.check(self.lib.mppi_build_controls(N.dptr(eps), N.dptr(m), N.dptr(sd), self.N, self.H, self.dof,
+                                             int(null_count), N.dptr(u)))
+        r = self.evaluate(0, u, None, dts, gamma, terminal_weight, th, thd)
+        w = np.empty(self.N)
+        rc = self.lib.mppi_particle_weights(N.dptr(r["totals"]), self.N, float(beta), N.dptr(w))
+        if rc:
+            w[:] = np.nan  # the step itself failed (no finite totals): no weights to report
+        return {"positions": r["positions"], "velocities": r["velocities"], "accelerations": r["accelerations"],
+                "step_costs": r["step_costs"],
+                "term_breakdown": {nm: r["terms"][i] for i, nm in enumerate(TERM_NAMES)},
+                "total_per_particle": r["totals"], "weights": w}
+
     def get_bundle(self) -> dict:
         """Instance 0's last-iteration bundle (plan created with dump=1)."""
         n, H, d = self.N, self.H, self.dof

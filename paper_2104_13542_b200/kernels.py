@@ -15,6 +15,8 @@ would materialise every link pose of every configuration).
 
 from __future__ import annotations
 
+from contextlib import contextmanager
+
 import numpy as np
 
 from . import _native as N
@@ -101,14 +103,42 @@ _EXPORTED = ("fk_batch", "jacobian_batch", "manip_batch", "self_collision_batch"
              "env_collision_batch", "integrate_batch")
 
 
+_BACKEND_NAMES = ("cuda", BACKEND_NAME)
+
+
 def get_backend(name: str = "cuda"):
-    """Only one backend exists; kept for call-site compatibility with
-    kernels.get_backend (kernels/__init__.py:25-33)."""
+    """The kernel module for `name` (kernels/__init__.py:25-33). This build has
+    exactly one backend, the sm_100a seam; the reference's "numpy"/"numba"
+    names raise ValueError, as the reference does for unknown names — there is
+    no CPU fallback to select."""
     import sys
 
-    if name not in ("cuda", BACKEND_NAME):
+    if name not in _BACKEND_NAMES:
         raise ValueError(f"unknown kernel backend {name!r} (this build has only {BACKEND_NAME!r})")
     return sys.modules[__name__]
+
+
+def active_backend():
+    """The kernel module in effect (kernels/__init__.py:44-46)."""
+    import sys
+
+    return sys.modules[__name__]
+
+
+@contextmanager
+def use_backend(name: str):
+    """Temporarily rebind the six exported functions to the named backend
+    (kernels/__init__.py:69-83). Consumers resolve ``kernels.fk_batch`` at call
+    time, so rebinding the module attributes redirects them all. Not thread
+    safe (the reference's contract): for tests and benchmarks, not the loop."""
+    module = get_backend(name)
+    g = globals()
+    saved = {fn: g[fn] for fn in _EXPORTED}
+    g.update({fn: getattr(module, fn) for fn in _EXPORTED})
+    try:
+        yield module
+    finally:
+        g.update(saved)
 
 
 def install_into(module) -> dict:

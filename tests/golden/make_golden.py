@@ -267,6 +267,114 @@ def episode_fixtures():
     episode_fixture("episode_c3", 3, steps=5, particles=128, script=hold, world=world)
 
 
+def cost_term_fixtures():
+    """The reference's cost-term free functions (costs.py:76-173) and
+    jacobian_dot_times_qdot (kinematics.py:235-245) on seeded inputs, with
+    manipulability values straddling k_m and states outside the limits."""
+    from jointmpc import costs as rc
+    from jointmpc.kinematics import fk_batch as rfk, jacobian_dot_times_qdot
+    from jointmpc.rollout import make_dt_schedule
+
+    rng = np.random.default_rng(21)
+    arm7 = load_chain("arm7.chain")
+    q = random_q(arm7, rng, 6 * 5, margin=-0.15).reshape(6, 5, 7)  # some beyond the limits
+    rot, trans = rfk(arm7, q)  # (6,5,7,3,3), (6,5,7,3)
+    goal_full = GoalSpec(target_pose=Pose(rotation=_rpy_matrix(0.3, -0.2, 1.1),
+                                          translation=np.array([0.3, -0.1, 0.6])), mode=FULL_POSE)
+    goal_pos = goal_at_position([0.45, 0.1, 0.55])
+    a_rot, a_trans = np.array([30.0, 20.0, 10.0]), np.array([150.0, 120.0, 90.0])
+    sched = make_dt_schedule(30, 0.05, "two_phase")
+    vel = rng.normal(scale=2.0, size=(4, 30, 7))
+    manip_vals = np.concatenate([rng.uniform(0.0, 0.1, 40), [0.05, 0.05 - 1e-9, 0.05 + 1e-9, 0.0, 1.0]])
+    world = WorldModel(spheres=np.array([[0.35, 0.25, 0.55, 0.08], [0.1, -0.3, 0.4, 0.12]]),
+                       boxes=np.array([[0.2, -0.1, 0.3, 0.45, 0.15, 0.5], [-0.5, -0.5, 0.0, -0.2, -0.2, 0.3]]),
+                       bounds_min=np.full(3, -1.0), bounds_max=np.full(3, 1.0))
+    qd = rng.normal(size=(3, 7))
+    save("cost_terms", q=q, ee_rot=rot[..., -1, :, :], ee_trans=trans[..., -1, :],
+         goal_full_R=goal_full.target_pose.rotation, goal_full_t=goal_full.target_pose.translation,
+         goal_pos_t=goal_pos.target_pose.translation, a_rot=a_rot, a_trans=a_trans,
+         pose_full=rc.pose_cost(rot[..., -1, :, :], trans[..., -1, :], goal_full, a_rot, a_trans),
+         pose_pos=rc.pose_cost(rot[..., -1, :, :], trans[..., -1, :], goal_pos, a_rot, a_trans),
+         dts=sched.dts, braking=rc.braking_limits(arm7.accel_limits, sched), vel=vel,
+         stop=rc.stop_cost(vel, arm7.accel_limits, sched),
+         shrunk_lo=rc.shrunken_limits(arm7, 0.1)[0], shrunk_hi=rc.shrunken_limits(arm7, 0.1)[1],
+         joint=rc.joint_limit_cost(q, arm7, 0.1), joint_k02=rc.joint_limit_cost(q, arm7, 0.2),
+         manip_vals=manip_vals, manip_from_values=rc.manipulability_cost_from_values(manip_vals, 0.05),
+         manip=rc.manipulability_cost(arm7, q, 0.05),
+         spheres=world.spheres, boxes=world.boxes, envcoll=rc.env_collision_cost(rot, trans, arm7, world),
+         qd=qd, jdot_qd=np.stack([jacobian_dot_times_qdot(arm7, q[0, i], qd[i]) for i in range(3)]),
+         jdot_zero=jacobian_dot_times_qdot(arm7, q[0, 0], np.zeros(7)))
+
+
+def topk_fixture():
+    """The reference bridge's telemetry selection (bridge.py:196-203) on its own
+    bundle: config 2, N=500, the second closed-loop step."""
+    from jointmpc.kinematics import fk_batch as rfk
+
+    c = reach_controller(2)
+    state = JointState(theta=configs.REACH_START.copy(), theta_dot=np.zeros(7), theta_ddot=np.zeros(7))
+    cmd, _ = c.control_step(state)
+    state = sim_step(state, cmd, 0.05)
+    means_in, variances_in = c.policy.means.copy(), c.policy.variances.copy()
+    cmd, diag = c.control_step(state)
+    k = 8
+    order = np.argsort(diag.bundle.total_per_particle)[:k]
+    q_paths = diag.bundle.positions[order]
+    _, path_trans = rfk(c.chain, q_paths.reshape(-1, 7))
+    save("topk", theta=np.stack([configs.REACH_START, state.theta]),
+         theta_dot=np.stack([np.zeros(7), state.theta_dot]), order=order, means_in=means_in,
+         variances_in=variances_in,
+         totals=diag.bundle.total_per_particle, ee_paths=path_trans[:, -1, :3].reshape(k, 30, 3))
+
+
+def tracking_fixture(particles=500, steps=3):
+    """Config 3 at the benched shape: configs.tracking_problem()'s
+    script and box world (built with the reference's FK), N=500, 3 closed-loop
+    steps, goal = the script's target at t = i*dt. Every step's inputs (state,
+    goal, the policy it starts from) and outputs (terms, totals, weights,
+    command, updated policy), so each GPU step can start from the reference's
+    own inputs and the decision-band rule can be applied per step."""
+    from jointmpc.kinematics import fk_batch as rfk
+    from jointmpc.simworld import target_at as rtarget_at
+
+    script, world = configs.tracking_problem(fk=rfk)
+    rworld = WorldModel(spheres=np.zeros((0, 4)), boxes=world.boxes, bounds_min=np.full(3, -1.0),
+                        bounds_max=np.full(3, 1.0))
+    rscript = TargetScript(times=script.times, positions=script.positions, interpolation="linear",
+                           mode="position_only")
+    c = reach_controller(3, particles, world=rworld)
+    state = JointState(theta=configs.REACH_START.copy(), theta_dot=np.zeros(7), theta_ddot=np.zeros(7))
+    rec = {"eps": c._fixed_eps, "boxes": world.boxes, "occupancy": world.voxel_grid.occupancy,
+           "script_times": script.times, "script_positions": script.positions}
+    cols = {k: [] for k in ("theta", "theta_dot", "goal", "means_in", "variances_in", "command", "means",
+                            "variances", "totals", "weights", "step_costs", "best_cost")}
+    terms = {k: [] for k in ("pose", "stop", "joint", "manip", "selfcoll", "envcoll")}
+    for i in range(steps):
+        goal = rtarget_at(rscript, i * 0.05)
+        c.set_goal(goal)
+        cols["theta"].append(state.theta.copy())
+        cols["theta_dot"].append(state.theta_dot.copy())
+        cols["goal"].append(goal.target_pose.translation.copy())
+        cols["means_in"].append(c.policy.means.copy())
+        cols["variances_in"].append(c.policy.variances.copy())
+        cmd, diag = c.control_step(state)
+        assert diag.fallback == "", diag.fallback
+        b = diag.bundle
+        cols["command"].append(cmd)
+        cols["means"].append(c.policy.means.copy())
+        cols["variances"].append(c.policy.variances.copy())
+        cols["totals"].append(b.total_per_particle)
+        cols["weights"].append(particle_weights(b.total_per_particle, c.update_cfg.beta))
+        cols["step_costs"].append(b.step_costs)
+        cols["best_cost"].append(diag.best_cost)
+        for k in terms:
+            terms[k].append(b.term_breakdown[k])
+        state = sim_step(state, cmd, 0.05)
+    rec.update({k: np.array(v) for k, v in cols.items()})
+    rec.update({f"term_{k}": np.array(v) for k, v in terms.items()})
+    save("step_c3", **rec)
+
+
 def training_fixtures():
     """Reference train_collision_surrogate runs (surrogate.py:146-206): a short
     one (3 epochs) for weight-level parity, one through both step-size halvings
@@ -299,6 +407,7 @@ if __name__ == "__main__":
             "step_c2_iso_k2": lambda: step_fixture("step_c2_iso_k2", 2, particles=256, steps=2,
                                                    policy_mode="isotropic", iterations=2),
             "step_world": world_fixture, "episode_parts": episode_parts, "episodes": episode_fixtures,
+            "cost_terms": cost_term_fixtures, "topk": topk_fixture, "step_c3": tracking_fixture,
             "training": training_fixtures}
     for name, fn in jobs.items():
         if not which or name in which:

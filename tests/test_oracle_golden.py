@@ -168,3 +168,54 @@ def test_world_step_matches_reference(arm7):
     np.testing.assert_allclose(cmd, g["command"], atol=1e-9)
     np.testing.assert_allclose(c.variances, g["variances"], atol=1e-9)
     assert g["term_envcoll"].any()  # the world is actually hit
+
+
+def test_obstacle_margin_decides_like_first_hit(arm7):
+    """The decision-band margin (tests/band.py) is < 0 exactly where the
+    reference reports a hit (kinematics golden: its own hit indices)."""
+    g = golden("kinematics")
+    rot, trans = O.link_poses(g["env_q"], arm7)
+    m = O.obstacle_margin(rot, trans, arm7, g["env_spheres"], g["env_boxes"])
+    np.testing.assert_array_equal(m < 0, g["env_hit"] >= 0)
+    m = O.obstacle_margin(rot, trans, arm7, np.zeros((0, 4)), g["env_boxes"])
+    np.testing.assert_array_equal(m < 0, g["env_hit_boxes_only"] >= 0)
+
+
+def test_chunked_rollout_scores_equal_unchunked(arm7, surrogate_state):
+    """The chunked oracle driver for N >= 65k (SURVEY §8(c) scale limits):
+    rows are independent, so per-chunk evaluation + one full-N update equals
+    the one-shot evaluation."""
+    rng = np.random.default_rng(3)
+    u = rng.normal(scale=0.7, size=(300, 30, 7))
+    dts = O.dt_schedule(30, 0.05, "two_phase")
+    args = (configs.REACH_START, np.zeros(7), u, dts, arm7, configs.make_weights(2), configs.reach_goal_rotation(),
+            configs.REACH_GOAL_POS, True, 0.99, 1.0)
+    kw = dict(provider="learned", mlp_state=surrogate_state)
+    one = O.rollout_scores(*args, keep=("terms", "decisions"), **kw)
+    chunked = O.rollout_scores(*args, chunk=128, keep=("terms", "decisions"), **kw)
+    np.testing.assert_allclose(chunked["totals"], one["totals"], rtol=1e-14)
+    for k in O.TERMS:
+        np.testing.assert_allclose(chunked["terms"][k], one["terms"][k], rtol=1e-14, atol=0)
+    np.testing.assert_array_equal(chunked["decisions"]["manip"], one["decisions"]["manip"])
+
+
+def test_tracking_step_matches_reference(arm7):
+    """Config 3 at the benched shape (configs.tracking_problem boxes, N=500):
+    the oracle's rollout of the reference's first step equals the reference's
+    terms and totals (tests/golden/step_c3.npz)."""
+    g = golden("step_c3")
+    kw = configs.CONTROLLER_KW
+    ms, vs = O.shifted(g["means_in"][0], g["variances_in"][0], 0.0, kw["sigma0_sq"])
+    u = O.shape_controls(g["eps"], ms, vs, 2)
+    dts = O.dt_schedule(30, 0.05, "two_phase")
+    res = O.rollout_scores(g["theta"][0], g["theta_dot"][0], u, dts, arm7, configs.make_weights(3), np.eye(3),
+                           g["goal"][0], False, kw["gamma"], 1.0, provider="oracle", spheres=np.zeros((0, 4)),
+                           boxes=g["boxes"], keep=("terms", "decisions"))
+    for k in O.TERMS:
+        np.testing.assert_allclose(res["terms"][k], g[f"term_{k}"][0], rtol=1e-10, atol=1e-10, err_msg=k)
+    np.testing.assert_allclose(res["totals"], g["totals"][0], rtol=1e-11)
+    env = res["decisions"]["env"]
+    np.testing.assert_array_equal(env < 0, g["term_envcoll"][0] > 0)
+    w = O.weights_from_totals(res["totals"], kw["beta"])
+    mu, _ = O.blend_policy(ms, vs, u, w, kw["alpha_mu"], kw["alpha_sigma"], kw["sigma_sq_min"], kw["sigma0_sq"])
+    np.testing.assert_allclose(mu[0], g["command"][0], atol=1e-10)
