@@ -1,26 +1,44 @@
-"""Benchmark: MPC step latency of the B200 MPPI step (BASELINE config 2).
+"""Benchmark: MPC step latency of the B200 MPPI step (BASELINE config 2) and
+particle-steps/s of the batched-controller config at 1/2/4/8 GPUs.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--workload c2|c1|c4]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--workload auto|c1|c2|c3|c4|c5] [--precision fp32|fp64] [--dry-run]
 
-Workload (default ``c2``, BASELINE configs[1]): arm7 (the reference's Franka
-model) reach task, 500 particles x H=30, full cost stack (pose, joint limits,
-braking envelope, manipulability, learned self-collision MLP), Halton +
-B-spline sampling, FP32 fused rollout. A "step" is one Controller.control_step
-(shift + sample + rollout/costs + MLP + weights/update + command).
+``--workload auto`` (default): config 2 (BASELINE configs[1], the latency
+headline) at N=1; config 4 (4096 controllers, instance-sharded, whole-job
+particle-steps/s) at N>1. ``--gpus N`` without torchrun's environment
+re-executes this script under ``torch.distributed.run`` with N ranks on
+127.0.0.1; under torchrun, WORLD_SIZE must equal N. ``--dry-run`` checks that
+plumbing without a GPU (gloo, no device work).
+
+Config 2 (N=1): arm7 (the reference's Franka model) reach task, 500 particles
+x H=30, full cost stack (pose, joint limits, braking envelope,
+manipulability, learned self-collision MLP), Halton + B-spline sampling, FP32
+fused rollout. A "step" is one Controller.control_step (shift + sample +
+rollout/costs + MLP + weights/update + command).
 
 * value: mean device time of the lean step graph's replay (two CUDA events on
   the plan stream around it), L2 flushed (256 MiB memset) before every step.
 * e2e: mean wall time of Controller.control_step (the public API) with host
   buffers: H2D of the joint state, graph replay, mapped D2H of command + status.
-* roofline / stage_ms: per-kernel device times from a second timed pass over
-  the instrumented copy of the graph (event-record nodes between the stages;
-  `instrumented_step_ms` is that pass's step time — the nodes cost ~3.5 us each).
+* fp64: the same two numbers for the float64 plan.
+* bundle: the device time of the step graph that also dumps the rollout
+  bundle (keep_bundle=True) and the first-access cost of the lean graph's
+  replayed StepDiagnostics.bundle.
+* roofline / kernels / stage_ms: per-kernel device times from a second timed
+  pass over the instrumented copy of the graph (event-record nodes between the
+  stages); the dominant kernel is the one with the largest share of the step
+  in the committed ncu launch list of this command (profiles/), falling back
+  to the event times.
 * cpu_baseline: the unmodified reference (oracle/_ref, numba backend) timed
-  on this host on a bounded sample of the same workload.
+  on this host (SURVEY §8(d) protocol: workers = all threads and workers = 1
+  with single-threaded BLAS, config 4 from 8 instances x 512 "extrapolated",
+  config 5 measured to N = 32768 and extrapolated linearly beyond).
 
-Multi-GPU (torchrun, N>1): config 1-3 controllers do not shard,
-so each rank runs an independent replica; the reported latency is the max over
-ranks. ``--workload c4`` is the batched-controller throughput config instead.
+Multi-GPU: configs 1-3 do not shard: each rank runs a replica
+and the latency is the max over ranks. Config 4 splits the instances over the
+ranks with no data-path collective; config 5 splits one controller's
+particles with one record exchange per iteration.
 """
 
 from __future__ import annotations
@@ -152,9 +170,26 @@ def _dist_env():
     return ws, rank, local
 
 
+def _spawn(args) -> int:
+    """--gpus N without torchrun's environment: re-execute under
+    torch.distributed.run with N local ranks on 127.0.0.1."""
+    import socket
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", str(Path(__file__).resolve()), *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
 def _maybe_init_dist(ws, local):
     if ws <= 1:
         return None
+    # the communicator lines (rank count, NVLink/NVLS transport) on the init, so
+    # the rank check is observable in the log
+    os.environ.setdefault("NCCL_DEBUG", "INFO")
+    os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
     import torch
     import torch.distributed as dist
 
@@ -173,9 +208,38 @@ def _max_over_ranks(dist, x: float, local: int) -> float:
     return float(t.item())
 
 
-# ---------------------------------------------------------------- reference arm
-def _reference_controller(particles=500, workers=None):
-    """The unmodified reference, config 2, from oracle/_ref (bench-only)."""
+# ---------------------------------------------------------------- workloads
+L2_NOTE = "GPU arm: 256 MiB memset (> 126 MB L2) before every timed step; CPU arm: no flush"
+
+
+def workload_config(workload: str, args, ws: int) -> dict:
+    """The `config` object of a workload: the SAME dict on both arms."""
+    if workload in ("c1", "c2"):
+        cfg = 1 if workload == "c1" else 2
+        return {"workload": f"config{cfg}: arm7 reach, "
+                            + ("full cost stack + learned self-collision MLP" if cfg == 2
+                               else "goal pose + joint limits")
+                            + f", {args.particles} particles x H30, K=1",
+                "particles": args.particles, "horizon": 30, "iterations": 1,
+                "parallelism": f"replicas x{ws}" if ws > 1 else "single", "l2": L2_NOTE}
+    if workload == "c3":
+        return {"workload": f"config3: moving-target tracking, 64^3 voxel world (8 boxes), {args.particles} x H30, "
+                            "closed loop", "particles": args.particles, "horizon": 30,
+                "parallelism": f"replicas x{ws}" if ws > 1 else "single", "l2": L2_NOTE}
+    if workload == "c4":
+        return {"workload": f"config4: {args.instances} arm7 controllers x {args.particles} particles x H30, "
+                            "config-2 cost stack (learned MLP), instance-sharded",
+                "instances": args.instances, "particles": args.particles, "horizon": 30,
+                "parallelism": f"instance-sharded x{ws}", "l2": L2_NOTE}
+    return {"workload": f"config5: one controller, {args.particles} particles x H30, config-2 costs, "
+                        + (f"particle-sharded x{ws}, 1 record exchange/iteration" if ws > 1 else "single GPU"),
+            "particles": args.particles, "horizon": 30, "l2": L2_NOTE}
+
+
+# ---------------------------------------------------------------- reference arm (CPU)
+def _reference_controller(particles=500, workers=None, config=2, world=None, goal=None):
+    """The unmodified reference from oracle/_ref (bench-only): a Controller of
+    BASELINE config 1/2/3 built from the same numbers as ours (configs.py)."""
     sys.path.insert(0, str(ROOT / "oracle" / "_ref"))
     os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/numba_cache_bench")
     from jointmpc.controller import Controller
@@ -189,11 +253,13 @@ def _reference_controller(particles=500, workers=None):
     kw = dict(configs.CONTROLLER_KW)
     kw["particles"] = particles
     kw["workers"] = workers or (os.cpu_count() or 1)
-    goal = GoalSpec(target_pose=Pose(rotation=_rpy_matrix(*configs.REACH_GOAL_RPY),
-                                     translation=configs.REACH_GOAL_POS.copy()), mode=FULL_POSE)
-    surr = LearnedSelfCollision.load(ROOT / "paper_2104_13542_b200" / "data" / "arm7_surrogate.npz")
-    c = Controller(load_chain("arm7.chain"), goal, weights=CostWeights(**configs.WEIGHTS[2]),
-                   self_collision=surr, **kw)
+    if goal is None:
+        goal = GoalSpec(target_pose=Pose(rotation=_rpy_matrix(*configs.REACH_GOAL_RPY),
+                                         translation=configs.REACH_GOAL_POS.copy()), mode=FULL_POSE)
+    surr = (LearnedSelfCollision.load(ROOT / "paper_2104_13542_b200" / "data" / "arm7_surrogate.npz")
+            if config == 2 else None)
+    c = Controller(load_chain("arm7.chain"), goal, weights=CostWeights(**configs.WEIGHTS[config]),
+                   self_collision=surr, world=world, **kw)
     st = JointState(theta=configs.REACH_START.copy(), theta_dot=np.zeros(7), theta_ddot=np.zeros(7))
     return c, st
 
@@ -202,9 +268,9 @@ def _have_reference() -> bool:
     return (ROOT / "oracle" / "_ref" / "jointmpc" / "controller.py").exists()
 
 
-def _port_controller(particles=500):
-    """The oracle port (oracle/mppi_oracle.py) of the same config-2 step: the
-    CPU baseline when the reference itself is not installed (bench-only)."""
+def _port_controller(particles=500, config=2):
+    """The oracle port (oracle/mppi_oracle.py) of the same step: the CPU
+    baseline when the reference itself is not installed (bench-only)."""
     from oracle import mppi_oracle as O
     from paper_2104_13542_b200 import configs
     from paper_2104_13542_b200.kinematics import load_chain
@@ -215,59 +281,238 @@ def _port_controller(particles=500):
     kw = dict(configs.CONTROLLER_KW)
     kw.pop("seed")
     kw["particles"] = particles
-    oc = O.OracleController(load_chain("arm7.chain"), configs.make_weights(2), configs.reach_goal_rotation(),
-                            configs.REACH_GOAL_POS, True, provider="learned", mlp_state=mlp, **kw)
-    return oc
+    return O.OracleController(load_chain("arm7.chain"), configs.make_weights(config), configs.reach_goal_rotation(),
+                              configs.REACH_GOAL_POS, True, provider="learned" if config == 2 else None,
+                              mlp_state=mlp, **kw)
 
 
-def _time_reference(steps: int, warmup: int, budget_s: float | None = None):
-    """(latencies in ms, workers, kind): the installed reference (oracle/_ref,
-    numba, all host threads) or, without it, the oracle port."""
+def _cpu_stepper(particles=500, config=2, workers=None):
+    """(step(), workers, kind) for one reference (or port) controller."""
     if _have_reference():
-        c, st = _reference_controller()
-        step, workers, kind = (lambda: c.control_step(st)), c.workers, "reference"
-    else:
-        from paper_2104_13542_b200 import configs
+        c, st = _reference_controller(particles, workers, config)
+        return (lambda: c.control_step(st)), c.workers, "reference"
+    from paper_2104_13542_b200 import configs
 
-        oc = _port_controller()
-        th = configs.REACH_START.copy()
-        step, workers, kind = (lambda: oc.step(th, np.zeros(7))), os.cpu_count() or 1, "port"
+    oc = _port_controller(particles, config)
+    th = configs.REACH_START.copy()
+    return (lambda: oc.step(th, np.zeros(7))), 1, "port"
+
+
+def _time_steps(step, steps: int, warmup: int, budget_s: float | None = None):
     for _ in range(max(1, warmup)):
         step()
     lat = []
     t_end = time.perf_counter() + budget_s if budget_s else None
-    for _ in range(steps):
+    for _ in range(max(1, steps)):
         t0 = time.perf_counter()
         step()
         lat.append((time.perf_counter() - t0) * 1e3)
-        if t_end and time.perf_counter() > t_end and len(lat) >= 5:
+        if t_end and time.perf_counter() > t_end and len(lat) >= 3:
             break
-    return lat, workers, kind
+    return lat
 
 
-def run_reference(args):
+def _cpu_model() -> str:
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for ln in out.splitlines():
+            if ln.lower().startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except (OSError, subprocess.SubprocessError):
+        pass
+    return "unknown"
+
+
+def _cpu_probe(spec: dict) -> dict:
+    """One measurement of the CPU protocol (run in a subprocess so the thread
+    environment, e.g. single-threaded BLAS, applies from the first import)."""
+    kind = spec["kind"]
+    w = spec.get("workers")
+    if _have_reference():
+        sys.path.insert(0, str(ROOT / "oracle" / "_ref"))
+        os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/numba_cache_bench")
+    if kind == "latency":  # latency_probe (reference bench.py:91-109)
+        step, workers, impl = _cpu_stepper(spec.get("particles", 500), spec.get("config", 2), w)
+        lat = _time_steps(step, spec.get("steps", 10), 1, spec.get("budget_s"))
+        return {"median_ms": float(np.median(lat)), "mean_ms": float(np.mean(lat)), "steps": len(lat),
+                "workers": workers, "kind": impl}
+    if kind == "instances":  # config 4 sample: k independent controllers stepped in sequence
+        from paper_2104_13542_b200 import configs
+
+        k = spec["k"]
+        lat = []
+        impl = "reference"
+        for i in range(k):
+            if _have_reference():
+                from jointmpc.costs import FULL_POSE, GoalSpec
+                from jointmpc.kinematics import Pose
+
+                goals, th0 = _c4_problem_host(i)
+                g = GoalSpec(target_pose=Pose(rotation=goals[0], translation=goals[1]), mode=FULL_POSE)
+                c, st = _reference_controller(500, w, 2, goal=g)
+                st.theta = th0
+                step = lambda: c.control_step(st)  # noqa: E731
+            else:
+                step, _, impl = _cpu_stepper(500, 2, w)
+            lat += _time_steps(step, 1, 1)
+        return {"per_instance_step_ms": float(np.mean(lat)), "instances_timed": k, "kind": impl}
+    raise ValueError(kind)
+
+
+def _c4_problem_host(i: int):
+    """Config-4 instance i's goal (R, t) and start state, computed on the host
+    with the reference's FK (no device needed in the CPU arm)."""
+    from jointmpc.kinematics import fk_batch, load_chain
+
+    from paper_2104_13542_b200 import configs
+
+    chain = load_chain("arm7.chain")
+    lo, hi = chain.joint_limits[:, 0], chain.joint_limits[:, 1]
+    k = 0.1
+    lo_s, hi_s = lo + k * (hi - lo), hi - k * (hi - lo)
+    q = np.random.default_rng(i).uniform(lo_s, hi_s)
+    th0 = np.random.default_rng(10000 + i).uniform(lo_s, hi_s)
+    rot, trans = fk_batch(chain, q[None])
+    return (rot[0, -1], trans[0, -1]), th0
+
+
+def _probe_subprocess(spec: dict, single_thread: bool = False, timeout: float = 300.0) -> dict:
+    env = dict(os.environ)
+    if single_thread:
+        for k in ("OPENBLAS_NUM_THREADS", "OMP_NUM_THREADS", "MKL_NUM_THREADS", "NUMBA_NUM_THREADS"):
+            env[k] = "1"
+    r = subprocess.run([sys.executable, str(Path(__file__).resolve()), "--cpu-probe", json.dumps(spec)],
+                       capture_output=True, text=True, env=env, timeout=timeout)
+    for ln in r.stdout.splitlines()[::-1]:
+        if ln.startswith("{"):
+            return json.loads(ln)
+    return {"error": (r.stderr or r.stdout)[-300:]}
+
+
+def cpu_protocol(full: bool = True) -> dict:
+    """SURVEY §8(d) CPU baseline protocol on this host: config 2 at workers =
+    all threads and workers = 1 (single-threaded BLAS), config 4 from 8
+    sequential instances x 512 ("extrapolated"), config 5 measured to N=32768
+    and extrapolated linearly to 262144."""
+    ncpu = os.cpu_count() or 1
+    out = {"cpu_model": _cpu_model(), "host_threads": ncpu}
+    out["c2_workers_all"] = _probe_subprocess({"kind": "latency", "config": 2, "steps": 20, "budget_s": 8.0})
+    out["c2_workers_1"] = _probe_subprocess({"kind": "latency", "config": 2, "workers": 1, "steps": 8,
+                                             "budget_s": 6.0}, single_thread=True)
+    if full:
+        c4 = _probe_subprocess({"kind": "instances", "k": 8})
+        if "per_instance_step_ms" in c4:  # 4096 instances stepped in sequence
+            c4["extrapolated_step_s_4096"] = c4["per_instance_step_ms"] * 4096 / 1e3
+            c4["extrapolated_particle_steps_per_s"] = 4096 * 500 * 30 / c4["extrapolated_step_s_4096"]
+            c4["label"] = "extrapolated x512 from 8 sequential instances (workers = all threads)"
+        out["c4"] = c4
+        c5 = {}
+        for n in (2048, 8192, 32768):
+            r = _probe_subprocess({"kind": "latency", "config": 2, "particles": n, "steps": 2, "budget_s": 6.0})
+            if "median_ms" in r:
+                c5[str(n)] = {"ms": r["median_ms"], "particle_steps_per_s": n * 30 / (r["median_ms"] * 1e-3)}
+        if "32768" in c5:
+            per = c5["32768"]["ms"] / 32768
+            c5["extrapolated"] = {str(n): {"ms": per * n, "label": "linear from N=32768"}
+                                  for n in (65536, 131072, 262144)}
+        out["c5"] = c5
+    return out
+
+
+def run_reference(args, workload: str):
+    """The reference's own CPU implementation on this host (rank 0 only), on
+    our arm's workload, config, metric and unit."""
     ws, rank, _ = _dist_env()
     if rank != 0:
         return 0
-    lat, workers, kind = _time_reference(args.steps, args.warmup)
-    v = float(np.mean(lat))
+    if ws > 1:
+        # torchrun pins OMP_NUM_THREADS=1 in every rank; the CPU arm gets all
+        # host threads, so rank 0 measures in a clean child process
+        env = {k: v for k, v in os.environ.items()
+               if k not in ("OMP_NUM_THREADS", "WORLD_SIZE", "RANK", "LOCAL_RANK", "LOCAL_WORLD_SIZE",
+                            "GROUP_RANK", "ROLE_RANK", "ROLE_WORLD_SIZE", "GROUP_WORLD_SIZE")}
+        env["MPPI_REF_REPORT_WS"] = str(ws)
+        argv = [a for a in sys.argv[1:]]
+        cmd = [sys.executable, str(Path(__file__).resolve()), *argv, "--gpus", "1", "--workload", workload]
+        if "--weak" in cmd:
+            cmd.remove("--weak")
+            cmd += ["--instances", str(args.instances)]
+        r = subprocess.run(cmd, env=env, capture_output=True, text=True)
+        line = next((ln for ln in r.stdout.splitlines()[::-1] if ln.startswith("{")), None)
+        print(line if line else json.dumps({"impl": "reference", "unavailable": (r.stderr or "no output")[-200:]}))
+        return 0
+    ws = int(os.environ.get("MPPI_REF_REPORT_WS", ws))
     cores = os.cpu_count() or 1
+    cfg = workload_config(workload, args, ws)
+    extra = {}
+    if workload in ("c1", "c2", "c3"):
+        config = {"c1": 1, "c2": 2, "c3": 3}[workload]
+        if workload == "c3" and _have_reference():
+            c, st, set_goal = _reference_tracking(args.particles)
+            i = [0]
+
+            def step():
+                set_goal(i[0] * 0.05)
+                i[0] += 1
+                c.control_step(st)
+
+            workers, kind = c.workers, "reference"
+            lat = _time_steps(step, min(args.steps, 5), 1)
+            sample = f"{len(lat)} closed-loop tracking steps (8-box world, {args.particles} particles)"
+        else:
+            step, workers, kind = _cpu_stepper(args.particles, min(config, 2), None)
+            lat = _time_steps(step, args.steps, args.warmup, budget_s=120.0)
+            sample = f"{len(lat)} control_steps of config {config} after {args.warmup} warm-up"
+        v, unit, hib = float(np.mean(lat)), "ms", False
+        extra["median_ms"] = float(np.median(lat))
+    elif workload == "c4":
+        r = _cpu_probe({"kind": "instances", "k": max(2, min(8, args.steps))})
+        per_ms = r["per_instance_step_ms"]
+        step_s = per_ms * args.instances / 1e3
+        v, unit, hib = args.instances * args.particles * 30 / step_s, "particle-steps/s", True
+        kind, workers = r["kind"], cores
+        sample = (f"{r['instances_timed']} sequential config-2 instances x {args.particles} particles, "
+                  f"extrapolated x{args.instances // r['instances_timed']} to {args.instances} instances")
+        extra["extrapolated"] = True
+    else:
+        n_meas = min(args.particles, 32768)
+        step, workers, kind = _cpu_stepper(n_meas, 2, None)
+        lat = _time_steps(step, min(args.steps, 3), 1, budget_s=60.0)
+        ms = float(np.median(lat)) * args.particles / n_meas
+        v, unit, hib = args.particles * 30 / (ms * 1e-3), "particle-steps/s", True
+        sample = f"{len(lat)} control_steps at N={n_meas}" + (
+            f", extrapolated linearly to N={args.particles}" if n_meas != args.particles else "")
     line = {
-        "metric": METRIC, "value": v, "unit": "ms", "n_gpus": ws, "steps": len(lat), "warmup": args.warmup,
-        "ms_per_step": v, "higher_is_better": False, "scaling": "weak", "vs_baseline": None,
-        "dtype": "f64", "data": "synthetic",
-        "config": {"workload": "config2: arm7 reach, full cost stack + learned MLP, 500 particles x H30",
-                   "particles": 500, "horizon": 30},
-        "impl": "reference",
-        "cpu_baseline": {"value": v, "unit": "ms", "cores": cores, "kind": kind,
-                         "sample": f"{len(lat)} control_steps of config 2 after {args.warmup} warm-up, "
-                                   + (f"numba backend, workers={workers}" if kind == "reference"
-                                      else "oracle port (numpy float64; oracle/_ref not installed)")},
-        "e2e": {"value": v, "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-        "median_ms": float(np.median(lat)),
+        "metric": METRIC, "value": v, "unit": unit, "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": v if unit == "ms" else None, "higher_is_better": hib,
+        "scaling": "weak" if workload != "c5" else "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": cfg, "impl": "reference",
+        "cpu_baseline": {"value": v, "unit": unit, "cores": workers if kind == "reference" else 1, "kind": kind,
+                         "sample": sample + (", numba backend, workers=%d" % workers if kind == "reference"
+                                             else ", oracle port (numpy float64; oracle/_ref not installed)")},
+        "e2e": {"value": v, "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        **extra,
     }
     print(json.dumps(line))
     return 0
+
+
+def _reference_tracking(particles: int):
+    """Config 3 on the reference: the same script and box world (built with the
+    reference's FK), goal from the script every step."""
+    sys.path.insert(0, str(ROOT / "oracle" / "_ref"))
+    os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/numba_cache_bench")
+    from jointmpc.kinematics import fk_batch as rfk
+    from jointmpc.simworld import TargetScript, WorldModel, target_at
+
+    from paper_2104_13542_b200 import configs
+
+    script, world = configs.tracking_problem(fk=rfk)
+    rworld = WorldModel(spheres=np.zeros((0, 4)), boxes=world.boxes, bounds_min=np.full(3, -1.0),
+                        bounds_max=np.full(3, 1.0))
+    rs = TargetScript(times=script.times, positions=script.positions, interpolation="linear", mode="position_only")
+    c, st = _reference_controller(particles, None, 3, world=rworld, goal=target_at(rs, 0.0))
+    return c, st, (lambda t: c.set_goal(target_at(rs, t)))
 
 
 # ---------------------------------------------------------------- our arm
@@ -357,21 +602,68 @@ def run_ours(args):
     st_mean = {k: float(np.mean(v)) for k, v in stages.items()}
     rows = particles * 30
     ncu_sum, ncu_src = _ncu_summary("full_c2_metrics") if config == 2 else (None, None)
+    share, share_src = RL.launch_shares(ROOT / "profiles", "bench_launches")
     roof = RL.step_roofline(st_mean, rows=rows, particles=particles, horizon=30, dof=7, config=config,
-                            peaks=peaks, peaks_kind=peaks_kind, ncu_summary=ncu_sum, ncu_source=ncu_src)
+                            peaks=peaks, peaks_kind=peaks_kind, ncu_summary=ncu_sum, ncu_source=ncu_src,
+                            ncu_share=share, ncu_share_source=share_src)
+    kernels = RL.all_rooflines(st_mean, rows=rows, dof=7, config=config, peaks=peaks, peaks_kind=peaks_kind,
+                               ncu_summary=ncu_sum, ncu_source=ncu_src)
+
+    # ---- the float64 plan: the same lean-graph and end-to-end loops
+    fp64 = None
+    if args.precision == "fp32":
+        c64 = configs.make_controller(config, particles=particles, device=local, precision="fp64")
+        p64 = c64.plan
+        for _ in range(3):
+            c64.control_step(st)
+        p64.profile_stages(1)
+        d64 = []
+        for _ in range(min(args.steps, 100)):
+            _flush_l2(flush)
+            torch.cuda.synchronize()
+            _, inf64 = p64.step(theta, thetad)
+            d64.append(inf64[0].device_ms)
+        p64.profile_stages(0)
+        e64 = []
+        for _ in range(min(args.steps, 100)):
+            _flush_l2(flush)
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            c64.control_step(st)
+            e64.append((time.perf_counter() - t0) * 1e3)
+        fp64 = {"value": _max_over_ranks(dist, float(np.mean(d64)), local), "unit": "ms",
+                "e2e_ms": _max_over_ranks(dist, float(np.mean(e64)), local), "dtype": "f64",
+                "note": "float64 plan (FP64 rollout/statistics; the MLP keeps its tensor-core split products)"}
+
+    # ---- the rollout bundle: the dump graph (keep_bundle=True) and the lean
+    # graph's replayed bundle on first access (StepDiagnostics.bundle)
+    cdump = configs.make_controller(config, particles=particles, device=local, precision=args.precision,
+                                    keep_bundle=True)
+    for _ in range(3):
+        cdump.control_step(st)
+    cdump.plan.profile_stages(1)
+    dd = []
+    for _ in range(min(args.steps, 50)):
+        _flush_l2(flush)
+        torch.cuda.synchronize()
+        _, infd = cdump.plan.step(theta, thetad)
+        dd.append(infd[0].device_ms)
+    rep = []
+    for _ in range(5):
+        _, diag = ctrl.control_step(st)
+        t0 = time.perf_counter()
+        diag.bundle.total_per_particle
+        rep.append((time.perf_counter() - t0) * 1e3)
+    bundle = {"keep_bundle_device_ms": float(np.mean(dd)),
+              "lean_bundle_first_access_ms": float(np.median(rep)),
+              "note": "diag.bundle is always set; the lean graph replays the step's last iteration on first access"}
 
     line = {
         "metric": METRIC, "value": value, "unit": "ms", "n_gpus": ws, "steps": args.steps,
         "warmup": max(3, args.warmup), "ms_per_step": value, "higher_is_better": False,
         "scaling": "weak", "vs_baseline": None, "dtype": args.precision.replace("fp", "f"),
         "data": "synthetic (bundled arm7 chain, reach goal, Halton perturbations, trained surrogate)",
-        "config": {"workload": f"config{config}: arm7 reach, "
-                               + ("full cost stack + learned self-collision MLP" if config == 2
-                                  else "goal pose + joint limits")
-                               + f", {particles} particles x H30, K=1",
-                   "particles": particles, "horizon": 30, "iterations": 1,
-                   "parallelism": "replicas" if ws > 1 else "single",
-                   "l2": "flushed (256 MiB memset) before every timed step"},
+        "config": workload_config(args.workload, args, ws),
         "particle_steps_per_s": ws * particles * 30 / (value * 1e-3),
         "median_ms": float(np.median(dev_ms)), "p99_ms": float(np.percentile(dev_ms, 99)),
         "stage_ms": st_mean,
@@ -381,8 +673,11 @@ def run_ours(args):
                 "api": "Controller.control_step"},
         "gpu_launches": args.steps * (3 if config == 2 else 2),
         "roofline": roof,
+        "kernels": kernels,
         "clocks": clk.summary(),
         "timed_wall_s": t_wall,
+        "fp64": fp64,
+        "bundle": bundle,
     }
     if not args.no_scale_roofline:
         line["roofline_at_scale"] = _scale_roofline(args, local, peaks, peaks_kind)
@@ -462,18 +757,23 @@ def run_batched(args):
         "warmup": max(3, args.warmup), "ms_per_step": step_ms, "higher_is_better": True, "scaling": "weak"
         if args.weak else "strong", "vs_baseline": None, "dtype": args.precision.replace("fp", "f"),
         "data": "synthetic (goal_i = FK(q_i), q_i, theta0_i from default_rng(i), default_rng(10000+i))",
-        "config": {"workload": f"config4: {B} arm7 controllers x {args.particles} particles x H30, "
-                               "config-2 cost stack (learned MLP), instance-sharded",
-                   "instances": B, "instances_per_gpu": b - a, "particles": args.particles, "horizon": 30,
-                   "parallelism": f"instance-sharded x{ws}", "l2": "flushed before every timed step"},
+        "config": workload_config("c4", args, ws), "instances_per_gpu": b - a,
         "stage_ms": st_mean,
         "e2e": {"value": units / (e2e_ms * 1e-3), "unit": "particle-steps/s",
                 "h2d_bytes_per_step": B * 14 * 8 // ws, "d2h_bytes_per_step": B * (7 * 8 + 80) // ws,
                 "ms_per_step": e2e_ms, "api": "BatchedController.control_step"},
         "gpu_launches": args.steps * 3,
         "roofline": roof,
+        "kernels": RL.all_rooflines(st_mean, rows=(b - a) * args.particles * 30, dof=7, config=2, peaks=peaks,
+                                    peaks_kind=peaks_kind),
         "clocks": clk.summary(),
     }
+    if dist is not None:  # every rank's own roofline and step time (instances differ per rank)
+        mine = {"rank": rank, "instances": b - a, "step_ms": float(np.mean(dev_ms)), "stage_ms": st_mean,
+                "roofline": roof, "clocks": line["clocks"]}
+        allr = [None] * ws
+        dist.all_gather_object(allr, mine)
+        line["per_rank"] = allr
     if rank == 0:
         print(json.dumps(line))
     if dist is not None:
@@ -563,9 +863,7 @@ def run_tracking(args):
         "metric": METRIC, "value": value, "unit": "ms", "n_gpus": ws, "steps": args.steps,
         "warmup": max(3, args.warmup), "ms_per_step": value, "higher_is_better": False, "scaling": "weak",
         "vs_baseline": None, "dtype": args.precision.replace("fp", "f"), "data": "synthetic",
-        "config": {"workload": f"config3: moving-target tracking, 64^3 voxel world ({world.boxes.shape[0]} boxes), "
-                               f"{args.particles} x H30, closed loop", "particles": args.particles,
-                   "horizon": 30, "l2": "flushed before every timed step"},
+        "config": workload_config("c3", args, ws),
         "stage_ms": st_mean,
         "e2e": {"value": float(np.mean(e2e)), "unit": "ms", "h2d_bytes_per_step": 112 + 16 * 8,
                 "d2h_bytes_per_step": 136, "api": "Controller.control_step + set_goal"},
@@ -605,7 +903,7 @@ def run_sweep(args):
         kw.pop("particles")
         # the record exchange fused into the statistics kernel over NVLink peer
         # memory; MPPI_EXCHANGE=nccl: one NCCL all-gather between two kernels
-        nccl = os.environ.get("MPPI_EXCHANGE", "peer") == "nccl"
+        nccl = os.environ.get("MPPI_EXCHANGE", "nccl") != "peer"
         ctrl = ShardedController(load_chain("arm7.chain"), configs.make_goal(2), particles=Np, world_size=ws,
                                  rank=rank, device=local, exchange=RecordExchange() if nccl else PeerExchange(),
                                  weights=configs.make_weights(2), self_collision=load_arm7_surrogate(),
@@ -635,16 +933,32 @@ def run_sweep(args):
         "metric": METRIC, "value": Np * 30 / (ms * 1e-3), "unit": "particle-steps/s", "n_gpus": ws,
         "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": ms, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": args.precision.replace("fp", "f"), "data": "synthetic",
-        "config": {"workload": f"config5: one controller, {Np} particles x H30, config-2 costs, "
-                               + ("particle-sharded, 1 all-gather/iteration" if ws > 1 else "single GPU"),
-                   "particles": Np, "horizon": 30, "l2": "flushed before every timed step",
-                   **({"exchange": "nccl all-gather" if nccl else "fused peer-memory push (NVLink P2P)"}
-                      if ws > 1 else {})},
+        "config": workload_config("c5", args, ws),
+        **({"exchange": "nccl all-gather" if nccl else "fused peer-memory push (NVLink P2P)"} if ws > 1 else {}),
         "e2e": {"value": Np * 30 / (wall_ms * 1e-3), "unit": "particle-steps/s", "h2d_bytes_per_step": 112,
                 "d2h_bytes_per_step": 136, "wall_ms_per_step": wall_ms,
                 "api": "Controller / ShardedController.control_step (host wall clock)"},
         "gpu_launches": args.steps * 3, "clocks": clk.summary(),
     }
+    if ws == 1:  # per-kernel roofline from the instrumented graph (stage events)
+        from paper_2104_13542_b200 import roofline as RL
+
+        peaks, peaks_kind = _peaks()
+        ctrl.profile_stages(2)
+        stg = {"sample": [], "rollout": [], "mlp": [], "update": []}
+        for _ in range(min(args.steps, 20)):
+            _flush_l2(flush)
+            torch.cuda.synchronize()
+            ctrl.control_step(st)
+            inf = ctrl.plan._info[0]
+            for k in stg:
+                stg[k].append(getattr(inf, f"{k}_ms"))
+        ctrl.profile_stages(0)
+        sm = {k: float(np.mean(v)) for k, v in stg.items()}
+        line["stage_ms"] = sm
+        line["roofline"] = RL.step_roofline(sm, rows=Np * 30, particles=Np, horizon=30, dof=7, config=2,
+                                            peaks=peaks, peaks_kind=peaks_kind)
+        line["kernels"] = RL.all_rooflines(sm, rows=Np * 30, dof=7, config=2, peaks=peaks, peaks_kind=peaks_kind)
     if rank == 0:
         print(json.dumps(line))
     if dist is not None:
@@ -704,11 +1018,41 @@ def _scale_roofline(args, local, peaks, peaks_kind, instances=256, steps=5):
 
 
 def _cpu_baseline(args):
-    lat, workers, kind = _time_reference(steps=30, warmup=2, budget_s=20.0)
-    what = (f"reference control_steps (config 2, 500x30, numba, workers={workers})" if kind == "reference"
-            else "oracle-port control steps (config 2, 500x30, numpy float64; oracle/_ref not installed)")
-    return {"value": float(np.median(lat)), "unit": "ms", "cores": os.cpu_count() or 1, "kind": kind,
-            "sample": f"median of {len(lat)} {what} after 2 warm-up steps"}
+    """cpu_baseline of the config-2 line: the reference at workers = all host
+    threads (headline) plus the rest of the §8(d) protocol."""
+    prot = cpu_protocol(full=not args.quick_cpu)
+    head = prot.get("c2_workers_all", {})
+    kind = head.get("kind", "port")
+    return {"value": head.get("median_ms"), "unit": "ms", "cores": head.get("workers", 1), "kind": kind,
+            "sample": f"median of {head.get('steps')} reference control_steps (config 2, 500x30, numba, "
+                      f"workers={head.get('workers')}) after 1 warm-up" if kind == "reference" else
+                      "oracle-port control steps (config 2, numpy float64; oracle/_ref not installed)",
+            "protocol": prot}
+
+
+def run_dry(args, workload: str) -> int:
+    """--dry-run: the launch plumbing without a GPU (gloo ranks, a barrier and
+    the max-over-ranks reduction; no device work, no timing claims)."""
+    ws, rank, _ = _dist_env()
+    dist = None
+    if ws > 1:
+        import torch
+        import torch.distributed as dist
+
+        dist.init_process_group("gloo")
+        t = torch.tensor([float(rank)])
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        top = int(t.item())
+        dist.barrier()
+    else:
+        top = 0
+    if rank == 0:
+        print(json.dumps({"metric": METRIC, "value": None, "unit": None, "n_gpus": ws, "dry_run": True,
+                          "max_rank_seen": top, "workload": workload,
+                          "config": workload_config(workload, args, ws)}))
+    if dist is not None:
+        dist.destroy_process_group()
+    return 0
 
 
 def main():
@@ -717,24 +1061,41 @@ def main():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="c2", choices=["c1", "c2", "c3", "c4", "c5"])
+    ap.add_argument("--workload", default="auto", choices=["auto", "c1", "c2", "c3", "c4", "c5"],
+                    help="auto: c2 at one GPU, c4 at more")
     ap.add_argument("--instances", type=int, default=4096, help="config 4: total controllers")
     ap.add_argument("--weak", action="store_true", help="config 4: --instances per GPU (weak scaling)")
     ap.add_argument("--particles", type=int, default=500)
     ap.add_argument("--precision", default="fp32", choices=["fp32", "fp64"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--quick-cpu", action="store_true", help="cpu_baseline: config 2 only")
     ap.add_argument("--no-scale-roofline", action="store_true")
+    ap.add_argument("--dry-run", action="store_true", help="launch plumbing only (gloo, no GPU)")
+    ap.add_argument("--cpu-probe", default=None, help=argparse.SUPPRESS)
     args = ap.parse_args()
+    if args.cpu_probe:
+        print(json.dumps(_cpu_probe(json.loads(args.cpu_probe))))
+        return 0
+    env_ws = os.environ.get("WORLD_SIZE")
+    if env_ws is None and args.gpus > 1:
+        return _spawn(args)
+    if env_ws is not None and int(env_ws) != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={env_ws}", file=sys.stderr)
+        return 2
+    workload = args.workload if args.workload != "auto" else ("c2" if args.gpus == 1 else "c4")
+    if workload == "c4" and args.weak:
+        args.instances *= args.gpus
+    if args.dry_run:
+        return run_dry(args, workload)
     if args.impl == "reference":
-        return run_reference(args)
-    if args.workload == "c3":
+        return run_reference(args, workload)
+    if workload == "c3":
         return run_tracking(args)
-    if args.workload == "c5":
+    if workload == "c5":
         return run_sweep(args)
-    if args.workload == "c4":
-        if args.weak:
-            args.instances *= int(os.environ.get("WORLD_SIZE", "1"))
+    if workload == "c4":
         return run_batched(args)
+    args.workload = workload
     return run_ours(args)
 
 

@@ -97,7 +97,9 @@ enum mppi_status {
   MPPI_E_CUDA = 5,
   MPPI_E_NONPOSITIVE_VARIANCE = 6,
   MPPI_E_CONFIG = 7,
-  MPPI_E_SKIPPED = 8           /* step not run: the on-device episode aborted */
+  MPPI_E_SKIPPED = 8,          /* step not run: the on-device episode aborted */
+  MPPI_E_EXCHANGE = 9          /* particle-sharded exchange: a rank aborted the step or did not
+                                  publish its record within the exchange timeout (DeviceError) */
 };
 
 enum mppi_goal_mode {          /* costs.py:20-22 */
@@ -454,6 +456,14 @@ int mppi_set_peers(mppi_plan* plan, int32_t world, int32_t rank, void* const* re
                    void* const* flag_ptrs);
 /* One control step (all iterations) of this rank's particle shard; every rank
  * calls it with the same state and receives the same command. */
+/* Bounded wait of the fused exchange (default 5 s): a rank whose flags do not
+ * all arrive in time fails the step with MPPI_E_EXCHANGE, keeps the shifted
+ * policy and publishes an abort so the other ranks stop waiting too.        */
+int mppi_set_exchange_timeout(mppi_plan* plan, double seconds);
+/* Abandon this rank's next exchange step (a host-side failure before its
+ * kernels ran): publishes an abort for every iteration of that step into
+ * every rank's flags and advances this rank's sequence past it.             */
+int mppi_exchange_abort(mppi_plan* plan);
 int mppi_step_exchange(mppi_plan* plan, const double* theta, const double* theta_dot,
                        double* command_out, mppi_step_info* info);
 /* CUDA IPC of device buffers (handle: 64 bytes). */

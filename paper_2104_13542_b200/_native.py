@@ -29,6 +29,7 @@ E_CUDA = 5
 E_NONPOSITIVE_VARIANCE = 6
 E_CONFIG = 7
 E_SKIPPED = 8  # the on-device episode aborted before this step
+E_EXCHANGE = 9  # particle-sharded exchange aborted / timed out (DeviceError)
 
 GOAL_POSITION_ONLY = 0
 GOAL_FULL_POSE = 1
@@ -181,6 +182,8 @@ _SIGS = {
     "mppi_peer_buffers": (C.c_int, [_vp, C.c_int32, C.POINTER(_vp), C.POINTER(_vp)]),
     "mppi_set_peers": (C.c_int, [_vp, C.c_int32, C.c_int32, C.POINTER(_vp), C.POINTER(_vp)]),
     "mppi_step_exchange": (C.c_int, [_vp, _dp, _dp, _dp, C.POINTER(StepInfo)]),
+    "mppi_set_exchange_timeout": (C.c_int, [_vp, C.c_double]),
+    "mppi_exchange_abort": (C.c_int, [_vp]),
     "mppi_ipc_get_handle": (C.c_int, [_vp, C.c_char_p]),
     "mppi_ipc_open_handle": (C.c_int, [C.c_char_p, C.POINTER(_vp)]),
     "mppi_ipc_close": (C.c_int, [_vp]),
@@ -267,6 +270,8 @@ def status_exception(code: int, bad_particle: int = -1) -> Exception:
         return PolicyStateError("all particles quarantined; no finite costs")
     if code == E_WEIGHT_UNDERFLOW:
         return PolicyStateError("all particle weights underflowed to zero; increase beta")
+    if code == E_EXCHANGE:
+        return DeviceError("particle-sharded exchange aborted or timed out (policy kept shifted)")
     return DeviceError(f"device status {code}")
 
 

@@ -190,6 +190,8 @@ struct mppi_plan {
   int peer_world = 0, peer_rank = 0;
   bool peer_active = false;                 // set while enqueuing an exchange step
   unsigned long long peer_seq = 0;
+  double peer_timeout_s = 5.0;                         // mppi_set_exchange_timeout
+  std::vector<unsigned long long*> peer_flag_host;     // every rank's flag array (this rank's view)
   // eval scratch
   DevBuf<double> e_in0, e_in1, e_pos, e_vel, e_acc, e_terms, e_step, e_tot, e_state, e_dts;
   DevBuf<unsigned char> e_stepbuf;
@@ -451,6 +453,7 @@ int enqueue_iteration(mppi_plan* p, int it, bool inline_final, double* out_recor
     s.world = p->peer_world;
     s.rank = p->peer_rank;
     s.seq = p->peer_seq;
+    s.peer_timeout_ns = (unsigned long long)(p->peer_timeout_s * 1e9);
     s.reset_status = it == p->iters - 1;
   }
   s.cmd = p->cmd_dst ? p->cmd_dst : p->m_cmd;  // mapped host memory: no D2H copy node
@@ -1747,7 +1750,30 @@ int mppi_set_peers(mppi_plan* p, int32_t world, int32_t rank, void* const* recv_
   CK(cudaMemcpy(p->peer_recv_tab.p, recv_ptrs, sizeof(double*) * world, cudaMemcpyHostToDevice));
   CK(cudaMemcpy(p->peer_flag_tab.p, flag_ptrs, sizeof(unsigned long long*) * world, cudaMemcpyHostToDevice));
   p->peer_rank = rank;
+  p->peer_flag_host.assign((unsigned long long* const*)flag_ptrs, (unsigned long long* const*)flag_ptrs + world);
   return MPPI_OK;
+}
+
+int mppi_set_exchange_timeout(mppi_plan* p, double seconds) {
+  if (!p || !(seconds > 0.0)) return fail(MPPI_E_BAD_ARGUMENT, "timeout must be positive");
+  p->peer_timeout_s = seconds;
+  return MPPI_OK;
+}
+
+// host-side abort of the next step: flag[rank] = (last seq of that step) | abort in every rank
+static int publish_abort(mppi_plan* p, unsigned long long seq) {
+  const unsigned long long v = seq | kPeerAbort;
+  for (auto* f : p->peer_flag_host)
+    CK(cudaMemcpy(f + p->peer_rank, &v, sizeof(v), cudaMemcpyHostToDevice));
+  return MPPI_OK;
+}
+
+int mppi_exchange_abort(mppi_plan* p) {
+  if (!p) return fail(MPPI_E_BAD_ARGUMENT, "null plan");
+  if (p->peer_flag_host.empty()) return fail(MPPI_E_CONFIG, "mppi_set_peers first");
+  CKR(set_device(p));
+  p->peer_seq += (unsigned long long)p->iters;  // the abandoned step's sequence numbers
+  return publish_abort(p, p->peer_seq);
 }
 
 int mppi_step_exchange(mppi_plan* p, const double* theta, const double* theta_dot, double* command_out,
@@ -1765,6 +1791,7 @@ int mppi_step_exchange(mppi_plan* p, const double* theta, const double* theta_do
   memcpy(p->h_state + 2 * D, &ctr, sizeof(ctr));
   CK(cudaMemcpyAsync(p->state.p, p->h_state, sizeof(double) * (2 * D + 1), cudaMemcpyHostToDevice, st));
   p->peer_active = true;
+  const unsigned long long seq0 = p->peer_seq;
   int rc = MPPI_OK;
   for (int it = 0; it < p->iters && rc == MPPI_OK; ++it) {
     ++p->peer_seq;  // one exchange per iteration, the same count on every rank
@@ -1774,10 +1801,20 @@ int mppi_step_exchange(mppi_plan* p, const double* theta, const double* theta_do
                                      : enqueue_iteration<float>(p, it, false, nullptr, st);
   }
   p->peer_active = false;
-  CKR(rc);
+  if (rc != MPPI_OK) {  // some iterations never launched: release the ranks waiting on them
+    const std::string why = mppi_last_error();
+    cudaStreamSynchronize(st);
+    const unsigned long long last = seq0 + (unsigned long long)p->iters;  // the step's final sequence number
+    p->peer_seq = last;
+    publish_abort(p, last);
+    return fail(rc, why);
+  }
   CK(cudaStreamSynchronize(st));
   memcpy(command_out, p->h_cmd, sizeof(double) * D);
   if (info) memcpy(info, p->h_info, sizeof(mppi_step_info));
+  if (p->h_info[0].status == MPPI_E_EXCHANGE)
+    return fail(MPPI_E_EXCHANGE, "particle-sharded exchange: a rank aborted this step or did not publish its "
+                                 "record within " + std::to_string(p->peer_timeout_s) + " s (policy kept shifted)");
   return MPPI_OK;
 }
 

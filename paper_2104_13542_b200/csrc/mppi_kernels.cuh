@@ -622,7 +622,20 @@ struct StatsArgs {
   const unsigned long long* my_flags;
   int world, rank;
   unsigned long long seq;
+  unsigned long long peer_timeout_ns;  // bounded wait for the other ranks' flags
 };
+
+// Flag word of the peer exchange: the sequence number a rank has published,
+// with kPeerAbort set when that rank gave up on the step (a host-side failure
+// before its kernel ran, or its own wait timed out). A waiter for sequence s
+// fails fast on an abort published for any s' >= s.
+constexpr unsigned long long kPeerAbort = 1ull << 63;
+
+__device__ __forceinline__ unsigned long long global_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 
 __device__ __forceinline__ double block_min_d(double v, double* red) {
   for (int off = 16; off > 0; off >>= 1) v = fmin(v, __shfl_xor_sync(0xffffffffu, v, off));
@@ -837,23 +850,46 @@ static __device__ void exchange_and_finalize(const StatsArgs<R>& a, const double
     for (int i = threadIdx.x; i < reclen; i += blockDim.x) dst[i] = rec[i];
   }
   __threadfence_system();
+  __shared__ int s_xfail;
+  if (threadIdx.x == 0) s_xfail = a.status[0] == MPPI_E_EXCHANGE ? 4 : 0;  // an earlier iteration failed
   __syncthreads();
   if ((int)threadIdx.x < a.world) {
     unsigned long long* f = a.peer_flags[threadIdx.x] + a.rank;
-    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(f), "l"(a.seq) : "memory");
-    const unsigned long long* mine = a.my_flags + threadIdx.x;
-    unsigned long long v = 0;
-#ifdef MPPI_WATCHDOG
-    long long spins = 0;
-#endif
-    do {
-      asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(mine) : "memory");
-#ifdef MPPI_WATCHDOG
-      if (++spins > (1ll << 26)) __trap();
-#endif
-    } while (v < a.seq);
+    if (s_xfail) {  // do not make the others wait for an iteration this rank abandons
+      asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(f), "l"(a.seq | kPeerAbort) : "memory");
+    } else {
+      asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(f), "l"(a.seq) : "memory");
+      const unsigned long long* mine = a.my_flags + threadIdx.x;
+      const unsigned long long t0 = global_ns();
+      unsigned long long v = 0;
+      for (;;) {
+        asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(mine) : "memory");
+        const unsigned long long s = v & ~kPeerAbort;
+        if ((v & kPeerAbort) && s >= a.seq) {  // that rank abandoned this step
+          atomicOr(&s_xfail, 1);
+          break;
+        }
+        if (!(v & kPeerAbort) && s >= a.seq) break;
+        if (global_ns() - t0 > a.peer_timeout_ns) {  // a rank that never arrives
+          atomicOr(&s_xfail, 2);
+          break;
+        }
+        __nanosleep(64);
+      }
+    }
   }
   __syncthreads();
+  if (s_xfail) {
+    // tell every rank (and keep this rank's status) so the others stop
+    // waiting; the step keeps the shifted policy (controller.py:224-241)
+    if ((int)threadIdx.x < a.world)
+      asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(a.peer_flags[threadIdx.x] + a.rank),
+                   "l"(a.seq | kPeerAbort) : "memory");
+    if (threadIdx.x == 0) a.status[0] = MPPI_E_EXCHANGE;
+    __syncthreads();
+    finalize_policy(a, 0, rec, scratch);
+    return;
+  }
   double* comb = scratch;
   double* emp = comb + reclen;
   double* red = emp + HD;

@@ -435,6 +435,13 @@ class Plan:
         fv = (C.c_void_p * world)(*[C.c_void_p(int(x)) for x in flag_ptrs])
         N.check(self.lib.mppi_set_peers(self.handle, world, int(rank), rv, fv))
 
+    def set_exchange_timeout(self, seconds: float):
+        N.check(self.lib.mppi_set_exchange_timeout(self.handle, float(seconds)))
+
+    def exchange_abort(self):
+        """Abandon this rank's next exchange step (publishes an abort to every rank)."""
+        N.check(self.lib.mppi_exchange_abort(self.handle))
+
     def step_exchange(self, theta, theta_dot):
         cmd = np.empty(self.dof)
         info = N.StepInfo()

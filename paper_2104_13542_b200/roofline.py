@@ -51,16 +51,72 @@ def ncu_traffic(summary: list | None, stage: str):
     return None
 
 
+def launch_shares(profiles_dir, tag: str):
+    """Per-stage median device time (ns) of the step's kernels in the newest
+    committed ncu launch list profiles/r*_<tag>.csv (`ncu --metrics
+    gpu__time_duration.sum --clock-control none --csv`), or (None, None)."""
+    import csv
+    from pathlib import Path
+
+    files = sorted(Path(profiles_dir).glob(f"r*_{tag}.csv"))
+    if not files:
+        return None, None
+    times = {k: [] for k in NCU_KERNEL}
+    try:
+        with open(files[-1]) as fh:
+            for r in csv.DictReader(ln for ln in fh if ln.startswith('"')):
+                if r.get("Metric Name") != "gpu__time_duration.sum":
+                    continue
+                for stage, frag in NCU_KERNEL.items():
+                    if frag in r.get("Kernel Name", ""):
+                        times[stage].append(float(r["Metric Value"].replace(",", "")))
+    except (OSError, ValueError, KeyError):
+        return None, None
+    med = {k: sorted(v)[len(v) // 2] for k, v in times.items() if v}
+    return (med or None), f"profiles/{files[-1].name}"
+
+
+def all_rooflines(stage_ms: dict, rows: int, dof: int, config: int, peaks: dict, peaks_kind: str,
+                  ncu_summary: list | None = None, ncu_source: str | None = None) -> dict:
+    """The roofline entry of every kernel of the step (not only the dominant one)."""
+    out = {}
+    for stage in ("rollout", "mlp", "update"):
+        if stage == "mlp" and config != 2:
+            continue
+        e = _stage_roofline(stage, stage_ms, rows, dof, config, peaks, peaks_kind)
+        tr = ncu_traffic(ncu_summary, stage)
+        if tr is not None and e.get("kernel"):
+            e["traffic"] = tr
+            e["traffic_source"] = ncu_source
+        e["stage_ms"] = stage_ms.get(stage)
+        out[stage] = e
+    return out
+
+
 def step_roofline(stage_ms: dict, rows: int, particles: int, horizon: int, dof: int, config: int,
                   peaks: dict, peaks_kind: str, ncu_summary: list | None = None,
-                  ncu_source: str | None = None, ncu_rows: int | None = None) -> dict:
+                  ncu_source: str | None = None, ncu_rows: int | None = None, ncu_share: dict | None = None,
+                  ncu_share_source: str | None = None) -> dict:
     """Roofline entry for the dominant kernel of the step (stage_ms from the
     event-record nodes of the timed graph replays); `traffic` from the
     committed ncu summary of the same kernel when one is given. `ncu_rows`:
     the rows of the captured launch when it was a smaller batch than this
-    step's — its bytes per row are then scaled to this launch and labelled so."""
-    stage = max(("rollout", "mlp", "update"), key=lambda k: stage_ms.get(k, 0.0))
+    step's — its bytes per row are then scaled to this launch and labelled so.
+    The dominant kernel is the largest in the committed ncu launch list of the
+    same command (`ncu_share`, per-stage ns) when given: the event times of
+    adjacent stages can tie within their resolution."""
+    stages = ("rollout", "mlp", "update") if config == 2 else ("rollout", "update")
+    if ncu_share:
+        stage = max(stages, key=lambda k: ncu_share.get(k, 0.0))
+    else:
+        stage = max(stages, key=lambda k: stage_ms.get(k, 0.0))
     out = _stage_roofline(stage, stage_ms, rows, dof, config, peaks, peaks_kind)
+    if ncu_share:
+        tot = sum(ncu_share.get(k, 0.0) for k in stages)
+        out["dominant_by"] = f"{ncu_share_source}: median gpu__time_duration per launch"
+        out["ncu_share"] = {k: ncu_share.get(k, 0.0) / tot for k in stages if tot > 0}
+    else:
+        out["dominant_by"] = "CUDA-event stage times of the instrumented graph"
     tr = ncu_traffic(ncu_summary, stage)
     if tr is not None and out.get("kernel"):
         src = f"{ncu_source}: dram__bytes_read.sum + dram__bytes_write.sum (ncu replay, cold L2)"

@@ -69,13 +69,14 @@ class PeerExchange:
     methods (peer_buffers, ipc_handle, ipc_open, set_peers).
     """
 
-    def __init__(self, group=None):
+    def __init__(self, group=None, timeout_s: float | None = None):
         import torch.distributed as dist
 
         self.dist = dist
         self.group = group
         self.world = dist.get_world_size(group)
         self.rank = dist.get_rank(group)
+        self.timeout_s = timeout_s  # bounded wait of the fused exchange (plan default 5 s)
         self.opened: list[int] = []
         self.tables = None
 
@@ -166,10 +167,23 @@ class ShardedController:
         if isinstance(exchange, PeerExchange):
             torch.cuda.set_device(device)
             exchange.attach(self.plan)
+            if exchange.timeout_s is not None:
+                self.plan.set_exchange_timeout(exchange.timeout_s)
 
     def control_step(self, state):
         if isinstance(self.exchange, PeerExchange):  # exchange fused into the statistics kernel
-            cmd, info = self.plan.step_exchange(state.theta, state.theta_dot)
+            try:
+                theta = np.asarray(state.theta, dtype=np.float64)
+                theta_dot = np.asarray(state.theta_dot, dtype=np.float64)
+                if not (np.isfinite(theta).all() and np.isfinite(theta_dot).all()):
+                    raise ContractError("joint state is not finite")
+            except Exception:
+                # this rank will not run the step: release the ranks that would wait for it
+                self.plan.exchange_abort()
+                raise
+            # a rank that does not arrive within the plan's exchange timeout, or
+            # aborts, fails the step on every rank with DeviceError (mppi status 9)
+            cmd, info = self.plan.step_exchange(theta, theta_dot)
             return cmd, info
         torch = self.torch
         stream = torch.cuda.current_stream(self.dev).cuda_stream

@@ -322,3 +322,78 @@ def test_sharded_goal_change_on_caller_stream():
             cmd, info = p.finalize_dev(rec.data_ptr(), 1, side.cuda_stream)
         assert info.status == 0
         np.testing.assert_allclose(cmd, cmd_ref, atol=1e-9, err_msg=f"step {step}")
+
+
+def _exchange_pair(n=300):
+    """Two single-instance plans wired as ranks 0 and 1 of a two-rank
+    exchange on one GPU. Only rank 0 is ever stepped: rank 1 is a rank that
+    never arrives (or that aborts from the host), so no two kernels wait on
+    each other."""
+    from paper_2104_13542_b200 import configs
+    from paper_2104_13542_b200 import _native as N
+    from paper_2104_13542_b200.engine import Plan, PlanSpec
+    from paper_2104_13542_b200.kinematics import load_chain
+    from paper_2104_13542_b200.rollout import make_dt_schedule
+
+    chain = load_chain("arm7.chain")
+    goal = configs.make_goal(1)
+    plans = []
+    for r in range(2):
+        spec = PlanSpec(horizon=30, particles=n // 2, dts=make_dt_schedule(30, 0.05, "two_phase").dts,
+                        null_count=2, precision=N.FP32, particle_offset=r * (n // 2), particles_total=n, gamma=0.99,
+                        beta=1.0, alpha_mu=0.9, alpha_sigma=0.5, sigma0_sq=0.5, sigma_sq_min=0.01, sigma_sq_max=0.5,
+                        knots=5)
+        p = Plan(chain, configs.make_weights(1), spec)
+        p.init_noise()
+        p.set_goal(goal.target_pose.rotation, goal.target_pose.translation, goal.mode_code, 0)
+        plans.append(p)
+    bufs = [p.peer_buffers(2) for p in plans]
+    recv, flags = [b[0] for b in bufs], [b[1] for b in bufs]
+    for r, p in enumerate(plans):
+        p.set_peers(r, recv, flags)
+    return plans
+
+
+def test_peer_exchange_rank_that_never_arrives_times_out():
+    """ADVICE/VERDICT r1: the fused exchange's wait is bounded. Rank 1 never
+    runs: rank 0's step fails with DeviceError (status 9) after the timeout
+    instead of hanging, and its policy is the shifted warm start."""
+    import time
+
+    from paper_2104_13542_b200 import configs
+    from paper_2104_13542_b200.errors import DeviceError
+
+    r0, _ = _exchange_pair()
+    rng = np.random.default_rng(0)
+    m0, v0 = rng.normal(size=(30, 7)), np.full((30, 7), 0.3)
+    r0.set_policy(m0, v0, 0)
+    r0.set_exchange_timeout(0.2)
+    st = configs.start_state()
+    t0 = time.perf_counter()
+    with pytest.raises(DeviceError, match="exchange"):
+        r0.step_exchange(st.theta, st.theta_dot)
+    dt = time.perf_counter() - t0
+    assert dt < 5.0, dt
+    m, v = r0.get_policy(0)
+    np.testing.assert_array_equal(m[:-1], m0[1:])  # shift stands (controller.py:200, 224-241)
+    np.testing.assert_array_equal(m[-1], 0.0)
+    np.testing.assert_array_equal(v[:-1], v0[1:])
+
+
+def test_peer_exchange_abort_releases_waiting_rank():
+    """A rank that fails on the host before its kernels run publishes an abort
+    (mppi_exchange_abort); the waiting rank fails fast with DeviceError,
+    well inside a long timeout."""
+    import time
+
+    from paper_2104_13542_b200 import configs
+    from paper_2104_13542_b200.errors import DeviceError
+
+    r0, r1 = _exchange_pair()
+    r0.set_exchange_timeout(30.0)
+    r1.exchange_abort()  # rank 1 abandons its first step
+    st = configs.start_state()
+    t0 = time.perf_counter()
+    with pytest.raises(DeviceError, match="exchange"):
+        r0.step_exchange(st.theta, st.theta_dot)
+    assert time.perf_counter() - t0 < 10.0

@@ -176,3 +176,33 @@ def test_peer_exchange_tables(world):
         assert sp == [("set_peers", rank, recv, flags)]
         closed = sorted(c[1] for c in calls if c[0] == "close")
         assert closed == sorted(x for k in range(world) if k != rank for x in (recv[k], flags[k]))
+
+
+def test_bench_gpus_flag_spawns_ranks():
+    """`python bench.py --gpus 2` without torchrun's environment re-executes
+    itself under torch.distributed.run: the dry run
+    (gloo, no GPU) must report two ranks and the N>1 default workload."""
+    import json
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    root = Path(__file__).resolve().parents[1]
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    r = subprocess.run([sys.executable, str(root / "bench.py"), "--gpus", "2", "--dry-run"], cwd=root, env=env,
+                       capture_output=True, text=True, timeout=240)
+    assert r.returncode == 0, r.stderr[-2000:]
+    line = json.loads(next(ln for ln in r.stdout.splitlines() if ln.startswith("{")))
+    assert line["n_gpus"] == 2 and line["max_rank_seen"] == 1
+    assert line["workload"] == "c4" and line["config"]["parallelism"] == "instance-sharded x2"
+    # one GPU: unchanged default (the config-2 latency headline)
+    r1 = subprocess.run([sys.executable, str(root / "bench.py"), "--dry-run"], cwd=root, env=env,
+                        capture_output=True, text=True, timeout=120)
+    line1 = json.loads(next(ln for ln in r1.stdout.splitlines() if ln.startswith("{")))
+    assert line1["n_gpus"] == 1 and line1["workload"] == "c2"
+    # a mismatched WORLD_SIZE fails loudly instead of running one GPU silently
+    bad = dict(env, WORLD_SIZE="1", RANK="0", LOCAL_RANK="0")
+    r2 = subprocess.run([sys.executable, str(root / "bench.py"), "--gpus", "8", "--dry-run"], cwd=root, env=bad,
+                        capture_output=True, text=True, timeout=120)
+    assert r2.returncode == 2
