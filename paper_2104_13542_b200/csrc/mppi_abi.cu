@@ -372,6 +372,10 @@ int enqueue_iteration(mppi_plan* p, int it, bool inline_final, double* out_recor
   a.goal = p->goal.p;
   a.step = reinterpret_cast<R*>(p->stepbuf.p);
   a.mlp_x = p->learned() ? p->mlp_x.p : nullptr;
+  // float plans hand the MLP 32-byte position rows instead of 64-byte encodings
+  // (it recomputes the same fp32 sincos_); float64 plans keep the encodings of
+  // their float64 positions
+  a.mlp_x_q = std::is_same<R, float>::value && getenv("MPPI_MLP_POSENC") == nullptr ? 1 : 0;
   a.status = p->status.p;
   a.bad = p->bad.p;
   if (p->dump) {
@@ -417,7 +421,7 @@ int enqueue_iteration(mppi_plan* p, int it, bool inline_final, double* out_recor
       p->capture_inl->push_back(std::move(n));
     }
     if ((stages & 2u) && p->learned())
-      CK(mlp_forward(p->mlp, p->mlp_x.p, (long long)p->B * p->N * p->H, p->mlp_d.p, st));
+      CK(mlp_forward(p->mlp, p->mlp_x.p, (long long)p->B * p->N * p->H, p->mlp_d.p, st, a.mlp_x_q));
   }
   StatsArgs<R> s;
   stats_static<R>(p, p->H, p->gamma, p->tw, s);

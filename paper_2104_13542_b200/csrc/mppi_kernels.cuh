@@ -63,7 +63,9 @@ struct RolloutArgs {
   const double* in0;
   const double* in1;
   R* step;               // (B*N*H) step cost excluding the learned self-collision term
-  float* mlp_x;          // (B*N*H,16) positional encoding (surrogate.py:24-28) or NULL
+  float* mlp_x;          // (B*N*H,16) positional encoding (surrogate.py:24-28), or (B*N*H,8) joint
+                         // positions when mlp_x_q (the MLP encodes them itself), or NULL
+  int mlp_x_q;
   int* status;
   int* bad;
   double* out_pos;       // dumps, instance 0 only; (n,H,d)
@@ -511,7 +513,14 @@ __device__ __forceinline__ bool rollout_particle(const RolloutArgs<R>& a, long l
   if (act) {
     const size_t m = (size_t)g * H + h;
     a.step[m] = stepc;
-    if (a.mlp_x != nullptr) {  // one 64-byte row, four 16-byte stores
+    if (a.mlp_x != nullptr && a.mlp_x_q) {  // one 32-byte row of positions: the MLP's X loader
+      float xr[8];                           // computes [sin q, cos q] with the same sincos_
+#pragma unroll
+      for (int k = 0; k < 8; ++k) xr[k] = k < D ? (float)p[k] : 0.f;
+      float4* x4 = reinterpret_cast<float4*>(a.mlp_x + m * 8);
+      x4[0] = make_float4(xr[0], xr[1], xr[2], xr[3]);
+      x4[1] = make_float4(xr[4], xr[5], xr[6], xr[7]);
+    } else if (a.mlp_x != nullptr) {  // one 64-byte row, four 16-byte stores
       float xr[16];
 #pragma unroll
       for (int k = 0; k < D; ++k) {

@@ -357,7 +357,7 @@ static __device__ unsigned long long* mlp_dbg = nullptr;
 template <bool ONE_TILE>
 static __global__ void __maxnreg__(88)
     mlp_tcgen05_kernel(const float* __restrict__ x, long long M, const unsigned char* __restrict__ img,
-                       float* __restrict__ out, int early) {
+                       float* __restrict__ out, int early, int x_q, int in_d) {
   extern __shared__ __align__(1024) unsigned char mlp_smem[];
   unsigned char* sm = mlp_smem;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -498,7 +498,28 @@ static __global__ void __maxnreg__(88)
     const float* w3 = b2 + kMlpH2;
     auto load_x = [&](long long t, float* xv) {  // threads < 256: row tid % 128, 8 of 16 columns
       const long long r = t * 128 + (tid & 127);
-      if (tid < 256 && t < ntiles && r < M) {
+      if (x_q && tid < 256 && t < ntiles && r < M) {
+        // joint positions (8 floats per row) -> columns 8*(tid >> 7) .. +7 of
+        // [sin q, cos q, 0...] (surrogate.py:24-28), the rollout's own sincos_
+        const float4* src = reinterpret_cast<const float4*>(x + r * 8);
+        const float4 f0 = __ldg(src), f1 = __ldg(src + 1);
+        const float q[8] = {f0.x, f0.y, f0.z, f0.w, f1.x, f1.y, f1.z, f1.w};
+        float sn[8], cs[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) sincos_(q[j], &sn[j], &cs[j]);
+        const int c0 = (tid >> 7) * 8;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const int c = c0 + i;
+          float v = 0.f;
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            v = (c == j && j < in_d) ? sn[j] : v;
+            v = (c == in_d + j && j < in_d) ? cs[j] : v;
+          }
+          xv[i] = v;
+        }
+      } else if (tid < 256 && t < ntiles && r < M) {
         const float4* src = reinterpret_cast<const float4*>(x + r * 16 + (tid >> 7) * 8);
         const float4 f0 = __ldg(src), f1 = __ldg(src + 1);
         xv[0] = f0.x; xv[1] = f0.y; xv[2] = f0.z; xv[3] = f0.w;
@@ -670,8 +691,10 @@ inline cudaError_t mlp_upload(MlpWeights& m, int in_dim, const double* W0, const
   return cudaStreamSynchronize(st);
 }
 
+// x_q = 0: x holds (rows,16) positional encodings; 1: (rows,8) joint positions
+// (the d = in_dim/2 joints, zero padded), encoded inside the kernel.
 inline cudaError_t mlp_forward(const MlpWeights& m, const float* x, long long rows, float* out,
-                               cudaStream_t st) {
+                               cudaStream_t st, int x_q = 0) {
   static bool attr_set[64] = {};
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
@@ -688,7 +711,8 @@ inline cudaError_t mlp_forward(const MlpWeights& m, const float* x, long long ro
   auto kern = (tiles <= sms && getenv("MPPI_MLP_GENERAL") == nullptr) ? mlp_tcgen05_kernel<true>
                                                                        : mlp_tcgen05_kernel<false>;
   if (!(pdl_mask() & (PDL_MLP | PDL_EARLY))) {  // plain launch: no programmatic edge in a captured graph
-    kern<<<grid, kMlpThreads, kMlpKernelSmem, st>>>(x, rows, (const unsigned char*)m.img, out, 0);
+    kern<<<grid, kMlpThreads, kMlpKernelSmem, st>>>(x, rows, (const unsigned char*)m.img, out, 0, x_q,
+                                                    m.in_dim / 2);
     return cudaGetLastError();
   }
   cudaLaunchConfig_t cfg = {};
@@ -702,7 +726,7 @@ inline cudaError_t mlp_forward(const MlpWeights& m, const float* x, long long ro
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   return cudaLaunchKernelEx(&cfg, kern, x, rows, (const unsigned char*)m.img, out,
-                            (pdl_mask() & PDL_EARLY) ? 1 : 0);
+                            (pdl_mask() & PDL_EARLY) ? 1 : 0, x_q, m.in_dim / 2);
 }
 
 inline void mlp_release(MlpWeights& m) {
