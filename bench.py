@@ -333,7 +333,7 @@ def _cpu_probe(spec: dict) -> dict:
         os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/numba_cache_bench")
     if kind == "latency":  # latency_probe (reference bench.py:91-109)
         step, workers, impl = _cpu_stepper(spec.get("particles", 500), spec.get("config", 2), w)
-        lat = _time_steps(step, spec.get("steps", 10), 1, spec.get("budget_s"))
+        lat = _time_steps(step, spec.get("steps", 10), spec.get("warmup", 1), spec.get("budget_s"))
         return {"median_ms": float(np.median(lat)), "mean_ms": float(np.mean(lat)), "steps": len(lat),
                 "workers": workers, "kind": impl}
     if kind == "instances":  # config 4 sample: k independent controllers stepped in sequence
@@ -378,6 +378,7 @@ def _c4_problem_host(i: int):
 
 def _probe_subprocess(spec: dict, single_thread: bool = False, timeout: float = 300.0) -> dict:
     env = dict(os.environ)
+    env.pop("OMP_NUM_THREADS", None)  # torchrun's per-rank pin does not apply to the CPU arm
     if single_thread:
         for k in ("OPENBLAS_NUM_THREADS", "OMP_NUM_THREADS", "MKL_NUM_THREADS", "NUMBA_NUM_THREADS"):
             env[k] = "1"
@@ -397,6 +398,8 @@ def cpu_protocol(full: bool = True) -> dict:
     ncpu = os.cpu_count() or 1
     out = {"cpu_model": _cpu_model(), "host_threads": ncpu}
     out["c2_workers_all"] = _probe_subprocess({"kind": "latency", "config": 2, "steps": 20, "budget_s": 8.0})
+    out["c2_workers_all_blas1"] = _probe_subprocess({"kind": "latency", "config": 2, "steps": 20, "budget_s": 8.0},
+                                                    single_thread=True)
     out["c2_workers_1"] = _probe_subprocess({"kind": "latency", "config": 2, "workers": 1, "steps": 8,
                                              "budget_s": 6.0}, single_thread=True)
     if full:
@@ -459,12 +462,32 @@ def run_reference(args, workload: str):
             workers, kind = c.workers, "reference"
             lat = _time_steps(step, min(args.steps, 5), 1)
             sample = f"{len(lat)} closed-loop tracking steps (8-box world, {args.particles} particles)"
+        elif _have_reference():
+            # the reference's best thread setup on this host: its rollout workers
+            # and numpy's BLAS threads compete for the same cores, so all three
+            # are measured (each in its own process, the thread environment set
+            # before numpy loads) and the fastest is the reported arm
+            spec = {"kind": "latency", "config": config, "particles": args.particles, "steps": args.steps,
+                    "warmup": args.warmup, "budget_s": 60.0}
+            runs = {"workers=all, default BLAS threads": _probe_subprocess(spec),
+                    "workers=all, single-threaded BLAS": _probe_subprocess(spec, single_thread=True),
+                    "workers=1, single-threaded BLAS": _probe_subprocess(dict(spec, workers=1), single_thread=True)}
+            ok = {k: r for k, r in runs.items() if "mean_ms" in r}
+            best = min(ok, key=lambda k: ok[k]["mean_ms"])
+            r = ok[best]
+            lat = [r["mean_ms"]]
+            workers, kind = r["workers"], r["kind"]
+            sample = (f"{r['steps']} control_steps of config {config} after {args.warmup} warm-up, the fastest of "
+                      f"three thread setups ({best})")
+            extra["thread_setups"] = {k: {"mean_ms": v.get("mean_ms"), "median_ms": v.get("median_ms")}
+                                      for k, v in runs.items()}
+            extra["median_ms"] = r["median_ms"]
         else:
             step, workers, kind = _cpu_stepper(args.particles, min(config, 2), None)
             lat = _time_steps(step, args.steps, args.warmup, budget_s=120.0)
             sample = f"{len(lat)} control_steps of config {config} after {args.warmup} warm-up"
         v, unit, hib = float(np.mean(lat)), "ms", False
-        extra["median_ms"] = float(np.median(lat))
+        extra.setdefault("median_ms", float(np.median(lat)))
     elif workload == "c4":
         r = _cpu_probe({"kind": "instances", "k": max(2, min(8, args.steps))})
         per_ms = r["per_instance_step_ms"]
@@ -1021,11 +1044,14 @@ def _cpu_baseline(args):
     """cpu_baseline of the config-2 line: the reference at workers = all host
     threads (headline) plus the rest of the §8(d) protocol."""
     prot = cpu_protocol(full=not args.quick_cpu)
-    head = prot.get("c2_workers_all", {})
+    cands = [prot.get(k, {}) for k in ("c2_workers_all", "c2_workers_all_blas1", "c2_workers_1")]
+    cands = [c for c in cands if "median_ms" in c]
+    head = min(cands, key=lambda c: c["median_ms"]) if cands else {}
     kind = head.get("kind", "port")
     return {"value": head.get("median_ms"), "unit": "ms", "cores": head.get("workers", 1), "kind": kind,
             "sample": f"median of {head.get('steps')} reference control_steps (config 2, 500x30, numba, "
-                      f"workers={head.get('workers')}) after 1 warm-up" if kind == "reference" else
+                      f"workers={head.get('workers')}; the fastest thread setup of protocol.c2_*) after 1 warm-up"
+                      if kind == "reference" else
                       "oracle-port control steps (config 2, numpy float64; oracle/_ref not installed)",
             "protocol": prot}
 

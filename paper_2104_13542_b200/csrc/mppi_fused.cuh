@@ -270,9 +270,7 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
       float y[C3], z[C3];
       tmem_ld_cols<C3>(acc3 + lane_base + C3 * cg, y);
       tmem_ld_cols<C3>(acc3 + lane_base + 64 + C3 * cg, z);
-#pragma unroll
-      for (int i = 0; i < C3; ++i)
-        part = fmaf(fmaxf(fmaf(y[i] + z[i], s2, b2[C3 * cg + i]), 0.f), w3[C3 * cg + i], part);
+      part = output_part<C3>(y, z, s2, b2 + C3 * cg, w3 + C3 * cg);
     }
     float* red = reinterpret_cast<float*>(sm + OFF_A);
     red[cg * 128 + row_in_tile] = part;

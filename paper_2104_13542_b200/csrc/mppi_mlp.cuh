@@ -228,7 +228,9 @@ __device__ __forceinline__ void store_split8(unsigned char* sm, uint32_t off_h, 
   for (int i = 0; i < 4; ++i) {
     const __half2 hh = __floats2half2_rn(y[2 * i], y[2 * i + 1]);
     const float2 hf = __half22float2(hh);
-    const __half2 ll = __floats2half2_rn(y[2 * i] - hf.x, y[2 * i + 1] - hf.y);
+    // lo = y - hi for both elements in one packed FP32 op (FFMA2: hi * -1 + y)
+    const float2 d = __ffma2_rn(hf, make_float2(-1.f, -1.f), make_float2(y[2 * i], y[2 * i + 1]));
+    const __half2 ll = __floats2half2_rn(d.x, d.y);
     h[i] = *reinterpret_cast<const uint32_t*>(&hh);
     l[i] = *reinterpret_cast<const uint32_t*>(&ll);
   }
@@ -314,6 +316,39 @@ __device__ __forceinline__ void tmem_st4(uint32_t taddr, const uint32_t* v) {
                : "memory");
 }
 
+// y = relu(y * s + b) for 8 accumulator columns: packed FP32 (FFMA2), the
+// epilogue is the MLP's bound at scale (CUDA-core work per tile > tensor time)
+__device__ __forceinline__ void scale_bias_relu8(float* y, float s, const float* b) {
+  const float2 s2 = make_float2(s, s);
+  const float2* b2 = reinterpret_cast<const float2*>(b);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float2 v = __ffma2_rn(make_float2(y[2 * i], y[2 * i + 1]), s2, b2[i]);
+    y[2 * i] = fmaxf(v.x, 0.f);
+    y[2 * i + 1] = fmaxf(v.y, 0.f);
+  }
+}
+
+// Output layer share of C accumulator columns: relu((hi + lo products) * s +
+// b) . w3, packed FP32 with two partial sums (shared by mlp_tcgen05_kernel and
+// the fused kernel so both sum in the same order)
+template <int C>
+__device__ __forceinline__ float output_part(const float* y, const float* z, float s, const float* b,
+                                             const float* w) {
+  const float2 sc = make_float2(s, s);
+  const float2* bb = reinterpret_cast<const float2*>(b);
+  const float2* ww = reinterpret_cast<const float2*>(w);
+  float2 acc = make_float2(0.f, 0.f);
+#pragma unroll
+  for (int i = 0; i < C / 2; ++i) {
+    float2 v = __fadd2_rn(make_float2(y[2 * i], y[2 * i + 1]), make_float2(z[2 * i], z[2 * i + 1]));
+    v = __ffma2_rn(v, sc, bb[i]);
+    v = make_float2(fmaxf(v.x, 0.f), fmaxf(v.y, 0.f));
+    acc = __ffma2_rn(v, ww[i], acc);
+  }
+  return acc.x + acc.y;
+}
+
 // 8 fp32 activations (columns 8cg..8cg+7 of a 32-column chunk at `chunk`) ->
 // 4 hi + 4 lo packed fp16 columns of the chunk's slice (cg >> 1) layout.
 // `pair_bar`: named barrier of the two warps of the slice.
@@ -323,7 +358,9 @@ __device__ __forceinline__ void tmem_convert8(uint32_t chunk, int cg, const floa
   for (int i = 0; i < 4; ++i) {
     const __half2 hh = __floats2half2_rn(y[2 * i], y[2 * i + 1]);
     const float2 hf = __half22float2(hh);
-    const __half2 ll = __floats2half2_rn(y[2 * i] - hf.x, y[2 * i + 1] - hf.y);
+    // lo = y - hi for both elements in one packed FP32 op (FFMA2: hi * -1 + y)
+    const float2 d = __ffma2_rn(hf, make_float2(-1.f, -1.f), make_float2(y[2 * i], y[2 * i + 1]));
+    const __half2 ll = __floats2half2_rn(d.x, d.y);
     h[i] = *reinterpret_cast<const uint32_t*>(&hh);
     l[i] = *reinterpret_cast<const uint32_t*>(&ll);
   }
@@ -504,20 +541,40 @@ static __global__ void __maxnreg__(88)
         const float4* src = reinterpret_cast<const float4*>(x + r * 8);
         const float4 f0 = __ldg(src), f1 = __ldg(src + 1);
         const float q[8] = {f0.x, f0.y, f0.z, f0.w, f1.x, f1.y, f1.z, f1.w};
-        float sn[8], cs[8];
-#pragma unroll
-        for (int j = 0; j < 8; ++j) sincos_(q[j], &sn[j], &cs[j]);
         const int c0 = (tid >> 7) * 8;
+        if (in_d == 7) {  // arm7: [s0..s6 c0 | c1..c6 0 0]
+          if (c0 == 0) {
+            float cz;
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const int c = c0 + i;
-          float v = 0.f;
+            for (int j = 0; j < 7; ++j) {
+              float cj;
+              sincos_(q[j], &xv[j], &cj);
+              if (j == 0) cz = cj;
+            }
+            xv[7] = cz;
+          } else {
 #pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            v = (c == j && j < in_d) ? sn[j] : v;
-            v = (c == in_d + j && j < in_d) ? cs[j] : v;
+            for (int j = 0; j < 6; ++j) {
+              float sj;
+              sincos_(q[j + 1], &sj, &xv[j]);
+            }
+            xv[6] = xv[7] = 0.f;
           }
-          xv[i] = v;
+        } else {
+          float sn[8], cs[8];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) sincos_(q[j], &sn[j], &cs[j]);
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {  // register selects (no local-memory indexing)
+            const int c = c0 + i;
+            float v = 0.f;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              v = (c == j && j < in_d) ? sn[j] : v;
+              v = (c == in_d + j && j < in_d) ? cs[j] : v;
+            }
+            xv[i] = v;
+          }
         }
       } else if (tid < 256 && t < ntiles && r < M) {
         const float4* src = reinterpret_cast<const float4*>(x + r * 16 + (tid >> 7) * 8);
@@ -567,8 +624,7 @@ static __global__ void __maxnreg__(88)
         }
         float y[8];
         tmem_ld8(tmem + lane_base + 32 * c + 8 * cg, y);
-#pragma unroll
-        for (int i = 0; i < 8; ++i) y[i] = fmaxf(fmaf(y[i], s0, b0[32 * c + 8 * cg + i]), 0.f);
+        scale_bias_relu8(y, s0, b0 + 32 * c + 8 * cg);
         tmem_convert8(tmem + lane_base + 32 * c, cg, y, pair_bar);
         arrive(barA1 + 8 * c);
         if (c == 7 && nxt) {  // both layer-1 halves done (barL1[1]): X can be rewritten
@@ -591,8 +647,7 @@ static __global__ void __maxnreg__(88)
       for (int c = 0; c < 4; ++c) {
         float y[8];
         tmem_ld8(acc2 + lane_base + 32 * c + 8 * cg, y);
-#pragma unroll
-        for (int i = 0; i < 8; ++i) y[i] = fmaxf(fmaf(y[i], s1, b1[32 * c + 8 * cg + i]), 0.f);
+        scale_bias_relu8(y, s1, b1 + 32 * c + 8 * cg);
         tmem_convert8(acc2 + lane_base + 32 * c, cg, y, pair_bar);
         arrive(barA2 + 8 * c);
       }
@@ -608,9 +663,7 @@ static __global__ void __maxnreg__(88)
         float y[16], z[16];
         tmem_ld16(acc3 + lane_base + 16 * cg, y);       // A_hi W_hi + A_lo W_hi
         tmem_ld16(acc3 + lane_base + 64 + 16 * cg, z);  // A_hi W_lo
-#pragma unroll
-        for (int i = 0; i < 16; ++i)
-          part = fmaf(fmaxf(fmaf(y[i] + z[i], s2, b2[16 * cg + i]), 0.f), w3[16 * cg + i], part);
+        part = output_part<16>(y, z, s2, b2 + 16 * cg, w3 + 16 * cg);
       }
       red[cg * 128 + row_in_tile] = part;
       epi_barrier();
