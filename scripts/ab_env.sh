@@ -1,8 +1,20 @@
-# A/B the step latency over environment settings:
-#   bash scripts/ab_env.sh "A=1 B=2" "A=0" ...   (each argument is one setting; "-" = none)
-for i in $(seq ${REPS:-2}); do
-  for setting in "$@"; do
-    env_args=(); [ "$setting" != "-" ] && read -ra env_args <<< "$setting"
-    env "${env_args[@]}" python bench.py --steps 500 --warmup 20 --no-cpu-baseline --no-scale-roofline 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read().strip().splitlines()[-1]); print('$setting'.ljust(30), round(d['value']*1e3,2), round(d['median_ms']*1e3,2), round(d['instrumented_step_ms']*1e3,2), round(d['e2e']['value']*1e3,2))"
+#!/bin/bash
+# A/B of one environment knob on configs 4 and 2, interleaved twice:
+#   bash scripts/ab_env.sh OUTDIR VAR "valA valB"
+OUT=$1; VAR=$2; VALS=$3
+mkdir -p "$OUT"
+for rep in 1 2; do
+  for v in $VALS; do
+    export $VAR=$v
+    python bench.py --workload c4 --steps 20 --warmup 3 > "$OUT/c4_${v}_$rep.log" 2>&1
+    python bench.py --workload c2 --steps 200 --warmup 10 --no-cpu-baseline --no-scale-roofline > "$OUT/c2_${v}_$rep.log" 2>&1
+    python - "$OUT/c4_${v}_$rep.log" "$OUT/c2_${v}_$rep.log" "$VAR=$v" <<'PY'
+import json, sys
+for f in sys.argv[1:3]:
+    for l in open(f):
+        if l.startswith('{'):
+            d = json.loads(l)
+            print(sys.argv[3], f.split('/')[-1], '%.4g' % d['value'], {k: round(v, 4) for k, v in (d.get('stage_ms') or {}).items()}, d['clocks']['sm_mhz'], d['clocks']['reasons'])
+PY
   done
 done
