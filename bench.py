@@ -105,15 +105,21 @@ class ClockSampler:
             bits = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20,
                     "sw_power_cap": 0x4}
 
+            mx = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+
+            def sample():
+                sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+                r = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                act = ["Active" if r & b else "Not Active" for b in bits.values()]
+                self.lines.append(f"{sm}, {mx}, {r}, " + ", ".join(act))
+
             def poll():
-                mx = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
                 while not self._stop.is_set():
-                    sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
-                    r = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
-                    act = ["Active" if r & b else "Not Active" for b in bits.values()]
-                    self.lines.append(f"{sm}, {mx}, {r}, " + ", ".join(act))
+                    sample()
                     time.sleep(0.005)
 
+            self._sample = sample
+            sample()  # one sample at the start of the timed region, however short it is
             self.t = threading.Thread(target=poll, daemon=True)
             self.t.start()
             return self
@@ -135,6 +141,11 @@ class ClockSampler:
 
     def __exit__(self, *exc):
         self._stop.set()
+        if getattr(self, "_sample", None) is not None:  # one sample at the end of the timed region
+            try:
+                self._sample()
+            except Exception:
+                pass
         if getattr(self, "t", None) is not None and self.proc is None:
             self.t.join(timeout=1)
         if self.proc is not None:

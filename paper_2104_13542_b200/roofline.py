@@ -61,18 +61,26 @@ def launch_shares(profiles_dir, tag: str):
     files = sorted(Path(profiles_dir).glob(f"r*_{tag}.csv"))
     if not files:
         return None, None
-    times = {k: [] for k in NCU_KERNEL}
+    # per stage, the most frequently launched kernel instantiation: the timed
+    # loop's (the same command also launches the FP64 and bundle-dumping
+    # variants a few times)
+    times = {k: {} for k in NCU_KERNEL}
     try:
         with open(files[-1]) as fh:
             for r in csv.DictReader(ln for ln in fh if ln.startswith('"')):
                 if r.get("Metric Name") != "gpu__time_duration.sum":
                     continue
+                name = r.get("Kernel Name", "")
                 for stage, frag in NCU_KERNEL.items():
-                    if frag in r.get("Kernel Name", ""):
-                        times[stage].append(float(r["Metric Value"].replace(",", "")))
+                    if frag in name:
+                        times[stage].setdefault(name, []).append(float(r["Metric Value"].replace(",", "")))
     except (OSError, ValueError, KeyError):
         return None, None
-    med = {k: sorted(v)[len(v) // 2] for k, v in times.items() if v}
+    med = {}
+    for stage, by_name in times.items():
+        if by_name:
+            v = sorted(max(by_name.values(), key=len))
+            med[stage] = v[len(v) // 2]
     return (med or None), f"profiles/{files[-1].name}"
 
 
