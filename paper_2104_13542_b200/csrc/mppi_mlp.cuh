@@ -259,6 +259,22 @@ __device__ __forceinline__ void tmem_ld8(uint32_t taddr, float* v) {
   for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+// Split form for software pipelining: the load is issued now, its registers
+// are valid after tmem_wait_ld8 (which takes them as read-write operands, so
+// no use can be scheduled ahead of the wait).
+__device__ __forceinline__ void tmem_ld8_async(uint32_t taddr, uint32_t* r) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+                 "=r"(r[7])
+               : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_wait_ld8(uint32_t* r) {
+  asm volatile("tcgen05.wait::ld.sync.aligned;"
+               : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7])
+               :
+               : "memory");
+}
+
 __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
 }
@@ -298,7 +314,7 @@ constexpr int kMlpBars = 3 + 2 + 8 + 1 + 4 + 1 + 1;
 constexpr uint32_t OFF_KBAR = OFF_XL + 128 * 16 * 2;
 constexpr uint32_t OFF_KTMEMPTR = OFF_KBAR + kMlpBars * 8;
 constexpr uint32_t OFF_KRED = (OFF_KTMEMPTR + 16 + 15) / 16 * 16;
-constexpr uint32_t kMlpKernelSmem = OFF_KRED + 4 * 128 * 4;
+constexpr uint32_t kMlpKernelSmem = OFF_KRED + 2 * 4 * 128 * 4;  // output partial sums, double-buffered
 static_assert(kMlpKernelSmem <= 232448, "MLP does not fit shared memory");
 
 __device__ __forceinline__ void umma_f16_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t b, uint32_t idesc,
@@ -536,46 +552,13 @@ static __global__ void __maxnreg__(88)
     auto load_x = [&](long long t, float* xv) {  // threads < 256: row tid % 128, 8 of 16 columns
       const long long r = t * 128 + (tid & 127);
       if (x_q && tid < 256 && t < ntiles && r < M) {
-        // joint positions (8 floats per row) -> columns 8*(tid >> 7) .. +7 of
-        // [sin q, cos q, 0...] (surrogate.py:24-28), the rollout's own sincos_
+        // joint positions (8 floats per row); encode_x turns them into the
+        // row's encoding columns right before the shared-memory store, so the
+        // load latency stays hidden behind the epilogue that follows
         const float4* src = reinterpret_cast<const float4*>(x + r * 8);
         const float4 f0 = __ldg(src), f1 = __ldg(src + 1);
-        const float q[8] = {f0.x, f0.y, f0.z, f0.w, f1.x, f1.y, f1.z, f1.w};
-        const int c0 = (tid >> 7) * 8;
-        if (in_d == 7) {  // arm7: [s0..s6 c0 | c1..c6 0 0]
-          if (c0 == 0) {
-            float cz;
-#pragma unroll
-            for (int j = 0; j < 7; ++j) {
-              float cj;
-              sincos_(q[j], &xv[j], &cj);
-              if (j == 0) cz = cj;
-            }
-            xv[7] = cz;
-          } else {
-#pragma unroll
-            for (int j = 0; j < 6; ++j) {
-              float sj;
-              sincos_(q[j + 1], &sj, &xv[j]);
-            }
-            xv[6] = xv[7] = 0.f;
-          }
-        } else {
-          float sn[8], cs[8];
-#pragma unroll
-          for (int j = 0; j < 8; ++j) sincos_(q[j], &sn[j], &cs[j]);
-#pragma unroll
-          for (int i = 0; i < 8; ++i) {  // register selects (no local-memory indexing)
-            const int c = c0 + i;
-            float v = 0.f;
-#pragma unroll
-            for (int j = 0; j < 8; ++j) {
-              v = (c == j && j < in_d) ? sn[j] : v;
-              v = (c == in_d + j && j < in_d) ? cs[j] : v;
-            }
-            xv[i] = v;
-          }
-        }
+        xv[0] = f0.x; xv[1] = f0.y; xv[2] = f0.z; xv[3] = f0.w;
+        xv[4] = f1.x; xv[5] = f1.y; xv[6] = f1.z; xv[7] = f1.w;
       } else if (tid < 256 && t < ntiles && r < M) {
         const float4* src = reinterpret_cast<const float4*>(x + r * 16 + (tid >> 7) * 8);
         const float4 f0 = __ldg(src), f1 = __ldg(src + 1);
@@ -584,6 +567,49 @@ static __global__ void __maxnreg__(88)
       } else {
 #pragma unroll
         for (int i = 0; i < 8; ++i) xv[i] = 0.f;
+      }
+    };
+    // x_q: joint positions in xv -> columns 8*(tid >> 7) .. +7 of [sin q,
+    // cos q, 0...] (surrogate.py:24-28) with the rollout's own sincos_
+    auto encode_x = [&](float* xv) {
+      if (!x_q || tid >= 256) return;
+      float q[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) q[j] = xv[j];
+      const int c0 = (tid >> 7) * 8;
+      if (in_d == 7) {  // arm7: [s0..s6 c0 | c1..c6 0 0]
+        if (c0 == 0) {
+          float cz;
+#pragma unroll
+          for (int j = 0; j < 7; ++j) {
+            float cj;
+            sincos_(q[j], &xv[j], &cj);
+            if (j == 0) cz = cj;
+          }
+          xv[7] = cz;
+        } else {
+#pragma unroll
+          for (int j = 0; j < 6; ++j) {
+            float sj;
+            sincos_(q[j + 1], &sj, &xv[j]);
+          }
+          xv[6] = xv[7] = 0.f;
+        }
+      } else {
+        float sn[8], cs[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) sincos_(q[j], &sn[j], &cs[j]);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {  // register selects (no local-memory indexing)
+          const int c = c0 + i;
+          float v = 0.f;
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            v = (c == j && j < in_d) ? sn[j] : v;
+            v = (c == in_d + j && j < in_d) ? cs[j] : v;
+          }
+          xv[i] = v;
+        }
       }
     };
     auto arrive = [&](uint32_t bar) {
@@ -598,6 +624,7 @@ static __global__ void __maxnreg__(88)
     pdl_wait();  // the rollout's positional encodings are complete past this point
     if (tile < ntiles) {
       load_x(tile, xv);
+      encode_x(xv);
       if (tid < 256) store_split8(sm, OFF_XH, OFF_XL, umma_off(tid & 127, (tid >> 7) * 8, 16), xv);
       fence_async_smem();
       arrive(barX);
@@ -613,6 +640,9 @@ static __global__ void __maxnreg__(88)
     auto epilogue_l1 = [&](long long t) {
       const bool nxt = !ONE_TILE && t + G < ntiles;
       if (nxt) load_x(t + G, xv);
+      // chunk c+1's TMEM load is in flight while chunk c is converted (within
+      // one layer-1 half: the second half waits for its own MMA barrier)
+      uint32_t rb[2][8];
 #pragma unroll
       for (int c = 0; c < 8; ++c) {
         if ((c & 3) == 0) {
@@ -621,13 +651,18 @@ static __global__ void __maxnreg__(88)
           if (tid == 0 && hb == 0 && t == blockIdx.x) MLP_STAMP(3);
           phL1 ^= 1u << hb;
           tc_fence_after();
+          tmem_ld8_async(tmem + lane_base + 32 * c + 8 * cg, rb[c & 1]);
         }
+        tmem_wait_ld8(rb[c & 1]);
+        if ((c & 3) != 3) tmem_ld8_async(tmem + lane_base + 32 * (c + 1) + 8 * cg, rb[(c + 1) & 1]);
         float y[8];
-        tmem_ld8(tmem + lane_base + 32 * c + 8 * cg, y);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) y[i] = __uint_as_float(rb[c & 1][i]);
         scale_bias_relu8(y, s0, b0 + 32 * c + 8 * cg);
         tmem_convert8(tmem + lane_base + 32 * c, cg, y, pair_bar);
         arrive(barA1 + 8 * c);
         if (c == 7 && nxt) {  // both layer-1 halves done (barL1[1]): X can be rewritten
+          encode_x(xv);
           if (tid < 256) store_split8(sm, OFF_XH, OFF_XL, umma_off(tid & 127, (tid >> 7) * 8, 16), xv);
           fence_async_smem();
           arrive(barX);
@@ -643,10 +678,15 @@ static __global__ void __maxnreg__(88)
       mbar_wait(barL2done, ph);
       if (tid == 0 && tile == blockIdx.x) MLP_STAMP(5);
       tc_fence_after();
+      uint32_t r2[2][8];
+      tmem_ld8_async(acc2 + lane_base + 8 * cg, r2[0]);
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
+      for (int c = 0; c < 4; ++c) {  // chunk c+1's TMEM load in flight under chunk c
+        tmem_wait_ld8(r2[c & 1]);
+        if (c < 3) tmem_ld8_async(acc2 + lane_base + 32 * (c + 1) + 8 * cg, r2[(c + 1) & 1]);
         float y[8];
-        tmem_ld8(acc2 + lane_base + 32 * c + 8 * cg, y);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) y[i] = __uint_as_float(r2[c & 1][i]);
         scale_bias_relu8(y, s1, b1 + 32 * c + 8 * cg);
         tmem_convert8(acc2 + lane_base + 32 * c, cg, y, pair_bar);
         arrive(barA2 + 8 * c);
@@ -665,19 +705,23 @@ static __global__ void __maxnreg__(88)
         tmem_ld16(acc3 + lane_base + 64 + 16 * cg, z);  // A_hi W_lo
         part = output_part<16>(y, z, s2, b2 + 16 * cg, w3 + 16 * cg);
       }
-      red[cg * 128 + row_in_tile] = part;
-      epi_barrier();
+      // the four column-group warps of a lane quadrant combine their rows: a
+      // 128-thread barrier per quadrant, partial sums double-buffered by tile
+      // parity (the buffer is rewritten two tiles later, after the quadrant's
+      // next barrier, which its reader has passed)
+      float* rq = red + (ph & 1u) * 512;
+      rq[cg * 128 + row_in_tile] = part;
+      asm volatile("bar.sync %0, 128;" ::"r"(10 + quad) : "memory");
       if (cg == 0) {
         const long long row = tile * 128 + row_in_tile;
-        const float o = par[kMlpH0 + kMlpH1 + 2 * kMlpH2] + red[row_in_tile] + red[128 + row_in_tile] +
-                        red[256 + row_in_tile] + red[384 + row_in_tile];
+        const float o = par[kMlpH0 + kMlpH1 + 2 * kMlpH2] + rq[row_in_tile] + rq[128 + row_in_tile] +
+                        rq[256 + row_in_tile] + rq[384 + row_in_tile];
         if (row < M) out[row] = o;
       }
-      tc_fence_before();
-      epi_barrier();
       if (tid == 0 && tile == blockIdx.x) MLP_STAMP(8);
     }
   }
+  tc_fence_before();  // every TMEM read of this CTA is ordered before the dealloc
   __syncthreads();
   if (warp == 0) {
     tc_fence_after();
