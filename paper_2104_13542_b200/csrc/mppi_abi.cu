@@ -280,10 +280,49 @@ WorldT<R> world_of(mppi_plan* p) {
   return w;
 }
 
+// FkFold of the chain (float64 on the host): K = skew(axis), K^2 = a a^T - I.
+void fill_fold(const HostChain& c, FkFold& f) {
+  memset(&f, 0, sizeof(f));
+  for (int k = 0; k < c.dof; ++k) {
+    const double* ax = &c.axes[3 * k];
+    const double K[3][3] = {{0.0, -ax[2], ax[1]}, {ax[2], 0.0, -ax[0]}, {-ax[1], ax[0], 0.0}};
+    double K2[3][3];
+    for (int i = 0; i < 3; ++i)
+      for (int j = 0; j < 3; ++j) {
+        double s = 0.0;
+        for (int m = 0; m < 3; ++m) s += K[i][m] * K[m][j];
+        K2[i][j] = s;
+      }
+    const double* O = &c.orot[9 * k];
+    const double* t = &c.otrans[3 * k];
+    for (int i = 0; i < 3; ++i) {
+      for (int j = 0; j < 3; ++j) {
+        double sa = 0.0, sb = 0.0;
+        for (int m = 0; m < 3; ++m) {
+          sa += K[i][m] * O[3 * m + j];
+          sb += K2[i][m] * O[3 * m + j];
+        }
+        f.O[k][i][j] = (float)O[3 * i + j];
+        f.A[k][i][j] = (float)sa;
+        f.B[k][i][j] = (float)sb;
+      }
+      double ta = 0.0, tb = 0.0;
+      for (int m = 0; m < 3; ++m) {
+        ta += K[i][m] * t[m];
+        tb += K2[i][m] * t[m];
+      }
+      f.t[k][i] = (float)t[i];
+      f.a[k][i] = (float)ta;
+      f.b[k][i] = (float)tb;
+    }
+  }
+}
+
 // Build the static part of the rollout arguments for horizon H and dt schedule.
 template <typename R>
 void rollout_static(mppi_plan* p, int H, const double* dts, RolloutArgs<R>& a) {
   memset(&a, 0, sizeof(a));
+  if (std::is_same<R, float>::value) fill_fold(p->chain, a.fold);
   fill_chain(p->chain, p->costs.k_jl, a.chain);
   fill_cost(p->costs, p->chain.n_pairs > 0, (p->ns + p->nb) > 0, a.cost);
   a.world = world_of<R>(p);

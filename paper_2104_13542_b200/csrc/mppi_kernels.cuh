@@ -16,6 +16,7 @@
 #pragma once
 
 #include <cooperative_groups.h>
+#include <type_traits>
 
 #include "mppi_common.cuh"
 
@@ -38,8 +39,22 @@ __host__ __device__ inline int stats_groups(int nblk) {
 }
 __host__ __device__ inline int stats_rec_stride(int nblk) { return nblk + stats_groups(nblk); }
 
+// FP32 fast path of each revolute link: the joint rotation Rm(q) = I + s K +
+// (1 - c) K^2 (Rodrigues, jit.py:70-86) enters the link transform only through
+// Rm·orot and Rm·otrans, so those are folded on the host (float64) into
+//   Rm·orot = O + s A + (1 - c) B,   Rm·otrans = t + s a + (1 - c) b
+// with A = K orot, B = K^2 orot, a = K otrans, b = K^2 otrans: 12 instead of
+// 45 FP32 operations per link for the rotation, generic over the chain data
+// (no structural zeros assumed). Rows padded to 4 so column pairs load as one
+// aligned 8-byte constant for FFMA2.
+struct FkFold {
+  float O[MAXD][3][4], A[MAXD][3][4], B[MAXD][3][4];
+  float t[MAXD][4], a[MAXD][4], b[MAXD][4];
+};
+
 template <typename R>
 struct RolloutArgs {
+  FkFold fold;  // read by FP32 rollouts (see FkFold)
   ChainT<R> chain;
   CostT<R> cost;
   WorldT<R> world;
@@ -220,7 +235,12 @@ __host__ __device__ __forceinline__ bool rollout_needs_caps(const CostT<R>& cs) 
 // capsule staging, no capsule self-collision oracle, no world — so the
 // kernel's code holds only what a config-1/2 step executes (the latency
 // build fetches its instructions cold after an L2 flush).
-template <typename R, int D, bool LEAN = false>
+// FOLD: the FkFold link transform (FP32 only) — taken by the many-waves
+// throughput build, where it saves issue slots (config 4 rollout -2 %); the
+// latency build keeps the Rodrigues form, whose operands are already in
+// registers (the fold's extra per-thread constant loads cost the cold
+// 500 x 30 step ~0.5 us).
+template <typename R, int D, bool LEAN = false, bool FOLD = false>
 __device__ __forceinline__ bool rollout_particle(const RolloutArgs<R>& a, long long g, int lane, R* cap,
                                                  float* enc) {
   const int b = (int)(g / a.N);
@@ -333,10 +353,38 @@ __device__ __forceinline__ bool rollout_particle(const RolloutArgs<R>& a, long l
     sq[k] = s;
     cq[k] = c;
     if (ch.jtype[k] == 0) {
-      R Rm[9];
-      axis_rotation(ch.axes[k], s, R(1) - c, Rm);
-      mat33_mul(Rm, ch.orot[k], Rmo);
-      mat33_vec(Rm, ch.otrans[k], tmo);
+      bool folded = false;
+#ifndef MPPI_FK_UNFOLDED  // (A/B build: the Rodrigues form for FP32 too)
+      if constexpr (FOLD && std::is_same<R, float>::value) {
+        {  // FkFold: Rmo = O + s A + c1 B, tmo = t + s a + c1 b
+          const FkFold& f = a.fold;
+          const float c1 = 1.f - c;
+          const float2 s2 = make_float2(s, s), c2 = make_float2(c1, c1);
+#pragma unroll
+          for (int i = 0; i < 3; ++i) {
+            const float2 r = __ffma2_rn(c2, make_float2(f.B[k][i][0], f.B[k][i][1]),
+                                        __ffma2_rn(s2, make_float2(f.A[k][i][0], f.A[k][i][1]),
+                                                   make_float2(f.O[k][i][0], f.O[k][i][1])));
+            Rmo[3 * i] = r.x;
+            Rmo[3 * i + 1] = r.y;
+            Rmo[3 * i + 2] = fmaf(c1, f.B[k][i][2], fmaf(s, f.A[k][i][2], f.O[k][i][2]));
+          }
+          const float2 tt = __ffma2_rn(c2, make_float2(f.b[k][0], f.b[k][1]),
+                                       __ffma2_rn(s2, make_float2(f.a[k][0], f.a[k][1]),
+                                                  make_float2(f.t[k][0], f.t[k][1])));
+          tmo[0] = tt.x;
+          tmo[1] = tt.y;
+          tmo[2] = fmaf(c1, f.b[k][2], fmaf(s, f.a[k][2], f.t[k][2]));
+          folded = true;
+        }
+      }
+#endif
+      if (!folded) {
+        R Rm[9];
+        axis_rotation(ch.axes[k], s, R(1) - c, Rm);
+        mat33_mul(Rm, ch.orot[k], Rmo);
+        mat33_vec(Rm, ch.otrans[k], tmo);
+      }
     } else {
 #pragma unroll
       for (int i = 0; i < 9; ++i) Rmo[i] = ch.orot[k][i];
@@ -577,7 +625,7 @@ __global__ void __launch_bounds__(kRolloutWarps * 32, MINB)
       (a.dbg != nullptr && threadIdx.x == 0 && blockIdx.x < 256) ? a.dbg + 16 * blockIdx.x : nullptr;
   MPPI_TSTAMP(dbg, 0);
   R* cap = reinterpret_cast<R*>(smem_raw) + (size_t)wib * a.chain.n_caps * 6 * 32;
-  rollout_particle<R, D, LEAN>(a, g, lane, cap, nullptr);
+  rollout_particle<R, D, LEAN, (MINB > 1)>(a, g, lane, cap, nullptr);
   MPPI_TSTAMP(dbg, 1);
 #ifdef MPPI_DEBUG_TIMERS
   if (a.dbg != nullptr && lane == 0) {  // latest warp end over the grid
