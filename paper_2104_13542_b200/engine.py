@@ -142,6 +142,12 @@ class Plan:
         proto = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p)
         self._step_raw = proto(C.cast(self.lib.mppi_step, C.c_void_p).value)
         self._a_cmd, self._a_info = self._cmd.ctypes.data, C.addressof(self._info)
+        # staging rows of instance 0 and every address the latency path passes,
+        # resolved once (an ndarray's .ctypes.data costs ~1-2 us per access,
+        # more than copying 7 doubles into a staging row)
+        self._th0, self._thd0 = self._th[0], self._thd[0]
+        self._a_th, self._a_thd = self._th.ctypes.data, self._thd.ctypes.data
+        self._h = self.handle.value
         # the same memory as a numpy record array: batched callers read whole
         # columns (status, costs) without touching B ctypes structs
         self.info_columns = np.ctypeslib.as_array(self._info)
@@ -247,11 +253,11 @@ class Plan:
         """step() for B = 1 with float64 (d,) inputs: no staging copies on the
         Python side. Returns (command (d,) view of the plan's output buffer,
         info of instance 0); the view is overwritten by the next step."""
-        if (type(theta) is np.ndarray and type(theta_dot) is np.ndarray and theta.dtype == _F64
-                and theta_dot.dtype == _F64 and theta.size == self.dof and theta_dot.size == self.dof
-                and theta.flags.c_contiguous and theta_dot.flags.c_contiguous):
-            rc = self._step_raw(self.handle.value, theta.ctypes.data, theta_dot.ctypes.data, self._a_cmd,
-                                self._a_info)
+        if (type(theta) is np.ndarray and type(theta_dot) is np.ndarray and theta.shape == self._th0.shape
+                and theta_dot.shape == self._th0.shape):
+            np.copyto(self._th0, theta)  # any real dtype / layout: numpy converts while copying
+            np.copyto(self._thd0, theta_dot)
+            rc = self._step_raw(self._h, self._a_th, self._a_thd, self._a_cmd, self._a_info)
             if rc:
                 N.check(rc)
             return self._cmd[0], self._info[0]
