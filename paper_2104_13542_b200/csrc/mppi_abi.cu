@@ -364,16 +364,16 @@ void choose_blocks(int N, int B, int& ppb, int& nblk) {
   // one block per instance, no record combine (4096 x 500: statistics 2.22
   // -> 1.59 ms; at 64 instances it would halve the parallelism). Otherwise 32
   // particles per block (latency: more blocks pull eps/step costs in
-  // parallel); up to 1024 particles grow the block to keep one <= 16-CTA
-  // cluster per instance (stats_cluster_kernel); beyond that at most 296
-  // blocks per instance (the record combine is linear in it)
+  // parallel); up to 16 * kClusterMaxPPB = 2048 particles grow the block to
+  // keep one <= 16-CTA cluster per instance (stats_cluster_kernel); beyond
+  // that at most 296 blocks per instance (the record combine is linear in it)
   if (B >= 148 && N <= 2048) {
     ppb = N;
     nblk = 1;
     return;
   }
   ppb = 32;
-  if (N > 16 * 32 && N <= 16 * 64) ppb = (N + 15) / 16;
+  if (N > 16 * 32 && N <= 16 * kClusterMaxPPB) ppb = (N + 15) / 16;
   // A/B knob, clamped to a layout the plan can launch: [1, min(N, 1024)]
   // particles per block (statistics shared memory stays < 64 KB at H*D <= 512)
   if (const char* ev = getenv("MPPI_STATS_PPB")) ppb = std::min(std::max(1, atoi(ev)), std::min(N, 1024));
