@@ -299,6 +299,14 @@ int mppi_get_step_inputs(mppi_plan* plan, int32_t instance, double* theta /* (d,
                          double* theta_dot /* (d,) */, double* means /* (H,d) */,
                          double* stddev /* (H,d) */);
 
+/* Instance 0's RolloutBundle of the last iteration of the last mppi_step on
+ * a plan without dumps (the lean latency graph), recomputed on the device from
+ * the iteration's recorded inputs: controls from the perturbation block and
+ * the policy view of that iteration, one evaluation pass (mppi_evaluate mode
+ * 0), the particle weights (NaN if that step failed). StepDiagnostics.bundle
+ * (controller.py:250-259) of Controller(keep_bundle=False).                 */
+int mppi_replay_bundle(mppi_plan* plan, mppi_eval_out* out, double* weights);
+
 /* Instance 0's RolloutBundle of the last iteration of the last mppi_step
  * (plan created with dump = 1), plus the particle weights (N,). */
 int mppi_get_bundle(mppi_plan* plan, mppi_eval_out* out, double* weights);

@@ -170,6 +170,7 @@ _SIGS = {
                                 _dp, _dp, _dp, _dp, C.POINTER(EvalOut)]),
     "mppi_get_bundle": (C.c_int, [_vp, C.POINTER(EvalOut), _dp]),
     "mppi_get_step_inputs": (C.c_int, [_vp, C.c_int32, _dp, _dp, _dp, _dp]),
+    "mppi_replay_bundle": (C.c_int, [_vp, C.POINTER(EvalOut), _dp]),
     "mppi_episode": (C.c_int, [_vp, C.POINTER(EpisodeDesc), _dp, _dp, C.POINTER(EpisodeState),
                                C.POINTER(EpisodeLogC), _ip, _dp]),
     "mppi_top_rollouts": (C.c_int, [_vp, C.c_int32, _ip, _dp, _dp]),

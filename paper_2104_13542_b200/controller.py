@@ -327,9 +327,7 @@ class LazyBundle:
             if c.keep_bundle:
                 self._data = c._plan.get_bundle()
             else:
-                cfg = c.update_cfg
-                self._data = c._plan.replay_bundle(c.sched.dts, cfg.gamma, c.terminal_weight, cfg.beta,
-                                                   c.null_count)
+                self._data = c._plan.replay_bundle()
         return self._data
 
     def __getattr__(self, name):

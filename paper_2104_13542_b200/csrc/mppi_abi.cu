@@ -197,6 +197,7 @@ struct mppi_plan {
   DevBuf<unsigned char> e_stepbuf;
   DevBuf<float> e_x, e_d;
   DevBuf<int> e_status;
+  DevBuf<double> e_w;  // mppi_replay_bundle: weights of the replayed iteration
   DevBuf<double> e_records;
   DevBuf<unsigned> e_counters;
   // closed-loop episode (mppi_episode): device state, log, script, noise,
@@ -931,6 +932,7 @@ int mppi_plan_destroy(mppi_plan* p) {
   p->status.release();
   p->bad.release();
   p->e_status.release();
+  p->e_w.release();
   p->info.release();
   p->ep_ilog.release();
   p->ep_info.release();
@@ -1355,7 +1357,8 @@ int mppi_evaluate(mppi_plan* p, int32_t mode, int32_t n, int32_t H, const double
     CKR(p->e_d.alloc(mlp_padded_rows(nh)));
     CK(cudaMemsetAsync(p->e_x.p, 0, sizeof(float) * mlp_padded_rows(nh) * 16, st));
   }
-  CK(cudaMemcpyAsync(p->e_in0.p, in0, sizeof(double) * nhd, cudaMemcpyHostToDevice, st));
+  if (in0 != p->e_in0.p)  // (mppi_replay_bundle builds the controls in e_in0 itself)
+    CK(cudaMemcpyAsync(p->e_in0.p, in0, sizeof(double) * nhd, cudaMemcpyHostToDevice, st));
   if (mode == 1) CK(cudaMemcpyAsync(p->e_in1.p, in1, sizeof(double) * nhd, cudaMemcpyHostToDevice, st));
   std::vector<double> s0(2 * D, 0.0);
   if (mode == 0) {
@@ -1429,6 +1432,48 @@ int mppi_evaluate(mppi_plan* p, int32_t mode, int32_t n, int32_t H, const double
   out->quarantined = q;
   if (hst[0] == MPPI_E_NONFINITE_CONTROL)
     return fail(MPPI_E_NONFINITE_CONTROL, "non-finite control in particle " + std::to_string(out->bad_particle));
+  return MPPI_OK;
+}
+
+int mppi_replay_bundle(mppi_plan* p, mppi_eval_out* out, double* weights) {
+  if (!p || !out) return fail(MPPI_E_BAD_ARGUMENT, "null argument");
+  if (p->step_counter == 0) return fail(MPPI_E_CONFIG, "no step has run on this plan");
+  CKR(set_device(p));
+  cudaStream_t st = p->stream;
+  const int n = p->N, H = p->H, D = p->D;
+  const size_t nhd = (size_t)n * H * D;
+  CK(cudaStreamSynchronize(st));
+  // u = mu + sd * eps of instance 0's last iteration (sampling.py:268-290),
+  // straight into the evaluation's control buffer
+  CKR(p->e_in0.alloc(nhd));
+  CKR(p->e_status.alloc(2));
+  CK(cudaMemsetAsync(p->e_status.p, 0, sizeof(int), st));
+  build_controls_kernel<<<grid_for((long long)nhd, 256), 256, 0, st>>>(p->eps.p, p->prev_means.p, p->prev_sd.p, n, H,
+                                                                        D, p->null_count, p->e_in0.p,
+                                                                        p->e_status.p);
+  CK(cudaGetLastError());
+  std::vector<double> th(p->h_state, p->h_state + D), thd(p->h_state + D, p->h_state + 2 * D);
+  double* totals = out->totals;
+  std::vector<double> tot_tmp;
+  if (weights && !totals) {
+    tot_tmp.resize(n);
+    out->totals = tot_tmp.data();
+  }
+  const int rc = mppi_evaluate(p, 0, n, H, p->dts.data(), p->gamma, p->tw, th.data(), thd.data(), p->e_in0.p,
+                               nullptr, out);
+  out->totals = totals;
+  if (rc != MPPI_OK) return rc;
+  if (weights) {  // particle_weights (policy.py:103-121) of the replayed totals
+    CKR(p->e_w.alloc(n));
+    CK(cudaMemsetAsync(p->e_status.p, 0, sizeof(int), st));
+    weights_kernel<<<1, 1024, 0, st>>>(p->e_tot.p, n, p->beta, p->e_w.p, p->e_status.p);
+    CK(cudaGetLastError());
+    int wst = 0;
+    CK(cudaMemcpyAsync(weights, p->e_w.p, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(&wst, p->e_status.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (wst) for (int i = 0; i < n; ++i) weights[i] = NAN;  // the step itself failed: no weights
+  }
   return MPPI_OK;
 }
 

@@ -300,32 +300,18 @@ class Plan:
                                               N.dptr(sd)))
         return th, thd, m, sd
 
-    def replay_bundle(self, dts, gamma: float, terminal_weight: float, beta: float, null_count: int,
-                      instance: int = 0) -> dict:
+    def replay_bundle(self) -> dict:
         """The last step's last-iteration RolloutBundle of a lean plan (dump=0),
-        recomputed on the device from its inputs: controls from the perturbation
-        block and the policy view of that iteration, then one evaluation pass
-        (rollout, cost stack, MLP, discounted totals) and the particle weights.
-        Equal to the step's own rollouts up to the plan precision's rounding."""
+        recomputed on the device from its inputs (mppi_replay_bundle): controls
+        from the perturbation block and the policy view of that iteration, one
+        evaluation pass (rollout, cost stack, MLP, discounted totals) and the
+        particle weights. Equal to the step's own rollouts up to the plan
+        precision's rounding."""
+        return self._bundle(self.lib.mppi_replay_bundle)
+
+    def _bundle(self, fn) -> dict:
         from .costs import TERM_NAMES
 
-        th, thd, m, sd = self.get_step_inputs(instance)
-        eps = self.get_noise()
-        u = np.empty_like(eps)
-        N.check(self.lib.mppi_build_controls(N.dptr(eps), N.dptr(m), N.dptr(sd), self.N, self.H, self.dof,
-                                             int(null_count), N.dptr(u)))
-        r = self.evaluate(0, u, None, dts, gamma, terminal_weight, th, thd)
-        w = np.empty(self.N)
-        rc = self.lib.mppi_particle_weights(N.dptr(r["totals"]), self.N, float(beta), N.dptr(w))
-        if rc:
-            w[:] = np.nan  # the step itself failed (no finite totals): no weights to report
-        return {"positions": r["positions"], "velocities": r["velocities"], "accelerations": r["accelerations"],
-                "step_costs": r["step_costs"],
-                "term_breakdown": {nm: r["terms"][i] for i, nm in enumerate(TERM_NAMES)},
-                "total_per_particle": r["totals"], "weights": w}
-
-    def get_bundle(self) -> dict:
-        """Instance 0's last-iteration bundle (plan created with dump=1)."""
         n, H, d = self.N, self.H, self.dof
         res = {"positions": np.empty((n, H, d)), "velocities": np.empty((n, H, d)),
                "accelerations": np.empty((n, H, d)), "step_costs": np.empty((n, H)),
@@ -333,13 +319,15 @@ class Plan:
         out = N.EvalOut()
         for k in ("positions", "velocities", "accelerations", "step_costs", "terms", "totals"):
             setattr(out, k, N.dptr(res[k]))
-        N.check(self.lib.mppi_get_bundle(self.handle, C.byref(out), N.dptr(res["weights"])))
-        from .costs import TERM_NAMES
-
+        N.check(fn(self.handle, C.byref(out), N.dptr(res["weights"])))
         return {"positions": res["positions"], "velocities": res["velocities"],
                 "accelerations": res["accelerations"], "step_costs": res["step_costs"],
                 "term_breakdown": {nm: res["terms"][i] for i, nm in enumerate(TERM_NAMES)},
                 "total_per_particle": res["totals"], "weights": res["weights"]}
+
+    def get_bundle(self) -> dict:
+        """Instance 0's last-iteration bundle (plan created with dump=1)."""
+        return self._bundle(self.lib.mppi_get_bundle)
 
     def episode(self, steps: int, dt: float, filter_lambda: float, theta0, theta_dot0, *,
                 prev_command=None, fallback_armed: bool = False, script=None, noise=None) -> dict:
