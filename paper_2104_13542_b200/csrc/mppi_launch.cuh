@@ -53,6 +53,14 @@ inline size_t stats_multi_smem_bytes(int G, int N, int HD) {
   return sizeof(double) * (2 * (size_t)G * N + (size_t)G * (kRecHead + 2 * HD) + HD) + sizeof(int) * (size_t)N;
 }
 
+// CTAs per SM of the many-waves rollout build (__launch_bounds__ minimum):
+// 5 -> 96 registers (A/B at 4096 x 500: rollout 4.27 ms at 6 / 80 registers
+// with spills, 4.02 ms at 5, 4.30 ms at 4; -DMPPI_ROLLOUT_MINB=n)
+#ifndef MPPI_ROLLOUT_MINB
+#define MPPI_ROLLOUT_MINB 5
+#endif
+constexpr int kRolloutMinBlocks = MPPI_ROLLOUT_MINB;
+
 #ifdef MPPI_LAUNCH_IMPL
 template <typename R, int D>
 cudaError_t launch_rollout_d(const RolloutArgs<R>& a, long long warps, cudaStream_t st) {
@@ -64,7 +72,8 @@ cudaError_t launch_rollout_d(const RolloutArgs<R>& a, long long warps, cudaStrea
   // float64 exact path and the evaluation modes keep the general kernel)
   const bool lean = std::is_same<R, float>::value && a.mode == 0 && !rollout_needs_caps(a.cost) &&
                     getenv("MPPI_ROLLOUT_GENERAL") == nullptr;
-  auto kern = many ? (lean ? rollout_kernel<R, D, 6, std::is_same<R, float>::value> : rollout_kernel<R, D, 6>)
+  auto kern = many ? (lean ? rollout_kernel<R, D, kRolloutMinBlocks, std::is_same<R, float>::value>
+                           : rollout_kernel<R, D, kRolloutMinBlocks>)
                    : (lean ? rollout_kernel<R, D, 1, std::is_same<R, float>::value> : rollout_kernel<R, D, 1>);
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
