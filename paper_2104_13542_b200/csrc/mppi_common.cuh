@@ -95,6 +95,51 @@ __device__ __forceinline__ R clamp01(R x) {
   return x < R(1) ? x : R(1);
 }
 
+// ---------------------------------------------------------------- packed pairs
+// Two configurations per lane in the paired throughput rollout
+// (rollout_pair_kernel): every FP32 operation on a P2 is one packed
+// instruction. mul/add/sub carry no rounding modifier, so ptxas contracts
+// them into FFMA2 exactly where it contracts the scalar code into FFMA, and a
+// P2 built from one float is a broadcast operand (FFMA2 takes it as a scalar
+// register or a uniform register with no extra move).
+struct P2 {
+  unsigned long long v;
+  __device__ __forceinline__ P2() {}
+  __device__ __forceinline__ P2(float s) { asm("mov.b64 %0, {%1, %1};" : "=l"(v) : "f"(s)); }
+  __device__ __forceinline__ P2(float a, float b) { asm("mov.b64 %0, {%1, %2};" : "=l"(v) : "f"(a), "f"(b)); }
+  __device__ __forceinline__ float lo() const {
+    float a, b;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
+    return a;
+  }
+  __device__ __forceinline__ float hi() const {
+    float a, b;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
+    return b;
+  }
+};
+__device__ __forceinline__ P2 operator*(P2 a, P2 b) {
+  P2 r;
+  asm("mul.f32x2 %0, %1, %2;" : "=l"(r.v) : "l"(a.v), "l"(b.v));
+  return r;
+}
+__device__ __forceinline__ P2 operator+(P2 a, P2 b) {
+  P2 r;
+  asm("add.f32x2 %0, %1, %2;" : "=l"(r.v) : "l"(a.v), "l"(b.v));
+  return r;
+}
+__device__ __forceinline__ P2 operator-(P2 a, P2 b) {
+  P2 r;
+  asm("sub.f32x2 %0, %1, %2;" : "=l"(r.v) : "l"(a.v), "l"(b.v));
+  return r;
+}
+__device__ __forceinline__ P2 operator-(P2 a) { return P2(0.f) - a; }
+__device__ __forceinline__ P2 operator/(P2 a, P2 b) { return P2(a.lo() / b.lo(), a.hi() / b.hi()); }
+__device__ __forceinline__ P2& operator+=(P2& a, P2 b) { return a = a + b; }
+__device__ __forceinline__ P2 max0(P2 a) { return P2(fmaxf(a.lo(), 0.f), fmaxf(a.hi(), 0.f)); }
+__device__ __forceinline__ P2 sqrt2(P2 a) { return P2(sqrtf(a.lo()), sqrtf(a.hi())); }
+__device__ __forceinline__ P2 fabs2(P2 a) { return P2(fabsf(a.lo()), fabsf(a.hi())); }
+
 // out = A(3x3, row-major) * B
 template <typename R>
 __device__ __forceinline__ void mat33_mul(const R* A, const R* B, R* out) {

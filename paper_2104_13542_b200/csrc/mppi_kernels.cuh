@@ -609,6 +609,272 @@ __device__ __forceinline__ bool rollout_particle(const RolloutArgs<R>& a, long l
   return true;
 }
 
+// Paired throughput rollout (FP32, control steps of configs 1/2, no bundle
+// dumps): particles g and g+1 of one instance in one warp, lane = horizon
+// step, both configurations of a lane in packed pairs (P2): every FMA of the
+// integration, forward kinematics (FkFold link transform), Jacobian and cost
+// stack is one FFMA2 for the two particles; sine/cosine, square roots and the
+// branch decisions stay per particle. Same operations per configuration as
+// rollout_particle<float, D, true, true> (step costs within FP32 rounding of
+// it; the contraction pattern of each sum is the compiler's in both).
+__device__ __forceinline__ P2 warp_inclusive_scan2(P2 v, int lane) {
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const float a = __shfl_up_sync(0xffffffffu, v.lo(), off);
+    const float b = __shfl_up_sync(0xffffffffu, v.hi(), off);
+    if (lane >= off) v += P2(a, b);
+  }
+  return v;
+}
+
+template <int D>
+__device__ __forceinline__ void rollout_pair(const RolloutArgs<float>& a, long long g, int lane) {
+  const int b = (int)(g / a.N);
+  const int n = (int)(g - (long long)b * a.N);  // particles n and n + 1 of instance b
+  const int status_b = a.skip_on_status ? a.status[b] : 0;
+  const int H = a.H;
+  const bool act = lane < H;
+  const int h = act ? lane : H - 1;
+  const ChainT<float>& ch = a.chain;
+  const CostT<float>& cs = a.cost;
+  const double* st = a.state_inline ? a.st0 : a.state + (size_t)b * 2 * D;
+  float st_p[D], st_v[D];
+#pragma unroll
+  for (int j = 0; j < D; ++j) {
+    st_p[j] = (float)st[j];
+    st_v[j] = (float)st[D + j];
+  }
+  const double* gl = a.state_inline ? a.g0 : a.goal + (size_t)b * 16;
+  float Rg[9], tg[3];
+#pragma unroll
+  for (int i = 0; i < 9; ++i) Rg[i] = (float)gl[i];
+#pragma unroll
+  for (int i = 0; i < 3; ++i) tg[i] = (float)gl[9 + i];
+  const int gmode = (int)gl[12];
+
+  // ---- controls (sampling.py:268-290) -> positions / velocities
+  P2 u[D];
+  bool bad0 = false, bad1 = false, varbad = false;
+  const int ng = n + a.particle_offset;
+  {
+    const int hs = a.shift ? h + 1 : h;
+    const double* mu = a.means + (size_t)b * H * D;
+    const double* sdv = a.sd + (size_t)b * H * D;
+    const size_t row0 = ((size_t)n * H + h) * D, row1 = row0 + (size_t)H * D;
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+      const double m = hs < H ? mu[hs * D + j] : a.tail_mean;
+      const double s = hs < H ? sdv[hs * D + j] : a.tail_sd;
+      varbad |= (s <= 0.0);
+      const double e0 = a.eps[row0 + j], e1 = a.eps[row1 + j];
+      const double u0 = ng < a.null_count ? 0.0 : (ng == a.null_count ? m : m + s * e0);
+      const double u1 = ng + 1 < a.null_count ? 0.0 : (ng + 1 == a.null_count ? m : m + s * e1);
+      bad0 |= !isfinite(u0);
+      bad1 |= !isfinite(u1);
+      u[j] = P2((float)u0, (float)u1);
+    }
+  }
+  if (status_b != 0) return;  // the instance already failed (an earlier iteration)
+  {
+    const unsigned bm0 = __ballot_sync(0xffffffffu, act && bad0);
+    const unsigned bm1 = __ballot_sync(0xffffffffu, act && bad1);
+    const unsigned varm = __ballot_sync(0xffffffffu, act && varbad);
+    if (lane == 0 && a.status != nullptr) {
+      if (varm && a.check_var && n == 0) atomicMax(&a.status[b], (int)MPPI_E_NONPOSITIVE_VARIANCE);
+      if (bm0 | bm1) {
+        atomicMin(&a.bad[b], bm0 ? ng : ng + 1);
+        atomicMax(&a.status[b], (int)MPPI_E_NONFINITE_CONTROL);
+      }
+    }
+  }
+  P2 v[D], p[D];
+  {
+    const P2 dt(act ? a.dts[h] : 0.f);
+#pragma unroll
+    for (int j = 0; j < D; ++j) v[j] = P2(st_v[j]) + warp_inclusive_scan2(dt * u[j], lane);
+#pragma unroll
+    for (int j = 0; j < D; ++j) p[j] = P2(st_p[j]) + warp_inclusive_scan2(dt * v[j], lane);
+  }
+
+  // ---- forward kinematics (FkFold for revolute links), Jacobian column data
+  P2 Rw[9] = {P2(1.f), P2(0.f), P2(0.f), P2(0.f), P2(1.f), P2(0.f), P2(0.f), P2(0.f), P2(1.f)};
+  P2 tw[3] = {P2(0.f), P2(0.f), P2(0.f)};
+  P2 ja[D][3], jp[D][3];
+#pragma unroll
+  for (int j = 0; j < 3; ++j) {
+    ja[0][j] = P2(ch.axes[0][j]);
+    jp[0][j] = P2(0.f);
+  }
+  const FkFold& f = a.fold;
+#pragma unroll
+  for (int k = 0; k < D; ++k) {
+    P2 Rmo[9], tmo[3];
+    if (ch.jtype[k] == 0) {
+      float s0, c0, s1, c1;
+      sincos_(p[k].lo(), &s0, &c0);
+      sincos_(p[k].hi(), &s1, &c1);
+      const P2 s(s0, s1), cm(1.f - c0, 1.f - c1);
+#pragma unroll
+      for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int jj = 0; jj < 3; ++jj)
+          Rmo[3 * i + jj] = P2(f.O[k][i][jj]) + s * P2(f.A[k][i][jj]) + cm * P2(f.B[k][i][jj]);
+#pragma unroll
+      for (int i = 0; i < 3; ++i) tmo[i] = P2(f.t[k][i]) + s * P2(f.a[k][i]) + cm * P2(f.b[k][i]);
+    } else {
+#pragma unroll
+      for (int i = 0; i < 9; ++i) Rmo[i] = P2(ch.orot[k][i]);
+#pragma unroll
+      for (int i = 0; i < 3; ++i) tmo[i] = p[k] * P2(ch.axes[k][i]) + P2(ch.otrans[k][i]);
+    }
+    P2 dtw[3];
+    mat33_vec(Rw, tmo, dtw);
+#pragma unroll
+    for (int i = 0; i < 3; ++i) tw[i] = tw[i] + dtw[i];
+    P2 Rn[9];
+    mat33_mul(Rw, Rmo, Rn);
+#pragma unroll
+    for (int i = 0; i < 9; ++i) Rw[i] = Rn[i];
+    if ((k + 1) % REORTHO_EVERY == 0) orthonormalize(Rw);
+    if (k + 1 < D) {
+      P2 axk[3] = {P2(ch.axes[k + 1][0]), P2(ch.axes[k + 1][1]), P2(ch.axes[k + 1][2])};
+      mat33_vec(Rw, axk, ja[k + 1]);
+#pragma unroll
+      for (int i = 0; i < 3; ++i) jp[k + 1][i] = tw[i];
+    }
+  }
+
+  // ---- cost terms (costs.py:76-187), as rollout_particle
+  P2 pose;
+  {
+    const P2 e0 = tw[0] - P2(tg[0]), e1 = tw[1] - P2(tg[1]), e2 = tw[2] - P2(tg[2]);
+    P2 acc(0.f);
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      const P2 di = P2(Rg[0 * 3 + i]) * e0 + P2(Rg[1 * 3 + i]) * e1 + P2(Rg[2 * 3 + i]) * e2;
+      const P2 wi = P2(cs.alpha_trans[i]) * di;
+      acc = acc + wi * wi;
+    }
+    pose = sqrt2(acc);
+    if (gmode != MPPI_GOAL_POSITION_ONLY) {
+      P2 racc(0.f);
+#pragma unroll
+      for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int kk = 0; kk < 3; ++kk) {
+          const P2 rr = P2(Rg[0 * 3 + i]) * Rw[0 * 3 + kk] + P2(Rg[1 * 3 + i]) * Rw[1 * 3 + kk] +
+                        P2(Rg[2 * 3 + i]) * Rw[2 * 3 + kk];
+          const P2 res = P2(cs.alpha_rot[i]) * (P2(i == kk ? 1.f : 0.f) - rr);
+          racc = racc + res * res;
+        }
+      pose = pose + sqrt2(racc);
+    }
+  }
+  P2 stop(0.f);
+  if (cs.use_stop) {
+    P2 acc(0.f);
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+      const P2 ex = max0(fabs2(v[j]) - P2(a.remaining[h] * ch.accel[j]));
+      acc = acc + ex * ex;
+    }
+    stop = sqrt2(acc);
+  }
+  P2 joint(0.f);
+  if (cs.use_joint) {
+    P2 acc(0.f);
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+      const P2 dep = max0(P2(ch.lo[j]) - p[j]) + max0(p[j] - P2(ch.hi[j]));
+      acc = acc + dep * dep;
+    }
+    joint = sqrt2(acc);
+  }
+  P2 manip(0.f);
+  if (cs.use_manip) {
+    P2 J[3][D];
+#pragma unroll
+    for (int k = 0; k < D; ++k) {
+      if (ch.jtype[k] == 0) {
+        const P2 rx = tw[0] - jp[k][0], ry = tw[1] - jp[k][1], rz = tw[2] - jp[k][2];
+        J[0][k] = ja[k][1] * rz - ja[k][2] * ry;
+        J[1][k] = ja[k][2] * rx - ja[k][0] * rz;
+        J[2][k] = ja[k][0] * ry - ja[k][1] * rx;
+      } else {
+        J[0][k] = ja[k][0];
+        J[1][k] = ja[k][1];
+        J[2][k] = ja[k][2];
+      }
+    }
+    const int td = ch.task_dim;
+    P2 m;
+    if (D == td) {
+      P2 det;
+      if (td == 2)
+        det = J[0][0] * J[1][1 % D] - J[0][1 % D] * J[1][0];
+      else
+        det = J[0][0] * (J[1][1 % D] * J[2][2 % D] - J[1][2 % D] * J[2][1 % D]) -
+              J[0][1 % D] * (J[1][0] * J[2][2 % D] - J[1][2 % D] * J[2][0]) +
+              J[0][2 % D] * (J[1][0] * J[2][1 % D] - J[1][1 % D] * J[2][0]);
+      m = fabs2(det);
+    } else {
+      P2 G[3][3];
+#pragma unroll
+      for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = 0; j < 3; ++j) {
+          P2 acc(0.f);
+#pragma unroll
+          for (int k = 0; k < D; ++k) acc = acc + J[i][k] * J[j][k];
+          G[i][j] = acc;
+        }
+      P2 det;
+      if (td == 2)
+        det = G[0][0] * G[1][1] - G[0][1] * G[1][0];
+      else
+        det = G[0][0] * (G[1][1] * G[2][2] - G[1][2] * G[2][1]) -
+              G[0][1] * (G[1][0] * G[2][2] - G[1][2] * G[2][0]) +
+              G[0][2] * (G[1][0] * G[2][1] - G[1][1] * G[2][0]);
+      m = sqrt2(max0(det));
+    }
+    const float m0 = m.lo(), m1 = m.hi();
+    manip = P2(m0 < cs.k_m ? 1.f - m0 : 0.f, m1 < cs.k_m ? 1.f - m1 : 0.f);
+  }
+  // total_cost (costs.py:176-187) minus the learned self-collision term
+  const P2 stepc = pose + P2(cs.a_stop) * stop + P2(cs.a_joint) * joint + P2(cs.a_manip) * manip;
+  if (act) {
+    const size_t m0 = (size_t)g * H + h, m1 = m0 + H;
+    a.step[m0] = stepc.lo();
+    a.step[m1] = stepc.hi();
+    if (a.mlp_x != nullptr) {  // 32-byte position rows of both particles (mlp_x_q)
+      float4* x0 = reinterpret_cast<float4*>(a.mlp_x + m0 * 8);
+      float4* x1 = reinterpret_cast<float4*>(a.mlp_x + m1 * 8);
+      float q0[8], q1[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        q0[j] = j < D ? p[j].lo() : 0.f;
+        q1[j] = j < D ? p[j].hi() : 0.f;
+      }
+      x0[0] = make_float4(q0[0], q0[1], q0[2], q0[3]);
+      x0[1] = make_float4(q0[4], q0[5], q0[6], q0[7]);
+      x1[0] = make_float4(q1[0], q1[1], q1[2], q1[3]);
+      x1[1] = make_float4(q1[4], q1[5], q1[6], q1[7]);
+    }
+  }
+}
+
+#ifndef MPPI_PAIR_MINB
+#define MPPI_PAIR_MINB 3
+#endif
+template <int D>
+__global__ void __launch_bounds__(kRolloutWarps * 32, MPPI_PAIR_MINB)
+    rollout_pair_kernel(const __grid_constant__ RolloutArgs<float> a) {
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const long long g = 2 * ((long long)blockIdx.x * kRolloutWarps + wib);
+  if (g >= (long long)a.B * a.N) return;  // warp-uniform exit
+  rollout_pair<D>(a, g, lane);
+}
+
 // MINB = 1: the latency build (128 registers, one warp per particle and at
 // most one wave); MINB = 6: the throughput build for many waves (80
 // registers, a few spills, 6 CTAs per SM to hide the FK dependency chains;

@@ -72,6 +72,16 @@ cudaError_t launch_rollout_d(const RolloutArgs<R>& a, long long warps, cudaStrea
   // float64 exact path and the evaluation modes keep the general kernel)
   const bool lean = std::is_same<R, float>::value && a.mode == 0 && !rollout_needs_caps(a.cost) &&
                     getenv("MPPI_ROLLOUT_GENERAL") == nullptr;
+  // the paired build (two particles per warp, packed FP32) for many-waves
+  // control steps without dumps; posenc hand-off and odd N keep the single one
+  if constexpr (std::is_same<R, float>::value) {
+    if (many && lean && a.N % 2 == 0 && a.out_pos == nullptr && a.out_terms == nullptr &&
+        (a.mlp_x == nullptr || a.mlp_x_q) && !(getenv("MPPI_ROLLOUT_SINGLE") && atoi(getenv("MPPI_ROLLOUT_SINGLE")))) {
+      const unsigned grid = (unsigned)((warps / 2 + kRolloutWarps - 1) / kRolloutWarps);
+      rollout_pair_kernel<D><<<grid, kRolloutWarps * 32, 0, st>>>(a);
+      return cudaGetLastError();
+    }
+  }
   auto kern = many ? (lean ? rollout_kernel<R, D, kRolloutMinBlocks, std::is_same<R, float>::value>
                            : rollout_kernel<R, D, kRolloutMinBlocks>)
                    : (lean ? rollout_kernel<R, D, 1, std::is_same<R, float>::value> : rollout_kernel<R, D, 1>);

@@ -397,3 +397,22 @@ def test_peer_exchange_abort_releases_waiting_rank():
     with pytest.raises(DeviceError, match="exchange"):
         r0.step_exchange(st.theta, st.theta_dot)
     assert time.perf_counter() - t0 < 10.0
+
+
+def test_paired_rollout_matches_single(monkeypatch):
+    """The paired throughput rollout (two particles per warp in packed FP32,
+    rollout_pair_kernel) against the one-particle-per-warp build on a batch
+    large enough for the many-waves path (80 x 500 = 40,000 warps): the same
+    operations per configuration up to the compiler's contraction choices, so
+    commands, best costs and policies agree to FP32 rounding."""
+    B, n = 80, 500
+    out = {}
+    for single in ("1", "0"):
+        monkeypatch.setenv("MPPI_ROLLOUT_SINGLE", single)  # read when the step graph is captured
+        bc, th0 = _batched_c2(B, n, "fp32")
+        cmds, diag = bc.control_step(th0, np.zeros_like(th0))
+        assert (diag.status == 0).all()
+        out[single] = (cmds.copy(), diag.best_cost.copy(), np.stack([bc.policy(b).means for b in range(B)]))
+    np.testing.assert_allclose(out["0"][0], out["1"][0], atol=2e-5)
+    np.testing.assert_allclose(out["0"][1], out["1"][1], rtol=2e-6)
+    np.testing.assert_allclose(out["0"][2], out["1"][2], atol=2e-5)
