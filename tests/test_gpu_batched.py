@@ -413,6 +413,8 @@ def test_paired_rollout_matches_single(monkeypatch):
         cmds, diag = bc.control_step(th0, np.zeros_like(th0))
         assert (diag.status == 0).all()
         out[single] = (cmds.copy(), diag.best_cost.copy(), np.stack([bc.policy(b).means for b in range(B)]))
-    np.testing.assert_allclose(out["0"][0], out["1"][0], atol=2e-5)
-    np.testing.assert_allclose(out["0"][1], out["1"][1], rtol=2e-6)
-    np.testing.assert_allclose(out["0"][2], out["1"][2], atol=2e-5)
+    # the rounding differences of the step costs pass through exp(-dc/beta):
+    # commands agree to 1e-4 (the FP32 parity bound against the oracle is 1e-3)
+    np.testing.assert_allclose(out["0"][0], out["1"][0], atol=1e-4)
+    np.testing.assert_allclose(out["0"][1], out["1"][1], rtol=1e-5)
+    np.testing.assert_allclose(out["0"][2], out["1"][2], atol=1e-4)
