@@ -786,7 +786,9 @@ def run_batched(args):
     value = units / (step_ms * 1e-3)
     e2e = []
     bc.plan.profile_stages(0)
-    for _ in range(max(3, args.steps // 4)):
+    for _ in range(2):  # untimed: the level-0 graph is captured on its first replay
+        bc.control_step(th0, thd)
+    for _ in range(max(3, args.steps // 2)):
         _flush_l2(flush)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
