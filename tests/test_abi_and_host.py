@@ -185,3 +185,32 @@ def test_reference_arm_bench_line():
     assert line["e2e"]["value"] == line["value"] and line["e2e"]["h2d_bytes_per_step"] == 0
     assert line["cpu_baseline"]["kind"] == "reference" and line["cpu_baseline"]["cores"] >= 1
     assert line["value"] > 0.0
+
+
+def test_roofline_dominant_kernel_from_launch_list(tmp_path):
+    """bench.py's roofline picks the dominant kernel from the committed ncu
+    launch list (the timed instantiation of each stage), not from the event
+    times, which tie between adjacent stages (VERDICT r1 weak #7)."""
+    from paper_2104_13542_b200 import roofline as RL
+
+    rows = ['"ID","Kernel Name","Metric Name","Metric Unit","Metric Value"']
+    times = [("void mppi::rollout_kernel<float, 7, 1, 1>(x)", [7600, 7700, 7500]),
+             ("void mppi::rollout_kernel<double, 7, 1, 0>(x)", [10500]),  # the FP64 plan's, launched once
+             ("void mppi::mlp_tcgen05_kernel<1>(x)", [8900, 8800, 9000]),
+             ("void mppi::stats_cluster_kernel<float, 7, 1>(x)", [10000, 10100, 9900])]
+    i = 0
+    for name, ts in times:
+        for t in ts:
+            rows.append(f'"{i}","{name}","gpu__time_duration.sum","ns","{t}"')
+            i += 1
+    (tmp_path / "r9_bench_launches.csv").write_text("\n".join(rows) + "\n")
+    share, src = RL.launch_shares(tmp_path, "bench_launches")
+    assert src.endswith("r9_bench_launches.csv")
+    assert share == {"rollout": 7600.0, "mlp": 8900.0, "update": 10000.0}
+    peaks = {"hbm_gbs": 6000.0, "bf16_tflops": 1600.0, "sm_max_mhz": 1965.0}
+    stage_ms = {"rollout": 0.0120, "mlp": 0.0123, "update": 0.0122}  # events: the MLP looks longest
+    roof = RL.step_roofline(stage_ms, rows=15000, particles=500, horizon=30, dof=7, config=2, peaks=peaks,
+                            peaks_kind="measured", ncu_share=share, ncu_share_source=src)
+    assert roof["kernel"].startswith("stats") and roof["bound"] == "hbm"
+    kern = RL.all_rooflines(stage_ms, rows=15000, dof=7, config=2, peaks=peaks, peaks_kind="measured")
+    assert set(kern) == {"rollout", "mlp", "update"}
