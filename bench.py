@@ -812,10 +812,15 @@ def run_batched(args):
         e2e.append((time.perf_counter() - t0) * 1e3)
     e2e_ms = _max_over_ranks(dist, float(np.mean(e2e)), local)
     st_mean = {k: float(np.mean(v)) for k, v in stages.items()}
-    ncu_sum, ncu_src = _ncu_summary("full_b64_metrics")  # 64 controllers x 500 x 30 (scripts/profile_batched.py)
+    # the newest batch capture (scripts/profile_batched.py): 80 controllers (paired rollout), else 64
+    ncu_sum, ncu_src = _ncu_summary("full_b80_metrics")
+    ncu_rows = 80 * 500 * 30
+    if ncu_sum is None:
+        ncu_sum, ncu_src = _ncu_summary("full_b64_metrics")
+        ncu_rows = 64 * 500 * 30
     roof = RL.step_roofline(st_mean, rows=(b - a) * args.particles * 30, particles=(b - a) * args.particles,
                             horizon=30, dof=7, config=2, peaks=peaks, peaks_kind=peaks_kind, ncu_summary=ncu_sum,
-                            ncu_source=ncu_src, ncu_rows=64 * 500 * 30)
+                            ncu_source=ncu_src, ncu_rows=ncu_rows)
     line = {
         "metric": METRIC, "value": value, "unit": "particle-steps/s", "n_gpus": ws, "steps": args.steps,
         "warmup": max(3, args.warmup), "ms_per_step": step_ms, "higher_is_better": True, "scaling": "weak"

@@ -39,7 +39,7 @@ def update_bytes_per_unit(dof: int = 7) -> int:
 
 
 # kernel-name fragments of each stage in an ncu summary (scripts/ncu_summary.py)
-NCU_KERNEL = {"rollout": "rollout_kernel", "mlp": "mlp_tcgen05", "update": "stats_"}
+NCU_KERNEL = {"rollout": "rollout_", "mlp": "mlp_tcgen05", "update": "stats_"}
 
 
 def ncu_traffic(summary: list | None, stage: str):

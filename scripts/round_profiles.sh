@@ -12,9 +12,9 @@ done
 B="python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-scale-roofline"
 $B > /dev/null 2>&1 && ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
   --log-file $O/${R}_bench_launches.csv $B > /dev/null 2>&1
-P="python scripts/profile_batched.py 64 3"
+P="python scripts/profile_batched.py 80 3"   # 80 x 500 = 40,000 warps: the many-waves (paired) rollout
 $P > /dev/null 2>&1 && ncu --set full --clock-control none --import-source on \
-  -k regex:"rollout_kernel|mlp_tcgen05|stats_kernel" -s 3 -c 3 -o $O/${R}_full_b64 $P > $O/${R}_full_b64.log 2>&1
+  -k regex:"rollout_pair_kernel|rollout_kernel|mlp_tcgen05|stats_kernel" -s 3 -c 3 -o $O/${R}_full_b80 $P > $O/${R}_full_b80.log 2>&1
 S="python scripts/profile_step.py 6 500 2 --flush"
 $S > /dev/null 2>&1 && ncu --set full --clock-control none --import-source on \
   -k regex:"rollout_kernel|mlp_tcgen05|stats_cluster" -s 6 -c 3 -o $O/${R}_full_c2 $S > $O/${R}_full_c2.log 2>&1
