@@ -204,6 +204,9 @@ def _maybe_init_dist(ws, local):
     import torch
     import torch.distributed as dist
 
+    if torch.cuda.device_count() <= local:
+        raise SystemExit(f"bench.py: rank {local} needs GPU {local}, but only {torch.cuda.device_count()} "
+                         "visible (one process per GPU)")
     torch.cuda.set_device(local)
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     return dist
