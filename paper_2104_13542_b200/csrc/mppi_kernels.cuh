@@ -1493,7 +1493,9 @@ __global__ void __launch_bounds__(kStatsThreads, 1) stats_cluster_kernel(const _
   const int blk = (int)cluster.block_rank();
   const int nblk = (int)cluster.num_blocks();
   const int H = a.H, HD = H * D, N = a.N;
-  const int n0 = blk * a.ppb;
+  // particles of this CTA: the instance's CTAs in grid order (several clusters
+  // per instance in the multi-cluster layout, one record each)
+  const int n0 = (int)blockIdx.x * a.ppb;
   const int cnt = max(0, min(N, n0 + a.ppb) - n0);
   const int slots = max(a.ppb, kClusterEpsRegs);
   double* tot = sm;                      // [slots]
@@ -1688,7 +1690,9 @@ __global__ void __launch_bounds__(kStatsThreads, 1) stats_cluster_kernel(const _
     }
   if (!LEAN && !a.finalize_inline) {  // rank record for the particle-sharded exchange
     const bool peer = a.peer_recv != nullptr;
-    double* out = peer ? parts : a.out_record + (size_t)b * (kRecHead + 2 * HD);
+    const int nclu = (int)gridDim.x / nblk;  // clusters per instance
+    double* out = peer ? parts
+                       : a.out_record + ((size_t)b * nclu + blockIdx.x / nblk) * (kRecHead + 2 * HD);
     if (peer) __syncthreads();  // every thread has read its partial sums out of `parts`
     if (owner) {
       out[kRecHead + o] = S1;

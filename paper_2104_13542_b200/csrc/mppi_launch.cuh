@@ -125,8 +125,53 @@ cudaError_t launch_stats_cluster_d(const StatsArgs<R>& s, cudaStream_t st) {
   return cudaLaunchKernelEx(&cfg, kern, s);
 }
 
+template <typename R>
+cudaError_t launch_finalize(const StatsArgs<R>& s, const double* recs, int count, cudaStream_t st);
+
 template <typename R, int D>
 cudaError_t launch_stats_d(const StatsArgs<R>& s, cudaStream_t st) {
+  // one instance beyond one cluster, up to 8192 particles: clusters of 16
+  // CTAs of 32 particles reduce in distributed shared memory to one record
+  // each (relative to the cluster's own minimum), finalize_kernel combines the
+  // records in fixed order and applies the update — one global combine level
+  // instead of the block records' two (A/B, config 5: N = 4096 92.5 -> 84 us
+  // per step, 8192 124.5 -> 120 us; at 32768 the block records are faster;
+  // MPPI_MULTI_CLUSTER_PPB=p overrides the particles per CTA, 0 disables)
+  int mc_ppb = s.N <= kClusterMax * kClusterMax * 32 ? 32 : 0;
+  if (const char* e = getenv("MPPI_MULTI_CLUSTER_PPB")) mc_ppb = atoi(e) > 0 ? std::min(atoi(e), kClusterMaxPPB) : 0;
+  if (mc_ppb > 0 && !s.totals_only && s.B == 1 && s.finalize_inline && !s.peer_recv && !s.dump_step &&
+      !s.dump_terms && !s.dump_weights && s.N > kClusterMax * kClusterMaxPPB) {
+    StatsArgs<R> c = s;
+    c.ppb = mc_ppb;
+    c.nblk = kClusterMax;
+    c.finalize_inline = 0;
+    c.reset_status = 0;
+    c.out_record = s.records;
+    const int nclu = (s.N + kClusterMax * mc_ppb - 1) / (kClusterMax * mc_ppb);
+    auto kern = stats_cluster_kernel<R, D, false>;
+    const size_t smem = stats_cluster_smem_bytes(c.ppb, c.H * D);
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (e != cudaSuccess) return e;
+    if (smem > 48 * 1024) {
+      e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess) return e;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(nclu * kClusterMax, 1, 1);
+    cfg.blockDim = dim3(kStatsThreads, 1, 1);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = kClusterMax;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    e = cudaLaunchKernelEx(&cfg, kern, c);
+    if (e != cudaSuccess) return e;
+    return launch_finalize<R>(s, s.records, nclu, st);
+  }
   // latency path: one cluster per instance when the particles fit 16 CTAs
   if (!s.totals_only && s.B <= 8 && s.nblk <= kClusterMax && s.ppb <= kClusterMaxPPB &&
       getenv("MPPI_NO_CLUSTER") == nullptr)

@@ -345,13 +345,14 @@ def test_pseudorandom_injected_noise_vs_oracle(arm7, rng):
         np.testing.assert_allclose(cmd, ocmd, atol=1e-7)
 
 
-@pytest.mark.parametrize("particles", [1500, 2048, 2100, 9000])
+@pytest.mark.parametrize("particles", [1500, 2048, 2100, 8192, 9000])
 def test_many_statistics_blocks_vs_oracle(arm7, rng, particles):
     """Up to 2048 particles one 16-CTA cluster holds the instance (94 and 128
-    particles per CTA here, beyond the 32 rows each thread preloads); more
-    leave the cluster kernel: 32 particles per block with a record combine, in
-    two levels once there are more than 16 blocks (66 and 282 blocks here: 5
-    and 18 groups)."""
+    particles per CTA here, beyond the 32 rows each thread preloads); up to
+    8192, clusters of 16 CTAs of 32 particles each reduce to one record and a
+    finalize kernel combines them (5 and 16 clusters here); beyond, 32
+    particles per block with a record combine in two levels (282 blocks here:
+    18 groups)."""
     from paper_2104_13542_b200 import configs
 
     c = configs.make_controller(1, particles=particles, precision="fp64")
