@@ -139,15 +139,17 @@ cudaError_t launch_stats_d(const StatsArgs<R>& s, cudaStream_t st) {
   // MPPI_MULTI_CLUSTER_PPB=p overrides the particles per CTA, 0 disables)
   int mc_ppb = s.N <= kClusterMax * kClusterMax * 32 ? 32 : 0;
   if (const char* e = getenv("MPPI_MULTI_CLUSTER_PPB")) mc_ppb = atoi(e) > 0 ? std::min(atoi(e), kClusterMaxPPB) : 0;
+  const int mc_clusters = mc_ppb > 0 ? (s.N + kClusterMax * mc_ppb - 1) / (kClusterMax * mc_ppb) : 0;
   if (mc_ppb > 0 && !s.totals_only && s.B == 1 && s.finalize_inline && !s.peer_recv && !s.dump_step &&
-      !s.dump_terms && !s.dump_weights && s.N > kClusterMax * kClusterMaxPPB) {
+      !s.dump_terms && !s.dump_weights && s.N > kClusterMax * kClusterMaxPPB &&
+      mc_clusters <= stats_rec_stride(s.nblk)) {  // one record slot per cluster in the plan's buffer
     StatsArgs<R> c = s;
     c.ppb = mc_ppb;
     c.nblk = kClusterMax;
     c.finalize_inline = 0;
     c.reset_status = 0;
     c.out_record = s.records;
-    const int nclu = (s.N + kClusterMax * mc_ppb - 1) / (kClusterMax * mc_ppb);
+    const int nclu = mc_clusters;
     auto kern = stats_cluster_kernel<R, D, false>;
     const size_t smem = stats_cluster_smem_bytes(c.ppb, c.H * D);
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
