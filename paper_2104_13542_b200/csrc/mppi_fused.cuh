@@ -60,7 +60,7 @@ template <int CW>
 __device__ __forceinline__ void store_cols(unsigned char* sm, uint32_t off_h, uint32_t off_l, uint32_t row,
                                            uint32_t k0, const float* y) {
 #pragma unroll
-  for (int i = 0; i < CW / 8; ++i) store_split8(sm, off_h, off_l, umma_off(row, k0 + 8 * i, kAChunkK), y + 8 * i);
+  for (int i = 0; i < CW / 8; ++i) store_split8_act(sm, off_h, off_l, umma_off(row, k0 + 8 * i, kAChunkK), y + 8 * i);
 }
 
 template <typename R, int D>

@@ -184,6 +184,36 @@ __device__ __forceinline__ void umma_commit(uint32_t bar) {
                : "memory");
 }
 
+// Warp-wide issue forms: the whole (converged) warp executes them and one
+// elected lane issues, so the descriptors stay warp-uniform and ptxas keeps
+// them in uniform registers — no per-MMA R2UR moves or divergent-issue loop.
+// (The lane-0-only issuer spent ~8 instructions with dependent R2UR latency
+// on each MMA and starved while 4 epilogue warps shared its scheduler:
+// scripts/micro/mlp_trace.cu.) The same lane (the lowest, lane 0) issues
+// every MMA and commit, as tcgen05.commit tracks the issuing thread's MMAs.
+__device__ __forceinline__ void umma_f16_w(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc,
+                                           uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\telect.sync _|e, 0xffffffff;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void umma_f16_ts_w(uint32_t tmem_d, uint32_t tmem_a, uint64_t b, uint32_t idesc,
+                                              uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\telect.sync _|e, 0xffffffff;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(b), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void umma_commit_w(uint32_t bar) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n}" ::"r"(bar)
+      : "memory");
+}
+
 __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
   uint32_t r[16];
   asm volatile(
@@ -218,6 +248,35 @@ __device__ __forceinline__ void store_split16(unsigned char* sm, uint32_t off_h,
     *reinterpret_cast<uint4*>(sm + off_h + o) = make_uint4(h[4 * c], h[4 * c + 1], h[4 * c + 2], h[4 * c + 3]);
     *reinterpret_cast<uint4*>(sm + off_l + o) = make_uint4(l[4 * c], l[4 * c + 1], l[4 * c + 2], l[4 * c + 3]);
   }
+}
+
+// ReLU + hi/lo split of one activation pair (element 0 in the low half), in
+// five SASS instructions per pair with the scale/bias FFMA2 in front of it
+// (round 2 had eight: FMNMX x2, F2FP, HADD2.F32 x2, FFMA2, F2FP):
+//   hi = fp16_rz(relu(v))          F2FP.RELU.RZ  (truncation keeps v - hi >= 0)
+//   lo = fp16_rn(relu(v - hi))     FHFMA x2 (mixed f16 x f16 + f32), F2FP.RELU
+// For v <= 0 both halves are 0; for v > 0, 0 <= v - hi < ulp16(v), so the
+// relu on lo is a no-op and hi + lo carries ~21 significant bits (the
+// round-to-nearest hi of store_split8 gives ~22; measured MLP error vs the
+// float64 reference stays ~3e-7 m).
+__device__ __forceinline__ void split_relu2(float v0, float v1, uint32_t& h, uint32_t& l) {
+  asm("cvt.rz.relu.f16x2.f32 %0, %1, %2;" : "=r"(h) : "f"(v1), "f"(v0));
+  float d0, d1;
+  const unsigned short m1 = 0xBC00u;  // fp16 -1.0
+  asm("fma.rn.f32.f16 %0, %1, %2, %3;" : "=f"(d0) : "h"((unsigned short)(h & 0xffffu)), "h"(m1), "f"(v0));
+  asm("fma.rn.f32.f16 %0, %1, %2, %3;" : "=f"(d1) : "h"((unsigned short)(h >> 16)), "h"(m1), "f"(v1));
+  asm("cvt.rn.relu.f16x2.f32 %0, %1, %2;" : "=r"(l) : "f"(d1), "f"(d0));
+}
+
+// 8 ReLU activations (already >= 0) -> one hi and one lo 16-byte core-matrix
+// row with the split of split_relu2 (the fused kernel's A buffers).
+__device__ __forceinline__ void store_split8_act(unsigned char* sm, uint32_t off_h, uint32_t off_l, uint32_t o,
+                                                 const float* y) {
+  uint32_t h[4], l[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) split_relu2(y[2 * i], y[2 * i + 1], h[i], l[i]);
+  *reinterpret_cast<uint4*>(sm + off_h + o) = make_uint4(h[0], h[1], h[2], h[3]);
+  *reinterpret_cast<uint4*>(sm + off_l + o) = make_uint4(l[0], l[1], l[2], l[3]);
 }
 
 // 8 fp32 -> one hi and one lo 16-byte core-matrix row.
@@ -275,6 +334,33 @@ __device__ __forceinline__ void tmem_wait_ld8(uint32_t* r) {
                : "memory");
 }
 
+__device__ __forceinline__ void tmem_ld16_async(uint32_t taddr, uint32_t* r) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_wait_ld16(uint32_t* r) {
+  asm volatile("tcgen05.wait::ld.sync.aligned;"
+               : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7]),
+                 "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]), "+r"(r[13]), "+r"(r[14]),
+                 "+r"(r[15])
+               :
+               : "memory");
+}
+template <int X>
+__device__ __forceinline__ void tmem_ld_async(uint32_t taddr, uint32_t* r) {
+  if constexpr (X == 16) tmem_ld16_async(taddr, r);
+  else tmem_ld8_async(taddr, r);
+}
+template <int X>
+__device__ __forceinline__ void tmem_wait_ld(uint32_t* r) {
+  if constexpr (X == 16) tmem_wait_ld16(r);
+  else tmem_wait_ld8(r);
+}
+
 __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
 }
@@ -309,6 +395,23 @@ __device__ __forceinline__ void epi_barrier() {  // named barrier over the 512 e
 // layer-2 epilogue converts, and the next tile's layer-1 epilogue runs under
 // layer 3. 88 registers: 544 x 88 + a 128-thread rollout CTA fit one SM's 64K
 // register file (programmatic dependent launch, opt-in).
+// Epilogue geometry: each warp converts kEpiCols accumulator columns of its
+// lane quadrant per chunk; a chunk (4 column groups) is what one A1/A2
+// barrier hands to the issuer. 8 (default): two warps per 16-column K slice,
+// meeting at a named barrier, 32-column chunks. 16: a warp owns whole slices
+// (one 32x32b.x16 TMEM load and one x16 store per chunk, no pair barrier;
+// x16 accesses move ~1.4x the bytes per clock of x8, scripts/micro/tmem_bw.cu)
+// in 64-column chunks — measured equal at config 4 (4.20 vs 4.22e9
+// particle-steps/s) and 1.5 us slower in the config-2 MLP, whose one tile
+// per CTA streams into layer 2 at half the granularity (gpurun_out/ab_elect).
+#ifndef MPPI_MLP_EPI_COLS
+#define MPPI_MLP_EPI_COLS 8
+#endif
+constexpr int kEpiCols = MPPI_MLP_EPI_COLS;
+static_assert(kEpiCols == 8 || kEpiCols == 16, "epilogue columns per warp");
+constexpr int kChunkCols = 4 * kEpiCols;
+constexpr int kL1Chunks = kMlpH0 / kChunkCols, kL2Chunks = kMlpH1 / kChunkCols;
+constexpr int kSlicesPerChunk = kChunkCols / 16;
 // barriers: W0 W1 W2 | L1[2] | A1[8] | L2done | A2[4] | L3done | X
 constexpr int kMlpBars = 3 + 2 + 8 + 1 + 4 + 1 + 1;
 constexpr uint32_t OFF_KBAR = OFF_XL + 128 * 16 * 2;
@@ -332,19 +435,6 @@ __device__ __forceinline__ void tmem_st4(uint32_t taddr, const uint32_t* v) {
                : "memory");
 }
 
-// y = relu(y * s + b) for 8 accumulator columns: packed FP32 (FFMA2), the
-// epilogue is the MLP's bound at scale (CUDA-core work per tile > tensor time)
-__device__ __forceinline__ void scale_bias_relu8(float* y, float s, const float* b) {
-  const float2 s2 = make_float2(s, s);
-  const float2* b2 = reinterpret_cast<const float2*>(b);
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const float2 v = __ffma2_rn(make_float2(y[2 * i], y[2 * i + 1]), s2, b2[i]);
-    y[2 * i] = fmaxf(v.x, 0.f);
-    y[2 * i + 1] = fmaxf(v.y, 0.f);
-  }
-}
-
 // Output layer share of C accumulator columns: relu((hi + lo products) * s +
 // b) . w3, packed FP32 with two partial sums (shared by mlp_tcgen05_kernel and
 // the fused kernel so both sum in the same order)
@@ -365,26 +455,54 @@ __device__ __forceinline__ float output_part(const float* y, const float* z, flo
   return acc.x + acc.y;
 }
 
-// 8 fp32 activations (columns 8cg..8cg+7 of a 32-column chunk at `chunk`) ->
-// 4 hi + 4 lo packed fp16 columns of the chunk's slice (cg >> 1) layout.
-// `pair_bar`: named barrier of the two warps of the slice.
-__device__ __forceinline__ void tmem_convert8(uint32_t chunk, int cg, const float* y, int pair_bar) {
+// 8 fp32 accumulator columns (columns 8cg..8cg+7 of a 32-column chunk at
+// `chunk`) -> relu(y * s + b) -> 4 hi + 4 lo packed fp16 columns of the
+// chunk's slice (cg >> 1) layout. `pair_bar`: named barrier of the two warps
+// of the slice.
+__device__ __forceinline__ void tmem_convert8(uint32_t chunk, int cg, const float* y, float s, const float* b,
+                                              int pair_bar) {
   uint32_t h[4], l[4];
+  const float2 s2 = make_float2(s, s);
+  const float2* b2 = reinterpret_cast<const float2*>(b);
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
-    const __half2 hh = __floats2half2_rn(y[2 * i], y[2 * i + 1]);
-    const float2 hf = __half22float2(hh);
-    // lo = y - hi for both elements in one packed FP32 op (FFMA2: hi * -1 + y)
-    const float2 d = __ffma2_rn(hf, make_float2(-1.f, -1.f), make_float2(y[2 * i], y[2 * i + 1]));
-    const __half2 ll = __floats2half2_rn(d.x, d.y);
-    h[i] = *reinterpret_cast<const uint32_t*>(&hh);
-    l[i] = *reinterpret_cast<const uint32_t*>(&ll);
+    const float2 v = __ffma2_rn(make_float2(y[2 * i], y[2 * i + 1]), s2, b2[i]);
+    split_relu2(v.x, v.y, h[i], l[i]);
   }
   asm volatile("bar.sync %0, 64;" ::"r"(pair_bar) : "memory");  // both warps of the slice have read
   const uint32_t slice = chunk + 16 * (cg >> 1), half = 4 * (cg & 1);
   tmem_st4(slice + half, h);
   tmem_st4(slice + 8 + half, l);
   asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+}
+
+// 16 fp32 accumulator columns of one warp's own K slice (TMEM columns
+// [slice, slice + 16)) -> relu(y * s + b) -> 8 hi then 8 lo packed fp16
+// columns in the same 16 columns: one x16 store, no other warp involved.
+__device__ __forceinline__ void tmem_convert16(uint32_t slice, const float* y, float s, const float* b) {
+  uint32_t hl[16];
+  const float2 s2 = make_float2(s, s);
+  const float2* b2 = reinterpret_cast<const float2*>(b);
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const float2 v = __ffma2_rn(make_float2(y[2 * i], y[2 * i + 1]), s2, b2[i]);
+    split_relu2(v.x, v.y, hl[i], hl[8 + i]);
+  }
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(slice),
+      "r"(hl[0]), "r"(hl[1]), "r"(hl[2]), "r"(hl[3]), "r"(hl[4]), "r"(hl[5]), "r"(hl[6]), "r"(hl[7]), "r"(hl[8]),
+      "r"(hl[9]), "r"(hl[10]), "r"(hl[11]), "r"(hl[12]), "r"(hl[13]), "r"(hl[14]), "r"(hl[15])
+      : "memory");
+  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+}
+
+// one warp's share of an accumulator chunk starting at TMEM column `chunk`
+template <int X>
+__device__ __forceinline__ void tmem_convert(uint32_t chunk, int cg, const float* y, float s, const float* b,
+                                             int pair_bar) {
+  if constexpr (X == 16) tmem_convert16(chunk + 16 * cg, y, s, b);
+  else tmem_convert8(chunk, cg, y, s, b, pair_bar);
 }
 
 #ifdef MPPI_DEBUG_TIMERS
@@ -401,6 +519,18 @@ static __device__ unsigned long long* mlp_dbg = nullptr;
 #else
 #define MLP_STAMP(k) \
   do {               \
+  } while (0)
+#endif
+#ifdef MPPI_MLP_TRACE
+// per-tile event clocks of CTA 0 (scripts/micro/mlp_trace.cu): [local tile][event]
+__device__ long long mlp_trace[32 * 32];
+#define MLP_TRACE(k, e)                                                          \
+  do {                                                                         \
+    if (blockIdx.x == 0 && (k) < 32) mlp_trace[(k) * 32 + (e)] = clock64();    \
+  } while (0)
+#else
+#define MLP_TRACE(k, e) \
+  do {                  \
   } while (0)
 #endif
 
@@ -458,6 +588,9 @@ static __global__ void __maxnreg__(88)
         bulk_g2s(sb + OFF_W1H + o, img + OFF_W1H + o, min(32768u, kSeg1 - o), barW1);
       mbar_expect_tx(barW2, kSeg2);
       bulk_g2s(sb + OFF_W2H, img + OFF_W2H, kSeg2, barW2);
+    }
+    __syncwarp();
+    {  // the whole warp from here on: MMAs and commits issued by one elected lane
       const uint32_t id64 = umma_idesc(64), id128 = umma_idesc(128);
       const uint64_t dXH = umma_desc(sb + OFF_XH, 128, 256), dXL = umma_desc(sb + OFF_XL, 128, 256);
       const uint64_t dW0H = umma_desc(sb + OFF_W0H, 128, 256), dW0L = umma_desc(sb + OFF_W0L, 128, 256);
@@ -467,15 +600,16 @@ static __global__ void __maxnreg__(88)
 #pragma unroll
         for (int hf = 0; hf < 2; ++hf) {
           const uint64_t wo = umma_off(128 * hf, 0, 16) >> 4;
-          umma_f16(tmem + 128 * hf, dXH, dW0H + wo, id128, 0);
-          umma_f16(tmem + 128 * hf, dXH, dW0L + wo, id128, 1);
-          umma_f16(tmem + 128 * hf, dXL, dW0H + wo, id128, 1);
-          umma_commit(barL10 + 8 * hf);
+          umma_f16_w(tmem + 128 * hf, dXH, dW0H + wo, id128, 0);
+          umma_f16_w(tmem + 128 * hf, dXH, dW0L + wo, id128, 1);
+          umma_f16_w(tmem + 128 * hf, dXL, dW0H + wo, id128, 1);
+          umma_commit_w(barL10 + 8 * hf);
         }
       };
       uint32_t phX = 0, ph = 0;  // ph: parity of the once-per-tile barriers (A1[c], A2[c], L2done, L3done)
       bool first = true;
-      for (long long tile = blockIdx.x; tile < ntiles; tile += G, ph ^= 1u) {
+      int it = 0;
+      for (long long tile = blockIdx.x; tile < ntiles; tile += G, ph ^= 1u, ++it) {
         const bool has_next = !ONE_TILE && tile + G < ntiles;
         if (first) {
           mbar_wait(barX, phX);
@@ -485,53 +619,63 @@ static __global__ void __maxnreg__(88)
           issue_l1();
         }
 #pragma unroll
-        for (int c = 0; c < 8; ++c) {  // layer 2, K chunk c: slices 2c, 2c+1 of acc1 (in place)
+        for (int c = 0; c < kL1Chunks; ++c) {  // layer 2, K chunk c: its slices of acc1 (in place)
           mbar_wait(barA1 + 8 * c, ph);
+          if (c == 0 && lane == 0) MLP_TRACE(it, 8);
+          if (c == kL1Chunks - 1) if (lane == 0) MLP_TRACE(it, 9);
           if (first && c == 0) {
             mbar_wait(barW1, 0);
-            MLP_STAMP(9);
+            if (lane == 0) MLP_STAMP(9);
           }
           if (!first && c == 0) {  // acc2 is rewritten: the previous tile's layer 3 (its A reader) is done
             mbar_wait(barL3done, ph ^ 1u);
+            if (lane == 0) MLP_TRACE(it, 6);
           }
           tc_fence_after();
 #pragma unroll
-          for (int g = 0; g < 2; ++g) {
-            const int s = 2 * c + g;
+          for (int g = 0; g < kSlicesPerChunk; ++g) {
+            const int s = kSlicesPerChunk * c + g;
             const uint32_t ah = tmem + 16 * s, al = ah + 8;
             const uint64_t wj = (uint64_t)((2 * s) * 128 >> 4);
-            umma_f16_ts(acc2, ah, dW1H + wj, id128, s ? 1u : 0u);
-            umma_f16_ts(acc2, ah, dW1L + wj, id128, 1);
-            umma_f16_ts(acc2, al, dW1H + wj, id128, 1);
+            umma_f16_ts_w(acc2, ah, dW1H + wj, id128, s ? 1u : 0u);
+            umma_f16_ts_w(acc2, ah, dW1L + wj, id128, 1);
+            umma_f16_ts_w(acc2, al, dW1H + wj, id128, 1);
           }
         }
-        umma_commit(barL2done);
+        umma_commit_w(barL2done);
+        if (lane == 0) MLP_TRACE(it, 10);
         if (has_next) {  // acc1 is free once layer 2 has read it; X(t+1) staged by the epilogue
           mbar_wait(barL2done, ph);
+          if (lane == 0) MLP_TRACE(it, 11);
           mbar_wait(barX, phX);
+          if (lane == 0) MLP_TRACE(it, 16);
           phX ^= 1;
           tc_fence_after();
           issue_l1();
+          if (lane == 0) MLP_TRACE(it, 17);
         }
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {  // layer 3, K chunk c: slices 2c, 2c+1 of acc2 (in place)
+        for (int c = 0; c < kL2Chunks; ++c) {  // layer 3, K chunk c: its slices of acc2 (in place)
           mbar_wait(barA2 + 8 * c, ph);
+          if (c == 0 && lane == 0) MLP_TRACE(it, 12);
+          if (c == kL2Chunks - 1) if (lane == 0) MLP_TRACE(it, 13);
           if (first && c == 0) {
             mbar_wait(barW2, 0);
-            MLP_STAMP(10);
+            if (lane == 0) MLP_STAMP(10);
           }
           tc_fence_after();
 #pragma unroll
-          for (int g = 0; g < 2; ++g) {
-            const int s = 2 * c + g;
+          for (int g = 0; g < kSlicesPerChunk; ++g) {
+            const int s = kSlicesPerChunk * c + g;
             const uint32_t ah = acc2 + 16 * s, al = ah + 8;
             const uint64_t wj = (uint64_t)((2 * s) * 128 >> 4);
             // W2 hi and lo are adjacent 64-row operands: A_hi [W hi | W lo] in one N=128 MMA
-            umma_f16_ts(acc3, ah, dW2H + wj, id128, s ? 1u : 0u);
-            umma_f16_ts(acc3, al, dW2H + wj, id64, 1);
+            umma_f16_ts_w(acc3, ah, dW2H + wj, id128, s ? 1u : 0u);
+            umma_f16_ts_w(acc3, al, dW2H + wj, id64, 1);
           }
         }
-        umma_commit(barL3done);
+        umma_commit_w(barL3done);
+        if (lane == 0) MLP_TRACE(it, 14);
         first = false;
       }
       if (first) {
@@ -640,31 +784,37 @@ static __global__ void __maxnreg__(88)
     const float s2 = par[kMlpH0 + kMlpH1 + 2 * kMlpH2 + 3];
     uint32_t phL1 = 0;
     // layer-1 epilogue of tile t, in place in acc1; stages X(t + G) on the way
+    int eit = 0;  // local tile counter (trace)
     auto epilogue_l1 = [&](long long t) {
       const bool nxt = !ONE_TILE && t + G < ntiles;
       if (nxt) load_x(t + G, xv);
       // chunk c+1's TMEM load is in flight while chunk c is converted (within
       // one layer-1 half: the second half waits for its own MMA barrier)
-      uint32_t rb[2][8];
+      constexpr int HC = kL1Chunks / 2;  // chunks per layer-1 half (one MMA barrier each)
+      uint32_t rb[2][kEpiCols];
 #pragma unroll
-      for (int c = 0; c < 8; ++c) {
-        if ((c & 3) == 0) {
-          const int hb = c >> 2;
+      for (int c = 0; c < kL1Chunks; ++c) {
+        if (c % HC == 0) {
+          const int hb = c / HC;
           mbar_wait(barL10 + 8 * hb, (phL1 >> hb) & 1u);
           if (tid == 0 && hb == 0 && t == blockIdx.x) MLP_STAMP(3);
+          if (tid == 0 && hb == 0) MLP_TRACE(eit, 2);
           phL1 ^= 1u << hb;
           tc_fence_after();
-          tmem_ld8_async(tmem + lane_base + 32 * c + 8 * cg, rb[c & 1]);
+          tmem_ld_async<kEpiCols>(tmem + lane_base + kChunkCols * c + kEpiCols * cg, rb[c & 1]);
         }
-        tmem_wait_ld8(rb[c & 1]);
-        if ((c & 3) != 3) tmem_ld8_async(tmem + lane_base + 32 * (c + 1) + 8 * cg, rb[(c + 1) & 1]);
-        float y[8];
+        tmem_wait_ld<kEpiCols>(rb[c & 1]);
+        if (c % HC != HC - 1)
+          tmem_ld_async<kEpiCols>(tmem + lane_base + kChunkCols * (c + 1) + kEpiCols * cg, rb[(c + 1) & 1]);
+        float y[kEpiCols];
 #pragma unroll
-        for (int i = 0; i < 8; ++i) y[i] = __uint_as_float(rb[c & 1][i]);
-        scale_bias_relu8(y, s0, b0 + 32 * c + 8 * cg);
-        tmem_convert8(tmem + lane_base + 32 * c, cg, y, pair_bar);
+        for (int i = 0; i < kEpiCols; ++i) y[i] = __uint_as_float(rb[c & 1][i]);
+        tmem_convert<kEpiCols>(tmem + lane_base + kChunkCols * c, cg, y, s0, b0 + kChunkCols * c + kEpiCols * cg,
+                               pair_bar);
         arrive(barA1 + 8 * c);
-        if (c == 7 && nxt) {  // both layer-1 halves done (barL1[1]): X can be rewritten
+        if (tid == 0) MLP_TRACE(eit, 24 + c);
+        if (tid == 0 && c == kL1Chunks - 1) MLP_TRACE(eit, 3);
+        if (c == kL1Chunks - 1 && nxt) {  // both layer-1 halves done (barL1[1]): X can be rewritten
           encode_x(xv);
           if (tid < 256) store_split8(sm, OFF_XH, OFF_XL, umma_off(tid & 127, (tid >> 7) * 8, 16), xv);
           fence_async_smem();
@@ -680,26 +830,33 @@ static __global__ void __maxnreg__(88)
       // ---- layer-2 epilogue, in place in acc2
       mbar_wait(barL2done, ph);
       if (tid == 0 && tile == blockIdx.x) MLP_STAMP(5);
+      if (tid == 0) MLP_TRACE(eit, 0);
       tc_fence_after();
-      uint32_t r2[2][8];
-      tmem_ld8_async(acc2 + lane_base + 8 * cg, r2[0]);
+      uint32_t r2[2][kEpiCols];
+      tmem_ld_async<kEpiCols>(acc2 + lane_base + kEpiCols * cg, r2[0]);
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {  // chunk c+1's TMEM load in flight under chunk c
-        tmem_wait_ld8(r2[c & 1]);
-        if (c < 3) tmem_ld8_async(acc2 + lane_base + 32 * (c + 1) + 8 * cg, r2[(c + 1) & 1]);
-        float y[8];
+      for (int c = 0; c < kL2Chunks; ++c) {  // chunk c+1's TMEM load in flight under chunk c
+        tmem_wait_ld<kEpiCols>(r2[c & 1]);
+        if (c + 1 < kL2Chunks)
+          tmem_ld_async<kEpiCols>(acc2 + lane_base + kChunkCols * (c + 1) + kEpiCols * cg, r2[(c + 1) & 1]);
+        float y[kEpiCols];
 #pragma unroll
-        for (int i = 0; i < 8; ++i) y[i] = __uint_as_float(r2[c & 1][i]);
-        scale_bias_relu8(y, s1, b1 + 32 * c + 8 * cg);
-        tmem_convert8(acc2 + lane_base + 32 * c, cg, y, pair_bar);
+        for (int i = 0; i < kEpiCols; ++i) y[i] = __uint_as_float(r2[c & 1][i]);
+        tmem_convert<kEpiCols>(acc2 + lane_base + kChunkCols * c, cg, y, s1, b1 + kChunkCols * c + kEpiCols * cg,
+                               pair_bar);
         arrive(barA2 + 8 * c);
+        if (tid == 0) MLP_TRACE(eit, 20 + c);
       }
       if (tid == 0 && tile == blockIdx.x) MLP_STAMP(6);
+      if (tid == 0) MLP_TRACE(eit, 1);
+      ++eit;  // the next tile's layer-1 epilogue records under its own index
       // ---- the next tile's layer-1 epilogue runs under this tile's layer 3
       if (has_next) epilogue_l1(tile + G);
+      --eit;
       // ---- output layer of this tile
       mbar_wait(barL3done, ph);
       if (tid == 0 && tile == blockIdx.x) MLP_STAMP(7);
+      if (tid == 0) MLP_TRACE(eit, 4);
       tc_fence_after();
       float part = 0.f;
       {
@@ -722,6 +879,8 @@ static __global__ void __maxnreg__(88)
         if (row < M) out[row] = o;
       }
       if (tid == 0 && tile == blockIdx.x) MLP_STAMP(8);
+      if (tid == 0) MLP_TRACE(eit, 5);
+      ++eit;
     }
   }
   tc_fence_before();  // every TMEM read of this CTA is ordered before the dealloc
