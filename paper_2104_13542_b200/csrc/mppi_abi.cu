@@ -1297,7 +1297,7 @@ int mppi_step(mppi_plan* p, const double* theta, const double* theta_dot, double
     }
     for (int k = 0; k < p->nblk; ++k) {
       fprintf(stderr, "stats blk %2d:", k);
-      for (int j = 0; j < 8; ++j)
+      for (int j = 0; j < 14; ++j)
         fprintf(stderr, " %8.2f", t[k * 16 + j] ? (double)(long long)(t[k * 16 + j] - t0) * 1e-3 : -1.0);
       fprintf(stderr, "\n");
     }

@@ -1492,6 +1492,9 @@ __global__ void __launch_bounds__(kStatsThreads, 1) stats_cluster_kernel(const _
   const int b = blockIdx.y;
   const int blk = (int)cluster.block_rank();
   const int nblk = (int)cluster.num_blocks();
+  // the CTA that reduces the weighted sums and applies the update (rank 0;
+  // the last rank, which has the fewest particles, measured 0.2 us slower)
+  const int root = 0;
   const int H = a.H, HD = H * D, N = a.N;
   // particles of this CTA: the instance's CTAs in grid order (several clusters
   // per instance in the multi-cluster layout, one record each)
@@ -1515,7 +1518,7 @@ __global__ void __launch_bounds__(kStatsThreads, 1) stats_cluster_kernel(const _
     cbar_init(bar_min, 1);
     cbar_init(bar_sum, 1);
     cbar_arrive_expect(bar_min, 8u * nblk);
-    if (blk == 0) cbar_arrive_expect(bar_sum, (16u * HD + 32u) * nblk);
+    if (blk == root) cbar_arrive_expect(bar_sum, (16u * HD + 32u) * nblk);
   }
   cluster_init_fence_arrive();  // waited on before the first push
   // ---- requests that do not depend on this step's costs ----------------------
@@ -1534,6 +1537,7 @@ __global__ void __launch_bounds__(kStatsThreads, 1) stats_cluster_kernel(const _
   const double disc_l = lane < H - 1 ? a.disc[lane] : a.dlast;
   pdl_wait();
   const int status0 = a.status[b];
+  const int bad0 = a.bad[b];  // (final once the rollout is complete) read here, off the update's path
   const bool failed = status0 != 0;
   MPPI_STAMP(0);
 
@@ -1597,6 +1601,9 @@ __global__ void __launch_bounds__(kStatsThreads, 1) stats_cluster_kernel(const _
   __syncthreads();
   MPPI_STAMP(1);
   // ---- instance-wide best finite total: pushed to every peer -----------------
+  // (Weighing against each CTA's own minimum and rescaling the sums at the
+  // root instead — no round trip before the weights — measured 0.5 us slower:
+  // the root's extra exp/shuffles cost more than the exchange it saves.)
   cluster_wait();  // every peer's receive barriers are initialised
   if (wid == 0) {
     double v = CUDART_INF;
@@ -1605,6 +1612,26 @@ __global__ void __launch_bounds__(kStatsThreads, 1) stats_cluster_kernel(const _
     for (int off = 16; off > 0; off >>= 1) v = fmin(v, __shfl_xor_sync(0xffffffffu, v, off));
     if (lane < nblk) push_f64(mapa_rank(smem_addr(&mins[blk]), lane), v, mapa_rank(bar_min, lane));
   }
+  // deviations u - mu_old of the register rows (they do not depend on the
+  // costs), computed while the minimum exchange is in flight, branch-free;
+  // the null and mean rows (sampling.py:283-285) exist only in the CTA
+  // holding global particles 0..null_count and are patched there (a
+  // CTA-uniform branch), so the weighted sums below are one straight FMA
+  // schedule (per-row selects inside the sums compiled to 32 branches that
+  // serialised the chains: 1.05 -> 0.4 us)
+  if (owner) {
+    const int g0 = n0 + a.particle_offset;  // global index of this CTA's first particle
+#pragma unroll
+    for (int i = 0; i < kClusterEpsRegs; ++i) e[i] = (mo + so * e[i]) - mo;
+    if (g0 <= a.null_count) {  // dv = k1 * dv + k0: (1, 0) sampled, (0, -mu) null, (0, 0) mean row
+#pragma unroll
+      for (int i = 0; i < kClusterEpsRegs; ++i) {
+        const int ng = g0 + i;
+        e[i] = fma(ng > a.null_count ? 1.0 : 0.0, e[i], ng < a.null_count ? 0.0 - mo : 0.0);
+      }
+    }
+  }
+  MPPI_STAMP(13);  // (debug) deviations formed: the perturbation rows have arrived
   cbar_wait(bar_min, 0);
   double m = CUDART_INF;
   for (int k = 0; k < nblk; ++k) m = mins[k] < m ? mins[k] : m;  // finite or +inf, never NaN
@@ -1631,8 +1658,7 @@ __global__ void __launch_bounds__(kStatsThreads, 1) stats_cluster_kernel(const _
         const double2 w = w2[i / 2];
 #pragma unroll
         for (int u = 0; u < 2; ++u) {
-          const int ng = g0 + i + u;
-          const double dv = ng < a.null_count ? 0.0 - mo : (ng == a.null_count ? 0.0 : (mo + so * e[i + u]) - mo);
+          const double dv = e[i + u];
           const double wu = u ? w.y : w.x;
           s1[(i + u) & 3] += wu * dv;
           s2[(i + u) & 3] += wu * dv * dv;
@@ -1646,8 +1672,10 @@ __global__ void __launch_bounds__(kStatsThreads, 1) stats_cluster_kernel(const _
         s2[0] += wt[i] * dv * dv;
       }
     }
-    push_f64x2(mapa_rank(smem_addr(parts + ((size_t)blk * HD + o) * 2), 0), (s1[0] + s1[1]) + (s1[2] + s1[3]),
-               (s2[0] + s2[1]) + (s2[2] + s2[3]), mapa_rank(bar_sum, 0));
+    MPPI_STAMP(8);
+    push_f64x2(mapa_rank(smem_addr(parts + ((size_t)blk * HD + o) * 2), root), (s1[0] + s1[1]) + (s1[2] + s1[3]),
+               (s2[0] + s2[1]) + (s2[2] + s2[3]), mapa_rank(bar_sum, root));
+    MPPI_STAMP(9);
   }
   if (wid == nw - 1) {
     double s0 = 0.0, c = 0.0, sf = 0.0;
@@ -1662,11 +1690,11 @@ __global__ void __launch_bounds__(kStatsThreads, 1) stats_cluster_kernel(const _
     s0 = warp_sum(s0);
     c = warp_sum(c);
     sf = warp_sum(sf);
-    if (lane == 0) push_f64x2(mapa_rank(smem_addr(heads + blk * 4), 0), s0, c, mapa_rank(bar_sum, 0));
-    if (lane == 1) push_f64x2(mapa_rank(smem_addr(heads + blk * 4 + 2), 0), sf, 0.0, mapa_rank(bar_sum, 0));
+    if (lane == 0) push_f64x2(mapa_rank(smem_addr(heads + blk * 4), root), s0, c, mapa_rank(bar_sum, root));
+    if (lane == 1) push_f64x2(mapa_rank(smem_addr(heads + blk * 4 + 2), root), sf, 0.0, mapa_rank(bar_sum, root));
   }
   MPPI_STAMP(4);
-  if (blk != 0) return;  // peers are done: every push into them has landed
+  if (blk != root) return;  // peers are done: every push into them has landed
   cbar_wait(bar_sum, 0);
   MPPI_STAMP(5);
   // ---- rank 0: reduce in rank order, update in registers ---------------------
@@ -1683,11 +1711,18 @@ __global__ void __launch_bounds__(kStatsThreads, 1) stats_cluster_kernel(const _
     sumf = warp_sum(x2);
   }
   double S1 = 0.0, S2 = 0.0;
-  if (owner)
-    for (int k = 0; k < nblk; ++k) {
-      S1 += parts[((size_t)k * HD + o) * 2];
-      S2 += parts[((size_t)k * HD + o) * 2 + 1];
+  if (owner) {  // every peer row requested first, then summed in rank order
+    double2 pr[kClusterMax];
+#pragma unroll
+    for (int k = 0; k < kClusterMax; ++k)
+      pr[k] = k < nblk ? *reinterpret_cast<const double2*>(parts + ((size_t)k * HD + o) * 2) : make_double2(0.0, 0.0);
+#pragma unroll
+    for (int k = 0; k < kClusterMax; ++k) {
+      S1 += pr[k].x;
+      S2 += pr[k].y;
     }
+  }
+  MPPI_STAMP(10);
   if (!LEAN && !a.finalize_inline) {  // rank record for the particle-sharded exchange
     const bool peer = a.peer_recv != nullptr;
     const int nclu = (int)gridDim.x / nblk;  // clusters per instance
@@ -1704,7 +1739,7 @@ __global__ void __launch_bounds__(kStatsThreads, 1) stats_cluster_kernel(const _
       out[2] = cntf;
       out[3] = sumf;
       out[4] = (double)status0;
-      out[5] = (double)a.bad[b];
+      out[5] = (double)bad0;
     }
     if (peer) {
       __syncthreads();
@@ -1740,6 +1775,7 @@ __global__ void __launch_bounds__(kStatsThreads, 1) stats_cluster_kernel(const _
     varbad = (!(vn > 0.0) && !isnan(vn)) ? 1 : 0;
   }
   varbad = __syncthreads_or(varbad);
+  MPPI_STAMP(11);
   double* means = a.means + (size_t)b * HD;
   double* var = a.var + (size_t)b * HD;
   double* sd = a.sd + (size_t)b * HD;
@@ -1763,22 +1799,27 @@ __global__ void __launch_bounds__(kStatsThreads, 1) stats_cluster_kernel(const _
       sd[o] = so;
     }
   }
+  MPPI_STAMP(12);
   if (stt == 0 && o < D && a.cmd) a.cmd[(size_t)b * D + o] = mu_new;  // next_command "mean"
+  const int stt2 = (stt == 0 && varbad) ? MPPI_E_NONPOSITIVE_VARIANCE : stt;
+  // mppi_step_info (mapped host memory) as nine 8-byte words, one per thread
+  // of warp 2, so no single thread queues a chain of system-memory stores
+  constexpr int kInfoWords = (int)(sizeof(mppi_step_info) / 8);
+  static_assert(sizeof(mppi_step_info) % 8 == 0, "mppi_step_info words");
+  if (a.info && threadIdx.x >= 64 && threadIdx.x < 64 + kInfoWords) {
+    const int w = threadIdx.x - 64;
+    unsigned long long word = 0ull;
+    if (w == 0)
+      word = (unsigned)stt2 | ((unsigned long long)(unsigned)(bad0 >= 0x7f000000 ? -1 : bad0) << 32);
+    else if (w == 1)
+      word = (unsigned)(int)cntf;
+    else if (w == 2)
+      word = (unsigned long long)__double_as_longlong(cntf > 0.0 ? m : CUDART_NAN);
+    else if (w == 3)
+      word = (unsigned long long)__double_as_longlong(cntf > 0.0 ? sumf / cntf : CUDART_NAN);
+    reinterpret_cast<unsigned long long*>(a.info + b)[w] = word;  // words 4..8: the stage times, 0
+  }
   if (threadIdx.x == 0) {
-    const int stt2 = (stt == 0 && varbad) ? MPPI_E_NONPOSITIVE_VARIANCE : stt;
-    const int bad = a.bad[b];
-    if (a.info) {
-      mppi_step_info inf;
-      inf.status = stt2;
-      inf.bad_particle = bad >= 0x7f000000 ? -1 : bad;
-      inf.finite_count = (int)cntf;
-      inf._pad = 0;
-      inf.best_cost = cntf > 0.0 ? m : CUDART_NAN;
-      inf.mean_cost = cntf > 0.0 ? sumf / cntf : CUDART_NAN;
-      inf.device_ms = 0.0;
-      inf.sample_ms = inf.rollout_ms = inf.mlp_ms = inf.update_ms = 0.0;
-      a.info[b] = inf;
-    }
     if (a.reset_status) {
       a.status[b] = 0;
       a.bad[b] = 0x7f7f7f7f;
