@@ -242,6 +242,26 @@ def load_library(path: str | os.PathLike | None = None) -> C.CDLL:
     return lib
 
 
+_fast = False
+
+
+def fast_module():
+    """The CPython entry of the latency path (csrc/mppi_fast.c, built beside
+    the library), or None when it is not built or MPPI_NO_FAST is set (A/B):
+    callers then take the ctypes path to the same mppi_step."""
+    global _fast
+    if _fast is False:
+        _fast = None
+        if not os.environ.get("MPPI_NO_FAST"):
+            try:
+                from . import _mppi_fast as m  # noqa: PLC0415
+
+                _fast = m
+            except ImportError:
+                _fast = None
+    return _fast
+
+
 def last_error() -> str:
     return load_library().mppi_last_error().decode(errors="replace")
 

@@ -74,7 +74,33 @@ def build(verbose: bool = False, force: bool = False) -> Path:
         r = subprocess.run(link, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed: {r.stdout}\n{r.stderr}")
+    if not TAG:
+        build_fast(force)
     return OUT
+
+
+FAST_SRC = CSRC / "mppi_fast.c"
+
+
+def fast_path() -> Path:
+    import sysconfig
+
+    return PKG / ("_mppi_fast" + sysconfig.get_config_var("EXT_SUFFIX"))
+
+
+def build_fast(force: bool = False) -> Path:
+    """The CPython entry of the latency path (csrc/mppi_fast.c): a plain C
+    extension that passes the caller's float64 state arrays to mppi_step."""
+    import sysconfig
+
+    out = fast_path()
+    if force or _stale(out, [FAST_SRC]):
+        cc = shutil.which("gcc") or "cc"
+        cmd = [cc, "-O2", "-shared", "-fPIC", f"-I{sysconfig.get_paths()['include']}", str(FAST_SRC), "-o", str(out)]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError(f"cc failed: {' '.join(cmd)}\n{r.stdout}\n{r.stderr}")
+    return out
 
 
 if __name__ == "__main__":

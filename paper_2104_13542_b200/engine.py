@@ -148,6 +148,8 @@ class Plan:
         self._th0, self._thd0 = self._th[0], self._thd[0]
         self._a_th, self._a_thd = self._th.ctypes.data, self._thd.ctypes.data
         self._h = self.handle.value
+        self._fn = C.cast(self.lib.mppi_step, C.c_void_p).value
+        self._fast = N.fast_module() if self.B == 1 else None
         # the same memory as a numpy record array: batched callers read whole
         # columns (status, costs) without touching B ctypes structs
         self.info_columns = np.ctypeslib.as_array(self._info)
@@ -253,6 +255,12 @@ class Plan:
         """step() for B = 1 with float64 (d,) inputs: no staging copies on the
         Python side. Returns (command (d,) view of the plan's output buffer,
         info of instance 0); the view is overwritten by the next step."""
+        if self._fast is not None:  # caller float64 vectors straight to mppi_step (csrc/mppi_fast.c)
+            rc = self._fast.step(self._fn, self._h, theta, theta_dot, self._a_cmd, self._a_info, self.dof)
+            if rc is not NotImplemented:
+                if rc:
+                    N.check(rc)
+                return self._cmd[0], self._info[0]
         if (type(theta) is np.ndarray and type(theta_dot) is np.ndarray and theta.shape == self._th0.shape
                 and theta_dot.shape == self._th0.shape):
             np.copyto(self._th0, theta)  # any real dtype / layout: numpy converts while copying

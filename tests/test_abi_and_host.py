@@ -214,3 +214,23 @@ def test_roofline_dominant_kernel_from_launch_list(tmp_path):
     assert roof["kernel"].startswith("stats") and roof["bound"] == "hbm"
     kern = RL.all_rooflines(stage_ms, rows=15000, dof=7, config=2, peaks=peaks, peaks_kind="measured")
     assert set(kern) == {"rollout", "mlp", "update"}
+
+
+def test_fast_entry_declines_what_needs_a_conversion():
+    """The CPython latency entry (csrc/mppi_fast.c) takes only C-contiguous
+    float64 vectors of length d; anything else returns NotImplemented so the
+    caller converts on the ctypes path. No device call is made here."""
+    import numpy as np
+
+    from paper_2104_13542_b200 import _native as N
+
+    m = N.fast_module()
+    if m is None:
+        pytest.skip("fast entry not built")
+    ok = np.zeros(7)
+    assert m.step(1, 1, ok.astype(np.float32), ok, 0, 0, 7) is NotImplemented
+    assert m.step(1, 1, ok, np.zeros(6), 0, 0, 7) is NotImplemented
+    assert m.step(1, 1, np.zeros(14)[::2], ok, 0, 0, 7) is NotImplemented
+    assert m.step(1, 1, [0.0] * 7, ok, 0, 0, 7) is NotImplemented
+    with pytest.raises(ValueError):
+        m.step(0, 1, ok, ok, 0, 0, 7)
