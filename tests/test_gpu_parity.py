@@ -580,3 +580,33 @@ def test_state_parameter_reaches_both_step_graphs():
         ca, _ = a.control_step(st)
         cb, _ = b.control_step(st)
         np.testing.assert_array_equal(ca, cb)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("null_count", [0, 1, 5, 40])
+@pytest.mark.parametrize("keep_bundle", [False, True])
+def test_null_rows_any_count_vs_oracle(null_count, keep_bundle):
+    """The null (u = 0) and mean (u = mu) rows of sampling.py:283-285 at
+    counts other than the default 2, including 40 (they span two statistics
+    CTAs of 32 particles): the lean cluster kernel patches their deviations
+    in the CTAs that hold them (mppi_kernels.cuh), the bundle path selects
+    per row. FP64 plan, config 1, three closed-loop steps vs the oracle."""
+    from oracle import mppi_oracle as O
+    from paper_2104_13542_b200 import configs
+    from paper_2104_13542_b200.kinematics import load_chain
+
+    kw = dict(configs.CONTROLLER_KW)
+    kw.pop("seed")
+    kw["null_count"] = null_count
+    c = configs.make_controller(1, precision="fp64", keep_bundle=keep_bundle, null_count=null_count)
+    oc = O.OracleController(load_chain("arm7.chain"), configs.make_weights(1), configs.reach_goal_rotation(),
+                            configs.REACH_GOAL_POS, True, **kw)
+    st = configs.start_state()
+    for _ in range(3):
+        cmd, diag = c.control_step(st)
+        ocmd = oc.step(st.theta, st.theta_dot)
+        assert diag.fallback == ""
+        np.testing.assert_allclose(cmd, ocmd, atol=1e-7)
+        np.testing.assert_allclose(c.policy.means, oc.means, atol=1e-7)
+        np.testing.assert_allclose(c.policy.variances, oc.variances, atol=1e-7)
+        assert diag.best_cost == pytest.approx(oc.last["best_cost"], rel=1e-9)
