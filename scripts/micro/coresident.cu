@@ -1,0 +1,104 @@
+// Do rollout-shaped CTAs (128 threads, <= 96 registers) run on SMs that hold
+// an MLP-shaped persistent CTA (544 threads, 88 registers, 196 KB dynamic
+// shared memory, all 512 TMEM columns)? Kernel A occupies every SM for ~200
+// us; kernel B (another stream) launches right after; we count B's CTAs that
+// start before A ends.
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o scripts/micro/coresident scripts/micro/coresident.cu
+#include <cstdio>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+__device__ __forceinline__ unsigned long long gt() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+__global__ void __launch_bounds__(544, 1) kern_a(unsigned long long ns, unsigned long long* out) {
+  extern __shared__ unsigned char sm[];
+  __shared__ uint32_t slot;
+  const int warp = threadIdx.x >> 5;
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+        (uint32_t)__cvta_generic_to_shared(&slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  const unsigned long long t0 = gt();
+  sm[threadIdx.x] = (unsigned char)threadIdx.x;
+  float x[76];  // ~88 live registers, like the MLP kernel
+#pragma unroll
+  for (int i = 0; i < 76; ++i) x[i] = threadIdx.x * (i + 1);
+  while (gt() - t0 < ns) {
+#pragma unroll
+    for (int i = 0; i < 76; ++i) asm volatile("" : "+f"(x[i]));
+  }
+  float acc = 0.f;
+#pragma unroll
+  for (int i = 0; i < 76; ++i) acc += x[i];
+  __syncthreads();
+  if (threadIdx.x == 0) atomicMax(&out[0], gt() + (acc == 1234.5f ? 1 : 0));
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(slot));
+}
+
+template <int MINB>
+__global__ void __launch_bounds__(128, MINB) kern_b(unsigned long long ns, unsigned long long* out) {
+  __shared__ float buf[256];
+  const unsigned long long t0 = gt();
+  buf[threadIdx.x] = threadIdx.x;
+  float x[MINB == 5 ? 80 : 112];  // ~96 / ~128 live registers, like the rollout builds
+#pragma unroll
+  for (int i = 0; i < (MINB == 5 ? 80 : 112); ++i) x[i] = threadIdx.x * (i + 1);
+  while (gt() - t0 < ns) {
+#pragma unroll
+    for (int i = 0; i < (MINB == 5 ? 80 : 112); ++i) asm volatile("" : "+f"(x[i]));
+  }
+  float acc = 0.f;
+#pragma unroll
+  for (int i = 0; i < (MINB == 5 ? 80 : 112); ++i) acc += x[i];
+  if (threadIdx.x == 0) out[1 + blockIdx.x] = t0 + (acc == 1234.5f ? 1 : 0) + (unsigned long long)buf[5] * 0;
+}
+
+int main() {
+  const int nb = 4000;
+  unsigned long long* d;
+  cudaMalloc(&d, sizeof(unsigned long long) * (1 + nb));
+  const int smem = 195888;
+  cudaFuncSetAttribute(kern_a, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  int lo, hi;
+  cudaDeviceGetStreamPriorityRange(&lo, &hi);
+  cudaStream_t sa, sb;
+  cudaStreamCreateWithPriority(&sa, cudaStreamNonBlocking, hi);
+  cudaStreamCreateWithPriority(&sb, cudaStreamNonBlocking, lo);
+  for (int variant = 0; variant < 4; ++variant) {
+    if (variant >= 2) {
+      cudaFuncSetAttribute(kern_b<5>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+      cudaFuncSetAttribute(kern_b<1>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    }
+    cudaMemset(d, 0, sizeof(unsigned long long) * (1 + nb));
+    cudaDeviceSynchronize();
+    kern_a<<<148, 544, smem, sa>>>(200000ull, d);
+    if (variant & 1)
+      kern_b<1><<<nb, 128, 0, sb>>>(2000ull, d);
+    else
+      kern_b<5><<<nb, 128, 0, sb>>>(2000ull, d);
+    cudaError_t e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) {
+      printf("error %s\n", cudaGetErrorString(e));
+      return 1;
+    }
+    unsigned long long h[1 + nb];
+    cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
+    int before = 0;
+    unsigned long long first = ~0ull;
+    for (int i = 0; i < nb; ++i) {
+      if (h[1 + i] < h[0]) ++before;
+      if (h[1 + i] < first) first = h[1 + i];
+    }
+    printf("variant %d (B minBlocks %d, carveout %s): %d of %d B CTAs started while A ran (first B start %.1f us before A end)\n",
+           variant, (variant & 1) ? 1 : 5, variant >= 2 ? "max-shared" : "default", before, nb,
+           (double)((long long)h[0] - (long long)first) * 1e-3);
+  }
+  return 0;
+}
