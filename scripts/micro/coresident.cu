@@ -14,11 +14,11 @@ __device__ __forceinline__ unsigned long long gt() {
   return t;
 }
 
-__global__ void __launch_bounds__(544, 1) kern_a(unsigned long long ns, unsigned long long* out) {
+__global__ void __launch_bounds__(544, 1) kern_a(unsigned long long ns, unsigned long long* out, int tmem) {
   extern __shared__ unsigned char sm[];
   __shared__ uint32_t slot;
   const int warp = threadIdx.x >> 5;
-  if (warp == 0) {
+  if (warp == 0 && tmem) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
         (uint32_t)__cvta_generic_to_shared(&slot)));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
@@ -39,7 +39,7 @@ __global__ void __launch_bounds__(544, 1) kern_a(unsigned long long ns, unsigned
   for (int i = 0; i < 76; ++i) acc += x[i];
   __syncthreads();
   if (threadIdx.x == 0) atomicMax(&out[0], gt() + (acc == 1234.5f ? 1 : 0));
-  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(slot));
+  if (warp == 0 && tmem) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(slot));
 }
 
 template <int MINB>
@@ -71,18 +71,15 @@ int main() {
   cudaStream_t sa, sb;
   cudaStreamCreateWithPriority(&sa, cudaStreamNonBlocking, hi);
   cudaStreamCreateWithPriority(&sb, cudaStreamNonBlocking, lo);
-  for (int variant = 0; variant < 4; ++variant) {
-    if (variant >= 2) {
-      cudaFuncSetAttribute(kern_b<5>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-      cudaFuncSetAttribute(kern_b<1>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-    }
+  cudaFuncSetAttribute(kern_b<5>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+  struct V { int tmem, smem, threads; };
+  const V vs[] = {{1, 195888, 544}, {0, 195888, 544}, {1, 150000, 544}, {0, 150000, 544}, {0, 100000, 544},
+                  {0, 195888, 256}, {1, 195888, 256}};
+  for (const V& v : vs) {
     cudaMemset(d, 0, sizeof(unsigned long long) * (1 + nb));
     cudaDeviceSynchronize();
-    kern_a<<<148, 544, smem, sa>>>(200000ull, d);
-    if (variant & 1)
-      kern_b<1><<<nb, 128, 0, sb>>>(2000ull, d);
-    else
-      kern_b<5><<<nb, 128, 0, sb>>>(2000ull, d);
+    kern_a<<<148, v.threads, v.smem, sa>>>(200000ull, d, v.tmem);
+    kern_b<5><<<nb, 128, 0, sb>>>(2000ull, d);
     cudaError_t e = cudaDeviceSynchronize();
     if (e != cudaSuccess) {
       printf("error %s\n", cudaGetErrorString(e));
@@ -91,14 +88,10 @@ int main() {
     unsigned long long h[1 + nb];
     cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
     int before = 0;
-    unsigned long long first = ~0ull;
-    for (int i = 0; i < nb; ++i) {
+    for (int i = 0; i < nb; ++i)
       if (h[1 + i] < h[0]) ++before;
-      if (h[1 + i] < first) first = h[1 + i];
-    }
-    printf("variant %d (B minBlocks %d, carveout %s): %d of %d B CTAs started while A ran (first B start %.1f us before A end)\n",
-           variant, (variant & 1) ? 1 : 5, variant >= 2 ? "max-shared" : "default", before, nb,
-           (double)((long long)h[0] - (long long)first) * 1e-3);
+    printf("A: %d threads, %d B smem, TMEM %s | B: 128 threads, ~88 regs: %d of %d B CTAs started while A ran\n",
+           v.threads, v.smem, v.tmem ? "512 cols" : "none", before, nb);
   }
   return 0;
 }
