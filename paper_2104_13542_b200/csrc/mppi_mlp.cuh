@@ -537,8 +537,11 @@ __device__ long long mlp_trace[32 * 32];
 // ONE_TILE: every CTA owns at most one tile (the latency path: rows <= 128 x
 // SMs); the next-tile pipelining is compiled out, so the kernel's code holds
 // only what such a launch executes (its instructions are fetched cold).
+#ifndef MPPI_MLP_MAXNREG
+#define MPPI_MLP_MAXNREG 88
+#endif
 template <bool ONE_TILE>
-static __global__ void __maxnreg__(88)
+static __global__ void __maxnreg__(MPPI_MLP_MAXNREG)
     mlp_tcgen05_kernel(const float* __restrict__ x, long long M, const unsigned char* __restrict__ img,
                        float* __restrict__ out, int early, int x_q, int in_d) {
   extern __shared__ __align__(1024) unsigned char mlp_smem[];
