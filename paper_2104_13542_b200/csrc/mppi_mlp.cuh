@@ -300,10 +300,9 @@ __device__ __forceinline__ void store_split8(unsigned char* sm, uint32_t off_h, 
 // ------------------------------------------------------------------ the kernel
 // Warp-specialised: warps 0-15 are the epilogue (warp w serves TMEM lane
 // quadrant q = w % 4, i.e. rows 32q..32q+31 of the tile, and column group
-// cg = w / 4: 8 of every 32 accumulator columns); warp 16 is the producer:
-// it issues the weight TMA and every tcgen05.mma. Activations move through two
-// 32-wide smem buffers; the hand-off is mbarrier-only:
-//   epilogue --aready[b] (16 arrivals)--> issuer --tcgen05.commit--> epilogue
+// cg = w / 4); warp 16 is the producer: it issues the weight copies and every
+// tcgen05.mma. The hand-off is mbarrier-only:
+//   epilogue --A1[c]/A2[c] (16 arrivals)--> issuer --tcgen05.commit--> epilogue
 constexpr int kMlpEpiWarps = 16;
 constexpr int kMlpThreads = (kMlpEpiWarps + 1) * 32;
 
@@ -393,8 +392,10 @@ __device__ __forceinline__ void epi_barrier() {  // named barrier over the 512 e
 // (t+1)] -> [output layer (t)]; issuer = L2(t) -> (L2(t) done) L1(t+1) ->
 // L3(t) -> (L3(t) done) L2(t+1). Layer 1 of the next tile runs while the
 // layer-2 epilogue converts, and the next tile's layer-1 epilogue runs under
-// layer 3. 88 registers: 544 x 88 + a 128-thread rollout CTA fit one SM's 64K
-// register file (programmatic dependent launch, opt-in).
+// layer 3. 88 registers (MPPI_MLP_MAXNREG). Note that no 4-warp CTA of
+// another kernel fits beside this CTA even when the register total would:
+// the register file is split by SM sub-partition and 17 warps put 5 on one
+// (scripts/micro/coresident.cu).
 // Epilogue geometry: each warp converts kEpiCols accumulator columns of its
 // lane quadrant per chunk; a chunk (4 column groups) is what one A1/A2
 // barrier hands to the issuer. 8 (default): two warps per 16-column K slice,
