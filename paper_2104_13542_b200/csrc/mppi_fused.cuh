@@ -143,7 +143,8 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
 
   if (warp == kFusedEpiWarps) {
     // ======================= MMA issuer (one tile) ==========================
-    if (lane == 0) {
+    // the whole warp, MMAs/commits from one elect.sync-ed lane (mppi_mlp.cuh)
+    {
       const uint32_t id32 = umma_idesc(32), id64 = umma_idesc(64), id128 = umma_idesc(128);
       const uint64_t dXH = umma_desc(sb + OFF_XH, 128, 256), dXL = umma_desc(sb + OFF_XL, 128, 256);
       const uint64_t dW0H = umma_desc(sb + OFF_W0H, 128, 256), dW0L = umma_desc(sb + OFF_W0L, 128, 256);
@@ -156,10 +157,10 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
 #pragma unroll
       for (int hf = 0; hf < 2; ++hf) {  // layer 1 as two N=128 halves
         const uint64_t wo = umma_off(128 * hf, 0, 16) >> 4;
-        umma_f16(tmem + 128 * hf, dXH, dW0H + wo, id128, 0);
-        umma_f16(tmem + 128 * hf, dXH, dW0L + wo, id128, 1);
-        umma_f16(tmem + 128 * hf, dXL, dW0H + wo, id128, 1);
-        umma_commit(barL1[hf]);
+        umma_f16_w(tmem + 128 * hf, dXH, dW0H + wo, id128, 0);
+        umma_f16_w(tmem + 128 * hf, dXH, dW0L + wo, id128, 1);
+        umma_f16_w(tmem + 128 * hf, dXL, dW0H + wo, id128, 1);
+        umma_commit_w(barL1[hf]);
       }
       uint32_t phA = 0;  // parity bit per A buffer
 #pragma unroll
@@ -176,11 +177,11 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
 #pragma unroll
         for (int j = 0; j < 2; ++j) {
           const uint64_t aj = ao + (uint64_t)(j * 256 >> 4), wj = (uint64_t)((4 * c + 2 * j) * 128 >> 4);
-          umma_f16(acc2, dAH + aj, dW1H + wj, id128, (c | j) ? 1u : 0u);
-          umma_f16(acc2, dAH + aj, dW1L + wj, id128, 1);
-          umma_f16(acc2, dAL + aj, dW1H + wj, id128, 1);
+          umma_f16_w(acc2, dAH + aj, dW1H + wj, id128, (c | j) ? 1u : 0u);
+          umma_f16_w(acc2, dAH + aj, dW1L + wj, id128, 1);
+          umma_f16_w(acc2, dAL + aj, dW1H + wj, id128, 1);
         }
-        umma_commit(barL20 + 8 * bf);
+        umma_commit_w(barL20 + 8 * bf);
       }
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
@@ -196,10 +197,10 @@ __global__ void __launch_bounds__(kFusedThreads, 1)
 #pragma unroll
         for (int j = 0; j < 2; ++j) {
           const uint64_t aj = ao + (uint64_t)(j * 256 >> 4), wj = (uint64_t)((4 * c + 2 * j) * 128 >> 4);
-          umma_f16(acc3, dAH + aj, dW2H + wj, id128, (c | j) ? 1u : 0u);  // [W2 hi | W2 lo]
-          umma_f16(acc3, dAL + aj, dW2H + wj, id64, 1);
+          umma_f16_w(acc3, dAH + aj, dW2H + wj, id128, (c | j) ? 1u : 0u);  // [W2 hi | W2 lo]
+          umma_f16_w(acc3, dAL + aj, dW2H + wj, id64, 1);
         }
-        umma_commit(barL30 + 8 * bf);
+        umma_commit_w(barL30 + 8 * bf);
       }
       MPPI_TSTAMP(pdbg, 11);
     }
