@@ -408,11 +408,26 @@ __device__ __forceinline__ void epi_barrier() {  // named barrier over the 512 e
 #ifndef MPPI_MLP_EPI_COLS
 #define MPPI_MLP_EPI_COLS 8
 #endif
+// The layer-2 epilogue (which feeds layer 3) of the persistent many-tile
+// kernel uses 16 columns per warp: its x16 TMEM accesses shorten the
+// epilogue that layer 3 waits on (config-4 MLP 10.2 -> 10.0 ms,
+// gpurun_out/ab_h16); the one-tile latency kernel keeps 8 (0.1 us faster at
+// 500 x 30). MPPI_MLP_EPI_COLS_L2 overrides the many-tile value.
+#ifndef MPPI_MLP_EPI_COLS_L2
+#define MPPI_MLP_EPI_COLS_L2 16
+#endif
 constexpr int kEpiCols = MPPI_MLP_EPI_COLS;
-static_assert(kEpiCols == 8 || kEpiCols == 16, "epilogue columns per warp");
+static_assert((kEpiCols == 8 || kEpiCols == 16) && (MPPI_MLP_EPI_COLS_L2 == 8 || MPPI_MLP_EPI_COLS_L2 == 16),
+              "epilogue columns per warp");
 constexpr int kChunkCols = 4 * kEpiCols;
-constexpr int kL1Chunks = kMlpH0 / kChunkCols, kL2Chunks = kMlpH1 / kChunkCols;
+constexpr int kL1Chunks = kMlpH0 / kChunkCols;
 constexpr int kSlicesPerChunk = kChunkCols / 16;
+// layer-2 epilogue geometry of one kernel instantiation
+template <bool ONE_TILE>
+struct Epi2 {
+  static constexpr int cols = ONE_TILE ? kEpiCols : MPPI_MLP_EPI_COLS_L2;
+  static constexpr int chunk = 4 * cols, chunks = kMlpH1 / chunk, slices = chunk / 16;
+};
 // barriers: W0 W1 W2 | L1[2] | A1[8] | L2done | A2[4] | L3done | X
 constexpr int kMlpBars = 3 + 2 + 8 + 1 + 4 + 1 + 1;
 constexpr uint32_t OFF_KBAR = OFF_XL + 128 * 16 * 2;
@@ -580,6 +595,8 @@ static __global__ void __maxnreg__(MPPI_MLP_MAXNREG)
   const uint32_t acc2 = tmem + 256, acc3 = tmem + 384;  // acc1 at tmem
   const long long ntiles = (M + 127) / 128;
   const long long G = gridDim.x;
+  constexpr int kEpiCols2 = Epi2<ONE_TILE>::cols, kChunkCols2 = Epi2<ONE_TILE>::chunk;
+  constexpr int kL2Chunks = Epi2<ONE_TILE>::chunks, kSlicesPerChunk2 = Epi2<ONE_TILE>::slices;
 
   if (warp == kMlpEpiWarps) {
     // ============================== issuer ==================================
@@ -669,8 +686,8 @@ static __global__ void __maxnreg__(MPPI_MLP_MAXNREG)
           }
           tc_fence_after();
 #pragma unroll
-          for (int g = 0; g < kSlicesPerChunk; ++g) {
-            const int s = kSlicesPerChunk * c + g;
+          for (int g = 0; g < kSlicesPerChunk2; ++g) {
+            const int s = kSlicesPerChunk2 * c + g;
             const uint32_t ah = acc2 + 16 * s, al = ah + 8;
             const uint64_t wj = (uint64_t)((2 * s) * 128 >> 4);
             // W2 hi and lo are adjacent 64-row operands: A_hi [W hi | W lo] in one N=128 MMA
@@ -836,17 +853,17 @@ static __global__ void __maxnreg__(MPPI_MLP_MAXNREG)
       if (tid == 0 && tile == blockIdx.x) MLP_STAMP(5);
       if (tid == 0) MLP_TRACE(eit, 0);
       tc_fence_after();
-      uint32_t r2[2][kEpiCols];
-      tmem_ld_async<kEpiCols>(acc2 + lane_base + kEpiCols * cg, r2[0]);
+      uint32_t r2[2][kEpiCols2];
+      tmem_ld_async<kEpiCols2>(acc2 + lane_base + kEpiCols2 * cg, r2[0]);
 #pragma unroll
       for (int c = 0; c < kL2Chunks; ++c) {  // chunk c+1's TMEM load in flight under chunk c
-        tmem_wait_ld<kEpiCols>(r2[c & 1]);
+        tmem_wait_ld<kEpiCols2>(r2[c & 1]);
         if (c + 1 < kL2Chunks)
-          tmem_ld_async<kEpiCols>(acc2 + lane_base + kChunkCols * (c + 1) + kEpiCols * cg, r2[(c + 1) & 1]);
-        float y[kEpiCols];
+          tmem_ld_async<kEpiCols2>(acc2 + lane_base + kChunkCols2 * (c + 1) + kEpiCols2 * cg, r2[(c + 1) & 1]);
+        float y[kEpiCols2];
 #pragma unroll
-        for (int i = 0; i < kEpiCols; ++i) y[i] = __uint_as_float(r2[c & 1][i]);
-        tmem_convert<kEpiCols>(acc2 + lane_base + kChunkCols * c, cg, y, s1, b1 + kChunkCols * c + kEpiCols * cg,
+        for (int i = 0; i < kEpiCols2; ++i) y[i] = __uint_as_float(r2[c & 1][i]);
+        tmem_convert<kEpiCols2>(acc2 + lane_base + kChunkCols2 * c, cg, y, s1, b1 + kChunkCols2 * c + kEpiCols2 * cg,
                                pair_bar);
         arrive(barA2 + 8 * c);
         if (tid == 0) MLP_TRACE(eit, 20 + c);
