@@ -314,6 +314,9 @@ __device__ __forceinline__ bool rollout_particle(const RolloutArgs<R>& a, long l
     if (status_b != 0) return false;  // the instance already failed (an earlier iteration)
     const unsigned badm = __ballot_sync(0xffffffffu, act && bad);
     const unsigned varm = __ballot_sync(0xffffffffu, act && varbad);
+#ifdef MPPI_DEBUG_TIMERS
+    if (a.dbg != nullptr && threadIdx.x == 0 && blockIdx.x < 256) MPPI_TSTAMP(a.dbg + 16 * blockIdx.x, 5);  // controls formed
+#endif
     if (lane == 0 && a.status != nullptr) {
       if (varm && a.check_var && n == 0) atomicMax(&a.status[b], (int)MPPI_E_NONPOSITIVE_VARIANCE);
       if (badm) {
@@ -325,6 +328,9 @@ __device__ __forceinline__ bool rollout_particle(const RolloutArgs<R>& a, long l
     const R dt = act ? a.dts[h] : R(0);
 #pragma unroll
     for (int j = 0; j < D; ++j) v[j] = st_v[j] + warp_inclusive_scan(dt * u[j], lane);
+#ifdef MPPI_DEBUG_TIMERS
+    if (a.dbg != nullptr && threadIdx.x == 0 && blockIdx.x < 256 && v[D - 1] != R(12345)) MPPI_TSTAMP(a.dbg + 16 * blockIdx.x, 6);
+#endif
 #pragma unroll
     for (int j = 0; j < D; ++j) p[j] = st_p[j] + warp_inclusive_scan(dt * v[j], lane);
   }
