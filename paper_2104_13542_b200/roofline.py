@@ -164,4 +164,7 @@ def _stage_roofline(stage: str, stage_ms: dict, rows: int, dof: int, config: int
     return {"kernel": "stats/update (weights + mean/cov + shift)", "bound": "hbm", "achieved": achieved,
             "peak": peak, "unit": "GB/s", "frac": achieved / peak, "traffic": None,
             "peak_source": f"hbm_gbs ({peaks_kind})",
-            "algorithmic": f"{update_bytes_per_unit(dof)} B/particle-step x {rows}"}
+            "algorithmic": f"{update_bytes_per_unit(dof)} B/particle-step x {rows}",
+            "note": "operand bytes per particle-step, eps row counted per instance: a batch shares one eps "
+                    "block served from L2, so DRAM carries ~8 B/particle-step and the batched kernel is "
+                    "instruction-bound (profiles/r2c_full_c4_stats_multi_metrics.json: 75 % issue, 10.7 % DRAM)"}
