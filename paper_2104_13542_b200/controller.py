@@ -275,9 +275,11 @@ class Controller:
         if latency > self.latency_budget * 1e3:
             log.debug("control step overran budget: %.2f ms", latency)
         bundle = LazyBundle(self, self._step_serial)
-        # without profile_stages() the whole fused step is reported as rollout time
-        roll = info.rollout_ms + info.mlp_ms
         # positional: latency, sample, rollout, update, best, mean, fallback, bundle
+        if not self._plan.profile_level:  # no device timing: the stage fields are zero (4 ctypes reads saved)
+            return command, StepDiagnostics(latency, 0.0, latency, 0.0, info.best_cost, info.mean_cost, "", bundle)
+        # without per-stage events the whole fused step is reported as rollout time
+        roll = info.rollout_ms + info.mlp_ms
         return command, StepDiagnostics(latency, info.sample_ms, roll if roll > 0.0 else latency, info.update_ms,
                                         info.best_cost, info.mean_cost, "", bundle)
 

@@ -148,6 +148,7 @@ class Plan:
         self._th0, self._thd0 = self._th[0], self._thd[0]
         self._a_th, self._a_thd = self._th.ctypes.data, self._thd.ctypes.data
         self._h = self.handle.value
+        self.profile_level = 0  # device stage times are only filled when profiling
         self._fn = C.cast(self.lib.mppi_step, C.c_void_p).value
         self._fast = N.fast_module() if self.B == 1 else None
         # the same memory as a numpy record array: batched callers read whole
@@ -276,6 +277,7 @@ class Plan:
         """0: lean graph, no timing; 1: device_ms of the lean graph; 2: the
         instrumented graph with per-stage event times (see mppi_profile_stages)."""
         N.check(self.lib.mppi_profile_stages(self.handle, int(level)))
+        self.profile_level = int(level)
 
     def evaluate(self, mode: int, inputs0, inputs1, dts, gamma, terminal_weight, theta0=None,
                  theta_dot0=None, want=("positions", "velocities", "accelerations", "step_costs",
