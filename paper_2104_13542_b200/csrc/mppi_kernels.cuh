@@ -1984,7 +1984,23 @@ __global__ void __launch_bounds__(kStatsThreads, MINB) stats_multi_kernel(const 
 #pragma unroll
     for (int g = 0; g < G; ++g) s1[g] = s2[g] = 0.0;
     const double* ep = a.eps + o;
-    for (int k0 = 0; k0 < nnz; k0 += PD) {
+    // the null and mean rows (sampling.py:283-285) lead the ascending list:
+    // summed first with their selects, then every other row without any
+    // (same elements in the same order as before, so bit-identical)
+    int k1 = 0;
+    while (k1 < nnz && nz[k1] + a.particle_offset <= a.null_count) {
+      const int ng = nz[k1] + a.particle_offset;
+      const double ev = __ldg(ep + (size_t)nz[k1] * HD);
+#pragma unroll
+      for (int g = 0; g < G; ++g) {
+        const double dv = ng < a.null_count ? 0.0 - mo[g] : (ng == a.null_count ? 0.0 : (mo[g] + so[g] * ev) - mo[g]);
+        const double w = wt[g * N + nz[k1]];
+        s1[g] += w * dv;
+        s2[g] += w * dv * dv;
+      }
+      ++k1;
+    }
+    for (int k0 = k1; k0 < nnz; k0 += PD) {
       double e[PD];
       int ii[PD];
 #pragma unroll
@@ -1995,11 +2011,9 @@ __global__ void __launch_bounds__(kStatsThreads, MINB) stats_multi_kernel(const 
 #pragma unroll
       for (int u = 0; u < PD; ++u) {
         if (ii[u] < 0) break;
-        const int ng = ii[u] + a.particle_offset;
 #pragma unroll
         for (int g = 0; g < G; ++g) {
-          const double dv = ng < a.null_count ? 0.0 - mo[g]
-                                              : (ng == a.null_count ? 0.0 : (mo[g] + so[g] * e[u]) - mo[g]);
+          const double dv = (mo[g] + so[g] * e[u]) - mo[g];
           const double w = wt[g * N + ii[u]];
           s1[g] += w * dv;
           s2[g] += w * dv * dv;
