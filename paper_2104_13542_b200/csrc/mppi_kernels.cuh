@@ -1379,7 +1379,19 @@ __global__ void __launch_bounds__(kStatsThreads) stats_kernel(const __grid_const
     if (!failed) {
       const double* ep = a.eps + (size_t)n0 * HD + o;
       constexpr int PD = 16;
-      for (int k0 = 0; k0 < nnz; k0 += PD) {
+      // null and mean rows (sampling.py:283-285) lead the ascending list:
+      // summed first with their selects, the rest without (same order)
+      int k1 = 0;
+      while (k1 < nnz && n0 + nz[k1] + a.particle_offset <= a.null_count) {
+        const int ng = n0 + nz[k1] + a.particle_offset;
+        const double ev = __ldg(ep + (size_t)nz[k1] * HD);
+        const double dv = ng < a.null_count ? 0.0 - mo_pre : (ng == a.null_count ? 0.0 : (mo_pre + so_pre * ev) - mo_pre);
+        const double w = wt[nz[k1]];
+        s1 += w * dv;
+        s2 += w * dv * dv;
+        ++k1;
+      }
+      for (int k0 = k1; k0 < nnz; k0 += PD) {
         double e[PD];
         int ii[PD];
 #pragma unroll
@@ -1390,9 +1402,7 @@ __global__ void __launch_bounds__(kStatsThreads) stats_kernel(const __grid_const
 #pragma unroll
         for (int u = 0; u < PD; ++u) {
           if (ii[u] < 0) break;
-          const int ng = n0 + ii[u] + a.particle_offset;
-          const double dv = ng < a.null_count ? 0.0 - mo_pre
-                                              : (ng == a.null_count ? 0.0 : (mo_pre + so_pre * e[u]) - mo_pre);
+          const double dv = (mo_pre + so_pre * e[u]) - mo_pre;
           const double w = wt[ii[u]];
           s1 += w * dv;
           s2 += w * dv * dv;
